@@ -1,0 +1,146 @@
+/*
+ * bcn.h -- C ABI of libbcn.so, the sm_100a RNS-CKKS engine behind the
+ * ciphertext branch of Bi-CryptoNets (arXiv 2402.01296).
+ *
+ * Boundary: the reference's only plugin seam is the
+ * float64 slot-kernel module `ops` (pkg/src/bibranch/backend.py:12-27,
+ * _slotops_cy.pyx:16-101).  Real ciphertexts are not slot arrays, so this
+ * library sits one level up, behind the `bibranch.sim` API
+ * (pkg/src/bibranch/sim.py:142-283); each entry point below names the
+ * reference function whose semantics it realises.  The Python mirror
+ * (paper_2402_01296_b200/sim.py) binds these with ctypes; INTEGRATION.md
+ * shows the binding a maintainer adds to the reference.
+ *
+ * Conventions
+ *  - All buffers are DEVICE pointers to u64 residues (canonical, [0, q))
+ *    or float64, owned by the caller (torch).  The library owns only its
+ *    tables, the secret key, switching keys and a scratch arena.
+ *  - A ciphertext batch is u64[G][2][nlimb][N] in the bit-reversed NTT
+ *    domain; limb t is modulo basis prime t (q_0..q_L, then p_0..p_{K-1}).
+ *    A "level" l ciphertext uses limbs 0..l; `*_nlimb` arguments give the
+ *    limb count of the buffer layout (>= level+1) so higher-level inputs
+ *    are read in place (level = min semantics of sim.py:213).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t, may be NULL
+ *    for the legacy stream).  One context must be used from one stream.
+ *  - Return value: BCN_OK or an error code; bcn_last_error() gives a
+ *    thread-local message.  Codes map onto the reference's exception
+ *    classes (pkg/src/bibranch/errors.py:7-31) in the Python mirror.
+ */
+#ifndef BCN_H
+#define BCN_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BCN_OK 0
+#define BCN_ERR_PARAM 1      /* ParameterError / ShapeError       */
+#define BCN_ERR_DEPTH 2      /* DepthBudgetError                  */
+#define BCN_ERR_USAGE 3      /* UsageError                        */
+#define BCN_ERR_CUDA 4       /* DeviceError (new)                 */
+#define BCN_ERR_CAPACITY 5   /* CapacityError                     */
+
+typedef struct bcn_ctx bcn_ctx;
+
+const char *bcn_last_error(void);
+int bcn_version(void);
+
+/* make_context (sim.py:142-169): ring degree N = 2^logn (8 <= N <= 16384),
+ * ciphertext primes q[0..max_level], special primes p[0..n_special-1],
+ * dnum key-switching digits, Philox seed for sk / keys / encryption. */
+int bcn_ctx_create(bcn_ctx **out, int logn, int max_level, const uint64_t *q, int n_special,
+                   const uint64_t *p, int dnum, uint64_t seed, int device);
+/* upload the canonical-embedding table ksi[k] = exp(2 pi i k / 2N), k <= 2N
+ * (host float64 arrays of 2N+1 entries each, computed by numpy on the host so
+ * that engine and oracle share the same bits). Must be called once. */
+int bcn_ctx_set_fft(bcn_ctx *ctx, const double *re, const double *im);
+int bcn_ctx_destroy(bcn_ctx *ctx);
+/* bytes of device memory held by tables + keys + scratch */
+int bcn_ctx_memory(bcn_ctx *ctx, uint64_t *bytes);
+/* drop the scratch arena (between workloads) */
+int bcn_ctx_trim(bcn_ctx *ctx);
+
+/* ---- K1/K2: negacyclic NTT / INTT, in place.
+ * data: u64[npoly][nlimb][N]; limb t is modulo basis prime (prime0 + t). */
+int bcn_ntt_fwd(bcn_ctx *ctx, uint64_t *data, int npoly, int nlimb, int prime0, void *stream);
+int bcn_ntt_inv(bcn_ctx *ctx, uint64_t *data, int npoly, int nlimb, int prime0, void *stream);
+
+/* ---- K9: encode_plain (sim.py:172-181) + CKKS canonical embedding.
+ * vals: f64[nplain][vstride] (first vlen used, rest zero).  out:
+ * u64[nplain][level+1][N], NTT domain; montgomery != 0 stores x*2^64 mod q
+ * (the form bcn_mul_plain expects for multipliers). */
+int bcn_encode(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int nplain, double scale, int level,
+               int montgomery, uint64_t *out, void *stream);
+
+/* ---- K10: encrypt_vector (sim.py:184-189), secret-key RLWE.
+ * ct_out: u64[G][2][level+1][N]; ciphertext g uses Philox id counter0 + g. */
+int bcn_encrypt(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int G, int level, double scale,
+                uint64_t counter0, uint64_t *ct_out, void *stream);
+
+/* ---- K11: decrypt_vector (sim.py:192-196): c0 + c1 s, INTT, CRT, FFT.
+ * out: f64[G][nout] real slot values (nout <= N/2). */
+int bcn_decrypt(bcn_ctx *ctx, const uint64_t *ct, int ct_nlimb, int G, int level, double scale, double *out,
+                int nout, void *stream);
+/* decrypted plaintext polynomial (coefficient domain, limbs 0..min(level,1)) */
+int bcn_decrypt_poly(bcn_ctx *ctx, const uint64_t *ct, int ct_nlimb, int G, int level, uint64_t *out,
+                     void *stream);
+
+/* ---- K3: he_add (sim.py:208-218).  out = a + b (b_is_plain: b is a
+ * u64[Gb][level+1][N] plaintext added to c0 only, Gb in {1, G}). */
+int bcn_add(bcn_ctx *ctx, uint64_t *out, const uint64_t *a, int a_nlimb, const uint64_t *b, int b_nlimb,
+            int b_is_plain, int b_batch, int G, int level, void *stream);
+int bcn_sub(bcn_ctx *ctx, uint64_t *out, const uint64_t *a, int a_nlimb, const uint64_t *b, int b_nlimb,
+            int G, int level, void *stream);
+
+/* ---- K4+K5: he_mul ct x plain (sim.py:221-248): out(level-1) =
+ * rescale(ct (x) pt); pt_mont: u64[Gp][level+1][N] Montgomery, Gp in {1, G}. */
+int bcn_mul_plain(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb, const uint64_t *pt_mont,
+                  int pt_batch, int G, int level, void *stream);
+/* product without rescale (lazy-rescale accumulation), out at level */
+int bcn_mul_plain_norescale(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb,
+                            const uint64_t *pt_mont, int pt_batch, int G, int level, void *stream);
+/* K4 microbenchmark form: out[g] = sum_{t in [g*group, min((g+1)*group, n_items))} ct[t] (x) pt[t] */
+int bcn_mac(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, const uint64_t *pt_mont, int n_items, int group,
+            int nlimb, void *stream);
+
+/* ---- K5: rescale by q_level: in u64[G][2][in_nlimb][N] -> out u64[G][2][level][N] */
+int bcn_rescale(bcn_ctx *ctx, uint64_t *out, const uint64_t *in, int in_nlimb, int G, int level, void *stream);
+
+/* ---- K6+K7: he_mul ct x ct (square_act, layers.py:210-214): tensor,
+ * relinearise, rescale.  out: u64[G][2][level][N]. */
+int bcn_mul_cc(bcn_ctx *ctx, uint64_t *out, const uint64_t *a, int a_nlimb, const uint64_t *b, int b_nlimb,
+               int G, int level, int rescale, void *stream);
+
+/* ---- K7/K8: he_rotate (sim.py:251-256), hoisted form.
+ * bcn_modup: U = ModUp(c1) -> u64[G][ndig][level+1+K][N] (size: bcn_modup_words)
+ * bcn_rotate_hoisted: out = (sigma_g(c0) + KS0, KS1) using U and the Galois key of g
+ * bcn_rotate: both in one call (scratch U).  g = 5^r mod 2N; g = 1 copies. */
+int bcn_modup_words(bcn_ctx *ctx, int G, int level, uint64_t *words);
+int bcn_modup(bcn_ctx *ctx, uint64_t *U, const uint64_t *ct, int ct_nlimb, int G, int level, void *stream);
+int bcn_rotate_hoisted(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb, const uint64_t *U, int G,
+                       int level, uint64_t g, void *stream);
+int bcn_rotate(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb, int G, int level, uint64_t g,
+               void *stream);
+
+/* ---- switching keys (generated on device from the seed, cached) */
+int bcn_keygen_relin(bcn_ctx *ctx, void *stream);
+int bcn_keygen_galois(bcn_ctx *ctx, uint64_t g, void *stream);
+/* canonical copy of a key: out u64[dnum][2][nbasis][N] (key_id: 2 = relin, g = Galois) */
+int bcn_export_key(bcn_ctx *ctx, uint64_t key_id, uint64_t *out, void *stream);
+/* canonical NTT-domain secret key over the full basis: u64[nbasis][N] */
+int bcn_export_secret(bcn_ctx *ctx, uint64_t *out, void *stream);
+
+/* ---- utilities for benches / parity tests */
+int bcn_sample_uniform(bcn_ctx *ctx, uint64_t *out, int npoly, int nlimb, int prime0, uint64_t seed,
+                       uint64_t id0, void *stream);
+int bcn_to_montgomery(bcn_ctx *ctx, uint64_t *out, const uint64_t *in, int npoly, int nlimb, int prime0,
+                      void *stream);
+int bcn_automorph(bcn_ctx *ctx, uint64_t *out, const uint64_t *in, int npoly, int nlimb, uint64_t g, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

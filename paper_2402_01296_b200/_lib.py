@@ -1,0 +1,103 @@
+"""ctypes binding of libbcn.so (include/bcn.h).
+
+The extension is mandatory: importing the engine without it raises
+DeviceError -- there is no CPU or eager fallback anywhere in the product.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import (
+    CapacityError,
+    DepthBudgetError,
+    DeviceError,
+    ParameterError,
+    UsageError,
+)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbcn.so")
+
+BCN_OK, BCN_ERR_PARAM, BCN_ERR_DEPTH, BCN_ERR_USAGE, BCN_ERR_CUDA, BCN_ERR_CAPACITY = range(6)
+_ERRORS = {
+    BCN_ERR_PARAM: ParameterError,
+    BCN_ERR_DEPTH: DepthBudgetError,
+    BCN_ERR_USAGE: UsageError,
+    BCN_ERR_CUDA: DeviceError,
+    BCN_ERR_CAPACITY: CapacityError,
+}
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_U64 = ctypes.c_uint64
+_D = ctypes.c_double
+
+# name -> argtypes (all return int)
+SIGNATURES = {
+    "bcn_ctx_create": [ctypes.POINTER(_P), _I, _I, ctypes.POINTER(_U64), _I, ctypes.POINTER(_U64), _I, _U64, _I],
+    "bcn_ctx_set_fft": [_P, ctypes.POINTER(_D), ctypes.POINTER(_D)],
+    "bcn_ctx_destroy": [_P],
+    "bcn_ctx_memory": [_P, ctypes.POINTER(_U64)],
+    "bcn_ctx_trim": [_P],
+    "bcn_ntt_fwd": [_P, _P, _I, _I, _I, _P],
+    "bcn_ntt_inv": [_P, _P, _I, _I, _I, _P],
+    "bcn_encode": [_P, _P, _I, _I, _I, _D, _I, _I, _P, _P],
+    "bcn_encrypt": [_P, _P, _I, _I, _I, _I, _D, _U64, _P, _P],
+    "bcn_decrypt": [_P, _P, _I, _I, _I, _D, _P, _I, _P],
+    "bcn_decrypt_poly": [_P, _P, _I, _I, _I, _P, _P],
+    "bcn_add": [_P, _P, _P, _I, _P, _I, _I, _I, _I, _I, _P],
+    "bcn_sub": [_P, _P, _P, _I, _P, _I, _I, _I, _P],
+    "bcn_mul_plain": [_P, _P, _P, _I, _P, _I, _I, _I, _P],
+    "bcn_mul_plain_norescale": [_P, _P, _P, _I, _P, _I, _I, _I, _P],
+    "bcn_mac": [_P, _P, _P, _P, _I, _I, _I, _P],
+    "bcn_rescale": [_P, _P, _P, _I, _I, _I, _P],
+    "bcn_mul_cc": [_P, _P, _P, _I, _P, _I, _I, _I, _I, _P],
+    "bcn_modup_words": [_P, _I, _I, ctypes.POINTER(_U64)],
+    "bcn_modup": [_P, _P, _P, _I, _I, _I, _P],
+    "bcn_rotate_hoisted": [_P, _P, _P, _I, _P, _I, _I, _U64, _P],
+    "bcn_rotate": [_P, _P, _P, _I, _I, _I, _U64, _P],
+    "bcn_keygen_relin": [_P, _P],
+    "bcn_keygen_galois": [_P, _U64, _P],
+    "bcn_export_key": [_P, _U64, _P, _P],
+    "bcn_export_secret": [_P, _P, _P],
+    "bcn_sample_uniform": [_P, _P, _I, _I, _I, _U64, _U64, _P],
+    "bcn_to_montgomery": [_P, _P, _P, _I, _I, _I, _P],
+    "bcn_automorph": [_P, _P, _P, _I, _I, _U64, _P],
+}
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"libbcn.so not built at {LIB_PATH}; run __graft_entry__.build() "
+                "(the engine has no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        lib.bcn_last_error.restype = ctypes.c_char_p
+        lib.bcn_last_error.argtypes = []
+        lib.bcn_version.restype = _I
+        for name, argt in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = _I
+            fn.argtypes = argt
+        _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return ["bcn_last_error", "bcn_version", *SIGNATURES]
+
+
+def check(code: int, what: str = "") -> None:
+    if code != BCN_OK:
+        msg = load().bcn_last_error().decode(errors="replace")
+        raise _ERRORS.get(code, DeviceError)(f"{what}: {msg}" if what else msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,855 @@
+// api.cu -- the C ABI of libbcn.so (include/bcn.h): context, tables, keys,
+// scratch arena and the composition of kernels into HE operations.  This is
+// the native runtime behind paper_2402_01296_b200/sim.py; it never touches
+// host data on the hot path and never falls back to the CPU.
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/bcn.h"
+#include "common.cuh"
+#include "ops.cuh"
+
+
+using namespace bcn;
+typedef unsigned __int128 u128;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+#define CUDA_TRY(x)                                                                           \
+    do {                                                                                      \
+        cudaError_t _e = (x);                                                                 \
+        if (_e != cudaSuccess) return fail(BCN_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+// ------------------------------------------------------------ host math
+static u64 mulmod_h(u64 a, u64 b, u64 q) { return (u64)((u128)a * b % q); }
+static u64 powmod_h(u64 a, u64 e, u64 q) {
+    u64 r = 1 % q;
+    a %= q;
+    while (e) {
+        if (e & 1) r = mulmod_h(r, a, q);
+        a = mulmod_h(a, a, q);
+        e >>= 1;
+    }
+    return r;
+}
+static u64 inv_h(u64 a, u64 q) { return powmod_h(a, q - 2, q); }
+static u64 shoup_h(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+static u64 mont_h(u64 a, u64 q) { return (u64)(((u128)(a % q) << 64) % q); }
+
+static u64 primitive_root_2n(u64 q, u64 N) {
+    u64 e = (q - 1) / (2 * N);
+    for (u64 x = 2;; x++) {
+        u64 g = powmod_h(x, e, q);
+        if (powmod_h(g, N, q) == q - 1) return g;
+    }
+}
+
+static u32 brev_h(u32 x, int bits) {
+    u32 r = 0;
+    for (int i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+
+// ------------------------------------------------------------- context
+struct LevelTables {
+    ConvTable* modup = nullptr;     // [ndig]
+    ConvTable* moddown = nullptr;   // [1]
+    u64* pinv = nullptr;            // [2 * (level+1)] Shoup pairs of P^-1 mod q_i
+    u64* qlinv = nullptr;           // [2 * level] Shoup pairs of q_level^-1 mod q_i
+    int ndig = 0;
+};
+
+struct bcn_ctx {
+    int device = 0;
+    int logn = 0, N = 0, L = 0, nq = 0, K = 0, dnum = 0, alpha = 0, nbasis = 0;
+    u64 seed = 0;
+    std::vector<u64> primes;
+    std::vector<PrimeInfo> hpr;
+    PrimeInfo* pr = nullptr;
+    ulonglong2* tw = nullptr;
+    double* ksi_re = nullptr;
+    double* ksi_im = nullptr;
+    int* rot = nullptr;
+    u64* s_ntt = nullptr;    // canonical
+    u64* s_mont = nullptr;   // Montgomery
+    u64* pmod = nullptr;     // Shoup pairs of P mod q_i (i < nq)
+    std::map<int, LevelTables> lt;
+    std::map<u64, u64*> keys;
+    u64* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    size_t table_bytes = 0, key_bytes = 0;
+    u64 q0inv_q1 = 0, q0inv_q1_p = 0;
+
+    size_t key_words() const { return (size_t)dnum * 2 * nbasis * N; }
+};
+
+static cudaError_t dmalloc(void** p, size_t bytes, size_t* acc) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess && acc) *acc += bytes;
+    return e;
+}
+
+static u64* scratch_get(bcn_ctx* c, size_t words, int* err) {
+    size_t bytes = words * sizeof(u64);
+    if (bytes > c->scratch_bytes) {
+        if (c->scratch) cudaFree(c->scratch);   // synchronising: in-flight users are done
+        c->scratch = nullptr;
+        size_t nb = bytes + bytes / 4;
+        if (cudaMalloc(&c->scratch, nb) != cudaSuccess) {
+            c->scratch_bytes = 0;
+            *err = fail(BCN_ERR_CUDA, "scratch allocation of " + std::to_string(nb) + " bytes failed");
+            return nullptr;
+        }
+        c->scratch_bytes = nb;
+    }
+    return c->scratch;
+}
+
+static Limbs limbs_range(int prime0, int n) {
+    Limbs l;
+    l.n = n;
+    for (int i = 0; i < n && i < BCN_MAX_LIMBS; i++) l.prime[i] = (short)(prime0 + i);
+    return l;
+}
+
+// extended basis at level l: q_0..q_l, p_0..p_{K-1}
+static Limbs limbs_ext(const bcn_ctx* c, int level) {
+    Limbs l;
+    l.n = level + 1 + c->K;
+    for (int t = 0; t <= level; t++) l.prime[t] = (short)t;
+    for (int k = 0; k < c->K; k++) l.prime[level + 1 + k] = (short)(c->nq + k);
+    return l;
+}
+
+static int ndig_at(const bcn_ctx* c, int level) { return (level + c->alpha) / c->alpha; }
+
+static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, const Limbs& l) {
+    NttArgs a;
+    a.data = data;
+    a.poly_stride = poly_stride;
+    a.digit_stride = 0;
+    a.limbs = l;
+    a.tw = c->tw;
+    a.pr = c->pr;
+    a.skip_alpha = 0;
+    a.skip_dnum = 1;
+    a.skip_level = 0;
+    return a;
+}
+
+static cudaError_t ntt_run(const bcn_ctx* c, bool inv, u64* data, long long poly_stride, const Limbs& l, int npoly,
+                           cudaStream_t st) {
+    NttArgs a = ntt_args(c, data, poly_stride, l);
+    return ntt_launch(inv, c->logn, a, l.n, npoly, st);
+}
+
+static int build_level(bcn_ctx* c, int level, LevelTables** out) {
+    auto it = c->lt.find(level);
+    if (it != c->lt.end()) { *out = &it->second; return BCN_OK; }
+    LevelTables T;
+    const int ndig = ndig_at(c, level);
+    T.ndig = ndig;
+    const Limbs ext = limbs_ext(c, level);
+    std::vector<ConvTable> up(ndig);
+    for (int j = 0; j < ndig; j++) {
+        ConvTable& t = up[j];
+        memset(&t, 0, sizeof(t));
+        const int i0 = j * c->alpha, i1 = std::min((j + 1) * c->alpha, level + 1);
+        t.n_src = i1 - i0;
+        for (int i = i0; i < i1; i++) {
+            const u64 qi = c->primes[i];
+            u64 prod = 1;
+            for (int k = i0; k < i1; k++) if (k != i) prod = mulmod_h(prod, c->primes[k] % qi, qi);
+            const u64 hinv = inv_h(prod, qi);
+            t.hatinv[i - i0] = hinv;
+            t.hatinv_p[i - i0] = shoup_h(hinv, qi);
+            for (int e = 0; e < ext.n; e++) {
+                const u64 qt = c->primes[ext.prime[e]];
+                u64 pm = 1;
+                for (int k = i0; k < i1; k++) if (k != i) pm = mulmod_h(pm, c->primes[k] % qt, qt);
+                t.hat_m[(i - i0) * BCN_MAX_LIMBS + e] = mont_h(pm, qt);
+            }
+        }
+    }
+    ConvTable down;
+    memset(&down, 0, sizeof(down));
+    down.n_src = c->K;
+    for (int k = 0; k < c->K; k++) {
+        const u64 pk = c->primes[c->nq + k];
+        u64 prod = 1;
+        for (int k2 = 0; k2 < c->K; k2++) if (k2 != k) prod = mulmod_h(prod, c->primes[c->nq + k2] % pk, pk);
+        const u64 hinv = inv_h(prod, pk);
+        down.hatinv[k] = hinv;
+        down.hatinv_p[k] = shoup_h(hinv, pk);
+        for (int i = 0; i <= level; i++) {
+            const u64 qi = c->primes[i];
+            u64 pm = 1;
+            for (int k2 = 0; k2 < c->K; k2++) if (k2 != k) pm = mulmod_h(pm, c->primes[c->nq + k2] % qi, qi);
+            down.hat_m[k * BCN_MAX_LIMBS + i] = mont_h(pm, qi);
+        }
+    }
+    std::vector<u64> pinv(2 * (level + 1)), qlinv(2 * std::max(level, 1));
+    for (int i = 0; i <= level; i++) {
+        const u64 qi = c->primes[i];
+        u64 P = 1;
+        for (int k = 0; k < c->K; k++) P = mulmod_h(P, c->primes[c->nq + k] % qi, qi);
+        const u64 v = inv_h(P, qi);
+        pinv[2 * i] = v;
+        pinv[2 * i + 1] = shoup_h(v, qi);
+    }
+    for (int i = 0; i < level; i++) {
+        const u64 qi = c->primes[i];
+        const u64 v = inv_h(c->primes[level] % qi, qi);
+        qlinv[2 * i] = v;
+        qlinv[2 * i + 1] = shoup_h(v, qi);
+    }
+    CUDA_TRY(dmalloc((void**)&T.modup, sizeof(ConvTable) * ndig, &c->table_bytes));
+    CUDA_TRY(dmalloc((void**)&T.moddown, sizeof(ConvTable), &c->table_bytes));
+    CUDA_TRY(dmalloc((void**)&T.pinv, sizeof(u64) * pinv.size(), &c->table_bytes));
+    CUDA_TRY(dmalloc((void**)&T.qlinv, sizeof(u64) * qlinv.size(), &c->table_bytes));
+    CUDA_TRY(cudaMemcpy(T.modup, up.data(), sizeof(ConvTable) * ndig, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(T.moddown, &down, sizeof(ConvTable), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(T.pinv, pinv.data(), sizeof(u64) * pinv.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(T.qlinv, qlinv.data(), sizeof(u64) * qlinv.size(), cudaMemcpyHostToDevice));
+    c->lt[level] = T;
+    *out = &c->lt[level];
+    return BCN_OK;
+}
+
+static int check_level(const bcn_ctx* c, int level) {
+    if (level < 0 || level > c->L) return fail(BCN_ERR_PARAM, "level " + std::to_string(level) + " outside [0, " + std::to_string(c->L) + "]");
+    return BCN_OK;
+}
+
+static FftTab fft_tab(const bcn_ctx* c) {
+    FftTab f;
+    f.re = c->ksi_re;
+    f.im = c->ksi_im;
+    f.rot = c->rot;
+    return f;
+}
+
+extern "C" {
+
+const char* bcn_last_error(void) { return g_err.c_str(); }
+int bcn_version(void) { return 1; }
+
+int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, int n_special, const uint64_t* p,
+                   int dnum, uint64_t seed, int device) {
+    if (!out) return fail(BCN_ERR_PARAM, "null output pointer");
+    if (logn < 3 || logn > 14) return fail(BCN_ERR_PARAM, "logn must be in [3, 14]");
+    if (max_level < 0 || n_special < 1 || dnum < 1) return fail(BCN_ERR_PARAM, "bad level / special / dnum");
+    const int nq = max_level + 1, nb = nq + n_special;
+    if (nb > BCN_MAX_LIMBS) return fail(BCN_ERR_PARAM, "too many primes");
+    const int alpha = (nq + dnum - 1) / dnum;
+    if (alpha > BCN_MAX_ALPHA || n_special > BCN_MAX_ALPHA) return fail(BCN_ERR_PARAM, "digit too wide");
+    const u64 N = 1ull << logn;
+    std::unique_ptr<bcn_ctx> c(new bcn_ctx());
+    c->device = device;
+    CUDA_TRY(cudaSetDevice(device));
+    c->logn = logn; c->N = (int)N; c->L = max_level; c->nq = nq; c->K = n_special;
+    c->dnum = dnum; c->alpha = alpha; c->nbasis = nb; c->seed = seed;
+    for (int i = 0; i < nq; i++) c->primes.push_back(q[i]);
+    for (int k = 0; k < n_special; k++) c->primes.push_back(p[k]);
+    for (int i = 0; i < nb; i++) {
+        const u64 qi = c->primes[i];
+        if (qi >= (1ull << 61) || qi % (2 * N) != 1) return fail(BCN_ERR_PARAM, "prime " + std::to_string(qi) + " is not < 2^61 and 1 mod 2N");
+        for (int j = 0; j < i; j++) if (c->primes[j] == qi) return fail(BCN_ERR_PARAM, "duplicate prime");
+    }
+    // prime info + twiddles
+    c->hpr.resize(nb);
+    std::vector<ulonglong2> tw((size_t)nb * 2 * N);
+    std::vector<u64> pw(N), pwi(N);
+    for (int i = 0; i < nb; i++) {
+        const u64 qi = c->primes[i];
+        PrimeInfo& P = c->hpr[i];
+        memset(&P, 0, sizeof(P));
+        P.q = qi;
+        u64 inv = 1;   // Newton: q^-1 mod 2^64
+        for (int it = 0; it < 7; it++) inv *= 2 - qi * inv;
+        P.qinv_neg = (u64)0 - inv;
+        P.r1 = (u64)(((u128)1 << 64) % qi);
+        P.r1_shoup = shoup_h(P.r1, qi);
+        P.r2 = mulmod_h(P.r1, P.r1, qi);
+        const u64 ninv = inv_h(N % qi, qi);
+        P.pad[0] = ninv;
+        P.pad[1] = shoup_h(ninv, qi);
+        const u64 psi = primitive_root_2n(qi, N), psi_inv = inv_h(psi, qi);
+        u64 a = 1, b = 1;
+        for (u64 k = 0; k < N; k++) { pw[k] = a; pwi[k] = b; a = mulmod_h(a, psi, qi); b = mulmod_h(b, psi_inv, qi); }
+        ulonglong2* F = &tw[(size_t)i * 2 * N];
+        ulonglong2* I = F + N;
+        for (u64 k = 0; k < N; k++) {
+            const u64 w = pw[brev_h((u32)k, logn)], wi = pwi[brev_h((u32)k, logn)];
+            F[k] = make_ulonglong2(w, shoup_h(w, qi));
+            I[k] = make_ulonglong2(wi, shoup_h(wi, qi));
+        }
+        const u64 wn = mulmod_h(I[1].x, ninv, qi);
+        I[0] = make_ulonglong2(wn, shoup_h(wn, qi));
+    }
+    CUDA_TRY(dmalloc((void**)&c->pr, sizeof(PrimeInfo) * nb, &c->table_bytes));
+    CUDA_TRY(cudaMemcpy(c->pr, c->hpr.data(), sizeof(PrimeInfo) * nb, cudaMemcpyHostToDevice));
+    CUDA_TRY(dmalloc((void**)&c->tw, sizeof(ulonglong2) * tw.size(), &c->table_bytes));
+    CUDA_TRY(cudaMemcpy(c->tw, tw.data(), sizeof(ulonglong2) * tw.size(), cudaMemcpyHostToDevice));
+    // canonical-embedding tables: ksi[k] = exp(2 pi i k / M) as computed by numpy on the host
+    // are uploaded by the Python layer through bcn_ctx_set_fft (see below); rot[j] = 5^j mod M here.
+    const u64 M = 2 * N, S = N / 2;
+    std::vector<int> rot(S);
+    u64 v = 1;
+    for (u64 j = 0; j < S; j++) { rot[j] = (int)v; v = v * 5 % M; }
+    CUDA_TRY(dmalloc((void**)&c->rot, sizeof(int) * S, &c->table_bytes));
+    CUDA_TRY(cudaMemcpy(c->rot, rot.data(), sizeof(int) * S, cudaMemcpyHostToDevice));
+    CUDA_TRY(dmalloc((void**)&c->ksi_re, sizeof(double) * (M + 1), &c->table_bytes));
+    CUDA_TRY(dmalloc((void**)&c->ksi_im, sizeof(double) * (M + 1), &c->table_bytes));
+    // P mod q_i (Shoup pairs)
+    std::vector<u64> pmod(2 * nq);
+    for (int i = 0; i < nq; i++) {
+        const u64 qi = c->primes[i];
+        u64 P = 1;
+        for (int k = 0; k < n_special; k++) P = mulmod_h(P, c->primes[nq + k] % qi, qi);
+        pmod[2 * i] = P;
+        pmod[2 * i + 1] = shoup_h(P, qi);
+    }
+    CUDA_TRY(dmalloc((void**)&c->pmod, sizeof(u64) * pmod.size(), &c->table_bytes));
+    CUDA_TRY(cudaMemcpy(c->pmod, pmod.data(), sizeof(u64) * pmod.size(), cudaMemcpyHostToDevice));
+    if (nq >= 2) {
+        c->q0inv_q1 = inv_h(c->primes[0] % c->primes[1], c->primes[1]);
+        c->q0inv_q1_p = shoup_h(c->q0inv_q1, c->primes[1]);
+    }
+    // secret key: ternary (DOM_SECRET = 3, id 0) -> all basis limbs -> NTT
+    CUDA_TRY(dmalloc((void**)&c->s_ntt, sizeof(u64) * nb * N, &c->key_bytes));
+    CUDA_TRY(dmalloc((void**)&c->s_mont, sizeof(u64) * nb * N, &c->key_bytes));
+    Limbs all = limbs_range(0, nb);
+    CUDA_TRY(sample_small_op(c->s_ntt, (long long)nb * N, 1, nb, logn, all, c->pr, seed, 3u, 0, 0, 1, 0));
+    CUDA_TRY(ntt_run(c.get(), false, c->s_ntt, (long long)nb * N, all, 1, 0));
+    CUDA_TRY(to_mont_op(c->s_mont, c->s_ntt, 1, nb, logn, all, c->pr, 0));
+    CUDA_TRY(cudaDeviceSynchronize());
+    *out = c.release();
+    return BCN_OK;
+}
+
+// ksi table upload (float64[M+1] each): see paper_2402_01296_b200/params.py
+int bcn_ctx_set_fft(bcn_ctx* c, const double* re, const double* im) {
+    if (!c) return fail(BCN_ERR_PARAM, "null context");
+    const size_t M = 2 * (size_t)c->N;
+    CUDA_TRY(cudaMemcpy(c->ksi_re, re, sizeof(double) * (M + 1), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->ksi_im, im, sizeof(double) * (M + 1), cudaMemcpyHostToDevice));
+    return BCN_OK;
+}
+
+int bcn_ctx_destroy(bcn_ctx* c) {
+    if (!c) return BCN_OK;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : c->lt) {
+        cudaFree(kv.second.modup); cudaFree(kv.second.moddown);
+        cudaFree(kv.second.pinv); cudaFree(kv.second.qlinv);
+    }
+    for (auto& kv : c->keys) cudaFree(kv.second);
+    cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
+    cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod);
+    if (c->scratch) cudaFree(c->scratch);
+    delete c;
+    return BCN_OK;
+}
+
+int bcn_ctx_memory(bcn_ctx* c, uint64_t* bytes) {
+    *bytes = c->table_bytes + c->key_bytes + c->scratch_bytes;
+    return BCN_OK;
+}
+
+int bcn_ctx_trim(bcn_ctx* c) {
+    if (c->scratch) { cudaDeviceSynchronize(); cudaFree(c->scratch); }
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    return BCN_OK;
+}
+
+// ------------------------------------------------------------------ NTT
+int bcn_ntt_fwd(bcn_ctx* c, uint64_t* data, int npoly, int nlimb, int prime0, void* stream) {
+    if (prime0 < 0 || prime0 + nlimb > c->nbasis) return fail(BCN_ERR_PARAM, "limb range outside basis");
+    CUDA_TRY(ntt_run(c, false, (u64*)data, (long long)nlimb * c->N, limbs_range(prime0, nlimb), npoly, (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+int bcn_ntt_inv(bcn_ctx* c, uint64_t* data, int npoly, int nlimb, int prime0, void* stream) {
+    if (prime0 < 0 || prime0 + nlimb > c->nbasis) return fail(BCN_ERR_PARAM, "limb range outside basis");
+    CUDA_TRY(ntt_run(c, true, (u64*)data, (long long)nlimb * c->N, limbs_range(prime0, nlimb), npoly, (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+// --------------------------------------------------------------- encode
+int bcn_encode(bcn_ctx* c, const double* vals, int vlen, int vstride, int nplain, double scale, int level,
+               int montgomery, uint64_t* out, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (vlen > c->N / 2) return fail(BCN_ERR_CAPACITY, "vector exceeds slot count");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nl = level + 1;
+    Limbs l = limbs_range(0, nl);
+    CUDA_TRY(encode_op((u64*)out, (long long)nl * c->N, vals, vlen, vstride, nplain, scale, c->logn, l, c->pr,
+                       fft_tab(c), 0, 0, 0, st));
+    CUDA_TRY(ntt_run(c, false, (u64*)out, (long long)nl * c->N, l, nplain, st));
+    if (montgomery) CUDA_TRY(to_mont_op((u64*)out, (u64*)out, nplain, nl, c->logn, l, c->pr, st));
+    return BCN_OK;
+}
+
+int bcn_encrypt(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
+                uint64_t counter0, uint64_t* ct, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (vlen > c->N / 2) return fail(BCN_ERR_CAPACITY, "vector exceeds slot count");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nl = level + 1;
+    Limbs l = limbs_range(0, nl);
+    const long long cs = 2LL * nl * c->N;
+    CUDA_TRY(encode_op((u64*)ct, cs, vals, vlen, vstride, G, scale, c->logn, l, c->pr, fft_tab(c), 1, c->seed,
+                       counter0, st));
+    CUDA_TRY(ntt_run(c, false, (u64*)ct, cs, l, G, st));
+    CUDA_TRY(encrypt_combine_op((u64*)ct, G, nl, c->logn, l, c->pr, c->s_mont, c->seed, counter0, st));
+    return BCN_OK;
+}
+
+static int decrypt_poly_impl(bcn_ctx* c, const uint64_t* ct, int ct_nlimb, int G, int level, u64* out,
+                             cudaStream_t st) {
+    const int k = level >= 1 ? 2 : 1;
+    CUDA_TRY(decrypt_core_op(out, (const u64*)ct, 2LL * ct_nlimb * c->N, ct_nlimb, k, G, c->logn, c->pr, c->s_mont,
+                             0, st));
+    CUDA_TRY(ntt_run(c, true, out, (long long)k * c->N, limbs_range(0, k), G, st));
+    return BCN_OK;
+}
+
+int bcn_decrypt_poly(bcn_ctx* c, const uint64_t* ct, int ct_nlimb, int G, int level, uint64_t* out, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    return decrypt_poly_impl(c, ct, ct_nlimb, G, level, (u64*)out, (cudaStream_t)stream);
+}
+
+int bcn_decrypt(bcn_ctx* c, const uint64_t* ct, int ct_nlimb, int G, int level, double scale, double* out, int nout,
+                void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (nout > c->N / 2) return fail(BCN_ERR_PARAM, "nout exceeds slot count");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int k = level >= 1 ? 2 : 1;
+    int err = 0;
+    u64* tmp = scratch_get(c, (size_t)G * k * c->N, &err);
+    if (!tmp) return err;
+    e = decrypt_poly_impl(c, ct, ct_nlimb, G, level, tmp, st);
+    if (e) return e;
+    CUDA_TRY(decode_op(out, nout, tmp, (long long)k * c->N, k, G, scale, c->logn, c->pr, fft_tab(c), c->q0inv_q1,
+                       c->q0inv_q1_p, st));
+    return BCN_OK;
+}
+
+// ------------------------------------------------------------ add / sub
+int bcn_add(bcn_ctx* c, uint64_t* out, const uint64_t* a, int a_nlimb, const uint64_t* b, int b_nlimb,
+            int b_is_plain, int b_batch, int G, int level, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (a_nlimb < level + 1 || b_nlimb < level + 1) return fail(BCN_ERR_PARAM, "operand has too few limbs");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nl = level + 1;
+    const long long N = c->N;
+    Limbs l = limbs_range(0, nl);
+    if (!b_is_plain) {
+        CUDA_TRY(binary_op(0, (u64*)out, nl * N, (const u64*)a, a_nlimb * N, (const u64*)b, b_nlimb * N, 2 * G, nl,
+                           c->logn, l, c->pr, st));
+    } else {
+        const long long bs = (b_batch == 1) ? 0 : (long long)b_nlimb * N;
+        CUDA_TRY(binary_op(0, (u64*)out, 2 * nl * N, (const u64*)a, 2 * a_nlimb * N, (const u64*)b, bs, G, nl,
+                           c->logn, l, c->pr, st));
+        if ((const u64*)out != (const u64*)a || a_nlimb != nl)
+            CUDA_TRY(copy_limbs_op((u64*)out + nl * N, 2 * nl * N, (const u64*)a + a_nlimb * N, 2 * a_nlimb * N, G,
+                                   nl * N, st));
+    }
+    return BCN_OK;
+}
+
+int bcn_sub(bcn_ctx* c, uint64_t* out, const uint64_t* a, int a_nlimb, const uint64_t* b, int b_nlimb, int G,
+            int level, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    const int nl = level + 1;
+    const long long N = c->N;
+    CUDA_TRY(binary_op(1, (u64*)out, nl * N, (const u64*)a, a_nlimb * N, (const u64*)b, b_nlimb * N, 2 * G, nl,
+                       c->logn, limbs_range(0, nl), c->pr, (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+// -------------------------------------------------------------- rescale
+static int rescale_impl(bcn_ctx* c, u64* out, const u64* in, int in_nlimb, int G, int level, cudaStream_t st) {
+    if (level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    LevelTables* T;
+    int e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    const int npoly = 2 * G;
+    int err = 0;
+    u64* top = scratch_get(c, (size_t)npoly * N * (1 + level), &err);
+    if (!top) return err;
+    u64* W = top + (size_t)npoly * N;
+    CUDA_TRY(gather_limb_op(top, in, (long long)in_nlimb * N, (long long)level * N, npoly, c->logn, st));
+    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
+    Limbs ql = limbs_range(0, level);
+    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
+    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
+    CUDA_TRY(rescale_combine_op(out, (long long)level * N, in, (long long)in_nlimb * N, W, npoly, level, c->logn, ql,
+                                c->pr, T->qlinv, st));
+    return BCN_OK;
+}
+
+int bcn_rescale(bcn_ctx* c, uint64_t* out, const uint64_t* in, int in_nlimb, int G, int level, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    return rescale_impl(c, (u64*)out, (const u64*)in, in_nlimb, G, level, (cudaStream_t)stream);
+}
+
+// ----------------------------------------------------------- mul plain
+static int mul_plain_impl(bcn_ctx* c, u64* out, const u64* ct, int ct_nlimb, const u64* pt, int pt_batch, int G,
+                          int level, bool rescale, cudaStream_t st) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (rescale && level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    const int nl = level + 1;
+    const long long N = c->N;
+    Limbs l = limbs_range(0, nl);
+    const long long ps = (pt_batch == 1) ? 0 : nl * N;
+    // product on c0 and c1: treat as 2 polys per ct sharing the ct's plaintext
+    u64* prod = out;
+    int err = 0;
+    if (rescale) {
+        prod = scratch_get(c, (size_t)G * 2 * nl * N + (size_t)2 * G * N * (1 + level), &err);
+        if (!prod) return err;
+    }
+    for (int comp = 0; comp < 2; comp++)
+        CUDA_TRY(binary_op(2, prod + comp * nl * N, 2 * nl * N, ct + comp * (long long)ct_nlimb * N,
+                           2LL * ct_nlimb * N, pt, ps, G, nl, c->logn, l, c->pr, st));
+    if (!rescale) return BCN_OK;
+    // rescale needs its own scratch: place the product after it by re-running with an offset arena
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    const int npoly = 2 * G;
+    u64* top = prod + (size_t)G * 2 * nl * N;
+    u64* W = top + (size_t)npoly * N;
+    CUDA_TRY(gather_limb_op(top, prod, nl * N, (long long)level * N, npoly, c->logn, st));
+    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
+    Limbs ql = limbs_range(0, level);
+    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
+    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
+    CUDA_TRY(rescale_combine_op(out, (long long)level * N, prod, nl * N, W, npoly, level, c->logn, ql, c->pr,
+                                T->qlinv, st));
+    return BCN_OK;
+}
+
+int bcn_mul_plain(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, const uint64_t* pt_mont,
+                  int pt_batch, int G, int level, void* stream) {
+    return mul_plain_impl(c, (u64*)out, (const u64*)ct, ct_nlimb, (const u64*)pt_mont, pt_batch, G, level, true,
+                          (cudaStream_t)stream);
+}
+
+int bcn_mul_plain_norescale(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, const uint64_t* pt_mont,
+                            int pt_batch, int G, int level, void* stream) {
+    return mul_plain_impl(c, (u64*)out, (const u64*)ct, ct_nlimb, (const u64*)pt_mont, pt_batch, G, level, false,
+                          (cudaStream_t)stream);
+}
+
+int bcn_mac(bcn_ctx* c, uint64_t* out, const uint64_t* ct, const uint64_t* pt_mont, int n_items, int group,
+            int nlimb, void* stream) {
+    if (nlimb < 1 || nlimb > c->nbasis || group < 1) return fail(BCN_ERR_PARAM, "bad MAC shape");
+    const long long N = c->N;
+    CUDA_TRY(mac_op((u64*)out, (const u64*)ct, 2 * nlimb * N, (const u64*)pt_mont, nlimb * N, n_items, group, nlimb,
+                    c->logn, limbs_range(0, nlimb), c->pr, (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+// -------------------------------------------------------- key switching
+static u64* key_ptr(bcn_ctx* c, u64 id) {
+    auto it = c->keys.find(id);
+    return it == c->keys.end() ? nullptr : it->second;
+}
+
+static int gen_key(bcn_ctx* c, u64 key_id, const u64* sprime, cudaStream_t st) {
+    const long long N = c->N;
+    const int nb = c->nbasis;
+    u64* key = nullptr;
+    CUDA_TRY(dmalloc((void**)&key, sizeof(u64) * c->key_words(), &c->key_bytes));
+    int err = 0;
+    u64* e_ntt = scratch_get(c, (size_t)nb * N, &err);
+    if (!e_ntt) { cudaFree(key); return err; }
+    Limbs all = limbs_range(0, nb);
+    for (int j = 0; j < c->dnum; j++) {
+        const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, c->nq);
+        const u64 kid = key_id * 64 + j;
+        u64* b = key + (size_t)j * 2 * nb * N;
+        u64* a = b + (size_t)nb * N;
+        if (d0 >= c->nq) {   // empty digit (dnum > needed): zero key
+            CUDA_TRY(cudaMemsetAsync(b, 0, sizeof(u64) * 2 * nb * N, st));
+            continue;
+        }
+        CUDA_TRY(sample_small_op(e_ntt, nb * N, 1, nb, c->logn, all, c->pr, c->seed, 5u, kid, 0, 0, st));
+        CUDA_TRY(ntt_run(c, false, e_ntt, nb * N, all, 1, st));
+        CUDA_TRY(ksk_digit_op(b, a, e_ntt, c->s_mont, sprime, nb, d0, d1, c->logn, c->pr, c->pmod, c->seed, kid, st));
+    }
+    c->keys[key_id] = key;
+    return BCN_OK;
+}
+
+int bcn_keygen_relin(bcn_ctx* c, void* stream) {
+    if (key_ptr(c, 2)) return BCN_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long N = c->N;
+    const int nb = c->nbasis;
+    u64* s2 = nullptr;
+    CUDA_TRY(cudaMalloc(&s2, sizeof(u64) * nb * N));
+    CUDA_TRY(binary_op(2, s2, 0, c->s_ntt, 0, c->s_mont, 0, 1, nb, c->logn, limbs_range(0, nb), c->pr, st));
+    int e = gen_key(c, 2, s2, st);
+    cudaStreamSynchronize(st);
+    cudaFree(s2);
+    return e;
+}
+
+int bcn_keygen_galois(bcn_ctx* c, uint64_t g, void* stream) {
+    if (g == 1 || key_ptr(c, g)) return BCN_OK;
+    if ((g & 1) == 0 || g >= 2ull * c->N) return fail(BCN_ERR_PARAM, "Galois element must be odd and < 2N");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long N = c->N;
+    const int nb = c->nbasis;
+    u64* sg = nullptr;
+    CUDA_TRY(cudaMalloc(&sg, sizeof(u64) * nb * N));
+    CUDA_TRY(automorph_op(sg, N, c->s_ntt, N, 1, nb, c->logn, (u32)g, st));
+    int e = gen_key(c, g, sg, st);
+    cudaStreamSynchronize(st);
+    cudaFree(sg);
+    return e;
+}
+
+int bcn_export_key(bcn_ctx* c, uint64_t key_id, uint64_t* out, void* stream) {
+    u64* k = key_ptr(c, key_id);
+    if (!k) return fail(BCN_ERR_USAGE, "no key with id " + std::to_string(key_id));
+    CUDA_TRY(from_mont_op((u64*)out, k, c->N, c->nbasis, 2 * c->dnum, limbs_range(0, c->nbasis), c->pr,
+                          (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+int bcn_export_secret(bcn_ctx* c, uint64_t* out, void* stream) {
+    CUDA_TRY(cudaMemcpyAsync(out, c->s_ntt, sizeof(u64) * c->nbasis * c->N, cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+int bcn_modup_words(bcn_ctx* c, int G, int level, uint64_t* words) {
+    int e = check_level(c, level);
+    if (e) return e;
+    *words = (u64)G * ndig_at(c, level) * (level + 1 + c->K) * c->N;
+    return BCN_OK;
+}
+
+// U = ModUp(x) for x = poly 0 of each of G entries (stride x_stride), level l
+static int modup_impl(bcn_ctx* c, u64* U, const u64* x, long long x_stride, int G, int level, u64* tmp,
+                      cudaStream_t st) {
+    LevelTables* T;
+    int e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K, ndig = T->ndig;
+    Limbs ql = limbs_range(0, nl);
+    // coefficient-domain copy of x
+    CUDA_TRY(copy_limbs_op(tmp, nl * N, x, x_stride, G, nl * N, st));
+    CUDA_TRY(ntt_run(c, true, tmp, nl * N, ql, G, st));
+    Limbs ext = limbs_ext(c, level);
+    // x_ntt is read from x itself (stride x_stride); x_coef from tmp (stride nl*N): pass both with the same stride
+    // by staging: modup kernel takes one stride, so copy x_ntt next to tmp when strides differ.
+    const u64* xn = x;
+    if (x_stride != nl * N) {
+        u64* xn2 = tmp + (size_t)G * nl * N;
+        CUDA_TRY(copy_limbs_op(xn2, nl * N, x, x_stride, G, nl * N, st));
+        xn = xn2;
+    }
+    CUDA_TRY(modup_op(U, tmp, xn, nl * N, G, nl, next, c->alpha, ndig, c->logn, ext, c->pr, T->modup, st));
+    NttArgs a = ntt_args(c, U, (long long)next * N, ext);
+    a.skip_alpha = c->alpha;
+    a.skip_dnum = ndig;
+    a.skip_level = level;
+    CUDA_TRY(ntt_launch(false, c->logn, a, next, G * ndig, st));
+    return BCN_OK;
+}
+
+int bcn_modup(bcn_ctx* c, uint64_t* U, const uint64_t* ct, int ct_nlimb, int G, int level, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    const long long N = c->N;
+    const int nl = level + 1;
+    int err = 0;
+    u64* tmp = scratch_get(c, (size_t)2 * G * nl * N, &err);
+    if (!tmp) return err;
+    return modup_impl(c, (u64*)U, (const u64*)ct + (long long)ct_nlimb * N, 2LL * ct_nlimb * N, G, level, tmp,
+                      (cudaStream_t)stream);
+}
+
+// out = addend (+ permuted c0) + ModDown(sum_j U_j (x) key_j)
+static int keyswitch_tail(bcn_ctx* c, u64* out, long long os, const u64* U, int G, int level, u64 g, const u64* key,
+                          const u64* addend, long long as, int add_c1, u64* tmp, cudaStream_t st) {
+    LevelTables* T;
+    int e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K, ndig = T->ndig;
+    Limbs ext = limbs_ext(c, level);
+    u64* A = tmp;                                   // [G][2][next][N]
+    u64* Z = A + (size_t)G * 2 * next * N;          // [G][2][nl][N]
+    CUDA_TRY(inner_op(A, U, G, next, ndig, c->logn, (u32)g, key, 2LL * c->nbasis * N, (long long)c->nbasis * N, ext,
+                      ext, c->pr, st));
+    // INTT of the special limbs of both components
+    Limbs pl;
+    pl.n = c->K;
+    for (int k = 0; k < c->K; k++) pl.prime[k] = (short)(c->nq + k);
+    CUDA_TRY(ntt_run(c, true, A + (size_t)nl * N, (long long)next * N, pl, 2 * G, st));
+    CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st));
+    Limbs ql = limbs_range(0, nl);
+    CUDA_TRY(ntt_run(c, false, Z, (long long)nl * N, ql, 2 * G, st));
+    CUDA_TRY(moddown_combine_op(out, os, A, next, Z, addend, as, add_c1, (u32)g, G, nl, c->logn, ql, c->pr, T->pinv,
+                                st));
+    return BCN_OK;
+}
+
+static size_t tail_words(const bcn_ctx* c, int G, int level) {
+    const int nl = level + 1, next = nl + c->K;
+    return (size_t)G * 2 * next * c->N + (size_t)G * 2 * nl * c->N;
+}
+
+int bcn_rotate_hoisted(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, const uint64_t* U, int G,
+                       int level, uint64_t g, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long N = c->N;
+    const int nl = level + 1;
+    if (g == 1) {
+        CUDA_TRY(copy_limbs_op((u64*)out, nl * N, (const u64*)ct, ct_nlimb * N, 2 * G, nl * N, st));
+        return BCN_OK;
+    }
+    u64* key = key_ptr(c, g);
+    if (!key) {
+        e = bcn_keygen_galois(c, g, stream);
+        if (e) return e;
+        key = key_ptr(c, g);
+    }
+    int err = 0;
+    u64* tmp = scratch_get(c, tail_words(c, G, level), &err);
+    if (!tmp) return err;
+    return keyswitch_tail(c, (u64*)out, 2LL * nl * N, (const u64*)U, G, level, g, key, (const u64*)ct,
+                          2LL * ct_nlimb * N, 0, tmp, st);
+}
+
+int bcn_rotate(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, int G, int level, uint64_t g,
+               void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long N = c->N;
+    const int nl = level + 1;
+    if (g == 1) return bcn_rotate_hoisted(c, out, ct, ct_nlimb, nullptr, G, level, g, stream);
+    if (!key_ptr(c, g)) {
+        e = bcn_keygen_galois(c, g, stream);
+        if (e) return e;
+    }
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    const size_t uw = (size_t)G * T->ndig * (nl + c->K) * N;
+    const size_t mw = (size_t)2 * G * nl * N;
+    const size_t tw = tail_words(c, G, level);
+    int err = 0;
+    u64* base = scratch_get(c, uw + std::max(mw, tw), &err);
+    if (!base) return err;
+    u64* U = base;
+    e = modup_impl(c, U, (const u64*)ct + (long long)ct_nlimb * N, 2LL * ct_nlimb * N, G, level, base + uw, st);
+    if (e) return e;
+    return keyswitch_tail(c, (u64*)out, 2LL * nl * N, U, G, level, g, key_ptr(c, g), (const u64*)ct,
+                          2LL * ct_nlimb * N, 0, base + uw, st);
+}
+
+int bcn_mul_cc(bcn_ctx* c, uint64_t* out, const uint64_t* a, int a_nlimb, const uint64_t* b, int b_nlimb, int G,
+               int level, int rescale, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (rescale && level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!key_ptr(c, 2)) {
+        e = bcn_keygen_relin(c, stream);
+        if (e) return e;
+    }
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    const int nl = level + 1;
+    const size_t dw = (size_t)G * 3 * nl * N;                 // d0, d1, d2
+    const size_t uw = (size_t)G * T->ndig * (nl + c->K) * N;  // ModUp(d2)
+    const size_t rw = (size_t)G * 2 * nl * N;                 // relinearised, pre-rescale
+    const size_t mw = (size_t)2 * G * nl * N;
+    const size_t tw = tail_words(c, G, level);
+    int err = 0;
+    u64* base = scratch_get(c, dw + uw + rw + std::max(mw, tw), &err);
+    if (!base) return err;
+    u64* d = base;
+    u64* U = d + dw;
+    u64* R = U + uw;
+    u64* tmp = R + rw;
+    CUDA_TRY(tensor_op(d, (const u64*)a, 2LL * a_nlimb * N, (const u64*)b, 2LL * b_nlimb * N, G, nl, c->logn,
+                       limbs_range(0, nl), c->pr, st));
+    e = modup_impl(c, U, d + 2 * nl * N, 3LL * nl * N, G, level, tmp, st);
+    if (e) return e;
+    u64* dst = rescale ? R : (u64*)out;
+    e = keyswitch_tail(c, dst, 2LL * nl * N, U, G, level, 1, key_ptr(c, 2), d, 3LL * nl * N, 1, tmp, st);
+    if (e) return e;
+    if (!rescale) return BCN_OK;
+    // rescale R -> out using the tail region as its scratch
+    u64* top = tmp;
+    u64* W = top + (size_t)2 * G * N;
+    const int npoly = 2 * G;
+    CUDA_TRY(gather_limb_op(top, R, nl * N, (long long)level * N, npoly, c->logn, st));
+    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
+    Limbs ql = limbs_range(0, level);
+    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
+    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
+    CUDA_TRY(rescale_combine_op((u64*)out, (long long)level * N, R, nl * N, W, npoly, level, c->logn, ql, c->pr,
+                                T->qlinv, st));
+    return BCN_OK;
+}
+
+// ----------------------------------------------------------- utilities
+int bcn_sample_uniform(bcn_ctx* c, uint64_t* out, int npoly, int nlimb, int prime0, uint64_t seed, uint64_t id0,
+                       void* stream) {
+    if (prime0 < 0 || prime0 + nlimb > c->nbasis) return fail(BCN_ERR_PARAM, "limb range outside basis");
+    CUDA_TRY(sample_uniform_op((u64*)out, (long long)nlimb * c->N, npoly, nlimb, c->logn, limbs_range(prime0, nlimb),
+                               c->pr, seed, 6u /*DOM_DATA*/, id0, 1, (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+int bcn_to_montgomery(bcn_ctx* c, uint64_t* out, const uint64_t* in, int npoly, int nlimb, int prime0, void* stream) {
+    if (prime0 < 0 || prime0 + nlimb > c->nbasis) return fail(BCN_ERR_PARAM, "limb range outside basis");
+    CUDA_TRY(to_mont_op((u64*)out, (const u64*)in, npoly, nlimb, c->logn, limbs_range(prime0, nlimb), c->pr,
+                        (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+int bcn_automorph(bcn_ctx* c, uint64_t* out, const uint64_t* in, int npoly, int nlimb, uint64_t g, void* stream) {
+    const long long N = c->N;
+    CUDA_TRY(automorph_op((u64*)out, nlimb * N, (const u64*)in, nlimb * N, npoly, nlimb, c->logn, (u32)g,
+                          (cudaStream_t)stream));
+    return BCN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,227 @@
+// ntt.cu -- batched negacyclic NTT / INTT over RNS limbs (K1/K2).
+//
+// One CTA transforms one limb-polynomial (N <= 2^14 u64 words = 128 KiB,
+// staged in shared memory).  Each thread owns E = 2^LOGE words; a pass
+// performs LOGE Cooley-Tukey (forward) or Gentleman-Sande (inverse) stages
+// entirely in registers on blocks of E words spaced t_last apart, so the
+// 13/14 stages cost 3 shared-memory round trips instead of 13/14.  Twiddles
+// {w, floor(w 2^64/q)} are interleaved 16-byte pairs (one LDG.128 each) and
+// stay L2-resident across the batch.  Harvey lazy butterflies keep values in
+// [0, 4q) (forward) / [0, 2q) (inverse); outputs are canonical.
+//
+// Ordering (the contract with oracle/ckks_oracle.c): forward output index k
+// holds a(psi^(2 brev(k) + 1)); the inverse takes that order back to
+// coefficients and folds N^-1 into its final stage.
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace bcn {
+
+template <int LOGN> struct NttCfg {
+    static constexpr int LOGE = (LOGN - 8) < 1 ? 1 : ((LOGN - 8) > 5 ? 5 : (LOGN - 8));
+    static constexpr int N = 1 << LOGN;
+    static constexpr int E = 1 << LOGE;
+    static constexpr int T = N / E;
+    static constexpr int R0 = (LOGN % LOGE) ? (LOGN % LOGE) : LOGE;
+    static constexpr int SWZ = (E < 16 ? E : 16) - 1;
+};
+
+template <int LOGE, int SWZ>
+__device__ __forceinline__ int swz(int j) { return j ^ ((j >> LOGE) & SWZ); }
+
+// ---------------------------------------------------------------- forward
+template <int LOGN, int S0, int R, bool FIRST, bool LAST>
+__device__ __forceinline__ void fwd_pass(u64* x, const u64* __restrict__ g, u64* sm,
+                                         const ulonglong2* __restrict__ W, u64 q, int tid) {
+    using C = NttCfg<LOGN>;
+    constexpr int BS = 1 << R;               // block size
+    constexpr int NB = C::E / BS;            // blocks per thread
+    constexpr int TL = C::N >> (S0 + R);     // element stride inside a block
+    const u64 q2 = 2 * q;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = tid + i * C::T;
+        const int gi = b / TL;
+        const int base = gi * (C::N >> S0) + (b % TL);
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = base + k * TL;
+            x[i * BS + k] = FIRST ? g[j] : sm[swz<C::LOGE, C::SWZ>(j)];
+        }
+#pragma unroll
+        for (int ls = 0; ls < R; ls++) {
+            constexpr int dummy = 0; (void)dummy;
+            const int h = BS >> (ls + 1);
+            const int s = S0 + ls;
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                if (k & h) continue;
+                const ulonglong2 w = W[(1 << s) + (gi << ls) + (k >> (R - ls))];
+                u64 u = x[i * BS + k];
+                if (u >= q2) u -= q2;
+                const u64 v = shoup_lazy(x[i * BS + k + h], w.x, w.y, q);
+                x[i * BS + k] = u + v;
+                x[i * BS + k + h] = u - v + q2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = base + k * TL;
+            u64 v = x[i * BS + k];
+            if (LAST) {
+                if (v >= q2) v -= q2;
+                if (v >= q) v -= q;
+            }
+            sm[swz<C::LOGE, C::SWZ>(j)] = v;
+        }
+    }
+}
+
+template <int LOGN, int S0>
+__device__ __forceinline__ void fwd_rest(u64* x, u64* sm, const ulonglong2* __restrict__ W, u64 q, int tid) {
+    using C = NttCfg<LOGN>;
+    if constexpr (S0 < LOGN) {
+        __syncthreads();
+        fwd_pass<LOGN, S0, C::LOGE, false, (S0 + C::LOGE >= LOGN)>(x, nullptr, sm, W, q, tid);
+        fwd_rest<LOGN, S0 + C::LOGE>(x, sm, W, q, tid);
+    }
+}
+
+__device__ __forceinline__ bool skip_limb(const NttArgs& a, int t, int poly) {
+    if (a.skip_alpha <= 0) return false;
+    const int d = poly % a.skip_dnum;
+    return t <= a.skip_level && t / a.skip_alpha == d;
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_fwd_kernel(NttArgs a) {
+    using C = NttCfg<LOGN>;
+    extern __shared__ u64 sm[];
+    const int t = blockIdx.x, poly = blockIdx.y;
+    if (skip_limb(a, t, poly)) return;
+    const int pidx = a.limbs.prime[t];
+    const u64 q = a.pr[pidx].q;
+    const ulonglong2* W = a.tw + (size_t)pidx * 2 * C::N;
+    u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    u64 x[C::E];
+    const int tid = threadIdx.x;
+    fwd_pass<LOGN, 0, C::R0, true, (C::R0 >= LOGN)>(x, g, sm, W, q, tid);
+    fwd_rest<LOGN, C::R0>(x, sm, W, q, tid);
+    __syncthreads();
+    for (int j = tid; j < C::N; j += C::T) g[j] = sm[swz<C::LOGE, C::SWZ>(j)];
+}
+
+// ---------------------------------------------------------------- inverse
+template <int LOGN, int S0, int R, bool LAST>
+__device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, u64* sm,
+                                         const ulonglong2* __restrict__ Wi, u64 q,
+                                         u64 ninv, u64 ninv_p, u64 wn, u64 wn_p, int tid) {
+    using C = NttCfg<LOGN>;
+    constexpr int BS = 1 << R;
+    constexpr int NB = C::E / BS;
+    constexpr int TL = C::N >> (S0 + R);
+    const u64 q2 = 2 * q;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = tid + i * C::T;
+        const int gi = b / TL;
+        const int base = gi * (C::N >> S0) + (b % TL);
+#pragma unroll
+        for (int k = 0; k < BS; k++) x[i * BS + k] = sm[swz<C::LOGE, C::SWZ>(base + k * TL)];
+#pragma unroll
+        for (int ls = R - 1; ls >= 0; ls--) {
+            const int h = BS >> (ls + 1);
+            const int s = S0 + ls;
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                if (k & h) continue;
+                const u64 u = x[i * BS + k], v = x[i * BS + k + h];
+                if (LAST && s == 0) {
+                    // final stage: fold N^-1 (x[k] *= n^-1, x[k+h] *= w n^-1)
+                    x[i * BS + k] = shoup(u + v, ninv, ninv_p, q);
+                    x[i * BS + k + h] = shoup(u - v + q2, wn, wn_p, q);
+                } else {
+                    const ulonglong2 w = Wi[(1 << s) + (gi << ls) + (k >> (R - ls))];
+                    u64 sum = u + v;
+                    if (sum >= q2) sum -= q2;
+                    x[i * BS + k] = sum;
+                    x[i * BS + k + h] = shoup_lazy(u - v + q2, w.x, w.y, q);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = base + k * TL;
+            if (LAST) g[j] = x[i * BS + k];
+            else sm[swz<C::LOGE, C::SWZ>(j)] = x[i * BS + k];
+        }
+    }
+}
+
+template <int LOGN, int S0>
+__device__ __forceinline__ void inv_rest(u64* x, u64* g, u64* sm, const ulonglong2* __restrict__ Wi, u64 q,
+                                         u64 ninv, u64 ninv_p, u64 wn, u64 wn_p, int tid) {
+    using C = NttCfg<LOGN>;
+    if constexpr (S0 >= C::R0) {
+        inv_pass<LOGN, S0, C::LOGE, false>(x, g, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
+        __syncthreads();
+        inv_rest<LOGN, S0 - C::LOGE>(x, g, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_inv_kernel(NttArgs a) {
+    using C = NttCfg<LOGN>;
+    extern __shared__ u64 sm[];
+    const int t = blockIdx.x, poly = blockIdx.y;
+    const int pidx = a.limbs.prime[t];
+    const PrimeInfo& P = a.pr[pidx];
+    const u64 q = P.q;
+    const ulonglong2* Wi = a.tw + (size_t)pidx * 2 * C::N + C::N;
+    u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    const int tid = threadIdx.x;
+    for (int j = tid; j < C::N; j += C::T) sm[swz<C::LOGE, C::SWZ>(j)] = g[j];
+    __syncthreads();
+    u64 x[C::E];
+    const u64 ninv = P.pad[0], ninv_p = P.pad[1];
+    const ulonglong2 wn = Wi[0];   // slot 0 of the inverse table holds {w1 n^-1, shoup}
+    inv_rest<LOGN, LOGN - C::LOGE>(x, g, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
+    inv_pass<LOGN, 0, C::R0, true>(x, g, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
+}
+
+template <int LOGN>
+static cudaError_t launch_one(bool inverse, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
+    using C = NttCfg<LOGN>;
+    const size_t smem = (size_t)C::N * sizeof(u64);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(ntt_fwd_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_inv_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid(nlimbs, npolys);
+    if (inverse) ntt_inv_kernel<LOGN><<<grid, C::T, smem, st>>>(a);
+    else ntt_fwd_kernel<LOGN><<<grid, C::T, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
+    if (nlimbs <= 0 || npolys <= 0) return cudaSuccess;
+    switch (logn) {
+        case 3: return launch_one<3>(inverse, a, nlimbs, npolys, st);
+        case 4: return launch_one<4>(inverse, a, nlimbs, npolys, st);
+        case 5: return launch_one<5>(inverse, a, nlimbs, npolys, st);
+        case 6: return launch_one<6>(inverse, a, nlimbs, npolys, st);
+        case 7: return launch_one<7>(inverse, a, nlimbs, npolys, st);
+        case 8: return launch_one<8>(inverse, a, nlimbs, npolys, st);
+        case 9: return launch_one<9>(inverse, a, nlimbs, npolys, st);
+        case 10: return launch_one<10>(inverse, a, nlimbs, npolys, st);
+        case 11: return launch_one<11>(inverse, a, nlimbs, npolys, st);
+        case 12: return launch_one<12>(inverse, a, nlimbs, npolys, st);
+        case 13: return launch_one<13>(inverse, a, nlimbs, npolys, st);
+        case 14: return launch_one<14>(inverse, a, nlimbs, npolys, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace bcn

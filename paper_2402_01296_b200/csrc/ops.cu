@@ -1,0 +1,452 @@
+// ops.cu -- HBM-streaming RNS kernels: modular add/sub/mul (K3), fused
+// ct x pt multiply-accumulate (K4), tensor square (K6), automorphism (K8),
+// ModUp / inner-product / ModDown pieces of hybrid key switching (K7) and
+// the rescale lift/combine (K5).  All are one pass over their operands with
+// every output written once; constants (Shoup pairs, Montgomery base-
+// conversion tables) are tiny and broadcast through L1.
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace bcn {
+
+static inline int blocks_for(long long n, int tpb) {
+    long long b = (n + tpb - 1) / tpb;
+    return (int)(b > 2147483647LL ? 2147483647LL : b);
+}
+
+// --------------------------------------------------------------- binary
+// out[p][t][n] = a[p][t][n] (op) b[p][t][n]; strides in words, 0 = broadcast.
+template <int OP>
+__global__ void binary_kernel(u64* __restrict__ out, long long os, const u64* __restrict__ a, long long as,
+                              const u64* __restrict__ b, long long bs, int nlimb, int logn, Limbs limbs,
+                              const PrimeInfo* __restrict__ pr, long long total) {
+    const int N = 1 << logn;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int n = (int)(idx & (N - 1));
+        const long long rest = idx >> logn;
+        const int t = (int)(rest % nlimb);
+        const long long p = rest / nlimb;
+        const PrimeInfo& P = pr[limbs.prime[t]];
+        const u64 x = a[p * as + (long long)t * N + n];
+        const u64 y = b[p * bs + (long long)t * N + n];
+        u64 r;
+        if (OP == 0) r = add_mod(x, y, P.q);
+        else if (OP == 1) r = sub_mod(x, y, P.q);
+        else r = mont_mul(x, y, P.q, P.qinv_neg);   // y in Montgomery form
+        out[p * os + (long long)t * N + n] = r;
+    }
+}
+
+cudaError_t binary_op(int op, u64* out, long long os, const u64* a, long long as, const u64* b, long long bs,
+                      int npoly, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st) {
+    long long total = (long long)npoly * nlimb << logn;
+    if (total == 0) return cudaSuccess;
+    int tpb = 256, nb = blocks_for(total, tpb);
+    if (op == 0) binary_kernel<0><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
+    else if (op == 1) binary_kernel<1><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
+    else binary_kernel<2><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
+    return cudaGetLastError();
+}
+
+// out = to_mont(a) (in place allowed)
+__global__ void to_mont_kernel(u64* out, const u64* a, int nlimb, int logn, Limbs limbs,
+                               const PrimeInfo* __restrict__ pr, long long total) {
+    const int N = 1 << logn;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int t = (int)((idx >> logn) % nlimb);
+        (void)N;
+        out[idx] = to_mont(a[idx], pr[limbs.prime[t]]);
+    }
+}
+
+cudaError_t to_mont_op(u64* out, const u64* a, int npoly, int nlimb, int logn, const Limbs& limbs,
+                       const PrimeInfo* pr, cudaStream_t st) {
+    long long total = (long long)npoly * nlimb << logn;
+    if (!total) return cudaSuccess;
+    to_mont_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, a, nlimb, logn, limbs, pr, total);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ MAC
+// out[g] = sum_{t in group g} ct[t] (x) pt_mont[t]   (2 polys per ct)
+// ct: [T][2][L][N] stride ct_stride; pt: [T][L][N] stride pt_stride;
+// out: [G][2][L][N].  Lazy u128 accumulation, one REDC per output word.
+__global__ void mac_kernel(u64* __restrict__ out, const u64* __restrict__ ct, long long ct_stride,
+                           const u64* __restrict__ pt, long long pt_stride, int n_items, int group,
+                           int nlimb, int logn, Limbs limbs, const PrimeInfo* __restrict__ pr) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int t = blockIdx.y;
+    const int gidx = blockIdx.z;
+    const PrimeInfo& P = pr[limbs.prime[t]];
+    const u64 q = P.q;
+    Acc128 a0, a1;
+    a0.zero(); a1.zero();
+    const int start = gidx * group;
+    const int end = min(start + group, n_items);
+    for (int k = start; k < end; k++) {
+        const u64 p = __ldg(pt + (long long)k * pt_stride + (long long)t * N + n);
+        const u64* c = ct + (long long)k * ct_stride + (long long)t * N + n;
+        a0.mac(__ldg(c), p, q);
+        a1.mac(__ldg(c + (long long)nlimb * N), p, q);
+    }
+    u64* o = out + (long long)gidx * 2 * nlimb * N + (long long)t * N + n;
+    o[0] = a0.reduce(q, P.qinv_neg);
+    o[(long long)nlimb * N] = a1.reduce(q, P.qinv_neg);
+}
+
+cudaError_t mac_op(u64* out, const u64* ct, long long ct_stride, const u64* pt, long long pt_stride,
+                   int n_items, int group, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr,
+                   cudaStream_t st) {
+    const int N = 1 << logn;
+    const int ngroups = (n_items + group - 1) / group;
+    if (!ngroups) return cudaSuccess;
+    int tpb = N < 256 ? N : 256;
+    dim3 grid((N + tpb - 1) / tpb, nlimb, ngroups);
+    mac_kernel<<<grid, tpb, 0, st>>>(out, ct, ct_stride, pt, pt_stride, n_items, group, nlimb, logn, limbs, pr);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- tensor (K6)
+// d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 for G ciphertext pairs.
+// a, b: [G][2][L][N] with strides; d: [G][3][L][N]
+__global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, long long as,
+                              const u64* __restrict__ b, long long bs, int nlimb, int logn, Limbs limbs,
+                              const PrimeInfo* __restrict__ pr, long long total) {
+    const int N = 1 << logn;
+    const long long LN = (long long)nlimb * N;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long g = idx / LN;
+        const long long off = idx - g * LN;
+        const int t = (int)(off >> logn);
+        const PrimeInfo& P = pr[limbs.prime[t]];
+        const u64 q = P.q;
+        const u64 a0 = a[g * as + off], a1 = a[g * as + LN + off];
+        const u64 b0 = to_mont(b[g * bs + off], P), b1 = to_mont(b[g * bs + LN + off], P);
+        u64* o = d + g * 3 * LN + off;
+        o[0] = mont_mul(a0, b0, q, P.qinv_neg);
+        Acc128 acc; acc.zero();
+        acc.mac(a0, b1, q);
+        acc.mac(a1, b0, q);
+        o[LN] = acc.reduce(q, P.qinv_neg);
+        o[2 * LN] = mont_mul(a1, b1, q, P.qinv_neg);
+    }
+}
+
+cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,
+                      int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st) {
+    long long total = (long long)G * nlimb << logn;
+    if (!total) return cudaSuccess;
+    tensor_kernel<<<blocks_for(total, 256), 256, 0, st>>>(d, a, as, b, bs, nlimb, logn, limbs, pr, total);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------- automorphism (K8)
+__global__ void automorph_kernel(u64* __restrict__ out, long long os, const u64* __restrict__ in, long long is,
+                                 int nlimb, int logn, u32 g, long long total) {
+    const int N = 1 << logn;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int n = (int)(idx & (N - 1));
+        const long long rest = idx >> logn;
+        const int t = (int)(rest % nlimb);
+        const long long p = rest / nlimb;
+        out[p * os + (long long)t * N + n] = in[p * is + (long long)t * N + automorph_src(n, g, logn)];
+    }
+}
+
+cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, int npoly, int nlimb, int logn,
+                         u32 g, cudaStream_t st) {
+    long long total = (long long)npoly * nlimb << logn;
+    if (!total) return cudaSuccess;
+    automorph_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, os, in, is, nlimb, logn, g, total);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- ModUp (K7)
+// For digit j (grid.z) of poly p (grid.y): y_i = [x_i * hatinv_i]_{q_i} for
+// the digit's limbs, then U[p][j][t] = REDC(sum_i y_i * hat_m[i][t]) for
+// every extended limb t outside the digit (coefficient domain; NTT'd by the
+// caller), and U[p][j][t] = x_ntt[t] (already NTT domain) inside it.
+__global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, const u64* __restrict__ xn,
+                             long long x_stride, int nq, int next, int alpha, int ndig, int logn,
+                             Limbs ext, const PrimeInfo* __restrict__ pr, const ConvTable* __restrict__ tab) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const long long p = blockIdx.y;
+    const int j = blockIdx.z;
+    const ConvTable& T = tab[j];
+    const int i0 = j * alpha;
+    const int na = T.n_src;
+    u64 y[BCN_MAX_ALPHA];
+    const u64* xcp = xc + p * x_stride + n;
+    const u64* xnp = xn + p * x_stride + n;
+    u64* Up = U + (p * ndig + j) * (long long)next * N + n;
+#pragma unroll 4
+    for (int i = 0; i < na; i++) {
+        const PrimeInfo& P = pr[ext.prime[i0 + i]];
+        y[i] = shoup(__ldg(xcp + (long long)(i0 + i) * N), T.hatinv[i], T.hatinv_p[i], P.q);
+        Up[(long long)(i0 + i) * N] = __ldg(xnp + (long long)(i0 + i) * N);
+    }
+    for (int t = 0; t < next; t++) {
+        if (t >= i0 && t < i0 + na) continue;
+        const PrimeInfo& P = pr[ext.prime[t]];
+        Acc128 acc; acc.zero();
+        for (int i = 0; i < na; i++) acc.mac(y[i], T.hat_m[i * BCN_MAX_LIMBS + t], P.q);
+        Up[(long long)t * N] = acc.reduce(P.q, P.qinv_neg);
+    }
+    (void)nq;
+}
+
+cudaError_t modup_op(u64* U, const u64* xc, const u64* xn, long long x_stride, int npoly, int nq, int next,
+                     int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab,
+                     cudaStream_t st) {
+    const int N = 1 << logn;
+    int tpb = N < 256 ? N : 256;
+    dim3 grid((N + tpb - 1) / tpb, npoly, ndig);
+    modup_kernel<<<grid, tpb, 0, st>>>(U, xc, xn, x_stride, nq, next, alpha, ndig, logn, ext, pr, tab);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------- key inner product (K7, K8)
+// A[p][c][t][n] = REDC( sum_j U[p][j][t][perm_g(n)] * key[j][c][kt(t)][n] )
+// One CTA = one aligned block of BLK output positions of one limb and poly.
+// Under X -> X^g an aligned block of the bit-reversed NTT domain is the
+// image of one aligned source block, so the gather is staged through smem
+// with coalesced loads.
+template <int BLK>
+__global__ void __launch_bounds__(256) inner_kernel(u64* __restrict__ A, const u64* __restrict__ U, int next,
+                                                    int ndig, int logn, u32 g, const u64* __restrict__ key,
+                                                    long long key_digit_stride, long long key_comp_stride,
+                                                    Limbs ext, Limbs keyl, const PrimeInfo* __restrict__ pr) {
+    extern __shared__ u64 sm[];
+    const int N = 1 << logn;
+    const int logb = __ffs(BLK) - 1;
+    const int blk = blockIdx.x;
+    const int t = blockIdx.y;
+    const long long p = blockIdx.z;
+    const PrimeInfo& P = pr[ext.prime[t]];
+    const u64 q = P.q;
+    const int dst0 = blk * BLK;
+    const int src_blk = (g == 1u) ? blk : (int)(automorph_src((u32)dst0, g, logn) >> logb);
+    for (int j = 0; j < ndig; j++) {
+        const u64* src = U + ((p * ndig + j) * (long long)next + t) * N + (long long)src_blk * BLK;
+        for (int i = threadIdx.x; i < BLK; i += blockDim.x) sm[j * BLK + i] = src[i];
+    }
+    __syncthreads();
+    const int kt = keyl.prime[t];
+    for (int i = threadIdx.x; i < BLK; i += blockDim.x) {
+        const int n = dst0 + i;
+        const int s = (g == 1u) ? i : (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
+        Acc128 a0, a1;
+        a0.zero(); a1.zero();
+        for (int j = 0; j < ndig; j++) {
+            const u64 u = sm[j * BLK + s];
+            const u64* kp = key + j * key_digit_stride + (long long)kt * N + n;
+            a0.mac(u, __ldg(kp), q);
+            a1.mac(u, __ldg(kp + key_comp_stride), q);
+        }
+        u64* o = A + (p * 2 * next + t) * (long long)N + n;
+        o[0] = a0.reduce(q, P.qinv_neg);
+        o[(long long)next * N] = a1.reduce(q, P.qinv_neg);
+    }
+}
+
+cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
+                     long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
+                     const PrimeInfo* pr, cudaStream_t st) {
+    const int N = 1 << logn;
+    if (N >= 1024) {
+        constexpr int BLK = 1024;
+        size_t smem = (size_t)ndig * BLK * sizeof(u64);
+        static bool cfg = false;
+        if (!cfg) { cudaFuncSetAttribute(inner_kernel<BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+        dim3 grid(N / BLK, next, npoly);
+        inner_kernel<BLK><<<grid, 256, smem, st>>>(A, U, next, ndig, logn, g, key, key_digit_stride,
+                                                   key_comp_stride, ext, keyl, pr);
+    } else {
+        // small rings: one block covers the whole polynomial
+        size_t smem = (size_t)ndig * N * sizeof(u64);
+        dim3 grid(1, next, npoly);
+        switch (N) {
+#define BCN_SMALL(NN) case NN: inner_kernel<NN><<<grid, 256, smem, st>>>(A, U, next, ndig, logn, g, key, \
+                        key_digit_stride, key_comp_stride, ext, keyl, pr); break;
+            BCN_SMALL(8) BCN_SMALL(16) BCN_SMALL(32) BCN_SMALL(64) BCN_SMALL(128) BCN_SMALL(256) BCN_SMALL(512)
+#undef BCN_SMALL
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    return cudaGetLastError();
+}
+
+// -------------------------------------------------------- ModDown (K7)
+// Z[p][i] = REDC(sum_k [xP_k * phatinv_k]_{p_k} * phat_m[k][i]) for i <= level
+// (coefficient domain), from the INTT'd special limbs of A.
+__global__ void moddown_conv_kernel(u64* __restrict__ Z, const u64* __restrict__ A, long long a_stride,
+                                    int nq, int K, int logn, Limbs ext, const PrimeInfo* __restrict__ pr,
+                                    const ConvTable* __restrict__ tab) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const long long p = blockIdx.y;
+    const ConvTable& T = *tab;
+    u64 y[BCN_MAX_ALPHA];
+    const u64* ap = A + p * a_stride + (long long)nq * N + n;
+    for (int k = 0; k < K; k++) {
+        const PrimeInfo& P = pr[ext.prime[nq + k]];
+        y[k] = shoup(__ldg(ap + (long long)k * N), T.hatinv[k], T.hatinv_p[k], P.q);
+    }
+    u64* zp = Z + p * (long long)nq * N + n;
+    for (int i = 0; i < nq; i++) {
+        const PrimeInfo& P = pr[ext.prime[i]];
+        Acc128 acc; acc.zero();
+        for (int k = 0; k < K; k++) acc.mac(y[k], T.hat_m[k * BCN_MAX_LIMBS + i], P.q);
+        zp[(long long)i * N] = acc.reduce(P.q, P.qinv_neg);
+    }
+}
+
+cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
+                            const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st) {
+    const int N = 1 << logn;
+    int tpb = N < 256 ? N : 256;
+    dim3 grid((N + tpb - 1) / tpb, npoly);
+    moddown_conv_kernel<<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab);
+    return cudaGetLastError();
+}
+
+// out[p][c][i] = addend[p][c][i] + (A[p][c][i] - Z[p][c][i]) * P^-1   (c = 0, 1)
+// addend (optional, stride as) is permuted by X -> X^g when g != 1 and
+// only applied to component 0 when add_c1 == 0.
+__global__ void moddown_combine_kernel(u64* __restrict__ out, long long os, const u64* __restrict__ A,
+                                       int next, const u64* __restrict__ Z, const u64* __restrict__ addend,
+                                       long long as, int add_c1, u32 g, int nq, int logn, Limbs ql,
+                                       const PrimeInfo* __restrict__ pr, const u64* __restrict__ pinv,
+                                       long long total) {
+    const int N = 1 << logn;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int n = (int)(idx & (N - 1));
+        long long rest = idx >> logn;
+        const int i = (int)(rest % nq);
+        rest /= nq;
+        const int c = (int)(rest & 1);
+        const long long p = rest >> 1;
+        const PrimeInfo& P = pr[ql.prime[i]];
+        const u64 q = P.q;
+        const u64 a = A[(p * 2 + c) * next * (long long)N + (long long)i * N + n];
+        const u64 z = Z[(p * 2 + c) * nq * (long long)N + (long long)i * N + n];
+        u64 r = shoup(a + q - z, pinv[2 * i], pinv[2 * i + 1], q);
+        if (addend && (c == 0 || add_c1)) {
+            const int src = (g == 1u) ? n : (int)automorph_src((u32)n, g, logn);
+            r = add_mod(r, addend[p * as + (long long)c * nq * N + (long long)i * N + src], q);
+        }
+        out[p * os + (long long)c * nq * N + (long long)i * N + n] = r;
+    }
+}
+
+cudaError_t moddown_combine_op(u64* out, long long os, const u64* A, int next, const u64* Z, const u64* addend,
+                               long long as, int add_c1, u32 g, int npoly, int nq, int logn, const Limbs& ql,
+                               const PrimeInfo* pr, const u64* pinv, cudaStream_t st) {
+    long long total = (long long)npoly * 2 * nq << logn;
+    if (!total) return cudaSuccess;
+    moddown_combine_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, os, A, next, Z, addend, as, add_c1, g,
+                                                                   nq, logn, ql, pr, pinv, total);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- rescale (K5)
+// W[p][i] = centred(top[p]) mod q_i, i < nq (coefficient domain)
+__global__ void rescale_lift_kernel(u64* __restrict__ W, const u64* __restrict__ top, int nq, u64 qtop,
+                                    int logn, Limbs ql, const PrimeInfo* __restrict__ pr, long long total) {
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int n = (int)(idx & ((1 << logn) - 1));
+        long long rest = idx >> logn;
+        const int i = (int)(rest % nq);
+        const long long p = rest / nq;
+        const u64 q = pr[ql.prime[i]].q;
+        const u64 v = top[(p << logn) + n];
+        u64 r = v % q;
+        if (v > (qtop >> 1)) r = sub_mod(r, qtop % q, q);   // v - qtop
+        W[idx] = r;
+    }
+}
+
+cudaError_t rescale_lift_op(u64* W, const u64* top, int npoly, int nq, u64 qtop, int logn, const Limbs& ql,
+                            const PrimeInfo* pr, cudaStream_t st) {
+    long long total = (long long)npoly * nq << logn;
+    if (!total) return cudaSuccess;
+    rescale_lift_kernel<<<blocks_for(total, 256), 256, 0, st>>>(W, top, nq, qtop, logn, ql, pr, total);
+    return cudaGetLastError();
+}
+
+// out[p][i] = (c[p][i] - W[p][i]) * q_top^-1
+__global__ void rescale_combine_kernel(u64* __restrict__ out, long long os, const u64* __restrict__ c,
+                                       long long cs, const u64* __restrict__ W, int nq, int logn, Limbs ql,
+                                       const PrimeInfo* __restrict__ pr, const u64* __restrict__ qinv,
+                                       long long total) {
+    const int N = 1 << logn;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int n = (int)(idx & (N - 1));
+        long long rest = idx >> logn;
+        const int i = (int)(rest % nq);
+        const long long p = rest / nq;
+        const u64 q = pr[ql.prime[i]].q;
+        const u64 a = c[p * cs + (long long)i * N + n];
+        out[p * os + (long long)i * N + n] = shoup(a + q - W[idx], qinv[2 * i], qinv[2 * i + 1], q);
+    }
+}
+
+cudaError_t rescale_combine_op(u64* out, long long os, const u64* c, long long cs, const u64* W, int npoly,
+                               int nq, int logn, const Limbs& ql, const PrimeInfo* pr, const u64* qinv,
+                               cudaStream_t st) {
+    long long total = (long long)npoly * nq << logn;
+    if (!total) return cudaSuccess;
+    rescale_combine_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, os, c, cs, W, nq, logn, ql, pr, qinv,
+                                                                   total);
+    return cudaGetLastError();
+}
+
+// gather one limb of every poly: dst[p][n] = src[p * stride + off + n]
+__global__ void gather_limb_kernel(u64* __restrict__ dst, const u64* __restrict__ src, long long stride,
+                                   long long off, int logn, long long total) {
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long p = idx >> logn;
+        dst[idx] = src[p * stride + off + (idx & ((1 << logn) - 1))];
+    }
+}
+
+cudaError_t gather_limb_op(u64* dst, const u64* src, long long stride, long long off, int npoly, int logn,
+                           cudaStream_t st) {
+    long long total = (long long)npoly << logn;
+    if (!total) return cudaSuccess;
+    gather_limb_kernel<<<blocks_for(total, 256), 256, 0, st>>>(dst, src, stride, off, logn, total);
+    return cudaGetLastError();
+}
+
+// copy limbs [0, nlimb) of each poly between differently-strided buffers
+__global__ void copy_limbs_kernel(u64* __restrict__ dst, long long ds, const u64* __restrict__ src, long long ss,
+                                  long long per_poly, long long total) {
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long p = idx / per_poly, o = idx - p * per_poly;
+        dst[p * ds + o] = src[p * ss + o];
+    }
+}
+
+cudaError_t copy_limbs_op(u64* dst, long long ds, const u64* src, long long ss, int npoly, long long per_poly,
+                          cudaStream_t st) {
+    long long total = (long long)npoly * per_poly;
+    if (!total) return cudaSuccess;
+    copy_limbs_kernel<<<blocks_for(total, 256), 256, 0, st>>>(dst, ds, src, ss, per_poly, total);
+    return cudaGetLastError();
+}
+
+}  // namespace bcn

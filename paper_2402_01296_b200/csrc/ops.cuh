@@ -1,0 +1,92 @@
+// ops.cuh -- launcher declarations shared by the kernel files and api.cu
+#pragma once
+#include "common.cuh"
+
+#define BCN_MAX_ALPHA 16
+
+// Fast base conversion constants for one source set (a ModUp digit or the
+// special primes): y_i = [x_i * hatinv_i]_{q_i}; out_t = sum_i y_i * hat_m[i][t]
+// with hat_m in Montgomery form (hat * 2^64 mod q_t) so one REDC finishes.
+struct ConvTable {
+    int n_src;
+    int pad;
+    u64 hatinv[BCN_MAX_ALPHA];
+    u64 hatinv_p[BCN_MAX_ALPHA];
+    u64 hat_m[BCN_MAX_ALPHA * BCN_MAX_LIMBS];
+};
+
+namespace bcn {
+
+struct NttArgs {
+    u64* data;
+    long long poly_stride;   // words between consecutive batch polys (grid.y)
+    long long digit_stride;  // unused unless skip_alpha > 0
+    Limbs limbs;             // limb t (grid.x) -> prime index
+    const ulonglong2* tw;    // [nprime][2][N] {w, w'}: forward then inverse
+    const PrimeInfo* pr;
+    int skip_alpha;          // ModUp: skip limb t of digit d when t/alpha == d and t <= skip_level
+    int skip_dnum;
+    int skip_level;
+};
+
+cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
+
+cudaError_t binary_op(int op, u64* out, long long os, const u64* a, long long as, const u64* b, long long bs,
+                      int npoly, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st);
+cudaError_t to_mont_op(u64* out, const u64* a, int npoly, int nlimb, int logn, const Limbs& limbs,
+                       const PrimeInfo* pr, cudaStream_t st);
+cudaError_t mac_op(u64* out, const u64* ct, long long ct_stride, const u64* pt, long long pt_stride,
+                   int n_items, int group, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr,
+                   cudaStream_t st);
+cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,
+                      int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st);
+cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, int npoly, int nlimb, int logn,
+                         u32 g, cudaStream_t st);
+cudaError_t modup_op(u64* U, const u64* xc, const u64* xn, long long x_stride, int npoly, int nq, int next,
+                     int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab,
+                     cudaStream_t st);
+cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
+                     long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
+                     const PrimeInfo* pr, cudaStream_t st);
+cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
+                            const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st);
+cudaError_t moddown_combine_op(u64* out, long long os, const u64* A, int next, const u64* Z, const u64* addend,
+                               long long as, int add_c1, u32 g, int npoly, int nq, int logn, const Limbs& ql,
+                               const PrimeInfo* pr, const u64* pinv, cudaStream_t st);
+cudaError_t rescale_lift_op(u64* W, const u64* top, int npoly, int nq, u64 qtop, int logn, const Limbs& ql,
+                            const PrimeInfo* pr, cudaStream_t st);
+cudaError_t rescale_combine_op(u64* out, long long os, const u64* c, long long cs, const u64* W, int npoly,
+                               int nq, int logn, const Limbs& ql, const PrimeInfo* pr, const u64* qinv,
+                               cudaStream_t st);
+cudaError_t gather_limb_op(u64* dst, const u64* src, long long stride, long long off, int npoly, int logn,
+                           cudaStream_t st);
+cudaError_t copy_limbs_op(u64* dst, long long ds, const u64* src, long long ss, int npoly, long long per_poly,
+                          cudaStream_t st);
+
+// encode.cu
+struct FftTab {
+    const double* re;
+    const double* im;
+    const int* rot;
+};
+cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long long vs, int nplain, double scale,
+                      int logn, const Limbs& limbs, const PrimeInfo* pr, const FftTab& ft, int add_err, u64 seed,
+                      u64 id_base, cudaStream_t st);
+cudaError_t decode_op(double* out, int nout, const u64* poly, long long ps, int k, int npoly, double scale, int logn,
+                      const PrimeInfo* pr, const FftTab& ft, u64 q0inv_mod_q1, u64 q0inv_p, cudaStream_t st);
+cudaError_t sample_uniform_op(u64* out, long long os, int npoly, int nlimb, int logn, const Limbs& limbs,
+                              const PrimeInfo* pr, u64 seed, u32 domain, u64 id_base, u64 id_step, cudaStream_t st);
+cudaError_t sample_small_op(u64* out, long long os, int npoly, int nlimb, int logn, const Limbs& limbs,
+                            const PrimeInfo* pr, u64 seed, u32 domain, u64 id_base, u64 id_step, int ternary,
+                            cudaStream_t st);
+cudaError_t encrypt_combine_op(u64* ct, int G, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr,
+                               const u64* s_mont, u64 seed, u64 id_base, cudaStream_t st);
+cudaError_t ksk_digit_op(u64* b_out, u64* a_out, const u64* e_ntt, const u64* s_mont, const u64* sprime,
+                         int nbasis, int d0, int d1, int logn, const PrimeInfo* pr, const u64* pmod, u64 seed,
+                         u64 kid, cudaStream_t st);
+cudaError_t decrypt_core_op(u64* out, const u64* ct, long long cs, int nlimb_ct, int k, int npoly, int logn,
+                            const PrimeInfo* pr, const u64* s_mont, long long s_stride, cudaStream_t st);
+cudaError_t from_mont_op(u64* out, const u64* in, long long n_words_per_limb, int nlimb, int npoly,
+                         const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st);
+
+}  // namespace bcn

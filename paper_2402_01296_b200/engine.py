@@ -1,0 +1,247 @@
+"""Device engine: one libbcn context per HeParams, with torch-owned buffers.
+
+Every method is a thin, asynchronous call into libbcn.so on the current
+torch CUDA stream; ciphertext batches are int64 tensors (u64 bit patterns)
+of shape (G, 2, limbs, N) in the bit-reversed NTT domain.  No method falls
+back to the host: a missing library or device raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import CapacityError, DeviceError, ParameterError
+from .params import HeParams, fft_table, galois_element
+
+RELIN_KEY_ID = 2
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Engine:
+    def __init__(self, params: HeParams, device: int | None = None):
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device: the RNS-CKKS engine runs on the GPU only")
+        lib = _lib.load()
+        self.params = params
+        self.N = params.N
+        self.logn = params.logn
+        self.L = params.max_level
+        self.K = params.K
+        self.nbasis = self.L + 1 + self.K
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        q = (ctypes.c_uint64 * len(params.q))(*params.q)
+        p = (ctypes.c_uint64 * len(params.p))(*params.p)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(lib.bcn_ctx_create(ctypes.byref(h), self.logn, self.L, q, len(params.p), p,
+                                          params.dnum, params.seed, self.device.index), "bcn_ctx_create")
+        self._h = h
+        re, im = fft_table(self.N)
+        _lib.call("bcn_ctx_set_fft", h, re.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                  im.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        self._counter = 1   # Philox id of the next encryption
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            try:
+                _lib._lib.bcn_ctx_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ---------------------------------------------------------- helpers
+    @property
+    def handle(self):
+        return self._h
+
+    def empty_ct(self, G: int, level: int) -> torch.Tensor:
+        return torch.empty((G, 2, level + 1, self.N), dtype=torch.int64, device=self.device)
+
+    def _dev_f64(self, vals) -> torch.Tensor:
+        if isinstance(vals, torch.Tensor):
+            t = vals.to(device=self.device, dtype=torch.float64)
+        else:
+            t = torch.as_tensor(np.asarray(vals, dtype=np.float64), device=self.device)
+        if t.dim() == 1:
+            t = t[None]
+        return t.contiguous()
+
+    def _check_mag(self, vals: torch.Tensor, scale: float) -> None:
+        # the canonical-embedding inverse is a contraction: |coef| <= scale * max|v|
+        if vals.numel():
+            m = float(vals.abs().max())
+            if not np.isfinite(m):
+                raise ParameterError("plaintext vector must contain only finite values")
+            if m * scale >= 2.0 ** 62:
+                raise ParameterError(f"value {m:.3g} at scale 2^{np.log2(scale):.1f} overflows 62-bit coefficients")
+
+    def next_counter(self, n: int = 1) -> int:
+        c = self._counter
+        self._counter += n
+        return c
+
+    # ---------------------------------------------------------- K1 / K2
+    def ntt(self, data: torch.Tensor, prime0: int = 0, inverse: bool = False) -> torch.Tensor:
+        """In-place NTT of int64[npoly, nlimb, N] (limb t mod basis prime prime0+t)."""
+        npoly, nlimb, N = data.shape
+        assert N == self.N and data.is_contiguous()
+        _lib.call("bcn_ntt_inv" if inverse else "bcn_ntt_fwd", self._h, _ptr(data), npoly, nlimb, prime0, _stream())
+        return data
+
+    # ---------------------------------------------------------- K9-K11
+    def encode(self, vals, level: int, scale: float, montgomery: bool = False) -> torch.Tensor:
+        v = self._dev_f64(vals)
+        if v.shape[1] > self.N // 2:
+            raise CapacityError(f"vector of length {v.shape[1]} exceeds {self.N // 2} slots")
+        self._check_mag(v, scale)
+        out = torch.empty((v.shape[0], level + 1, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_encode", self._h, _ptr(v), v.shape[1], v.shape[1], v.shape[0], float(scale), level,
+                  int(montgomery), _ptr(out), _stream())
+        return out
+
+    def encrypt(self, vals, level: int | None = None, scale: float | None = None,
+                counter: int | None = None) -> torch.Tensor:
+        v = self._dev_f64(vals)
+        if v.shape[1] > self.N // 2:
+            raise CapacityError(f"vector of length {v.shape[1]} exceeds {self.N // 2} slots")
+        level = self.L if level is None else level
+        scale = self.params.scale if scale is None else scale
+        self._check_mag(v, scale)
+        G = v.shape[0]
+        counter = self.next_counter(G) if counter is None else counter
+        ct = self.empty_ct(G, level)
+        _lib.call("bcn_encrypt", self._h, _ptr(v), v.shape[1], v.shape[1], G, level, float(scale), counter,
+                  _ptr(ct), _stream())
+        return ct
+
+    def decrypt(self, ct: torch.Tensor, level: int, scale: float, nout: int | None = None) -> torch.Tensor:
+        G, two, nl, N = ct.shape
+        nout = self.N // 2 if nout is None else nout
+        out = torch.empty((G, nout), dtype=torch.float64, device=self.device)
+        _lib.call("bcn_decrypt", self._h, _ptr(ct), nl, G, level, float(scale), _ptr(out), nout, _stream())
+        return out
+
+    def decrypt_poly(self, ct: torch.Tensor, level: int) -> torch.Tensor:
+        G, _, nl, N = ct.shape
+        k = 2 if level >= 1 else 1
+        out = torch.empty((G, k, N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_decrypt_poly", self._h, _ptr(ct), nl, G, level, _ptr(out), _stream())
+        return out
+
+    # ---------------------------------------------------------- K3-K8
+    def add(self, a: torch.Tensor, b: torch.Tensor, level: int) -> torch.Tensor:
+        G = a.shape[0]
+        out = self.empty_ct(G, level)
+        _lib.call("bcn_add", self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(b), b.shape[2], 0, G, G, level,
+                  _stream())
+        return out
+
+    def add_plain(self, a: torch.Tensor, pt: torch.Tensor, level: int) -> torch.Tensor:
+        G = a.shape[0]
+        out = self.empty_ct(G, level)
+        _lib.call("bcn_add", self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(pt), pt.shape[1], 1, pt.shape[0], G,
+                  level, _stream())
+        return out
+
+    def mul_plain(self, a: torch.Tensor, pt_mont: torch.Tensor, level: int, rescale: bool = True) -> torch.Tensor:
+        G = a.shape[0]
+        out = self.empty_ct(G, level - 1 if rescale else level)
+        name = "bcn_mul_plain" if rescale else "bcn_mul_plain_norescale"
+        _lib.call(name, self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(pt_mont), pt_mont.shape[0], G, level,
+                  _stream())
+        return out
+
+    def rescale(self, a: torch.Tensor, level: int) -> torch.Tensor:
+        G = a.shape[0]
+        out = self.empty_ct(G, level - 1)
+        _lib.call("bcn_rescale", self._h, _ptr(out), _ptr(a), a.shape[2], G, level, _stream())
+        return out
+
+    def mul_cc(self, a: torch.Tensor, b: torch.Tensor, level: int, rescale: bool = True) -> torch.Tensor:
+        G = a.shape[0]
+        out = self.empty_ct(G, level - 1 if rescale else level)
+        _lib.call("bcn_mul_cc", self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(b), b.shape[2], G, level,
+                  int(rescale), _stream())
+        return out
+
+    def modup(self, a: torch.Tensor, level: int) -> torch.Tensor:
+        G = a.shape[0]
+        w = ctypes.c_uint64()
+        _lib.call("bcn_modup_words", self._h, G, level, ctypes.byref(w))
+        U = torch.empty(int(w.value), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_modup", self._h, _ptr(U), _ptr(a), a.shape[2], G, level, _stream())
+        return U
+
+    def rotate(self, a: torch.Tensor, r: int, level: int, U: torch.Tensor | None = None) -> torch.Tensor:
+        G = a.shape[0]
+        g = galois_element(r, self.N)
+        out = self.empty_ct(G, level)
+        if U is None:
+            _lib.call("bcn_rotate", self._h, _ptr(out), _ptr(a), a.shape[2], G, level, g, _stream())
+        else:
+            _lib.call("bcn_rotate_hoisted", self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(U), G, level, g,
+                      _stream())
+        return out
+
+    def keygen_galois(self, g: int) -> None:
+        _lib.call("bcn_keygen_galois", self._h, g, _stream())
+
+    def keygen_relin(self) -> None:
+        _lib.call("bcn_keygen_relin", self._h, _stream())
+
+    def export_key(self, key_id: int) -> torch.Tensor:
+        out = torch.empty((self.params.dnum, 2, self.nbasis, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_export_key", self._h, key_id, _ptr(out), _stream())
+        return out
+
+    def export_secret(self) -> torch.Tensor:
+        out = torch.empty((self.nbasis, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_export_secret", self._h, _ptr(out), _stream())
+        return out
+
+    def mac(self, ct: torch.Tensor, pt_mont: torch.Tensor, group: int) -> torch.Tensor:
+        n_items, _, nl, N = ct.shape
+        ng = -(-n_items // group)
+        out = torch.empty((ng, 2, nl, N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_mac", self._h, _ptr(out), _ptr(ct), _ptr(pt_mont), n_items, group, nl, _stream())
+        return out
+
+    def sample_uniform(self, npoly: int, nlimb: int, prime0: int = 0, seed: int = 0, id0: int = 0) -> torch.Tensor:
+        out = torch.empty((npoly, nlimb, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_sample_uniform", self._h, _ptr(out), npoly, nlimb, prime0, seed, id0, _stream())
+        return out
+
+    def to_montgomery(self, x: torch.Tensor, prime0: int = 0) -> torch.Tensor:
+        npoly, nlimb, N = x.shape
+        out = torch.empty_like(x)
+        _lib.call("bcn_to_montgomery", self._h, _ptr(out), _ptr(x), npoly, nlimb, prime0, _stream())
+        return out
+
+    def automorph(self, x: torch.Tensor, g: int) -> torch.Tensor:
+        npoly, nlimb, N = x.shape
+        out = torch.empty_like(x)
+        _lib.call("bcn_automorph", self._h, _ptr(out), _ptr(x), npoly, nlimb, g, _stream())
+        return out
+
+    def memory_bytes(self) -> int:
+        b = ctypes.c_uint64()
+        _lib.call("bcn_ctx_memory", self._h, ctypes.byref(b))
+        return int(b.value)
+
+
+def to_numpy_u64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint64)

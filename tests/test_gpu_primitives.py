@@ -1,0 +1,175 @@
+"""Ciphertext-level parity: every libbcn primitive against the CPU oracle,
+bit for bit (canonical u64 residues), at sizes the oracle finishes quickly.
+Called through the C ABI (paper_2402_01296_b200/engine.py -> libbcn.so)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import ckks as O  # noqa: E402
+from paper_2402_01296_b200.engine import Engine, to_numpy_u64  # noqa: E402
+from paper_2402_01296_b200.params import make_params  # noqa: E402
+
+
+def _pair(N, L, scale_bits=40, dnum=2, seed=7):
+    hp = make_params(N, L, scale_bits, dnum=dnum, seed=seed)
+    op = O.make_params(N, L, scale_bits, dnum=dnum, seed=seed)
+    assert list(hp.q) == op.q and list(hp.p) == op.p
+    return Engine(hp), O.Oracle(op), hp
+
+
+def _ct_np(ct):
+    a = to_numpy_u64(ct)
+    return a[:, 0], a[:, 1]
+
+
+def _assert_ct(gpu_ct, oct_list):
+    c0, c1 = _ct_np(gpu_ct)
+    for g, oc in enumerate(oct_list):
+        np.testing.assert_array_equal(c0[g], oc.c0)
+        np.testing.assert_array_equal(c1[g], oc.c1)
+
+
+@pytest.mark.parametrize("logn", [3, 4, 6, 8, 9, 10, 11, 12, 13, 14])
+def test_ntt_matches_oracle(logn):
+    N = 1 << logn
+    eng, orc, hp = _pair(N, 3, 30 if logn < 12 else 40, dnum=2)
+    rng = np.random.default_rng(logn)
+    basis = list(hp.q) + list(hp.p)
+    x = np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in basis])[None].repeat(3, 0)
+    t = torch.from_numpy(x.view(np.int64).copy()).cuda()
+    eng.ntt(t, 0)
+    got = to_numpy_u64(t)
+    exp = np.stack([O.ntt(x[i], basis) for i in range(3)])
+    np.testing.assert_array_equal(got, exp)
+    eng.ntt(t, 0, inverse=True)
+    np.testing.assert_array_equal(to_numpy_u64(t), x)
+
+
+def test_secret_key_matches():
+    eng, orc, hp = _pair(64, 4)
+    np.testing.assert_array_equal(to_numpy_u64(eng.export_secret()), orc.keys.s_ntt)
+
+
+def test_encode_matches():
+    eng, orc, hp = _pair(256, 3)
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal((2, 100))
+    for lvl, scale in [(3, 2.0 ** 40), (1, float(hp.q[1]))]:
+        pt = eng.encode(v, lvl, scale)
+        got = to_numpy_u64(pt)
+        for g in range(2):
+            np.testing.assert_array_equal(got[g], orc.encode(v[g], lvl, scale))
+
+
+@pytest.mark.parametrize("N", [16, 1024, 16384])
+def test_encrypt_decrypt_matches(N):
+    eng, orc, hp = _pair(N, 3)
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal((2, N // 2))
+    ct = eng.encrypt(v, counter=11)
+    _assert_ct(ct, [orc.encrypt(v[0], 11), orc.encrypt(v[1], 12)])
+    dec = eng.decrypt(ct, hp.max_level, hp.scale).cpu().numpy()
+    for g in range(2):
+        ref = orc.decrypt(orc.encrypt(v[g], 11 + g))
+        np.testing.assert_allclose(dec[g], ref, rtol=0, atol=1e-12)
+        assert np.abs(dec[g] - v[g]).max() < 1e-6
+
+
+def _enc2(eng, orc, N, rng, counter=5):
+    v = rng.standard_normal((2, N // 2))
+    ct = eng.encrypt(v, counter=counter)
+    oc = [orc.encrypt(v[0], counter), orc.encrypt(v[1], counter + 1)]
+    return v, ct, oc
+
+
+def test_add_mulplain_rescale_match():
+    N = 512
+    eng, orc, hp = _pair(N, 4)
+    rng = np.random.default_rng(2)
+    v, ct, oc = _enc2(eng, orc, N, rng)
+    w, ct2, oc2 = _enc2(eng, orc, N, rng, counter=9)
+    L = hp.max_level
+    _assert_ct(eng.add(ct, ct2, L), [orc.add_cc(oc[i], oc2[i]) for i in range(2)])
+    p = rng.standard_normal(N // 2)
+    pt = eng.encode(p, L, hp.scale)
+    _assert_ct(eng.add_plain(ct, pt, L), [orc.add_plain(oc[i], p) for i in range(2)])
+    ptm = eng.encode(p, L, float(hp.q[L]), montgomery=True)
+    got = eng.mul_plain(ct, ptm, L)
+    _assert_ct(got, [orc.mul_plain(oc[i], p) for i in range(2)])
+    dec = eng.decrypt(got, L - 1, hp.scale).cpu().numpy()
+    assert np.abs(dec[0] - v[0] * p).max() < 1e-6
+
+
+@pytest.mark.parametrize("N,L,dnum", [(64, 4, 2), (2048, 5, 3), (16384, 6, 3)])
+def test_square_relin_matches(N, L, dnum):
+    eng, orc, hp = _pair(N, L, dnum=dnum)
+    rng = np.random.default_rng(3)
+    v, ct, oc = _enc2(eng, orc, N, rng)
+    eng.keygen_relin()
+    ok = orc.relin_key()
+    key = to_numpy_u64(eng.export_key(O.RELIN_KEY_ID))
+    for j in range(len(ok[0])):
+        np.testing.assert_array_equal(key[j, 0], ok[0][j])
+        np.testing.assert_array_equal(key[j, 1], ok[1][j])
+    got = eng.mul_cc(ct, ct, L)
+    _assert_ct(got, [orc.mul_cc(oc[i], oc[i]) for i in range(2)])
+    dec = eng.decrypt(got, L - 1, hp.scale ** 2 / hp.q[L]).cpu().numpy()
+    assert np.abs(dec[0] - v[0] ** 2).max() < 1e-5
+
+
+@pytest.mark.parametrize("N,L,dnum", [(64, 3, 2), (4096, 5, 2), (16384, 4, 3)])
+def test_rotate_matches(N, L, dnum):
+    eng, orc, hp = _pair(N, L, dnum=dnum)
+    rng = np.random.default_rng(4)
+    v, ct, oc = _enc2(eng, orc, N, rng)
+    for r in [1, 5, -1, N // 2 - 3]:
+        got = eng.rotate(ct, r, L)
+        _assert_ct(got, [orc.rotate(oc[i], r) for i in range(2)])
+        dec = eng.decrypt(got, L, hp.scale).cpu().numpy()
+        assert np.abs(dec[1] - np.roll(v[1], -r)).max() < 1e-6
+    U = eng.modup(ct, L)
+    for r in [2, 7]:
+        _assert_ct(eng.rotate(ct, r, L, U=U), [orc.rotate(oc[i], r) for i in range(2)])
+
+
+def test_rotate_at_lower_level_reads_in_place():
+    N = 256
+    eng, orc, hp = _pair(N, 4, dnum=2)
+    rng = np.random.default_rng(5)
+    v, ct, oc = _enc2(eng, orc, N, rng)
+    p = rng.standard_normal(N // 2)
+    m = eng.mul_plain(ct, eng.encode(p, 4, float(hp.q[4]), montgomery=True), 4)
+    om = [orc.mul_plain(oc[i], p) for i in range(2)]
+    got = eng.rotate(m, 3, 3)
+    _assert_ct(got, [orc.rotate(om[i], 3) for i in range(2)])
+    # level-2 view of a level-3 ciphertext (level = min on add, sim.py:213)
+    got2 = eng.add(m, got, 2)
+    exp = [orc.add_cc(O.Ct(om[i].c0[:3], om[i].c1[:3], 2, om[i].scale), orc.rotate(om[i], 3)) for i in range(2)]
+    _assert_ct(got2, exp)
+
+
+def test_mac_matches():
+    N = 1024
+    eng, orc, hp = _pair(N, 3, 60)
+    nl = 4
+    rng = np.random.default_rng(6)
+    basis = list(hp.q)
+    T, group = 53, 25
+    ct = np.stack([np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in basis])
+                             for _ in range(2)]) for _ in range(T)])
+    pt = np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in basis]) for _ in range(T)])
+    tct = torch.from_numpy(ct.view(np.int64).copy()).cuda()
+    tpt = eng.to_montgomery(torch.from_numpy(pt.view(np.int64).copy()).cuda())
+    got = to_numpy_u64(eng.mac(tct, tpt, group))
+    for g in range(3):
+        lo, hi = g * group, min((g + 1) * group, T)
+        for c in range(2):
+            for i, q in enumerate(basis):
+                exp = np.zeros(N, dtype=np.uint64)
+                O.lib().orc_mac(O._p(np.ascontiguousarray(ct[lo:hi, c, i])), O._p(np.ascontiguousarray(pt[lo:hi, i])),
+                                O._p(exp), hi - lo, N, q)
+                np.testing.assert_array_equal(got[g, c, i], exp)
