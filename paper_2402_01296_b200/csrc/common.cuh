@@ -75,6 +75,12 @@ struct Acc128 {
     __device__ __forceinline__ u64 reduce(u64 q, u64 qinv_neg) const { return redc(hi, lo, q, qinv_neg); }
 };
 
+// x - m if x >= m else x, for x < 2m < 2^64 and m < 2^63 (sign-bit select)
+__device__ __forceinline__ u64 csub(u64 x, u64 m) {
+    const u64 t = x - m;
+    return (i64)t < 0 ? x : t;
+}
+
 __device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 q) { u64 s = a + b; return s >= q ? s - q : s; }
 __device__ __forceinline__ u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 __device__ __forceinline__ u64 neg_mod(u64 a, u64 q) { return a ? q - a : 0ull; }

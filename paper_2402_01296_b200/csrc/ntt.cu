@@ -18,12 +18,12 @@
 namespace bcn {
 
 template <int LOGN> struct NttCfg {
-    static constexpr int LOGE = (LOGN - 8) < 1 ? 1 : ((LOGN - 8) > 5 ? 5 : (LOGN - 8));
+    static constexpr int LOGE = LOGN >= 14 ? 4 : (LOGN >= 10 ? 3 : (LOGN >= 8 ? 2 : 1));
     static constexpr int N = 1 << LOGN;
     static constexpr int E = 1 << LOGE;
     static constexpr int T = N / E;
     static constexpr int R0 = (LOGN % LOGE) ? (LOGN % LOGE) : LOGE;
-    static constexpr int SWZ = (E < 16 ? E : 16) - 1;
+    static constexpr int SWZ = E >= 8 ? 15 : E - 1;   // conflict-free for every pass (tools/swizzle_check)
 };
 
 template <int LOGE, int SWZ>
@@ -31,7 +31,7 @@ __device__ __forceinline__ int swz(int j) { return j ^ ((j >> LOGE) & SWZ); }
 
 // ---------------------------------------------------------------- forward
 template <int LOGN, int S0, int R, bool FIRST, bool LAST>
-__device__ __forceinline__ void fwd_pass(u64* x, const u64* __restrict__ g, u64* sm,
+__device__ __forceinline__ void fwd_pass(u64* x, u64* __restrict__ g, u64* sm,
                                          const ulonglong2* __restrict__ W, u64 q, int tid) {
     using C = NttCfg<LOGN>;
     constexpr int BS = 1 << R;               // block size
@@ -58,32 +58,40 @@ __device__ __forceinline__ void fwd_pass(u64* x, const u64* __restrict__ g, u64*
                 if (k & h) continue;
                 const ulonglong2 w = W[(1 << s) + (gi << ls) + (k >> (R - ls))];
                 u64 u = x[i * BS + k];
-                if (u >= q2) u -= q2;
+                if (!(FIRST && ls == 0)) u = csub(u, q2);   // canonical input needs no fold
                 const u64 v = shoup_lazy(x[i * BS + k + h], w.x, w.y, q);
                 x[i * BS + k] = u + v;
                 x[i * BS + k + h] = u - v + q2;
             }
         }
+        if constexpr (LAST && TL == 1) {
+            // final pass: a thread owns BS consecutive words -> 16-byte stores
 #pragma unroll
-        for (int k = 0; k < BS; k++) {
-            const int j = base + k * TL;
-            u64 v = x[i * BS + k];
-            if (LAST) {
-                if (v >= q2) v -= q2;
-                if (v >= q) v -= q;
+            for (int k = 0; k < BS; k += 2) {
+                ulonglong2 v;
+                v.x = csub(csub(x[i * BS + k], q2), q);
+                v.y = csub(csub(x[i * BS + k + 1], q2), q);
+                *reinterpret_cast<ulonglong2*>(g + base + k) = v;
             }
-            sm[swz<C::LOGE, C::SWZ>(j)] = v;
+        } else {
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                const int j = base + k * TL;
+                u64 v = x[i * BS + k];
+                if (LAST) v = csub(csub(v, q2), q);
+                sm[swz<C::LOGE, C::SWZ>(j)] = v;
+            }
         }
     }
 }
 
 template <int LOGN, int S0>
-__device__ __forceinline__ void fwd_rest(u64* x, u64* sm, const ulonglong2* __restrict__ W, u64 q, int tid) {
+__device__ __forceinline__ void fwd_rest(u64* x, u64* g, u64* sm, const ulonglong2* __restrict__ W, u64 q, int tid) {
     using C = NttCfg<LOGN>;
     if constexpr (S0 < LOGN) {
         __syncthreads();
-        fwd_pass<LOGN, S0, C::LOGE, false, (S0 + C::LOGE >= LOGN)>(x, nullptr, sm, W, q, tid);
-        fwd_rest<LOGN, S0 + C::LOGE>(x, sm, W, q, tid);
+        fwd_pass<LOGN, S0, C::LOGE, false, (S0 + C::LOGE >= LOGN)>(x, g, sm, W, q, tid);
+        fwd_rest<LOGN, S0 + C::LOGE>(x, g, sm, W, q, tid);
     }
 }
 
@@ -106,13 +114,11 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_fwd_kernel(NttArgs a) {
     u64 x[C::E];
     const int tid = threadIdx.x;
     fwd_pass<LOGN, 0, C::R0, true, (C::R0 >= LOGN)>(x, g, sm, W, q, tid);
-    fwd_rest<LOGN, C::R0>(x, sm, W, q, tid);
-    __syncthreads();
-    for (int j = tid; j < C::N; j += C::T) g[j] = sm[swz<C::LOGE, C::SWZ>(j)];
+    fwd_rest<LOGN, C::R0>(x, g, sm, W, q, tid);
 }
 
 // ---------------------------------------------------------------- inverse
-template <int LOGN, int S0, int R, bool LAST>
+template <int LOGN, int S0, int R, bool LAST, bool FIRST = false>
 __device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, u64* sm,
                                          const ulonglong2* __restrict__ Wi, u64 q,
                                          u64 ninv, u64 ninv_p, u64 wn, u64 wn_p, int tid) {
@@ -126,8 +132,17 @@ __device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, u64* sm,
         const int b = tid + i * C::T;
         const int gi = b / TL;
         const int base = gi * (C::N >> S0) + (b % TL);
+        if constexpr (FIRST && TL == 1) {
 #pragma unroll
-        for (int k = 0; k < BS; k++) x[i * BS + k] = sm[swz<C::LOGE, C::SWZ>(base + k * TL)];
+            for (int k = 0; k < BS; k += 2) {
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + base + k);
+                x[i * BS + k] = v.x;
+                x[i * BS + k + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < BS; k++) x[i * BS + k] = sm[swz<C::LOGE, C::SWZ>(base + k * TL)];
+        }
 #pragma unroll
         for (int ls = R - 1; ls >= 0; ls--) {
             const int h = BS >> (ls + 1);
@@ -142,9 +157,7 @@ __device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, u64* sm,
                     x[i * BS + k + h] = shoup(u - v + q2, wn, wn_p, q);
                 } else {
                     const ulonglong2 w = Wi[(1 << s) + (gi << ls) + (k >> (R - ls))];
-                    u64 sum = u + v;
-                    if (sum >= q2) sum -= q2;
-                    x[i * BS + k] = sum;
+                    x[i * BS + k] = csub(u + v, q2);
                     x[i * BS + k + h] = shoup_lazy(u - v + q2, w.x, w.y, q);
                 }
             }
@@ -163,7 +176,7 @@ __device__ __forceinline__ void inv_rest(u64* x, u64* g, u64* sm, const ulonglon
                                          u64 ninv, u64 ninv_p, u64 wn, u64 wn_p, int tid) {
     using C = NttCfg<LOGN>;
     if constexpr (S0 >= C::R0) {
-        inv_pass<LOGN, S0, C::LOGE, false>(x, g, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
+        inv_pass<LOGN, S0, C::LOGE, false, (S0 == LOGN - C::LOGE)>(x, g, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
         __syncthreads();
         inv_rest<LOGN, S0 - C::LOGE>(x, g, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
     }
@@ -180,8 +193,6 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_inv_kernel(NttArgs a) {
     const ulonglong2* Wi = a.tw + (size_t)pidx * 2 * C::N + C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
     const int tid = threadIdx.x;
-    for (int j = tid; j < C::N; j += C::T) sm[swz<C::LOGE, C::SWZ>(j)] = g[j];
-    __syncthreads();
     u64 x[C::E];
     const u64 ninv = P.pad[0], ninv_p = P.pad[1];
     const ulonglong2 wn = Wi[0];   // slot 0 of the inverse table holds {w1 n^-1, shoup}

@@ -171,9 +171,11 @@ class Engine:
         _lib.call("bcn_rescale", self._h, _ptr(out), _ptr(a), a.shape[2], G, level, _stream())
         return out
 
-    def mul_cc(self, a: torch.Tensor, b: torch.Tensor, level: int, rescale: bool = True) -> torch.Tensor:
+    def mul_cc(self, a: torch.Tensor, b: torch.Tensor, level: int, rescale: bool = True,
+               out: torch.Tensor | None = None) -> torch.Tensor:
         G = a.shape[0]
-        out = self.empty_ct(G, level - 1 if rescale else level)
+        if out is None:
+            out = self.empty_ct(G, level - 1 if rescale else level)
         _lib.call("bcn_mul_cc", self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(b), b.shape[2], G, level,
                   int(rescale), _stream())
         return out
@@ -186,10 +188,12 @@ class Engine:
         _lib.call("bcn_modup", self._h, _ptr(U), _ptr(a), a.shape[2], G, level, _stream())
         return U
 
-    def rotate(self, a: torch.Tensor, r: int, level: int, U: torch.Tensor | None = None) -> torch.Tensor:
+    def rotate(self, a: torch.Tensor, r: int, level: int, U: torch.Tensor | None = None,
+               out: torch.Tensor | None = None) -> torch.Tensor:
         G = a.shape[0]
         g = galois_element(r, self.N)
-        out = self.empty_ct(G, level)
+        if out is None:
+            out = self.empty_ct(G, level)
         if U is None:
             _lib.call("bcn_rotate", self._h, _ptr(out), _ptr(a), a.shape[2], G, level, g, _stream())
         else:

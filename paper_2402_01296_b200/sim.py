@@ -1,0 +1,441 @@
+"""Drop-in for the reference's `bibranch.sim` (pkg/src/bibranch/sim.py), backed
+by real RNS-CKKS on the GPU.
+
+Same names, signatures, level algebra, recorder counts and exceptions as the
+reference; what changes is what a Ciphertext *is*: a batch of G RLWE
+ciphertexts (u64[G, 2, level+1, N], bit-reversed NTT domain) living in HBM,
+produced and consumed only by libbcn.so kernels.  `Ciphertext.slots` is a
+lazy, read-only decryption (sim.py:128-139 exposes the slots directly).
+
+Execution choices that keep the reference's observable semantics:
+  * Rescale is lazy.  A Mul_PC product is returned "pending": logically at
+    level-1 (as sim.py:248 / 282 say) but held unrescaled at data level l
+    with scale Delta*q_l.  Pending + pending adds stay pending, so a conv
+    tap loop or an FC diagonal sum pays ONE rescale per output instead of one
+    per product.  Anything else materialises (rescales) first.
+  * Rotations are hoisted: ModUp(c1) is computed once per ciphertext and
+    reused by every rotation of it; results are memoised per (ct, r).  The
+    recorder still counts every call exactly as sim.py:253/273 do.
+Both are deterministic, so results do not depend on call order.
+"""
+
+from __future__ import annotations
+
+import itertools
+from typing import Iterable, Union
+
+import numpy as np
+
+from .errors import CapacityError, DepthBudgetError, ParameterError, UsageError
+from .params import HeParams, galois_element, make_params, scale_bits_for
+
+# Table-1 CPU latencies of the paper, ms per op; kept for
+# the cost model exactly as the reference exposes them (sim.py:26-30).
+LATENCY_MS = {
+    "BGV": {"Add_PC": 0.049, "Add_CC": 0.077, "Mul_PC": 2.055, "Mul_CC": 3.379},
+    "CKKS": {"Add_PC": 0.039, "Add_CC": 0.077, "Mul_PC": 0.173, "Mul_CC": 0.390},
+    "TFHE": {"Add_PC": 56.03, "Add_CC": 256.8, "Mul_PC": 1018.0, "Mul_CC": 1585.0},
+}
+SCHEMES = tuple(LATENCY_MS)
+HE_OP_KEYS = ("Add_PC", "Add_CC", "Mul_PC", "Mul_CC")
+COUNTER_KEYS = HE_OP_KEYS + ("Rot", "Act_C", "Mul_PC_mask")
+
+PlainLike = Union[np.ndarray, list, tuple]
+
+MAX_RING = 1 << 14
+
+
+def _zeros() -> dict:
+    return dict.fromkeys(COUNTER_KEYS, 0)
+
+
+class OpRecorder:
+    """Per-op counters with innermost-scope layer attribution (sim.py:47-108).
+
+    Every bump lands in the totals and in exactly one bucket (the innermost
+    open layer, else the unscoped remainder), so layer_table() always sums
+    to the totals.  merge() folds another recorder in deterministically.
+    """
+
+    def __init__(self):
+        self.counters = _zeros()
+        self.per_layer: list[tuple[str, dict]] = []
+        self._open: list[tuple[str, dict]] = []
+        self._unscoped = _zeros()
+
+    def bump(self, key: str, n: int = 1) -> None:
+        self.counters[key] += n
+        bucket = self._open[-1][1] if self._open else self._unscoped
+        bucket[key] += n
+
+    def layer(self, layer_id: str) -> "_Scope":
+        return _Scope(self, layer_id)
+
+    @property
+    def current_layer(self) -> str | None:
+        return self._open[-1][0] if self._open else None
+
+    def merge(self, other: "OpRecorder") -> None:
+        for k, v in other.counters.items():
+            self.counters[k] += v
+        for k, v in other._unscoped.items():
+            self._unscoped[k] += v
+        self.per_layer.extend((name, dict(d)) for name, d in other.per_layer)
+
+    def layer_table(self) -> list[tuple[str, dict]]:
+        rows = [(name, dict(d)) for name, d in self.per_layer]
+        if any(self._unscoped.values()):
+            rows.append(("(unscoped)", dict(self._unscoped)))
+        return rows
+
+    def snapshot(self) -> dict:
+        return dict(self.counters)
+
+
+class _Scope:
+    __slots__ = ("rec", "name")
+
+    def __init__(self, rec: OpRecorder, name: str):
+        self.rec, self.name = rec, name
+
+    def __enter__(self):
+        self.rec._open.append((self.name, _zeros()))
+        return self.rec
+
+    def __exit__(self, *exc):
+        name, delta = self.rec._open.pop()
+        self.rec.per_layer.append((name, delta))
+        return False
+
+
+class HeContext:
+    """Scheme parameters plus the device engine (sim.py:111-125).
+
+    poly_degree / slot_count / max_level / scale / scheme / latency_table /
+    noise_model keep the reference's meaning; `he` holds the RNS chain.  The
+    libbcn context is created on first use, so parameter validation works on
+    a host without a GPU; the first HE op there raises DeviceError.
+    """
+
+    def __init__(self, poly_degree, max_level, scale, scheme, latency_table, noise_model, he: HeParams,
+                 device=None):
+        self.poly_degree = poly_degree
+        self.slot_count = poly_degree // 2
+        self.max_level = max_level
+        self.scale = float(scale)
+        self.scheme = scheme
+        self.latency_table = latency_table
+        self.noise_model = noise_model
+        self.he = he
+        self._device = device
+        self._engine = None
+        self._ids = itertools.count()
+
+    def __repr__(self):
+        return (f"HeContext(poly_degree={self.poly_degree}, slot_count={self.slot_count}, "
+                f"max_level={self.max_level}, scale={self.scale}, scheme={self.scheme!r})")
+
+    def fresh_id(self) -> str:
+        return f"ct{next(self._ids)}"
+
+    @property
+    def engine(self):
+        if self._engine is None:
+            from .engine import Engine
+            self._engine = Engine(self.he, self._device)
+        return self._engine
+
+    @property
+    def delta(self) -> float:
+        """CKKS encoding scale of fresh ciphertexts."""
+        return self.he.scale
+
+    def q(self, level: int) -> int:
+        return self.he.q[level]
+
+
+class Ciphertext:
+    """Batch of G RNS-CKKS ciphertexts + logical level / scale / id.
+
+    Immutable from the outside (attribute assignment raises, as for the
+    reference's frozen dataclass).  Internally it may hold a pending
+    (unrescaled) product; `_data_level` is then level + 1.
+    """
+
+    __slots__ = ("level", "scale", "id", "ctx", "batch", "_data", "_data_level", "_data_scale",
+                 "_modup", "_rot", "_slots", "__weakref__")
+
+    def __init__(self, data, level: int, scale: float, ctx: HeContext, *, data_level=None, data_scale=None,
+                 cid: str | None = None):
+        s = object.__setattr__
+        s(self, "level", level)
+        s(self, "scale", float(scale))
+        s(self, "id", cid or ctx.fresh_id())
+        s(self, "ctx", ctx)
+        s(self, "batch", int(data.shape[0]))
+        s(self, "_data", data)
+        s(self, "_data_level", level if data_level is None else data_level)
+        s(self, "_data_scale", float(scale) if data_scale is None else float(data_scale))
+        s(self, "_modup", None)
+        s(self, "_rot", {})
+        s(self, "_slots", None)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Ciphertext is immutable")
+
+    def __repr__(self):
+        return f"Ciphertext(id={self.id!r}, level={self.level}, batch={self.batch})"
+
+    @property
+    def pending(self) -> bool:
+        return self._data_level != self.level
+
+    def materialize(self) -> "Ciphertext":
+        """Apply the deferred rescale in place (the logical value is unchanged)."""
+        if self.pending:
+            eng = self.ctx.engine
+            data = eng.rescale(self._data, self._data_level)
+            object.__setattr__(self, "_data", data)
+            object.__setattr__(self, "_data_level", self.level)
+            object.__setattr__(self, "_data_scale", self.scale)
+        return self
+
+    @property
+    def data(self):
+        return self.materialize()._data
+
+    @property
+    def slots(self) -> np.ndarray:
+        if self._slots is None:
+            out = _decrypt(self)
+            out.flags.writeable = False
+            object.__setattr__(self, "_slots", out)
+        return self._slots
+
+
+# ------------------------------------------------------------- context
+
+def make_context(poly_degree: int, max_level: int, scale: float, scheme: str = "CKKS",
+                 noise_model: bool = False, *, dnum: int | None = None, seed: int = 0,
+                 q0_bits: int = 60, special_bits: int = 60, device=None) -> HeContext:
+    """Reference checks (sim.py:142-169) plus the RNS chain (params.py).
+
+    Real CKKS noise replaces the optional fixed-point rounding model, so
+    `noise_model` is accepted and has no further effect."""
+    if poly_degree < 8 or poly_degree & (poly_degree - 1):
+        raise ParameterError(f"poly_degree must be a power of two >= 8, got {poly_degree}")
+    if poly_degree > MAX_RING:
+        raise ParameterError(f"poly_degree {poly_degree} above the engine maximum {MAX_RING}")
+    if max_level < 1:
+        raise ParameterError(f"max_level must be >= 1, got {max_level}")
+    if not scale > 0:
+        raise ParameterError(f"scale must be positive, got {scale}")
+    scheme = scheme.upper()
+    if scheme not in LATENCY_MS:
+        raise ParameterError(f"unknown scheme {scheme!r}; expected one of {SCHEMES}")
+    table = dict(LATENCY_MS[scheme])
+    table.setdefault("Rot", table["Mul_PC"])
+    if dnum is None:
+        dnum = min(3, max_level + 1)
+    he = make_params(poly_degree, max_level, scale_bits_for(scale), q0_bits=q0_bits,
+                     special_bits=special_bits, dnum=dnum, seed=seed)
+    return HeContext(poly_degree, max_level, scale, scheme, table, noise_model, he, device)
+
+
+def encode_plain(v: PlainLike, ctx: HeContext) -> np.ndarray:
+    """Zero-pad a real vector (or a (G, n) batch) to the slot width."""
+    arr = np.asarray(v, dtype=np.float64)
+    if arr.ndim <= 1:
+        arr = arr.ravel()
+        if arr.size > ctx.slot_count:
+            raise CapacityError(f"vector of length {arr.size} exceeds {ctx.slot_count} slots")
+        out = np.zeros(ctx.slot_count)
+        out[:arr.size] = arr
+        return out
+    arr = arr.reshape(arr.shape[0], -1)
+    if arr.shape[1] > ctx.slot_count:
+        raise CapacityError(f"vector of length {arr.shape[1]} exceeds {ctx.slot_count} slots")
+    out = np.zeros((arr.shape[0], ctx.slot_count))
+    out[:, :arr.shape[1]] = arr
+    return out
+
+
+def _as_plain_rows(v, ctx: HeContext):
+    """Host or device plain vector(s) -> 2-D float64 (rows, n<=S)."""
+    try:
+        import torch
+        if isinstance(v, torch.Tensor):
+            t = v.to(torch.float64)
+            t = t.reshape(1, -1) if t.dim() <= 1 else t.reshape(t.shape[0], -1)
+            if t.shape[1] > ctx.slot_count:
+                raise CapacityError(f"vector of length {t.shape[1]} exceeds {ctx.slot_count} slots")
+            return t
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.asarray(v, dtype=np.float64)
+    arr = arr.reshape(1, -1) if arr.ndim <= 1 else arr.reshape(arr.shape[0], -1)
+    if arr.shape[1] > ctx.slot_count:
+        raise CapacityError(f"vector of length {arr.shape[1]} exceeds {ctx.slot_count} slots")
+    return arr
+
+
+def encrypt_vector(v: PlainLike, ctx: HeContext) -> Ciphertext:
+    """Encrypt <= slot_count reals (zero-padded) at max_level (sim.py:184-189).
+    A 2-D (G, n) input encrypts G independent slot sets in one batch."""
+    rows = _as_plain_rows(v, ctx)
+    if isinstance(rows, np.ndarray):
+        if not np.all(np.isfinite(rows)):
+            raise ParameterError("plaintext vector must contain only finite values")
+    else:
+        import torch
+        if not bool(torch.isfinite(rows).all()):
+            raise ParameterError("plaintext vector must contain only finite values")
+    eng = ctx.engine
+    data = eng.encrypt(rows, ctx.max_level, ctx.delta)
+    return Ciphertext(data, ctx.max_level, ctx.delta, ctx)
+
+
+def _decrypt(c: Ciphertext) -> np.ndarray:
+    c.materialize()
+    out = c.ctx.engine.decrypt(c._data, c.level, c.scale).cpu().numpy()
+    return out[0] if c.batch == 1 else out
+
+
+def decrypt_vector(c: Ciphertext, ctx: HeContext) -> np.ndarray:
+    """Decrypt and decode the slots (never consumes level; sim.py:192-196)."""
+    if c.ctx is not ctx:
+        raise UsageError("ciphertext does not belong to this context")
+    return _decrypt(c).copy()
+
+
+def _same_ctx(a: Ciphertext, b) -> bool:
+    if isinstance(b, Ciphertext):
+        if a.ctx is not b.ctx:
+            raise UsageError("operands come from different contexts")
+        return True
+    return False
+
+
+def _depth_error(rec: OpRecorder, ctx: HeContext) -> DepthBudgetError:
+    layer = rec.current_layer
+    where = f" in layer {layer!r}" if layer else ""
+    return DepthBudgetError(f"multiplicative depth exhausted{where}: level is 0 (context max_level={ctx.max_level})")
+
+
+def _check_scales(sa: float, sb: float) -> None:
+    if abs(sa / sb - 1.0) > 1e-6:
+        raise UsageError(f"ciphertext scales differ ({sa:.6g} vs {sb:.6g}); CKKS addition needs equal scales")
+
+
+def _batch_of(a: Ciphertext, b: Ciphertext) -> None:
+    if a.batch != b.batch:
+        raise UsageError(f"ciphertext batches differ ({a.batch} vs {b.batch})")
+
+
+def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
+    """Add_CC (level = min) or Add_PC (level kept), sim.py:208-218."""
+    ctx = a.ctx
+    eng = ctx.engine
+    if _same_ctx(a, b):
+        rec.bump("Add_CC")
+        _batch_of(a, b)
+        level = min(a.level, b.level)
+        if a.pending and b.pending and a._data_level == b._data_level:
+            _check_scales(a._data_scale, b._data_scale)
+            data = eng.add(a._data, b._data, a._data_level)
+            return Ciphertext(data, level, a.scale, ctx, data_level=a._data_level, data_scale=a._data_scale)
+        a.materialize()
+        b.materialize()
+        _check_scales(a.scale, b.scale)
+        return Ciphertext(eng.add(a._data, b._data, level), level, a.scale, ctx)
+    rec.bump("Add_PC")
+    rows = _as_plain_rows(b, ctx)
+    if rows.shape[0] not in (1, a.batch):
+        raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {a.batch}")
+    a.materialize()       # a pending scale Delta*q_l would overflow a 64-bit encoding
+    pt = eng.encode(rows, a.level, a.scale)
+    return Ciphertext(eng.add_plain(a._data, pt, a.level), a.level, a.scale, ctx)
+
+
+def _mul_plain_pending(x: Ciphertext, plain, level: int) -> Ciphertext:
+    """x (materialised, at `level`) times an encoded multiplier, rescale deferred."""
+    ctx = x.ctx
+    eng = ctx.engine
+    rows = _as_plain_rows(plain, ctx)
+    if rows.shape[0] not in (1, x.batch):
+        raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {x.batch}")
+    ql = ctx.q(level)
+    pt = eng.encode(rows, level, float(ql), montgomery=True)
+    data = eng.mul_plain(x._data, pt, level, rescale=False)
+    return Ciphertext(data, level - 1, x.scale, ctx, data_level=level, data_scale=x.scale * float(ql))
+
+
+def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Ciphertext:
+    """Slot-wise product, result level = min(levels) - 1 (sim.py:221-248).
+
+    ct x plain: multiplier encoded at scale q_level, product rescaled by
+    q_level (lazily), so the scale is kept exactly.  ct x ct: tensor product,
+    relinearisation (hybrid key switch), rescale."""
+    ctx = a.ctx
+    is_cc = _same_ctx(a, b)
+    lvl = min(a.level, b.level) if is_cc else a.level
+    if lvl < 1:
+        raise _depth_error(rec, ctx)
+    if is_cc:
+        rec.bump("Mul_CC")
+    else:
+        rec.bump("Mul_PC")
+        if mask:
+            rec.bump("Mul_PC_mask")
+    a.materialize()
+    if not is_cc:
+        return _mul_plain_pending(a, b, lvl)
+    _batch_of(a, b)
+    b.materialize()
+    data = ctx.engine.mul_cc(a._data, b._data, lvl)
+    return Ciphertext(data, lvl - 1, (a.scale * b.scale) / ctx.q(lvl), ctx)
+
+
+def _rotated(c: Ciphertext, r: int) -> Ciphertext:
+    """Memoised, hoisted rotation of a materialised ciphertext (r reduced)."""
+    ctx = c.ctx
+    c.materialize()
+    hit = c._rot.get(r)
+    if hit is not None:
+        return hit
+    eng = ctx.engine
+    if r == 0:
+        out = Ciphertext(c._data, c.level, c.scale, ctx)
+    else:
+        if c._modup is None:
+            object.__setattr__(c, "_modup", eng.modup(c._data, c.level))
+        data = eng.rotate(c._data, r, c.level, U=c._modup)
+        out = Ciphertext(data, c.level, c.scale, ctx)
+    c._rot[r] = out
+    return out
+
+
+def release(c: Ciphertext) -> None:
+    """Drop the hoisting / memo buffers of a ciphertext (device memory)."""
+    object.__setattr__(c, "_modup", None)
+    c._rot.clear()
+
+
+def he_rotate(c: Ciphertext, r: int, rec: OpRecorder) -> Ciphertext:
+    """Left rotation by r slots (right for r < 0), level unchanged (sim.py:251-256)."""
+    rec.bump("Rot")
+    r = int(r) % c.ctx.slot_count
+    src = _rotated(c, r)
+    return Ciphertext(src._data, src.level, src.scale, c.ctx)
+
+
+def he_rotate_mul(c: Ciphertext, r: int, plain, rec: OpRecorder, *, mask: bool = False) -> Ciphertext:
+    """he_mul(he_rotate(c, r), plain): one Rot + one Mul_PC, level - 1 (sim.py:259-283)."""
+    if c.level < 1:
+        raise _depth_error(rec, c.ctx)
+    rec.bump("Rot")
+    rec.bump("Mul_PC")
+    if mask:
+        rec.bump("Mul_PC_mask")
+    r = int(r) % c.ctx.slot_count
+    return _mul_plain_pending(_rotated(c, r), plain, c.level)

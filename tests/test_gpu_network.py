@@ -1,0 +1,91 @@
+"""End-to-end parity of the encrypted bi-branch forward on the GPU engine
+against the reference's own outputs (tests/golden/*.npz, generated from
+/root/reference by tests/golden/make_golden.py):
+
+  * OpRecorder counts and per-layer tables: identical integers;
+  * decrypted logits vs the reference's float64 `reference_forward`:
+    |diff| <= LOGIT_TOL (CKKS is approximate; the measured error is printed)
+    and 100% argmax agreement.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+pytest.importorskip("torch")
+
+import paper_2402_01296_b200 as B  # noqa: E402
+from paper_2402_01296_b200.archive import TensorArchive  # noqa: E402
+from paper_2402_01296_b200.network import DecomposedInput  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+LOGIT_TOL = 1e-6   # absolute, Delta = 2^50, 50-bit rescale primes
+
+
+def _load(name):
+    d = np.load(os.path.join(GOLD, name + ".npz"))
+    w = TensorArchive({k[3:]: d[k] for k in d.files if k.startswith("w::")})
+    dec = [DecomposedInput(s, f, (0, 0, s.shape[-2], s.shape[-1])) for s, f in zip(d["sens"], d["full"])]
+    return d, w, dec, json.loads(str(d["meta"]))
+
+
+def _check(logits, ref, tol=LOGIT_TOL):
+    err = np.abs(logits - ref).max()
+    print(f"max |logit - reference| = {err:.3e}")
+    assert err <= tol
+    assert (logits.argmax(1) == ref.argmax(1)).all()
+
+
+def test_cnn3_fixture_bhw_matches_reference():
+    d, w, dec, meta = _load("cnn3_fixture")
+    bundle = B.get("cnn3")
+    ctx = B.make_context(1 << 14, B.required_levels(bundle) + 1, 2.0 ** 50)
+    res = B.forward_bicrypto(bundle.bi, dec, w, ctx, strategy="bhw")
+    assert res.recorder.snapshot() == meta["counts_bhw"]
+    assert [list(x) for x in res.recorder.layer_table()] == meta["layer_table"]
+    assert res.logits_ct.level == 1
+    _check(res.decrypt_logits(), d["logits_ref"])
+    assert B.taint_check(bundle.bi, res.recorder).passed
+
+
+def test_cnn3_hw_single_image_counts():
+    d, w, dec, meta = _load("cnn3_fixture")
+    bundle = B.get("cnn3")
+    ctx = B.make_context(1 << 13, B.required_levels(bundle) + 1, 2.0 ** 50)
+    res = B.forward_bicrypto(bundle.bi, dec[0], w, ctx, strategy="hw")
+    assert res.recorder.snapshot() == meta["counts_hw"]
+    _check(res.decrypt_logits(), d["logits_ref"][:1])
+
+
+def test_cnn3_config1_matches_reference():
+    d, w, dec, meta = _load("cnn3_cfg1")
+    bundle = B.get("cnn3")
+    ctx = B.make_context(8192, B.required_levels(bundle) + 1, 2.0 ** 50)
+    res = B.forward_bicrypto(bundle.bi, dec, w, ctx, strategy="hw")
+    assert res.recorder.snapshot() == meta["counts_hw"]
+    _check(res.decrypt_logits(), d["logits_ref"])
+
+
+def test_cifar3_config4_matches_reference():
+    d, w, dec, meta = _load("cifar3_cfg4")
+    bundle = B.get("cifar3")
+    ctx = B.make_context(1 << 14, B.required_levels(bundle) + 1, 2.0 ** 50)
+    res = B.forward_bicrypto(bundle.bi, dec, w, ctx, strategy="bhw")
+    assert res.recorder.snapshot() == meta["counts_bhw"]
+    assert [list(x) for x in res.recorder.layer_table()] == meta["layer_table"]
+    _check(res.decrypt_logits(), d["logits_ref"])
+
+
+def test_cifar3_group_batching_equals_single_sets():
+    d, w, dec, meta = _load("cifar3_cfg4")
+    bundle = B.get("cifar3")
+    ctx = B.make_context(1 << 14, B.required_levels(bundle) + 1, 2.0 ** 50)
+    res = B.forward_bicrypto(bundle.bi, dec[:7], w, ctx, strategy="bhw", group_size=3)   # G = 3, last padded
+    assert res.logits_ct.batch == 3
+    assert res.recorder.snapshot() == meta["counts_bhw"]   # one op set, independent of G
+    logits = res.decrypt_logits()
+    assert logits.shape == (7, 10)
+    _check(logits, d["logits_ref"][:7])
