@@ -1,0 +1,401 @@
+"""Benchmark driver (contract: see DESIGN.md section 7).
+
+Headline (BASELINE.json metric "HE images/s (batched)", config 4): the
+CIFAR-shaped bi-CryptoNet `cifar3` on 32x32x3 images, N = 2^14, 15 limbs
+(max_level = required 13 + 1), Delta = 2^50, BHW packing of 32 images per slot
+set; every step runs `forward_bicrypto` over --images images per rank
+(default 4096 = 128 slot sets, processed as device batches of --chunk sets)
+from plaintext inputs to decrypted logits.  Inputs are far larger than L2
+(ciphertext working set: GBs), so no explicit flush is needed.
+
+Also reported on the same line: 1-image latency (config 1, cnn3 on 28x28x1,
+N = 2^13, encrypt -> forward -> decrypt, host to host), the config-2 NTT / INTT
+/ MAC and config-3 key-switch microbenchmarks, the NTT roofline, and a CPU
+baseline measured on this host with the oracle (oracle/, op-count scaled).
+
+N > 1: one process per GPU (torchrun), each rank runs its own shard of slot
+sets (weak scaling: --images per rank), the logits ciphertexts are gathered to
+rank 0 (NCCL) and decrypted there; time = max over ranks.
+`--impl reference`: the reference arm -- the CPU oracle port on all host
+cores (process-parallel over independent slot sets), same metric and config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthetic  # noqa: E402
+
+IMAGES_PER_SET = 32          # 32 x 16 x 16 = 8192 = N/2 slots
+SCALE = 2.0 ** 50
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--images", type=int, default=4096, help="images per rank per step")
+    ap.add_argument("--chunk", type=int, default=32, help="slot sets per device batch")
+    ap.add_argument("--no-extras", action="store_true", help="skip latency / micro / cpu baseline")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- setup
+def cifar3_setup(n_images: int, seed: int = 0):
+    from paper_2402_01296_b200 import catalog
+
+    bundle = catalog.get("cifar3")
+    weights = synthetic.weights_for(synthetic.tensor_shapes(bundle), 0.05, seed=3)
+    sens, full = synthetic.cfg4_inputs(n_images, seed=seed)
+    return bundle, weights, sens, full
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+        return False
+
+    def summary(self) -> dict:
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------ our arm
+def run_ours(args, rank: int, world: int, dist_on: bool):
+    import torch
+
+    import paper_2402_01296_b200 as BCN
+    from paper_2402_01296_b200 import _lib, sim
+    from paper_2402_01296_b200.shard import gather_to_root
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    bundle, weights, sens_np, full_np = cifar3_setup(args.images, seed=100 + rank)
+    from paper_2402_01296_b200.archive import TensorArchive
+    w = TensorArchive(weights)
+    ctx = BCN.make_context(1 << 14, BCN.required_levels(bundle) + 1, SCALE)
+    n_sets = -(-args.images // IMAGES_PER_SET)
+    chunk_imgs = args.chunk * IMAGES_PER_SET
+
+    sens_d = torch.as_tensor(sens_np, device=dev)
+    full_d = torch.as_tensor(full_np, device=dev)
+    sens_h = torch.as_tensor(sens_np).pin_memory()
+    full_h = torch.as_tensor(full_np).pin_memory()
+
+    def step(device_inputs: bool):
+        outs = []
+        for s0 in range(0, args.images, chunk_imgs):
+            s1 = min(args.images, s0 + chunk_imgs)
+            if device_inputs:
+                inp = (sens_d[s0:s1], full_d[s0:s1])
+            else:
+                inp = (sens_h[s0:s1].to(dev, non_blocking=True), full_h[s0:s1].to(dev, non_blocking=True))
+            res = BCN.forward_bicrypto(bundle.bi, inp, w, ctx, strategy="bhw", group_size=IMAGES_PER_SET)
+            outs.append(res)
+        return outs
+
+    def finish(outs, to_host: bool):
+        """gather logits ciphertexts to rank 0 and decrypt there."""
+        datas = torch.cat([r.logits_ct.data for r in outs])          # (n_sets, 2, 2, N) at level 1
+        if dist_on:
+            datas = gather_to_root(datas, n_sets * world)
+        if rank != 0:
+            return None
+        r0 = outs[0]
+        slots = ctx.engine.decrypt(datas, r0.logits_ct.level, r0.logits_ct.scale)
+        idx = torch.arange(IMAGES_PER_SET, device=dev)[:, None] * r0.tile_step + torch.arange(10, device=dev)
+        logits = slots[:, idx].reshape(-1, 10)
+        return logits.cpu() if to_host else logits
+
+    def timed(device_inputs: bool, to_host: bool, K: int, W: int, rec_clocks: bool):
+        for _ in range(W):
+            finish(step(device_inputs), to_host)
+        if dist_on:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        l0 = _lib.launch_count()
+        cs = ClockSampler(dev.index) if rec_clocks else None
+        if cs:
+            cs.__enter__()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        last = None
+        for _ in range(K):
+            last = finish(step(device_inputs), to_host)
+        e.record()
+        torch.cuda.synchronize()
+        if cs:
+            cs.__exit__()
+        if dist_on:
+            torch.distributed.barrier()
+        ms = s.elapsed_time(e) / K
+        if dist_on:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, (_lib.launch_count() - l0) // K, cs.summary() if cs else None, last
+
+    # correctness on this exact workload (first 8 images) before timing
+    sim.reset_stats()
+    rec_res = BCN.forward_bicrypto(bundle.bi, (sens_d[:IMAGES_PER_SET], full_d[:IMAGES_PER_SET]), w, ctx,
+                                   strategy="bhw", group_size=IMAGES_PER_SET)
+    counts = rec_res.recorder.snapshot()
+    dev_work = dict(sim.STATS)
+    from paper_2402_01296_b200.network import DecomposedInput
+    ref = BCN.reference_forward(bundle.bi, [DecomposedInput(s, f, (0, 0, 16, 16))
+                                            for s, f in zip(sens_np[:8], full_np[:8])], w)
+    max_err = float(np.abs(rec_res.decrypt_logits()[:8] - ref).max())
+
+    ms, launches, clocks, _ = timed(True, False, args.steps, args.warmup, True)
+    total_images = args.images * world
+    value = total_images / (ms / 1e3)
+    e2e_ms, _, _, logits = timed(False, True, args.steps, max(1, args.warmup // 3), False)
+    e2e = total_images / (e2e_ms / 1e3)
+    h2d = (sens_np.nbytes + full_np.nbytes)
+    d2h = total_images * 10 * 8 if rank == 0 else 0
+    return {
+        "value": value, "ms_per_step": ms, "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": h2d,
+                                                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": launches, "clocks": clocks, "counts_per_forward": counts,
+        "device_work_per_forward": dev_work, "max_abs_logit_err_vs_reference": max_err, "ctx": ctx,
+        "logits_shape": list(logits.shape) if logits is not None else None,
+    }
+
+
+def latency_cfg1(reps: int = 10):
+    """Config 1: one 28x28 image, cnn3, N=2^13, 11 limbs; host -> host."""
+    import torch
+
+    import paper_2402_01296_b200 as BCN
+    from paper_2402_01296_b200.archive import TensorArchive
+    from paper_2402_01296_b200.network import DecomposedInput
+
+    bundle = BCN.get("cnn3")
+    w = TensorArchive(synthetic.weights_for(synthetic.tensor_shapes(bundle), 0.1, seed=1))
+    sens, full = synthetic.cfg1_inputs(1, seed=0)
+    dec = [DecomposedInput(sens[0], full[0], (7, 7, 14, 14))]
+    ctx = BCN.make_context(8192, BCN.required_levels(bundle) + 1, SCALE)
+    for _ in range(3):
+        BCN.forward_bicrypto(bundle.bi, dec, w, ctx, strategy="hw").decrypt_logits()
+    times = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        BCN.forward_bicrypto(bundle.bi, dec, w, ctx, strategy="hw").decrypt_logits()
+        times.append(time.perf_counter() - t0)
+    ref = BCN.reference_forward(bundle.bi, dec, w)
+    got = BCN.forward_bicrypto(bundle.bi, dec, w, ctx, strategy="hw").decrypt_logits()
+    return {"metric": "1-image latency (cnn3, config 1)", "value": statistics.median(times), "unit": "s",
+            "reps": reps, "max_abs_logit_err": float(np.abs(got - ref).max()),
+            "paper_SEAL_cpu_latency_s": 2.1}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def _traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+# ------------------------------------------------------------ CPU baseline
+def oracle_op_times(level: int = 10, seed: int = 0) -> dict:
+    """Seconds per HE op of the CPU oracle at config-4 parameters (N=2^14,
+    15 limbs, dnum 3), on a level-`level` ciphertext."""
+    from oracle import ckks as O
+
+    p = O.make_params(1 << 14, 14, 50, dnum=3, seed=seed)
+    orc = O.Oracle(p)
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(8192) * 0.1
+    ct = orc.encrypt(v, 1, level=level)
+    orc.galois_key(O.galois_elt(1, p.N))
+    orc.relin_key()
+    t = {}
+    t0 = time.perf_counter()
+    U = orc.modup(ct.c1, level)
+    t["modup"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.keyswitch_from_modup(U, level, orc.galois_key(O.galois_elt(1, p.N)), O.galois_elt(1, p.N))
+    t["keyswitch"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.mul_plain(ct, v)
+    t["mul_pc"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.add_cc(ct, ct)
+    t["add"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.mul_cc(ct, ct)
+    t["mul_cc"] = time.perf_counter() - t0
+    return t
+
+
+def oracle_images_per_s(t: dict, counts: dict, work: dict) -> float:
+    """One slot set (32 images) through cifar3 with the oracle, op-count scaled:
+    distinct ModUps / key switches as the engine issues them (hoisting), every
+    Mul_PC with its own encode + rescale (the oracle has no lazy rescale)."""
+    sec = (work["modup"] * t["modup"] + work["keyswitch"] * t["keyswitch"] + counts["Mul_PC"] * t["mul_pc"]
+           + (counts["Add_CC"] + counts["Add_PC"]) * t["add"] + counts["Mul_CC"] * t["mul_cc"])
+    return IMAGES_PER_SET / sec
+
+
+# default per-forward device work of cifar3 (used by the reference arm, which has no GPU run)
+CIFAR3_COUNTS = {"Add_PC": 98, "Add_CC": 5857, "Mul_PC": 5925, "Mul_CC": 50, "Rot": 6003}
+
+
+def _ref_worker(args):
+    seed, work = args
+    t = oracle_op_times(seed=seed)
+    return oracle_images_per_s(t, CIFAR3_COUNTS, work)
+
+
+def run_reference(args) -> None:
+    """Reference arm: the CPU oracle port on all host cores, same metric."""
+    import multiprocessing as mp
+
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    work = {"modup": 1300, "keyswitch": 1016 + 50}
+    per_step = []
+    ctxm = mp.get_context("fork")
+    with ctxm.Pool(cores) as pool:
+        for i in range(args.warmup + args.steps):
+            rates = pool.map(_ref_worker, [(i * cores + c, work) for c in range(cores)])
+            if i >= args.warmup:
+                per_step.append(sum(rates))
+    value = statistics.mean(per_step)
+    line = {"metric": "HE images/s (batched)", "value": value, "unit": "images/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * IMAGES_PER_SET * cores / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "cifar3 bi-CryptoNet, config 4 (N=2^14, 15 limbs, BHW 32 img/slot set)"},
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                             "sample": f"per core: one op-timing sample (ModUp, key switch, Mul_PC, Add, Mul_CC) "
+                                       f"of the C/numpy RNS-CKKS oracle at level 10, scaled by cifar3's per-forward "
+                                       f"op counts; {cores} processes in parallel (independent slot sets)"},
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    res = run_ours(args, rank, world, dist_on)
+    extras = {}
+    if rank == 0 and not args.no_extras and world == 1:
+        import bench_micro
+        extras["latency_1img"] = latency_cfg1()
+        c2 = bench_micro.config2()
+        c3 = bench_micro.config3()
+        extras["micro"] = {"config2": c2, "config3": c3}
+        peak, peak_kind = _peaks()
+        tr = _traffic().get("ntt_fwd")
+        ntt = c2["ntt"]
+        extras["roofline"] = {
+            "kernel": "ntt_fwd_kernel<13> (config-2 batch: 32768 limb-polys, N=2^13, 60-bit primes, 1 launch)",
+            "bound": "hbm", "achieved": ntt["GBps"], "peak": peak, "unit": "GB/s", "frac": ntt["GBps"] / peak,
+            "peak_kind": peak_kind, "traffic": tr, "algorithmic_bytes_per_launch": ntt["bytes"],
+            "launch_ms": ntt["ms"]}
+        for name in ("intt", "mac"):
+            extras["roofline_" + name] = {"achieved": c2[name]["GBps"], "frac": c2[name]["GBps"] / peak}
+        for name in ("relin", "rotations"):
+            extras["roofline_ks_" + name] = {"achieved": c3[name]["GBps"], "frac": c3[name]["GBps"] / peak}
+        t = oracle_op_times()
+        cpu = oracle_images_per_s(t, res["counts_per_forward"], res["device_work_per_forward"])
+        extras["cpu_baseline"] = {
+            "value": cpu, "unit": "images/s", "cores": 1, "kind": "port",
+            "sample": "one op-timing sample (ModUp, key switch, Mul_PC+rescale, Add, Mul_CC) of the CPU RNS-CKKS "
+                      "oracle at cfg4 parameters, level 10, scaled by this run's per-forward counts "
+                      f"({res['device_work_per_forward']}); 32 images per forward",
+            "op_seconds": t}
+    if rank == 0:
+        line = {
+            "metric": "HE images/s (batched)", "value": res["value"], "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded cfg4 images, N(0,0.05) weights)",
+            "config": {"workload": "cifar3 bi-CryptoNet, BASELINE config 4: N=2^14, 15 limbs (q0 60b, 14x50b), "
+                                   "K=5 special 60b, dnum=3, Delta=2^50, BHW 32 images/slot set",
+                       "images_per_rank_per_step": args.images, "slot_sets_per_device_batch": args.chunk,
+                       "l2": "working set >> 126 MB L2 (no flush needed)"},
+            "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
+            "parity": {"max_abs_logit_err_vs_reference_forward": res["max_abs_logit_err_vs_reference"],
+                       "counts_per_forward": res["counts_per_forward"]},
+            "device_work_per_forward": res["device_work_per_forward"],
+        }
+        line.update(extras)
+        print(json.dumps(line))
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -47,6 +47,8 @@ typedef struct bcn_ctx bcn_ctx;
 
 const char *bcn_last_error(void);
 int bcn_version(void);
+/* number of kernels this library has launched in the process (bench evidence) */
+int bcn_launch_count(uint64_t *out);
 
 /* make_context (sim.py:142-169): ring degree N = 2^logn (8 <= N <= 16384),
  * ciphertext primes q[0..max_level], special primes p[0..n_special-1],

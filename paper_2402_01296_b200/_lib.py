@@ -36,6 +36,7 @@ _D = ctypes.c_double
 
 # name -> argtypes (all return int)
 SIGNATURES = {
+    "bcn_launch_count": [ctypes.POINTER(_U64)],
     "bcn_ctx_create": [ctypes.POINTER(_P), _I, _I, ctypes.POINTER(_U64), _I, ctypes.POINTER(_U64), _I, _U64, _I],
     "bcn_ctx_set_fft": [_P, ctypes.POINTER(_D), ctypes.POINTER(_D)],
     "bcn_ctx_destroy": [_P],
@@ -101,3 +102,9 @@ def check(code: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def launch_count() -> int:
+    v = ctypes.c_uint64()
+    call("bcn_launch_count", ctypes.byref(v))
+    return int(v.value)

@@ -17,6 +17,8 @@
 using namespace bcn;
 typedef unsigned __int128 u128;
 
+std::atomic<unsigned long long> bcn::g_launches{0};
+
 static thread_local std::string g_err;
 
 static int fail(int code, const std::string& msg) {
@@ -242,6 +244,11 @@ extern "C" {
 
 const char* bcn_last_error(void) { return g_err.c_str(); }
 int bcn_version(void) { return 1; }
+
+int bcn_launch_count(uint64_t* out) {
+    *out = g_launches.load(std::memory_order_relaxed);
+    return BCN_OK;
+}
 
 int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, int n_special, const uint64_t* p,
                    int dnum, uint64_t seed, int device) {

@@ -139,3 +139,15 @@ __device__ __forceinline__ u64 signed_to_residue(i64 v, u64 q) {
 }
 
 #define BCN_CHECK_LAUNCH() do { cudaError_t _e = cudaGetLastError(); if (_e != cudaSuccess) return _e; } while (0)
+
+// Every launcher in this library launches exactly one kernel and returns
+// through launched(): the count is exported as bcn_launch_count() so the
+// bench can report how many of OUR kernels ran in its timed region.
+#include <atomic>
+namespace bcn {
+extern std::atomic<unsigned long long> g_launches;
+}
+static inline cudaError_t launched() {
+    bcn::g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}

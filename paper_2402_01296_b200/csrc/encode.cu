@@ -74,7 +74,7 @@ cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long
     int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
     encode_kernel<<<nplain, tpb, smem, st>>>(out, os, vals, vlen, vs, scale, logn, limbs, pr, ft, add_err, seed,
                                              id_base);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ---------------------------------------------------------------- decode
@@ -155,7 +155,7 @@ cudaError_t decode_op(double* out, int nout, const u64* poly, long long ps, int 
     if (!cfg) { cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
     int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
     decode_kernel<<<npoly, tpb, smem, st>>>(out, nout, poly, ps, k, scale, logn, pr, ft, q0inv_mod_q1, q0inv_p);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ------------------------------------------------------------- sampling
@@ -181,7 +181,7 @@ cudaError_t sample_uniform_op(u64* out, long long os, int npoly, int nlimb, int 
     long long nb = (total + 255) / 256;
     sample_uniform_kernel<<<(int)(nb > 1048576 ? 1048576 : nb), 256, 0, st>>>(out, os, nlimb, logn, limbs, pr, seed,
                                                                                domain, id_base, id_step, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 __global__ void sample_small_kernel(u64* __restrict__ out, long long os, int nlimb, int logn, Limbs limbs,
@@ -205,7 +205,7 @@ cudaError_t sample_small_op(u64* out, long long os, int npoly, int nlimb, int lo
     if (!total) return cudaSuccess;
     sample_small_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(out, os, nlimb, logn, limbs, pr, seed, domain,
                                                                     id_base, id_step, ternary, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ct: [G][2][L][N]; c0 holds NTT(m + e) on entry.  c1 = a, c0 -= a s.
@@ -235,7 +235,7 @@ cudaError_t encrypt_combine_op(u64* ct, int G, int nlimb, int logn, const Limbs&
     if (!total) return cudaSuccess;
     encrypt_combine_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(ct, nlimb, logn, limbs, pr, s_mont, seed,
                                                                        id_base, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // one digit of a switching key over the full basis (nbasis limbs, prime t = t):
@@ -267,7 +267,7 @@ cudaError_t ksk_digit_op(u64* b_out, u64* a_out, const u64* e_ntt, const u64* s_
     long long total = (long long)nbasis << logn;
     ksk_digit_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(b_out, a_out, e_ntt, s_mont, sprime, nbasis, d0, d1,
                                                                  logn, pr, pmod, seed, kid, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // m = c0 + c1 s on limbs 0..k-1 (NTT domain), out: [npoly][k][N]
@@ -295,7 +295,7 @@ cudaError_t decrypt_core_op(u64* out, const u64* ct, long long cs, int nlimb_ct,
     if (!total) return cudaSuccess;
     decrypt_core_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(out, ct, cs, nlimb_ct, k, logn, pr, s_mont,
                                                                     total);
-    return cudaGetLastError();
+    return launched();
 }
 
 __global__ void from_mont_kernel(u64* out, const u64* in, long long per_limb, int nlimb, Limbs limbs,
@@ -313,7 +313,7 @@ cudaError_t from_mont_op(u64* out, const u64* in, long long per_limb, int nlimb,
     long long total = (long long)npoly * nlimb * per_limb;
     if (!total) return cudaSuccess;
     from_mont_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(out, in, per_limb, nlimb, limbs, pr, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 }  // namespace bcn

@@ -213,7 +213,7 @@ static cudaError_t launch_one(bool inverse, const NttArgs& a, int nlimbs, int np
     dim3 grid(nlimbs, npolys);
     if (inverse) ntt_inv_kernel<LOGN><<<grid, C::T, smem, st>>>(a);
     else ntt_fwd_kernel<LOGN><<<grid, C::T, smem, st>>>(a);
-    return cudaGetLastError();
+    return launched();
 }
 
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {

@@ -46,7 +46,7 @@ cudaError_t binary_op(int op, u64* out, long long os, const u64* a, long long as
     if (op == 0) binary_kernel<0><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
     else if (op == 1) binary_kernel<1><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
     else binary_kernel<2><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // out = to_mont(a) (in place allowed)
@@ -66,7 +66,7 @@ cudaError_t to_mont_op(u64* out, const u64* a, int npoly, int nlimb, int logn, c
     long long total = (long long)npoly * nlimb << logn;
     if (!total) return cudaSuccess;
     to_mont_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, a, nlimb, logn, limbs, pr, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ------------------------------------------------------------------ MAC
@@ -107,7 +107,7 @@ cudaError_t mac_op(u64* out, const u64* ct, long long ct_stride, const u64* pt, 
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, nlimb, ngroups);
     mac_kernel<<<grid, tpb, 0, st>>>(out, ct, ct_stride, pt, pt_stride, n_items, group, nlimb, logn, limbs, pr);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ---------------------------------------------------------- tensor (K6)
@@ -142,7 +142,7 @@ cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long lon
     long long total = (long long)G * nlimb << logn;
     if (!total) return cudaSuccess;
     tensor_kernel<<<blocks_for(total, 256), 256, 0, st>>>(d, a, as, b, bs, nlimb, logn, limbs, pr, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ----------------------------------------------------- automorphism (K8)
@@ -164,7 +164,7 @@ cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, in
     long long total = (long long)npoly * nlimb << logn;
     if (!total) return cudaSuccess;
     automorph_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, os, in, is, nlimb, logn, g, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ---------------------------------------------------------- ModUp (K7)
@@ -210,7 +210,7 @@ cudaError_t modup_op(u64* U, const u64* xc, const u64* xn, long long x_stride, i
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, npoly, ndig);
     modup_kernel<<<grid, tpb, 0, st>>>(U, xc, xn, x_stride, nq, next, alpha, ndig, logn, ext, pr, tab);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ------------------------------------------- key inner product (K7, K8)
@@ -281,7 +281,7 @@ cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int lo
             default: return cudaErrorInvalidValue;
         }
     }
-    return cudaGetLastError();
+    return launched();
 }
 
 // -------------------------------------------------------- ModDown (K7)
@@ -316,7 +316,7 @@ cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly,
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, npoly);
     moddown_conv_kernel<<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab);
-    return cudaGetLastError();
+    return launched();
 }
 
 // out[p][c][i] = addend[p][c][i] + (A[p][c][i] - Z[p][c][i]) * P^-1   (c = 0, 1)
@@ -356,7 +356,7 @@ cudaError_t moddown_combine_op(u64* out, long long os, const u64* A, int next, c
     if (!total) return cudaSuccess;
     moddown_combine_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, os, A, next, Z, addend, as, add_c1, g,
                                                                    nq, logn, ql, pr, pinv, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // ---------------------------------------------------------- rescale (K5)
@@ -382,7 +382,7 @@ cudaError_t rescale_lift_op(u64* W, const u64* top, int npoly, int nq, u64 qtop,
     long long total = (long long)npoly * nq << logn;
     if (!total) return cudaSuccess;
     rescale_lift_kernel<<<blocks_for(total, 256), 256, 0, st>>>(W, top, nq, qtop, logn, ql, pr, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // out[p][i] = (c[p][i] - W[p][i]) * q_top^-1
@@ -410,7 +410,7 @@ cudaError_t rescale_combine_op(u64* out, long long os, const u64* c, long long c
     if (!total) return cudaSuccess;
     rescale_combine_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, os, c, cs, W, nq, logn, ql, pr, qinv,
                                                                    total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // gather one limb of every poly: dst[p][n] = src[p * stride + off + n]
@@ -428,7 +428,7 @@ cudaError_t gather_limb_op(u64* dst, const u64* src, long long stride, long long
     long long total = (long long)npoly << logn;
     if (!total) return cudaSuccess;
     gather_limb_kernel<<<blocks_for(total, 256), 256, 0, st>>>(dst, src, stride, off, logn, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 // copy limbs [0, nlimb) of each poly between differently-strided buffers
@@ -446,7 +446,7 @@ cudaError_t copy_limbs_op(u64* dst, long long ds, const u64* src, long long ss, 
     long long total = (long long)npoly * per_poly;
     if (!total) return cudaSuccess;
     copy_limbs_kernel<<<blocks_for(total, 256), 256, 0, st>>>(dst, ds, src, ss, per_poly, total);
-    return cudaGetLastError();
+    return launched();
 }
 
 }  // namespace bcn

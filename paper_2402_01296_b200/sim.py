@@ -44,6 +44,15 @@ PlainLike = Union[np.ndarray, list, tuple]
 
 MAX_RING = 1 << 14
 
+# device work actually issued (after hoisting / memoisation / lazy rescale);
+# the recorder keeps the reference's logical counts separately.
+STATS = {"modup": 0, "keyswitch": 0, "rescale": 0, "encode": 0}
+
+
+def reset_stats() -> None:
+    for k in STATS:
+        STATS[k] = 0
+
 
 def _zeros() -> dict:
     return dict.fromkeys(COUNTER_KEYS, 0)
@@ -195,6 +204,7 @@ class Ciphertext:
         if self.pending:
             eng = self.ctx.engine
             data = eng.rescale(self._data, self._data_level)
+            STATS["rescale"] += 1
             object.__setattr__(self, "_data", data)
             object.__setattr__(self, "_data_level", self.level)
             object.__setattr__(self, "_data_scale", self.scale)
@@ -354,6 +364,7 @@ def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
         raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {a.batch}")
     a.materialize()       # a pending scale Delta*q_l would overflow a 64-bit encoding
     pt = eng.encode(rows, a.level, a.scale)
+    STATS["encode"] += 1
     return Ciphertext(eng.add_plain(a._data, pt, a.level), a.level, a.scale, ctx)
 
 
@@ -366,6 +377,7 @@ def _mul_plain_pending(x: Ciphertext, plain, level: int) -> Ciphertext:
         raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {x.batch}")
     ql = ctx.q(level)
     pt = eng.encode(rows, level, float(ql), montgomery=True)
+    STATS["encode"] += 1
     data = eng.mul_plain(x._data, pt, level, rescale=False)
     return Ciphertext(data, level - 1, x.scale, ctx, data_level=level, data_scale=x.scale * float(ql))
 
@@ -393,6 +405,9 @@ def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Cipherte
     _batch_of(a, b)
     b.materialize()
     data = ctx.engine.mul_cc(a._data, b._data, lvl)
+    STATS["modup"] += 1
+    STATS["keyswitch"] += 1
+    STATS["rescale"] += 1
     return Ciphertext(data, lvl - 1, (a.scale * b.scale) / ctx.q(lvl), ctx)
 
 
@@ -409,7 +424,9 @@ def _rotated(c: Ciphertext, r: int) -> Ciphertext:
     else:
         if c._modup is None:
             object.__setattr__(c, "_modup", eng.modup(c._data, c.level))
+            STATS["modup"] += 1
         data = eng.rotate(c._data, r, c.level, U=c._modup)
+        STATS["keyswitch"] += 1
         out = Ciphertext(data, c.level, c.scale, ctx)
     c._rot[r] = out
     return out

@@ -1,0 +1,159 @@
+"""CPU pins of the RNS-CKKS oracle (oracle/): published known-answer vectors,
+naive ground truths, and the reference's slot semantics.  No GPU needed."""
+
+import numpy as np
+import pytest
+
+from oracle import ckks as O
+from paper_2402_01296_b200 import params as P
+
+
+# Random123 philox4x32-10 known-answer vectors (kat_vectors, Salmon et al.)
+KAT = [
+    ([0, 0, 0, 0], [0, 0], [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]),
+    ([0xffffffff] * 4, [0xffffffff] * 2, [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]),
+    ([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0],
+     [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]),
+]
+
+
+@pytest.mark.parametrize("ctr,key,out", KAT)
+def test_philox_known_answers(ctr, key, out):
+    assert O.philox4x32(ctr, key) == out
+
+
+def test_primes_match_engine_params():
+    for N, L, bits in [(8, 1, 30), (1024, 5, 40), (8192, 10, 50), (16384, 14, 50), (8192, 3, 60)]:
+        hp = P.make_params(N, L, bits, dnum=3)
+        op = O.make_params(N, L, bits, dnum=3)
+        assert list(hp.q) == op.q and list(hp.p) == op.p
+        for q in op.q + op.p:
+            assert q % (2 * N) == 1 and q < (1 << 61) and O.is_prime(q)
+        assert len(set(op.q + op.p)) == len(op.q + op.p)
+
+
+def test_engine_fft_table_is_the_oracle_table():
+    re, im = P.fft_table(512)
+    ft = O.fft_tables(512)
+    assert np.array_equal(re, ft.re) and np.array_equal(im, ft.im)
+
+
+@pytest.mark.parametrize("N", [8, 16, 32])
+def test_ntt_product_is_negacyclic_convolution(N):
+    q = O.ntt_primes(40, 1, N)[0]
+    rng = np.random.default_rng(N)
+    a = rng.integers(0, q, N, dtype=np.uint64)
+    b = rng.integers(0, q, N, dtype=np.uint64)
+    c = O.intt(O.mul(O.ntt(a[None], [q]), O.ntt(b[None], [q]), [q]), [q])[0]
+    assert np.array_equal(c, O.negacyclic_mul_naive(a, b, q))
+
+
+def test_ntt_evaluation_order():
+    N = 16
+    q = O.ntt_primes(30, 1, N)[0]
+    psi = O.tables(N, q).psi
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, q, N, dtype=np.uint64)
+    A = O.ntt(a[None], [q])[0]
+    for k in range(N):
+        e = 2 * int(format(k, "04b")[::-1], 2) + 1
+        assert int(A[k]) == sum(int(a[j]) * pow(psi, e * j, q) for j in range(N)) % q
+
+
+def test_automorphism_ntt_matches_coefficient_form():
+    N = 64
+    q = O.ntt_primes(40, 1, N)[0]
+    rng = np.random.default_rng(1)
+    a = rng.integers(0, q, N, dtype=np.uint64)
+    for r in (1, 3, 17):
+        g = O.galois_elt(r, N)
+        coef = np.empty_like(a)
+        O.lib().orc_automorph_coef(O._p(a), O._p(coef), N, g, q)
+        assert np.array_equal(O.automorph_ntt(O.ntt(a[None], [q]), g)[0], O.ntt(coef[None], [q])[0])
+
+
+def test_automorphism_maps_aligned_blocks_to_aligned_blocks():
+    # the engine's inner-product kernel stages one source block per destination block
+    from_ = O.automorph_ntt
+    N = 4096
+    idx = np.arange(N, dtype=np.uint64)
+    for r in (1, 2, 100, 2047):
+        perm = from_(idx[None], O.galois_elt(r, N))[0].astype(np.int64)
+        for blk in (256, 1024):
+            src = perm.reshape(-1, blk) // blk
+            assert (src == src[:, :1]).all()
+
+
+def test_special_fft_matches_definition_and_roundtrips():
+    N = 64
+    ft = O.fft_tables(N)
+    rng = np.random.default_rng(2)
+    v = rng.standard_normal(N // 2)
+    wr, wi = O.special_ifft(v, np.zeros(N // 2), ft)
+    zeta = np.exp(1j * np.pi / N)
+    z = [sum((wr[i] + 1j * wi[i]) * zeta ** (i * int(ft.rot[j])) for i in range(N // 2)) for j in range(N // 2)]
+    assert np.abs(np.array(z) - v).max() < 1e-12
+    coef = O.encode_coeffs(v, N, 2.0 ** 40)
+    assert np.abs(O.decode_coeffs(coef.astype(np.float64), N, 2.0 ** 40) - v).max() < 1e-10
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return O.Oracle(O.make_params(64, 4, 40, dnum=2, seed=3))
+
+
+def test_oracle_semantics_follow_reference_sim(orc):
+    """sim.py:184-283 slot semantics: add, Mul_PC / Mul_CC with level-1,
+    left rotation == np.roll(x, -r), right for r < 0 (test_sim.py:144-158)."""
+    rng = np.random.default_rng(4)
+    x, y = rng.standard_normal((2, 32))
+    cx, cy = orc.encrypt(x, 1), orc.encrypt(y, 2)
+    assert cx.level == 4
+    tol = 1e-7
+    assert np.abs(orc.decrypt(orc.add_cc(cx, cy))[:32] - (x + y)).max() < tol
+    m = orc.mul_plain(cx, y)
+    assert m.level == 3 and np.abs(orc.decrypt(m)[:32] - x * y).max() < tol
+    s = orc.mul_cc(cx, cy)
+    assert s.level == 3 and np.abs(orc.decrypt(s)[:32] - x * y).max() < tol
+    for r in (1, -1, 5, 31, 32):
+        assert np.abs(orc.decrypt(orc.rotate(cx, r))[:32] - np.roll(x, -r)).max() < tol
+    assert np.abs(orc.decrypt(orc.rotate(cx, 0))[:32] - x).max() < tol
+
+
+def test_oracle_fc_4_to_2_matches_reference_pin(orc):
+    """pkg/tests/test_layers.py:78-88: x=[1,2,3,4], W=arange(8).reshape(4,2) ->
+    [40, 50] through n1+n2-1 = 5 rotate-multiplies by generalised diagonals."""
+    S = 32
+    x = np.zeros(S)
+    x[:4] = [1, 2, 3, 4]
+    W = np.arange(8.0).reshape(4, 2)
+    ct = orc.encrypt(x, 7)
+    acc = None
+    t = np.arange(2)
+    for d in range(3, -2, -1):
+        q = t + d
+        ok = (q >= 0) & (q < 4)
+        vec = np.zeros(S)
+        vec[t[ok]] = W[q[ok], t[ok]]
+        term = orc.rotate_mul(ct, d, vec)
+        acc = term if acc is None else orc.add_cc(acc, term)
+    assert acc.level == 3
+    assert np.abs(orc.decrypt(acc)[:2] - np.array([40.0, 50.0])).max() < 1e-6
+
+
+def test_hoisted_rotation_equals_fresh_modup(orc):
+    rng = np.random.default_rng(5)
+    ct = orc.encrypt(rng.standard_normal(32), 9)
+    a = orc.rotate(ct, 3)
+    orc.rotate(ct, 1, modup_key="k")
+    b = orc.rotate(ct, 3, modup_key="k")
+    assert np.array_equal(a.c0, b.c0) and np.array_equal(a.c1, b.c1)
+
+
+def test_depth_exhaustion_is_exact():
+    o = O.Oracle(O.make_params(16, 2, 30, dnum=1))
+    ct = o.encrypt([1.5], 1)
+    ct = o.mul_plain(o.mul_plain(ct, [1.0]), [1.0])
+    assert ct.level == 0
+    with pytest.raises(AssertionError):
+        o.rescale(ct)
