@@ -104,6 +104,14 @@ int bcn_mul_plain(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb,
 /* product without rescale (lazy-rescale accumulation), out at level */
 int bcn_mul_plain_norescale(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb,
                             const uint64_t *pt_mont, int pt_batch, int G, int level, void *stream);
+/* K4 fused linear combination -- the conv-tap / FC-diagonal sum of
+ * conv_accumulate (layers.py:146-163) and fc_forward_multi (layers.py:275-314):
+ * out = sum_t ct_t (x) pt_t over n_terms (cts / pts: HOST arrays of DEVICE
+ * pointers; ct_t u64[G][2][level+1][N], pt_t Montgomery u64[G or 1][level+1][N]
+ * per pt_batched[t]); rescale != 0 -> out u64[G][2][level][N] at level-1,
+ * else out u64[G][2][level+1][N] unrescaled. */
+int bcn_mac_terms(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts, const uint64_t *const *pts,
+                  const int *pt_batched, int G, int level, int rescale, void *stream);
 /* K4 microbenchmark form: out[g] = sum_{t in [g*group, min((g+1)*group, n_items))} ct[t] (x) pt[t] */
 int bcn_mac(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, const uint64_t *pt_mont, int n_items, int group,
             int nlimb, void *stream);

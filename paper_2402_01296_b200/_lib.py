@@ -53,6 +53,7 @@ SIGNATURES = {
     "bcn_mul_plain": [_P, _P, _P, _I, _P, _I, _I, _I, _P],
     "bcn_mul_plain_norescale": [_P, _P, _P, _I, _P, _I, _I, _I, _P],
     "bcn_mac": [_P, _P, _P, _P, _I, _I, _I, _P],
+    "bcn_mac_terms": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _I, _P],
     "bcn_rescale": [_P, _P, _P, _I, _I, _I, _P],
     "bcn_mul_cc": [_P, _P, _P, _I, _P, _I, _I, _I, _I, _P],
     "bcn_modup_words": [_P, _I, _I, ctypes.POINTER(_U64)],

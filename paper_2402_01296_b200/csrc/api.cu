@@ -571,6 +571,49 @@ int bcn_mul_plain_norescale(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int c
                           (cudaStream_t)stream);
 }
 
+int bcn_mac_terms(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* cts, const uint64_t* const* pts,
+                  const int* pt_batched, int G, int level, int rescale, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (n_terms < 1) return fail(BCN_ERR_PARAM, "no terms");
+    if (rescale && level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nl = level + 1;
+    const long long N = c->N;
+    Limbs l = limbs_range(0, nl);
+    u64* acc = (u64*)out;
+    int err = 0;
+    if (rescale) {
+        acc = scratch_get(c, (size_t)G * 2 * nl * N + (size_t)2 * G * N * (1 + level), &err);
+        if (!acc) return err;
+    }
+    MacTerms T;
+    for (int t0 = 0; t0 < n_terms; t0 += BCN_MAC_TERMS) {
+        T.n = std::min(BCN_MAC_TERMS, n_terms - t0);
+        for (int k = 0; k < T.n; k++) {
+            T.ct[k] = (const u64*)cts[t0 + k];
+            T.pt[k] = (const u64*)pts[t0 + k];
+            T.pt_batched[k] = (unsigned char)(pt_batched[t0 + k] != 0);
+        }
+        CUDA_TRY(mac_terms_op(acc, T, G, nl, c->logn, l, c->pr, t0 > 0, st));
+    }
+    if (!rescale) return BCN_OK;
+    LevelTables* LT;
+    e = build_level(c, level, &LT);
+    if (e) return e;
+    const int npoly = 2 * G;
+    u64* top = acc + (size_t)G * 2 * nl * N;
+    u64* W = top + (size_t)npoly * N;
+    CUDA_TRY(gather_limb_op(top, acc, nl * N, (long long)level * N, npoly, c->logn, st));
+    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
+    Limbs ql = limbs_range(0, level);
+    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
+    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
+    CUDA_TRY(rescale_combine_op((u64*)out, (long long)level * N, acc, nl * N, W, npoly, level, c->logn, ql, c->pr,
+                                LT->qlinv, st));
+    return BCN_OK;
+}
+
 int bcn_mac(bcn_ctx* c, uint64_t* out, const uint64_t* ct, const uint64_t* pt_mont, int n_items, int group,
             int nlimb, void* stream) {
     if (nlimb < 1 || nlimb > c->nbasis || group < 1) return fail(BCN_ERR_PARAM, "bad MAC shape");

@@ -110,6 +110,52 @@ cudaError_t mac_op(u64* out, const u64* ct, long long ct_stride, const u64* pt, 
     return launched();
 }
 
+// ------------------------------------------- linear combination MAC (K4)
+// out[g][c] (+)= REDC( sum_t ct_t[g][c] * pt_t[g|0] ): the conv-tap / FC-
+// diagonal sum of the ciphertext branch in one pass -- every rotated input
+// and plaintext read once, u128 lazy accumulation, one REDC per word.
+__global__ void __launch_bounds__(256) mac_terms_kernel(u64* __restrict__ out, const MacTerms terms, int nlimb,
+                                                        int logn, Limbs limbs, const PrimeInfo* __restrict__ pr,
+                                                        int accumulate, long long total) {
+    const int N = 1 << logn;
+    const long long LN = (long long)nlimb << logn;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long g = idx / LN;
+        const long long off = idx - g * LN;
+        const int t = (int)(off >> logn);
+        const PrimeInfo& P = pr[limbs.prime[t]];
+        const u64 q = P.q;
+        Acc128 a0, a1;
+        a0.zero(); a1.zero();
+        const long long cbase = g * 2 * LN + off;
+        const long long pbase = g * LN + off;
+        for (int k = 0; k < terms.n; k++) {
+            const u64 p = __ldg(terms.pt[k] + (terms.pt_batched[k] ? pbase : off));
+            const u64* c = terms.ct[k] + cbase;
+            a0.mac(__ldg(c), p, q);
+            a1.mac(__ldg(c + LN), p, q);
+        }
+        u64 r0 = a0.reduce(q, P.qinv_neg), r1 = a1.reduce(q, P.qinv_neg);
+        u64* o = out + cbase;
+        if (accumulate) {
+            r0 = add_mod(r0, o[0], q);
+            r1 = add_mod(r1, o[LN], q);
+        }
+        o[0] = r0;
+        o[LN] = r1;
+        (void)N;
+    }
+}
+
+cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
+                         const PrimeInfo* pr, int accumulate, cudaStream_t st) {
+    long long total = (long long)G * nlimb << logn;
+    if (!total || terms.n <= 0) return cudaSuccess;
+    mac_terms_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, terms, nlimb, logn, limbs, pr, accumulate, total);
+    return launched();
+}
+
 // ---------------------------------------------------------- tensor (K6)
 // d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 for G ciphertext pairs.
 // a, b: [G][2][L][N] with strides; d: [G][3][L][N]

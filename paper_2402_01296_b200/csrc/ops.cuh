@@ -38,6 +38,17 @@ cudaError_t to_mont_op(u64* out, const u64* a, int npoly, int nlimb, int logn, c
 cudaError_t mac_op(u64* out, const u64* ct, long long ct_stride, const u64* pt, long long pt_stride,
                    int n_items, int group, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr,
                    cudaStream_t st);
+// Linear combination sum_t ct_t (x) pt_t of up to BCN_MAC_TERMS terms, each
+// ct_t a u64[G][2][nlimb][N] batch and pt_t a Montgomery u64[G or 1][nlimb][N].
+#define BCN_MAC_TERMS 160
+struct MacTerms {
+    int n;
+    const u64* ct[BCN_MAC_TERMS];
+    const u64* pt[BCN_MAC_TERMS];
+    unsigned char pt_batched[BCN_MAC_TERMS];
+};
+cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
+                         const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,
                       int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st);
 cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, int npoly, int nlimb, int logn,

@@ -56,7 +56,7 @@ class Engine:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and _lib._lib is not None:
+        if h is not None and _lib is not None and getattr(_lib, "_lib", None) is not None:
             try:
                 _lib._lib.bcn_ctx_destroy(h)
             except Exception:
@@ -80,10 +80,11 @@ class Engine:
             t = t[None]
         return t.contiguous()
 
-    def _check_mag(self, vals: torch.Tensor, scale: float) -> None:
-        # the canonical-embedding inverse is a contraction: |coef| <= scale * max|v|
-        if vals.numel():
-            m = float(vals.abs().max())
+    def _check_mag(self, vals, scale: float) -> None:
+        # the canonical-embedding inverse is a contraction: |coef| <= scale * max|v|.
+        # Checked on host data only: a device-side check would cost a sync per encode.
+        if isinstance(vals, np.ndarray) and vals.size:
+            m = float(np.abs(vals).max())
             if not np.isfinite(m):
                 raise ParameterError("plaintext vector must contain only finite values")
             if m * scale >= 2.0 ** 62:
@@ -104,10 +105,10 @@ class Engine:
 
     # ---------------------------------------------------------- K9-K11
     def encode(self, vals, level: int, scale: float, montgomery: bool = False) -> torch.Tensor:
+        self._check_mag(vals, scale)
         v = self._dev_f64(vals)
         if v.shape[1] > self.N // 2:
             raise CapacityError(f"vector of length {v.shape[1]} exceeds {self.N // 2} slots")
-        self._check_mag(v, scale)
         out = torch.empty((v.shape[0], level + 1, self.N), dtype=torch.int64, device=self.device)
         _lib.call("bcn_encode", self._h, _ptr(v), v.shape[1], v.shape[1], v.shape[0], float(scale), level,
                   int(montgomery), _ptr(out), _stream())
@@ -115,12 +116,12 @@ class Engine:
 
     def encrypt(self, vals, level: int | None = None, scale: float | None = None,
                 counter: int | None = None) -> torch.Tensor:
+        level = self.L if level is None else level
+        scale = self.params.scale if scale is None else scale
+        self._check_mag(vals, scale)
         v = self._dev_f64(vals)
         if v.shape[1] > self.N // 2:
             raise CapacityError(f"vector of length {v.shape[1]} exceeds {self.N // 2} slots")
-        level = self.L if level is None else level
-        scale = self.params.scale if scale is None else scale
-        self._check_mag(v, scale)
         G = v.shape[0]
         counter = self.next_counter(G) if counter is None else counter
         ct = self.empty_ct(G, level)
@@ -215,6 +216,18 @@ class Engine:
     def export_secret(self) -> torch.Tensor:
         out = torch.empty((self.nbasis, self.N), dtype=torch.int64, device=self.device)
         _lib.call("bcn_export_secret", self._h, _ptr(out), _stream())
+        return out
+
+    def mac_terms(self, terms, level: int, rescale: bool = True) -> torch.Tensor:
+        """sum_t ct_t (x) pt_t (one fused launch per 160 terms), optionally rescaled.
+        terms: [(ct u64[G,2,>=level+1,N] with exactly level+1 limbs, pt_mont u64[G|1,level+1,N])]."""
+        G = terms[0][0].shape[0]
+        n = len(terms)
+        cts = (ctypes.c_uint64 * n)(*[t[0].data_ptr() for t in terms])
+        pts = (ctypes.c_uint64 * n)(*[t[1].data_ptr() for t in terms])
+        bat = (ctypes.c_int * n)(*[int(t[1].shape[0] != 1) for t in terms])
+        out = self.empty_ct(G, level - 1 if rescale else level)
+        _lib.call("bcn_mac_terms", self._h, _ptr(out), n, cts, pts, bat, G, level, int(rescale), _stream())
         return out
 
     def mac(self, ct: torch.Tensor, pt_mont: torch.Tensor, group: int) -> torch.Tensor:

@@ -22,7 +22,9 @@ Both are deterministic, so results do not depend on call order.
 from __future__ import annotations
 
 import itertools
-from typing import Iterable, Union
+import os
+from collections import OrderedDict
+from typing import Union
 
 import numpy as np
 
@@ -46,7 +48,7 @@ MAX_RING = 1 << 14
 
 # device work actually issued (after hoisting / memoisation / lazy rescale);
 # the recorder keeps the reference's logical counts separately.
-STATS = {"modup": 0, "keyswitch": 0, "rescale": 0, "encode": 0}
+STATS = {"modup": 0, "keyswitch": 0, "rescale": 0, "encode": 0, "encode_hit": 0, "mac_launch": 0}
 
 
 def reset_stats() -> None:
@@ -139,6 +141,9 @@ class HeContext:
         self._device = device
         self._engine = None
         self._ids = itertools.count()
+        self._pt_cache = OrderedDict()
+        self._pt_bytes = 0
+        self.pt_cache_budget = int(float(os.environ.get("BCN_PT_CACHE_GB", "40")) * 2 ** 30)
 
     def __repr__(self):
         return (f"HeContext(poly_degree={self.poly_degree}, slot_count={self.slot_count}, "
@@ -163,27 +168,48 @@ class HeContext:
         return self.he.q[level]
 
 
+class KeyedPlain(np.ndarray):
+    """A plain multiplier / addend that carries a cache key.
+
+    Weight-derived vectors (conv taps, masks, FC diagonals) are identical on
+    every forward; the engine encodes each (key, level, scale) once and keeps
+    the NTT-domain plaintext in HBM (HeContext plaintext cache).  Results of
+    arithmetic on a KeyedPlain are ordinary, un-keyed vectors."""
+
+    def __new__(cls, arr, key):
+        obj = np.asarray(arr, dtype=np.float64).view(cls)
+        obj.bcn_key = key
+        return obj
+
+    def __array_finalize__(self, obj):
+        self.bcn_key = None
+
+
 class Ciphertext:
     """Batch of G RNS-CKKS ciphertexts + logical level / scale / id.
 
     Immutable from the outside (attribute assignment raises, as for the
-    reference's frozen dataclass).  Internally it may hold a pending
-    (unrescaled) product; `_data_level` is then level + 1.
+    reference's frozen dataclass).  Internally it is either materialised
+    (`_data`, exactly level+1 limbs) or a lazy linear combination
+    (`_terms`: (ct data, Montgomery plaintext) pairs at data level
+    level+1): Mul_PC / rotate-multiply results and sums of them stay lazy
+    until something else needs the value, then ONE fused MAC launch plus ONE
+    rescale materialises the whole sum.
     """
 
-    __slots__ = ("level", "scale", "id", "ctx", "batch", "_data", "_data_level", "_data_scale",
+    __slots__ = ("level", "scale", "id", "ctx", "batch", "_data", "_terms", "_data_scale",
                  "_modup", "_rot", "_slots", "__weakref__")
 
-    def __init__(self, data, level: int, scale: float, ctx: HeContext, *, data_level=None, data_scale=None,
+    def __init__(self, data, level: int, scale: float, ctx: HeContext, *, terms=None, data_scale=None,
                  cid: str | None = None):
         s = object.__setattr__
         s(self, "level", level)
         s(self, "scale", float(scale))
         s(self, "id", cid or ctx.fresh_id())
         s(self, "ctx", ctx)
-        s(self, "batch", int(data.shape[0]))
+        s(self, "batch", int((data if data is not None else terms[0][0]).shape[0]))
         s(self, "_data", data)
-        s(self, "_data_level", level if data_level is None else data_level)
+        s(self, "_terms", terms)
         s(self, "_data_scale", float(scale) if data_scale is None else float(data_scale))
         s(self, "_modup", None)
         s(self, "_rot", {})
@@ -197,16 +223,16 @@ class Ciphertext:
 
     @property
     def pending(self) -> bool:
-        return self._data_level != self.level
+        return self._terms is not None
 
     def materialize(self) -> "Ciphertext":
-        """Apply the deferred rescale in place (the logical value is unchanged)."""
-        if self.pending:
-            eng = self.ctx.engine
-            data = eng.rescale(self._data, self._data_level)
+        """Evaluate a lazy sum (fused MAC + one rescale) in place; value unchanged."""
+        if self._terms is not None:
+            data = self.ctx.engine.mac_terms(self._terms, self.level + 1, rescale=True)
             STATS["rescale"] += 1
+            STATS["mac_launch"] += 1
             object.__setattr__(self, "_data", data)
-            object.__setattr__(self, "_data_level", self.level)
+            object.__setattr__(self, "_terms", None)
             object.__setattr__(self, "_data_scale", self.scale)
         return self
 
@@ -342,6 +368,31 @@ def _batch_of(a: Ciphertext, b: Ciphertext) -> None:
         raise UsageError(f"ciphertext batches differ ({a.batch} vs {b.batch})")
 
 
+def _encode(ctx: HeContext, plain, level: int, scale: float, montgomery: bool, batch: int):
+    """Encode a plain vector; keyed (weight-derived) vectors are cached in HBM."""
+    key = getattr(plain, "bcn_key", None)
+    if key is not None:
+        k = (key, level, scale, montgomery)
+        hit = ctx._pt_cache.get(k)
+        if hit is not None:
+            ctx._pt_cache.move_to_end(k)
+            STATS["encode_hit"] += 1
+            return hit
+    rows = _as_plain_rows(plain, ctx)
+    if rows.shape[0] not in (1, batch):
+        raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {batch}")
+    pt = ctx.engine.encode(rows, level, scale, montgomery=montgomery)
+    STATS["encode"] += 1
+    if key is not None:
+        nb = pt.numel() * 8
+        ctx._pt_cache[k] = pt
+        ctx._pt_bytes += nb
+        while ctx._pt_bytes > ctx.pt_cache_budget and len(ctx._pt_cache) > 1:
+            _, old = ctx._pt_cache.popitem(last=False)
+            ctx._pt_bytes -= old.numel() * 8
+    return pt
+
+
 def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
     """Add_CC (level = min) or Add_PC (level kept), sim.py:208-218."""
     ctx = a.ctx
@@ -350,36 +401,27 @@ def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
         rec.bump("Add_CC")
         _batch_of(a, b)
         level = min(a.level, b.level)
-        if a.pending and b.pending and a._data_level == b._data_level:
+        if a.pending and b.pending and a.level == b.level:
             _check_scales(a._data_scale, b._data_scale)
-            data = eng.add(a._data, b._data, a._data_level)
-            return Ciphertext(data, level, a.scale, ctx, data_level=a._data_level, data_scale=a._data_scale)
+            return Ciphertext(None, level, a.scale, ctx, terms=a._terms + b._terms, data_scale=a._data_scale)
         a.materialize()
         b.materialize()
         _check_scales(a.scale, b.scale)
         return Ciphertext(eng.add(a._data, b._data, level), level, a.scale, ctx)
     rec.bump("Add_PC")
-    rows = _as_plain_rows(b, ctx)
-    if rows.shape[0] not in (1, a.batch):
-        raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {a.batch}")
-    a.materialize()       # a pending scale Delta*q_l would overflow a 64-bit encoding
-    pt = eng.encode(rows, a.level, a.scale)
-    STATS["encode"] += 1
+    a.materialize()       # a lazy sum's scale Delta*q_l would overflow a 64-bit encoding
+    pt = _encode(ctx, b, a.level, a.scale, False, a.batch)
     return Ciphertext(eng.add_plain(a._data, pt, a.level), a.level, a.scale, ctx)
 
 
-def _mul_plain_pending(x: Ciphertext, plain, level: int) -> Ciphertext:
-    """x (materialised, at `level`) times an encoded multiplier, rescale deferred."""
+def _times_plain(x: Ciphertext, plain) -> Ciphertext:
+    """x (materialised, at level l) times a multiplier encoded at scale q_l:
+    a one-term lazy sum at logical level l-1 with the scale kept exactly."""
     ctx = x.ctx
-    eng = ctx.engine
-    rows = _as_plain_rows(plain, ctx)
-    if rows.shape[0] not in (1, x.batch):
-        raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {x.batch}")
+    level = x.level
     ql = ctx.q(level)
-    pt = eng.encode(rows, level, float(ql), montgomery=True)
-    STATS["encode"] += 1
-    data = eng.mul_plain(x._data, pt, level, rescale=False)
-    return Ciphertext(data, level - 1, x.scale, ctx, data_level=level, data_scale=x.scale * float(ql))
+    pt = _encode(ctx, plain, level, float(ql), True, x.batch)
+    return Ciphertext(None, level - 1, x.scale, ctx, terms=((x._data, pt),), data_scale=x.scale * float(ql))
 
 
 def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Ciphertext:
@@ -401,7 +443,7 @@ def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Cipherte
             rec.bump("Mul_PC_mask")
     a.materialize()
     if not is_cc:
-        return _mul_plain_pending(a, b, lvl)
+        return _times_plain(a, b)
     _batch_of(a, b)
     b.materialize()
     data = ctx.engine.mul_cc(a._data, b._data, lvl)
@@ -455,4 +497,4 @@ def he_rotate_mul(c: Ciphertext, r: int, plain, rec: OpRecorder, *, mask: bool =
     if mask:
         rec.bump("Mul_PC_mask")
     r = int(r) % c.ctx.slot_count
-    return _mul_plain_pending(_rotated(c, r), plain, c.level)
+    return _times_plain(_rotated(c, r), plain)
