@@ -77,6 +77,11 @@ int bcn_ntt_inv(bcn_ctx *ctx, uint64_t *data, int npoly, int nlimb, int prime0, 
 int bcn_encode(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int nplain, double scale, int level,
                int montgomery, uint64_t *out, void *stream);
 
+/* encode over the extended basis q_0..q_level, p_0..p_{K-1}, Montgomery form:
+ * out u64[nplain][level+1+K][N] (multipliers for bcn_rotsum) */
+int bcn_encode_ext(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int nplain, double scale, int level,
+                   uint64_t *out, void *stream);
+
 /* ---- K10: encrypt_vector (sim.py:184-189), secret-key RLWE.
  * ct_out: u64[G][2][level+1][N]; ciphertext g uses Philox id counter0 + g. */
 int bcn_encrypt(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int G, int level, double scale,
@@ -112,6 +117,20 @@ int bcn_mul_plain_norescale(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int
  * else out u64[G][2][level+1][N] unrescaled. */
 int bcn_mac_terms(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts, const uint64_t *const *pts,
                   const int *pt_batched, int G, int level, int rescale, void *stream);
+/* same, accumulating into an existing unrescaled out u64[G][2][level+1][N] */
+int bcn_mac_terms_acc(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts,
+                      const uint64_t *const *pts, const int *pt_batched, int G, int level, void *stream);
+/* K7+K8+K4 hoisted rotations with lazy ModDown: for terms t
+ * = (U_t = bcn_modup of source ct_t, Galois element g_t, multiplier pt_t),
+ *   out = sum_t pt_t (x) rotate_{g_t}(ct_t)
+ * computed as (sum_t pt_t sigma(c0_t) + ModDown(B_0), ModDown(B_1)) with
+ * B = sum_t pt_t * sum_j sigma(U_t,j) (x) key_t,j in the extended basis: one
+ * ModDown for the whole sum.  pts: Montgomery, extended basis (bcn_encode_ext),
+ * u64[G or 1][level+1+K][N], or NULL for the multiplier 1.  out is unrescaled,
+ * u64[G][2][level+1][N]. */
+int bcn_rotsum(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *U, const uint64_t *const *cts,
+               const uint64_t *gal, const uint64_t *const *pts, const int *pt_batched, int G, int level,
+               void *stream);
 /* K4 microbenchmark form: out[g] = sum_{t in [g*group, min((g+1)*group, n_items))} ct[t] (x) pt[t] */
 int bcn_mac(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, const uint64_t *pt_mont, int n_items, int group,
             int nlimb, void *stream);

@@ -410,6 +410,21 @@ int bcn_encode(bcn_ctx* c, const double* vals, int vlen, int vstride, int nplain
     return BCN_OK;
 }
 
+// encode over the extended basis q_0..q_level, p_0..p_{K-1} (multipliers of lazy-ModDown sums)
+int bcn_encode_ext(bcn_ctx* c, const double* vals, int vlen, int vstride, int nplain, double scale, int level,
+                   uint64_t* out, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (vlen > c->N / 2) return fail(BCN_ERR_CAPACITY, "vector exceeds slot count");
+    cudaStream_t st = (cudaStream_t)stream;
+    Limbs l = limbs_ext(c, level);
+    const long long ps = (long long)l.n * c->N;
+    CUDA_TRY(encode_op((u64*)out, ps, vals, vlen, vstride, nplain, scale, c->logn, l, c->pr, fft_tab(c), 0, 0, 0, st));
+    CUDA_TRY(ntt_run(c, false, (u64*)out, ps, l, nplain, st));
+    CUDA_TRY(to_mont_op((u64*)out, (u64*)out, nplain, l.n, c->logn, l, c->pr, st));
+    return BCN_OK;
+}
+
 int bcn_encrypt(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
                 uint64_t counter0, uint64_t* ct, void* stream) {
     int e = check_level(c, level);
@@ -571,8 +586,23 @@ int bcn_mul_plain_norescale(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int c
                           (cudaStream_t)stream);
 }
 
+static int mac_terms_impl(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* cts,
+                          const uint64_t* const* pts, const int* pt_batched, int G, int level, int rescale,
+                          int accumulate, void* stream);
+
 int bcn_mac_terms(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* cts, const uint64_t* const* pts,
                   const int* pt_batched, int G, int level, int rescale, void* stream) {
+    return mac_terms_impl(c, out, n_terms, cts, pts, pt_batched, G, level, rescale, 0, stream);
+}
+
+int bcn_mac_terms_acc(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* cts, const uint64_t* const* pts,
+                      const int* pt_batched, int G, int level, void* stream) {
+    return mac_terms_impl(c, out, n_terms, cts, pts, pt_batched, G, level, 0, 1, stream);
+}
+
+static int mac_terms_impl(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* cts,
+                          const uint64_t* const* pts, const int* pt_batched, int G, int level, int rescale,
+                          int accumulate, void* stream) {
     int e = check_level(c, level);
     if (e) return e;
     if (n_terms < 1) return fail(BCN_ERR_PARAM, "no terms");
@@ -595,7 +625,7 @@ int bcn_mac_terms(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const*
             T.pt[k] = (const u64*)pts[t0 + k];
             T.pt_batched[k] = (unsigned char)(pt_batched[t0 + k] != 0);
         }
-        CUDA_TRY(mac_terms_op(acc, T, G, nl, c->logn, l, c->pr, t0 > 0, st));
+        CUDA_TRY(mac_terms_op(acc, T, G, nl, c->logn, l, c->pr, (t0 > 0) || accumulate, st));
     }
     if (!rescale) return BCN_OK;
     LevelTables* LT;
@@ -776,6 +806,58 @@ static int keyswitch_tail(bcn_ctx* c, u64* out, long long os, const u64* U, int 
 static size_t tail_words(const bcn_ctx* c, int G, int level) {
     const int nl = level + 1, next = nl + c->K;
     return (size_t)G * 2 * next * c->N + (size_t)G * 2 * nl * c->N;
+}
+
+// out = C0 + ModDown(B) with B = sum_t pt_t sum_j sigma_t(U_t,j) key_t,j (lazy ModDown)
+int bcn_rotsum(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* U, const uint64_t* const* cts,
+               const uint64_t* gal, const uint64_t* const* pts, const int* pt_batched, int G, int level,
+               void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (n_terms < 1) return fail(BCN_ERR_PARAM, "no terms");
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int k = 0; k < n_terms; k++) {
+        if (gal[k] == 1 || (gal[k] & 1) == 0) return fail(BCN_ERR_PARAM, "rotation sum needs odd Galois elements != 1");
+        if (!key_ptr(c, gal[k])) {
+            e = bcn_keygen_galois(c, gal[k], stream);
+            if (e) return e;
+        }
+    }
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K, ndig = T->ndig;
+    Limbs ext = limbs_ext(c, level);
+    int err = 0;
+    u64* B = scratch_get(c, (size_t)G * 2 * next * N + (size_t)G * nl * N + (size_t)G * 2 * nl * N, &err);
+    if (!B) return err;
+    u64* C0 = B + (size_t)G * 2 * next * N;
+    u64* Z = C0 + (size_t)G * nl * N;
+    RotTerms R;
+    for (int t0 = 0; t0 < n_terms; t0 += BCN_ROT_TERMS) {
+        R.n = std::min(BCN_ROT_TERMS, n_terms - t0);
+        for (int k = 0; k < R.n; k++) {
+            R.U[k] = (const u64*)U[t0 + k];
+            R.key[k] = key_ptr(c, gal[t0 + k]);
+            R.c0[k] = (const u64*)cts[t0 + k];
+            R.pt[k] = (const u64*)pts[t0 + k];
+            R.g[k] = (u32)gal[t0 + k];
+            R.pt_batched[k] = (unsigned char)(pt_batched[t0 + k] != 0);
+        }
+        CUDA_TRY(rotsum_op(B, C0, R, 2LL * nl * N, G, nl, next, ndig, c->logn, 2LL * c->nbasis * N,
+                           (long long)c->nbasis * N, ext, c->pr, t0 > 0, st));
+    }
+    Limbs pl;
+    pl.n = c->K;
+    for (int k = 0; k < c->K; k++) pl.prime[k] = (short)(c->nq + k);
+    CUDA_TRY(ntt_run(c, true, B + (size_t)nl * N, (long long)next * N, pl, 2 * G, st));
+    CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st));
+    Limbs ql = limbs_range(0, nl);
+    CUDA_TRY(ntt_run(c, false, Z, (long long)nl * N, ql, 2 * G, st));
+    CUDA_TRY(moddown_combine_op((u64*)out, 2LL * nl * N, B, next, Z, C0, (long long)nl * N, 0, 1u, G, nl, c->logn,
+                                ql, c->pr, T->pinv, st));
+    return BCN_OK;
 }
 
 int bcn_rotate_hoisted(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, const uint64_t* U, int G,

@@ -72,6 +72,18 @@ struct Acc128 {
         lo = nl;
         if (hi >= q) hi -= q;
     }
+    // unreduced MAC: a, b < q < 2^61 adds floor(ab / 2^64) + carry <= q/8 to hi,
+    // so up to 7 of these may follow a state with hi < q before fold() (hi < 2q -> < q)
+    __device__ __forceinline__ void mac_nr(u64 a, u64 b) {
+        u64 pl = a * b, ph = umulhi(a, b);
+        u64 nl = lo + pl;
+        hi += ph + (nl < lo ? 1ull : 0ull);
+        lo = nl;
+    }
+    __device__ __forceinline__ void fold(u64 q) {
+        const u64 t = hi - q;
+        hi = (i64)t < 0 ? hi : t;
+    }
     __device__ __forceinline__ u64 reduce(u64 q, u64 qinv_neg) const { return redc(hi, lo, q, qinv_neg); }
 };
 

@@ -133,9 +133,12 @@ __global__ void __launch_bounds__(256) mac_terms_kernel(u64* __restrict__ out, c
         for (int k = 0; k < terms.n; k++) {
             const u64 p = __ldg(terms.pt[k] + (terms.pt_batched[k] ? pbase : off));
             const u64* c = terms.ct[k] + cbase;
-            a0.mac(__ldg(c), p, q);
-            a1.mac(__ldg(c + LN), p, q);
+            a0.mac_nr(__ldg(c), p);
+            a1.mac_nr(__ldg(c + LN), p);
+            if (k % 7 == 6) { a0.fold(q); a1.fold(q); }
         }
+        a0.fold(q);
+        a1.fold(q);
         u64 r0 = a0.reduce(q, P.qinv_neg), r1 = a1.reduce(q, P.qinv_neg);
         u64* o = out + cbase;
         if (accumulate) {
@@ -324,6 +327,120 @@ cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int lo
                         key_digit_stride, key_comp_stride, ext, keyl, pr); break;
             BCN_SMALL(8) BCN_SMALL(16) BCN_SMALL(32) BCN_SMALL(64) BCN_SMALL(128) BCN_SMALL(256) BCN_SMALL(512)
 #undef BCN_SMALL
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    return launched();
+}
+
+// ------------------------------- lazy-ModDown rotation sum (K7 + K4 + K8)
+// For every output word (g, ext limb t, n) and every term k:
+//   a_c = REDC( sum_j sigma_gk(U_k,j)[n] * key_k[j][c][t][n] )      (c = 0, 1)
+//   B_c += a_c * pt_k[t][n],   C0 += sigma_gk(c0_k)[n] * pt_k[t][n]  (t <= l)
+// The ModDown of B happens ONCE for the whole sum (caller), instead of once
+// per rotation.  One CTA = one aligned source/destination block of BLK words
+// of one limb of one slot set; blockIdx.x is the slot set, so the G CTAs that
+// read the same key slice run back to back and share it through L2.
+template <int BLK>
+__global__ void __launch_bounds__(256) rotsum_kernel(u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T,
+                                                     long long c0_gstride, int nq, int next, int ndig, int logn,
+                                                     long long kds, long long kcs, Limbs ext,
+                                                     const PrimeInfo* __restrict__ pr, int accumulate) {
+    constexpr int TPB = BLK < 256 ? BLK : 256;
+    constexpr int PPT = BLK / TPB;
+    extern __shared__ u64 sm[];
+    const int N = 1 << logn;
+    const int logb = __ffs(BLK) - 1;
+    const long long p = blockIdx.x;
+    const int blk = blockIdx.y;
+    const int t = blockIdx.z;
+    const int kt = ext.prime[t];
+    const PrimeInfo& P = pr[kt];
+    const u64 q = P.q, qn = P.qinv_neg, one_m = P.r1;
+    const bool has_c0 = t < nq;
+    const int dst0 = blk * BLK;
+    const int tid = threadIdx.x;
+    Acc128 b0[PPT], b1[PPT], cc[PPT];
+#pragma unroll
+    for (int e = 0; e < PPT; e++) { b0[e].zero(); b1[e].zero(); cc[e].zero(); }
+    for (int k = 0; k < T.n; k++) {
+        const u32 g = T.g[k];
+        const int sblk = (int)(automorph_src((u32)dst0, g, logn) >> logb);
+        __syncthreads();
+        const u64* Uk = T.U[k] + ((p * ndig) * (long long)next + t) * N + (long long)sblk * BLK;
+        for (int j = 0; j < ndig; j++)
+            for (int i = tid; i < BLK; i += TPB) sm[j * BLK + i] = __ldg(Uk + (long long)j * next * N + i);
+        if (has_c0) {
+            const u64* c0k = T.c0[k] + p * c0_gstride + (long long)t * N + (long long)sblk * BLK;
+            for (int i = tid; i < BLK; i += TPB) sm[ndig * BLK + i] = __ldg(c0k + i);
+        }
+        __syncthreads();
+        const u64* pk = T.pt[k];
+        const long long pbase = T.pt_batched[k] ? p * (long long)next * N : 0;
+#pragma unroll
+        for (int e = 0; e < PPT; e++) {
+            const int i = tid + e * TPB;
+            const int n = dst0 + i;
+            const int s = (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
+            Acc128 a0, a1;
+            a0.zero(); a1.zero();
+            const u64* kp = T.key[k] + (long long)kt * N + n;
+            for (int j = 0; j < ndig; j++) {
+                const u64 u = sm[j * BLK + s];
+                a0.mac_nr(u, __ldg(kp + j * kds));
+                a1.mac_nr(u, __ldg(kp + j * kds + kcs));
+                if (j % 7 == 6) { a0.fold(q); a1.fold(q); }
+            }
+            a0.fold(q);
+            a1.fold(q);
+            const u64 w = pk ? __ldg(pk + pbase + (long long)t * N + n) : one_m;
+            b0[e].mac_nr(a0.reduce(q, qn), w);
+            b1[e].mac_nr(a1.reduce(q, qn), w);
+            if (has_c0) cc[e].mac_nr(sm[ndig * BLK + s], w);
+            if (k % 7 == 6) { b0[e].fold(q); b1[e].fold(q); cc[e].fold(q); }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < PPT; e++) { b0[e].fold(q); b1[e].fold(q); cc[e].fold(q); }
+#pragma unroll
+    for (int e = 0; e < PPT; e++) {
+        const int n = dst0 + tid + e * TPB;
+        u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
+        u64* o1 = o0 + (long long)next * N;
+        u64 r0 = b0[e].reduce(q, qn), r1 = b1[e].reduce(q, qn);
+        if (accumulate) { r0 = add_mod(r0, *o0, q); r1 = add_mod(r1, *o1, q); }
+        *o0 = r0;
+        *o1 = r1;
+        if (has_c0) {
+            u64* oc = C0 + p * (long long)nq * N + (long long)t * N + n;
+            u64 rc = cc[e].reduce(q, qn);
+            if (accumulate) rc = add_mod(rc, *oc, q);
+            *oc = rc;
+        }
+    }
+}
+
+cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
+                      int ndig, int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
+                      int accumulate, cudaStream_t st) {
+    const int N = 1 << logn;
+    if (terms.n <= 0 || G <= 0) return cudaSuccess;
+    if (N >= 1024) {
+        constexpr int BLK = 1024;
+        const size_t smem = (size_t)(ndig + 1) * BLK * sizeof(u64);
+        static bool cfg = false;
+        if (!cfg) { cudaFuncSetAttribute(rotsum_kernel<BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+        dim3 grid(G, N / BLK, next);
+        rotsum_kernel<BLK><<<grid, 256, smem, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, kds, kcs, ext, pr,
+                                                    accumulate);
+    } else {
+        const size_t smem = (size_t)(ndig + 1) * N * sizeof(u64);
+        dim3 grid(G, 1, next);
+        switch (N) {
+#define BCN_RS(NN) case NN: rotsum_kernel<NN><<<grid, (NN < 256 ? NN : 256), smem, st>>>(B, C0, terms, c0_gstride, \
+                        nq, next, ndig, logn, kds, kcs, ext, pr, accumulate); break;
+            BCN_RS(8) BCN_RS(16) BCN_RS(32) BCN_RS(64) BCN_RS(128) BCN_RS(256) BCN_RS(512)
+#undef BCN_RS
             default: return cudaErrorInvalidValue;
         }
     }

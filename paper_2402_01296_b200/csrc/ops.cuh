@@ -47,6 +47,21 @@ struct MacTerms {
     const u64* pt[BCN_MAC_TERMS];
     unsigned char pt_batched[BCN_MAC_TERMS];
 };
+// Lazy-ModDown rotation sum: B = sum_t pt_t * sum_j sigma_t(U_t,j) (x) key_t,j over
+// the extended basis and C0 = sum_t pt_t * sigma_t(c0_t) over q_0..q_l.
+#define BCN_ROT_TERMS 96
+struct RotTerms {
+    int n;
+    const u64* U[BCN_ROT_TERMS];     // [G][ndig][ext][N]
+    const u64* key[BCN_ROT_TERMS];   // [dnum][2][nbasis][N] Montgomery
+    const u64* c0[BCN_ROT_TERMS];    // component 0 of the source ct, [G] stride c0_gstride
+    const u64* pt[BCN_ROT_TERMS];    // Montgomery, ext basis [G|1][ext][N]; null = 1
+    u32 g[BCN_ROT_TERMS];
+    unsigned char pt_batched[BCN_ROT_TERMS];
+};
+cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
+                      int ndig, int logn, long long key_digit_stride, long long key_comp_stride, const Limbs& ext,
+                      const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
                          const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,

@@ -218,6 +218,41 @@ class Engine:
         _lib.call("bcn_export_secret", self._h, _ptr(out), _stream())
         return out
 
+    def encode_ext(self, vals, level: int, scale: float) -> torch.Tensor:
+        """Montgomery multiplier over the extended basis (limbs q_0..q_level, p_*)."""
+        self._check_mag(vals, scale)
+        v = self._dev_f64(vals)
+        if v.shape[1] > self.N // 2:
+            raise CapacityError(f"vector of length {v.shape[1]} exceeds {self.N // 2} slots")
+        out = torch.empty((v.shape[0], level + 1 + self.K, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_encode_ext", self._h, _ptr(v), v.shape[1], v.shape[1], v.shape[0], float(scale), level,
+                  _ptr(out), _stream())
+        return out
+
+    def rotsum(self, terms, level: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """sum_t pt_t (x) rot_{g_t}(ct_t) with ONE ModDown (unrescaled, at `level`).
+        terms: [(ct u64[G,2,level+1,N], U from modup(ct), g, pt_ext or None)]."""
+        G = terms[0][0].shape[0]
+        n = len(terms)
+        Us = (ctypes.c_uint64 * n)(*[t[1].data_ptr() for t in terms])
+        cts = (ctypes.c_uint64 * n)(*[t[0].data_ptr() for t in terms])
+        gal = (ctypes.c_uint64 * n)(*[int(t[2]) for t in terms])
+        pts = (ctypes.c_uint64 * n)(*[0 if t[3] is None else t[3].data_ptr() for t in terms])
+        bat = (ctypes.c_int * n)(*[int(t[3] is not None and t[3].shape[0] != 1) for t in terms])
+        if out is None:
+            out = self.empty_ct(G, level)
+        _lib.call("bcn_rotsum", self._h, _ptr(out), n, Us, cts, gal, pts, bat, G, level, _stream())
+        return out
+
+    def mac_terms_acc(self, out: torch.Tensor, terms, level: int) -> torch.Tensor:
+        G = terms[0][0].shape[0]
+        n = len(terms)
+        cts = (ctypes.c_uint64 * n)(*[t[0].data_ptr() for t in terms])
+        pts = (ctypes.c_uint64 * n)(*[t[1].data_ptr() for t in terms])
+        bat = (ctypes.c_int * n)(*[int(t[1].shape[0] != 1) for t in terms])
+        _lib.call("bcn_mac_terms_acc", self._h, _ptr(out), n, cts, pts, bat, G, level, _stream())
+        return out
+
     def mac_terms(self, terms, level: int, rescale: bool = True) -> torch.Tensor:
         """sum_t ct_t (x) pt_t (one fused launch per 160 terms), optionally rescaled.
         terms: [(ct u64[G,2,>=level+1,N] with exactly level+1 limbs, pt_mont u64[G|1,level+1,N])]."""

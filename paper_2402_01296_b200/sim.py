@@ -8,15 +8,16 @@ produced and consumed only by libbcn.so kernels.  `Ciphertext.slots` is a
 lazy, read-only decryption (sim.py:128-139 exposes the slots directly).
 
 Execution choices that keep the reference's observable semantics:
-  * Rescale is lazy.  A Mul_PC product is returned "pending": logically at
-    level-1 (as sim.py:248 / 282 say) but held unrescaled at data level l
-    with scale Delta*q_l.  Pending + pending adds stay pending, so a conv
-    tap loop or an FC diagonal sum pays ONE rescale per output instead of one
-    per product.  Anything else materialises (rescales) first.
+  * Lazy linear combinations.  A Mul_PC / rotate-multiply / rotation result
+    is returned as an unevaluated term list, logically at the reference's
+    level (sim.py:248, 256, 282).  Adding such lists concatenates them, so
+    a conv tap loop, an FC diagonal sum, a pooling window or a channel
+    concatenation is evaluated by ONE fused kernel, ONE ModDown and ONE
+    rescale per output instead of one per product.
   * Rotations are hoisted: ModUp(c1) is computed once per ciphertext and
-    reused by every rotation of it; results are memoised per (ct, r).  The
-    recorder still counts every call exactly as sim.py:253/273 do.
-Both are deterministic, so results do not depend on call order.
+    shared by all its rotations.  Rotations reused by several outputs
+    (multi-channel convs) are materialised once and memoised per (ct, r).
+The recorder still counts every reference call exactly (sim.py:209-283).
 """
 
 from __future__ import annotations
@@ -48,7 +49,12 @@ MAX_RING = 1 << 14
 
 # device work actually issued (after hoisting / memoisation / lazy rescale);
 # the recorder keeps the reference's logical counts separately.
-STATS = {"modup": 0, "keyswitch": 0, "rescale": 0, "encode": 0, "encode_hit": 0, "mac_launch": 0}
+STATS = {"modup": 0, "keyswitch": 0, "keyswitch_lazy": 0, "moddown": 0, "rescale": 0, "encode": 0,
+         "encode_hit": 0, "mac_launch": 0}
+
+
+def _term_batch(term) -> int:
+    return int((term[1]._data if term[0] == "rot" else term[1]).shape[0])
 
 
 def reset_stats() -> None:
@@ -197,19 +203,21 @@ class Ciphertext:
     rescale materialises the whole sum.
     """
 
-    __slots__ = ("level", "scale", "id", "ctx", "batch", "_data", "_terms", "_data_scale",
-                 "_modup", "_rot", "_slots", "__weakref__")
+    __slots__ = ("level", "scale", "id", "ctx", "batch", "_data", "_terms", "_scaled", "_data_scale",
+                 "_modup", "_rot", "_slots", "_eager", "__weakref__")
 
-    def __init__(self, data, level: int, scale: float, ctx: HeContext, *, terms=None, data_scale=None,
-                 cid: str | None = None):
+    def __init__(self, data, level: int, scale: float, ctx: HeContext, *, terms=None, scaled=True,
+                 data_scale=None, cid: str | None = None):
         s = object.__setattr__
         s(self, "level", level)
         s(self, "scale", float(scale))
         s(self, "id", cid or ctx.fresh_id())
         s(self, "ctx", ctx)
-        s(self, "batch", int((data if data is not None else terms[0][0]).shape[0]))
+        s(self, "batch", int(data.shape[0]) if data is not None else _term_batch(terms[0]))
         s(self, "_data", data)
         s(self, "_terms", terms)
+        s(self, "_scaled", scaled)
+        s(self, "_eager", False)
         s(self, "_data_scale", float(scale) if data_scale is None else float(data_scale))
         s(self, "_modup", None)
         s(self, "_rot", {})
@@ -225,15 +233,44 @@ class Ciphertext:
     def pending(self) -> bool:
         return self._terms is not None
 
+    @property
+    def data_level(self) -> int:
+        return self.level + 1 if (self._terms is not None and self._scaled) else self.level
+
     def materialize(self) -> "Ciphertext":
-        """Evaluate a lazy sum (fused MAC + one rescale) in place; value unchanged."""
-        if self._terms is not None:
-            data = self.ctx.engine.mac_terms(self._terms, self.level + 1, rescale=True)
+        """Evaluate a lazy sum in place (value unchanged): rotation terms by ONE
+        lazy-ModDown rotsum, plain-multiplier terms by ONE fused MAC, then one
+        rescale if the terms carry multipliers."""
+        if self._terms is None:
+            return self
+        eng = self.ctx.engine
+        lvl = self.data_level
+        rots = [t for t in self._terms if t[0] == "rot"]
+        cts = [t for t in self._terms if t[0] == "ct"]
+        out = None
+        if rots:
+            for t in rots:
+                src = t[1]
+                if src._modup is None:
+                    object.__setattr__(src, "_modup", eng.modup(src._data, src.level))
+                    STATS["modup"] += 1
+            out = eng.rotsum([(t[1]._data, t[1]._modup, t[2], t[3]) for t in rots], lvl)
+            STATS["moddown"] += 1
+            STATS["keyswitch_lazy"] += len(rots)
+        if cts:
+            if self._scaled:
+                pairs = [(t[1], t[2]) for t in cts]
+                out = eng.mac_terms(pairs, lvl, rescale=False) if out is None else eng.mac_terms_acc(out, pairs, lvl)
+                STATS["mac_launch"] += 1
+            else:
+                for t in cts:
+                    out = t[1] if out is None else eng.add(out, t[1], lvl)
+        if self._scaled:
+            out = eng.rescale(out, lvl)
             STATS["rescale"] += 1
-            STATS["mac_launch"] += 1
-            object.__setattr__(self, "_data", data)
-            object.__setattr__(self, "_terms", None)
-            object.__setattr__(self, "_data_scale", self.scale)
+        object.__setattr__(self, "_data", out)
+        object.__setattr__(self, "_terms", None)
+        object.__setattr__(self, "_data_scale", self.scale)
         return self
 
     @property
@@ -368,11 +405,12 @@ def _batch_of(a: Ciphertext, b: Ciphertext) -> None:
         raise UsageError(f"ciphertext batches differ ({a.batch} vs {b.batch})")
 
 
-def _encode(ctx: HeContext, plain, level: int, scale: float, montgomery: bool, batch: int):
-    """Encode a plain vector; keyed (weight-derived) vectors are cached in HBM."""
+def _encode(ctx: HeContext, plain, level: int, scale: float, montgomery: bool, batch: int, ext: bool = False):
+    """Encode a plain vector; keyed (weight-derived) vectors are cached in HBM.
+    ext=True: Montgomery multiplier over the extended basis (rotsum terms)."""
     key = getattr(plain, "bcn_key", None)
     if key is not None:
-        k = (key, level, scale, montgomery)
+        k = (key, level, scale, montgomery, ext)
         hit = ctx._pt_cache.get(k)
         if hit is not None:
             ctx._pt_cache.move_to_end(k)
@@ -381,7 +419,8 @@ def _encode(ctx: HeContext, plain, level: int, scale: float, montgomery: bool, b
     rows = _as_plain_rows(plain, ctx)
     if rows.shape[0] not in (1, batch):
         raise UsageError(f"plain batch {rows.shape[0]} does not match ciphertext batch {batch}")
-    pt = ctx.engine.encode(rows, level, scale, montgomery=montgomery)
+    pt = ctx.engine.encode_ext(rows, level, scale) if ext else ctx.engine.encode(rows, level, scale,
+                                                                                  montgomery=montgomery)
     STATS["encode"] += 1
     if key is not None:
         nb = pt.numel() * 8
@@ -401,9 +440,16 @@ def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
         rec.bump("Add_CC")
         _batch_of(a, b)
         level = min(a.level, b.level)
-        if a.pending and b.pending and a.level == b.level:
+        if a.pending and b.pending and a.level == b.level and a._scaled == b._scaled:
             _check_scales(a._data_scale, b._data_scale)
-            return Ciphertext(None, level, a.scale, ctx, terms=a._terms + b._terms, data_scale=a._data_scale)
+            return Ciphertext(None, level, a.scale, ctx, terms=a._terms + b._terms, scaled=a._scaled,
+                              data_scale=a._data_scale)
+        if a.level == b.level and (a.pending != b.pending):
+            lazy, done = (a, b) if a.pending else (b, a)
+            if not lazy._scaled:        # rotation sum + a materialised ciphertext: still one ModDown
+                _check_scales(lazy.scale, done.scale)
+                return Ciphertext(None, level, a.scale, ctx, terms=lazy._terms + (("ct", done._data, None),),
+                                  scaled=False)
         a.materialize()
         b.materialize()
         _check_scales(a.scale, b.scale)
@@ -421,7 +467,17 @@ def _times_plain(x: Ciphertext, plain) -> Ciphertext:
     level = x.level
     ql = ctx.q(level)
     pt = _encode(ctx, plain, level, float(ql), True, x.batch)
-    return Ciphertext(None, level - 1, x.scale, ctx, terms=((x._data, pt),), data_scale=x.scale * float(ql))
+    return Ciphertext(None, level - 1, x.scale, ctx, terms=(("ct", x._data, pt),), data_scale=x.scale * float(ql))
+
+
+def _rot_times_plain(c: Ciphertext, r: int, plain) -> Ciphertext:
+    """rotate(c, r) * plain as a lazy rotation term (ModDown deferred to the sum)."""
+    ctx = c.ctx
+    level = c.level
+    ql = ctx.q(level)
+    pt = _encode(ctx, plain, level, float(ql), True, c.batch, ext=True)
+    g = galois_element(r, ctx.poly_degree)
+    return Ciphertext(None, level - 1, c.scale, ctx, terms=(("rot", c, g, pt),), data_scale=c.scale * float(ql))
 
 
 def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Ciphertext:
@@ -481,11 +537,17 @@ def release(c: Ciphertext) -> None:
 
 
 def he_rotate(c: Ciphertext, r: int, rec: OpRecorder) -> Ciphertext:
-    """Left rotation by r slots (right for r < 0), level unchanged (sim.py:251-256)."""
+    """Left rotation by r slots (right for r < 0), level unchanged (sim.py:251-256).
+    Unless the source is marked for reuse, the result is a lazy rotation term:
+    sums of rotations (sum_pool, concat_flat) then share ONE ModDown."""
     rec.bump("Rot")
     r = int(r) % c.ctx.slot_count
-    src = _rotated(c, r)
-    return Ciphertext(src._data, src.level, src.scale, c.ctx)
+    c.materialize()
+    if r == 0 or c._eager or r in c._rot:
+        src = _rotated(c, r)
+        return Ciphertext(src._data, src.level, src.scale, c.ctx)
+    g = galois_element(r, c.ctx.poly_degree)
+    return Ciphertext(None, c.level, c.scale, c.ctx, terms=(("rot", c, g, None),), scaled=False)
 
 
 def he_rotate_mul(c: Ciphertext, r: int, plain, rec: OpRecorder, *, mask: bool = False) -> Ciphertext:
@@ -497,4 +559,13 @@ def he_rotate_mul(c: Ciphertext, r: int, plain, rec: OpRecorder, *, mask: bool =
     if mask:
         rec.bump("Mul_PC_mask")
     r = int(r) % c.ctx.slot_count
-    return _times_plain(_rotated(c, r), plain)
+    c.materialize()
+    if r == 0 or c._eager or r in c._rot:
+        return _times_plain(_rotated(c, r), plain)
+    return _rot_times_plain(c, r, plain)
+
+
+def mark_reused(c: Ciphertext) -> None:
+    """Rotations of c will be reused by several outputs (multi-channel conv):
+    materialise and memoise them instead of deferring their ModDown."""
+    object.__setattr__(c, "_eager", True)

@@ -152,6 +152,28 @@ def test_rotate_at_lower_level_reads_in_place():
     _assert_ct(got2, exp)
 
 
+@pytest.mark.parametrize("N,L,dnum", [(64, 3, 2), (2048, 5, 3), (16384, 6, 3)])
+def test_rotsum_lazy_moddown_matches(N, L, dnum):
+    """Hoisted rotations with ONE ModDown for the whole sum (bcn_rotsum) == oracle."""
+    eng, orc, hp = _pair(N, L, dnum=dnum)
+    rng = np.random.default_rng(8)
+    v, ct, oc = _enc2(eng, orc, N, rng)
+    w, ct2, oc2 = _enc2(eng, orc, N, rng, counter=21)
+    Ua, Ub = eng.modup(ct, L), eng.modup(ct2, L)
+    from paper_2402_01296_b200.params import galois_element as ge
+    p1, p2, p3 = rng.standard_normal((3, N // 2))
+    ql = float(hp.q[L])
+    terms = [(ct, Ua, ge(1, N), eng.encode_ext(p1, L, ql)), (ct, Ua, ge(5, N), eng.encode_ext(p2, L, ql)),
+             (ct2, Ub, ge(3, N), eng.encode_ext(p3, L, ql))]
+    got = eng.rotsum(terms, L)
+    _assert_ct(got, [orc.rotsum([(oc[i], 1, p1), (oc[i], 5, p2), (oc2[i], 3, p3)], L) for i in range(2)])
+    dec = eng.decrypt(eng.rescale(got, L), L - 1, hp.scale).cpu().numpy()[0]
+    want = np.roll(v[0], -1) * p1 + np.roll(v[0], -5) * p2 + np.roll(w[0], -3) * p3
+    assert np.abs(dec - want).max() < 1e-5
+    unit = eng.rotsum([(ct, Ua, ge(2, N), None), (ct2, Ub, ge(7, N), None)], L)
+    _assert_ct(unit, [orc.rotsum([(oc[i], 2, None), (oc2[i], 7, None)], L) for i in range(2)])
+
+
 def test_mac_matches():
     N = 1024
     eng, orc, hp = _pair(N, 3, 60)

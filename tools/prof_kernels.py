@@ -18,6 +18,23 @@ if what == "ntt":
         eng.ntt(data, 0, inverse=True)
         eng.mac(data.view(4096, 2, 4, 8192), pts, 25)
     torch.cuda.synchronize()
+elif what in ("rotsum", "mac"):
+    # fc1-like: one level-5 source (cifar3 chain), 96 rotate-multiply terms, G = 32 slot sets
+    from paper_2402_01296_b200.params import galois_element as ge
+    hp = make_params(16384, 14, 50, dnum=3)
+    eng = Engine(hp)
+    lvl, G = 5, 32
+    ct = eng.sample_uniform(2 * G, lvl + 1, 0, seed=5).view(G, 2, lvl + 1, 16384)
+    U = eng.modup(ct, lvl)
+    pts = [eng.to_montgomery(eng.sample_uniform(1, lvl + 1 + hp.K, 0, seed=100 + i)) for i in range(96)]
+    terms = [(ct, U, ge(i + 1, 16384), pts[i]) for i in range(96)]
+    qterms = [(ct, eng.to_montgomery(eng.sample_uniform(1, lvl + 1, 0, seed=300 + i))) for i in range(96)]
+    for _ in range(2):
+        if what == "rotsum":
+            eng.rotsum(terms, lvl)
+        else:
+            eng.mac_terms(qterms, lvl, rescale=False)
+    torch.cuda.synchronize()
 else:
     hp = make_params(16384, 7, 50, dnum=2, n_special=1)
     eng = Engine(hp)
