@@ -117,6 +117,11 @@ int bcn_mul_plain_norescale(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int
  * else out u64[G][2][level+1][N] unrescaled. */
 int bcn_mac_terms(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts, const uint64_t *const *pts,
                   const int *pt_batched, int G, int level, int rescale, void *stream);
+/* multi-output form for conv layers (conv output channels share their rotated
+ * inputs, network.py:220-228): out_o = sum_k ct_k (x) pt[o*n_terms + k] for
+ * o < n_out; out u64[n_out][G][2][level or level+1][N] (rescaled or not). */
+int bcn_mac_multi(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *cts,
+                  const uint64_t *const *pts, int G, int level, int rescale, void *stream);
 /* same, accumulating into an existing unrescaled out u64[G][2][level+1][N] */
 int bcn_mac_terms_acc(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts,
                       const uint64_t *const *pts, const int *pt_batched, int G, int level, void *stream);

@@ -54,6 +54,7 @@ SIGNATURES = {
     "bcn_mul_plain_norescale": [_P, _P, _P, _I, _P, _I, _I, _I, _P],
     "bcn_mac": [_P, _P, _P, _P, _I, _I, _I, _P],
     "bcn_mac_terms": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _I, _P],
+    "bcn_mac_multi": [_P, _P, _I, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), _I, _I, _I, _P],
     "bcn_mac_terms_acc": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],
     "bcn_rotsum": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64),
                    ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],

@@ -595,6 +595,52 @@ int bcn_mac_terms(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const*
     return mac_terms_impl(c, out, n_terms, cts, pts, pt_batched, G, level, rescale, 0, stream);
 }
 
+int bcn_mac_multi(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* cts,
+                  const uint64_t* const* pts, int G, int level, int rescale, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (n_out < 1 || n_terms < 1) return fail(BCN_ERR_PARAM, "no outputs / terms");
+    if (rescale && level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nl = level + 1;
+    const long long N = c->N;
+    const long long cw = (long long)G * 2 * nl * N;   // one output batch
+    Limbs l = limbs_range(0, nl);
+    u64* acc = (u64*)out;
+    int err = 0;
+    if (rescale) {
+        acc = scratch_get(c, (size_t)n_out * cw + (size_t)2 * n_out * G * N * (1 + level), &err);
+        if (!acc) return err;
+    }
+    MacMulti M;
+    for (int o0 = 0; o0 < n_out; o0 += BCN_MAC_OUT) {
+        M.n_out = std::min(BCN_MAC_OUT, n_out - o0);
+        for (int k0 = 0; k0 < n_terms; k0 += BCN_MULTI_TERMS) {
+            M.n_terms = std::min(BCN_MULTI_TERMS, n_terms - k0);
+            for (int k = 0; k < M.n_terms; k++) {
+                M.ct[k] = (const u64*)cts[k0 + k];
+                for (int o = 0; o < M.n_out; o++) M.pt[o][k] = (const u64*)pts[(size_t)(o0 + o) * n_terms + k0 + k];
+            }
+            CUDA_TRY(mac_multi_op(acc + o0 * cw, cw, M, G, nl, c->logn, l, c->pr, k0 > 0, st));
+        }
+    }
+    if (!rescale) return BCN_OK;
+    LevelTables* LT;
+    e = build_level(c, level, &LT);
+    if (e) return e;
+    const int npoly = 2 * n_out * G;
+    u64* top = acc + (size_t)n_out * cw;
+    u64* W = top + (size_t)npoly * N;
+    CUDA_TRY(gather_limb_op(top, acc, nl * N, (long long)level * N, npoly, c->logn, st));
+    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
+    Limbs ql = limbs_range(0, level);
+    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
+    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
+    CUDA_TRY(rescale_combine_op((u64*)out, (long long)level * N, acc, nl * N, W, npoly, level, c->logn, ql, c->pr,
+                                LT->qlinv, st));
+    return BCN_OK;
+}
+
 int bcn_mac_terms_acc(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* cts, const uint64_t* const* pts,
                       const int* pt_batched, int G, int level, void* stream) {
     return mac_terms_impl(c, out, n_terms, cts, pts, pt_batched, G, level, 0, 1, stream);

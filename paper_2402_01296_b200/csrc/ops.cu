@@ -159,6 +159,77 @@ cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int 
     return launched();
 }
 
+// ----------------------------------------- multi-output linear combination
+// out[o][g][c][t][n] (+)= REDC(sum_k ct_k[g][c][t][n] * pt[o][k][t][n]).
+// blockIdx.x = slot set g (fastest), so the G CTAs that multiply the same
+// plaintext slice by different ciphertexts run back to back and the
+// plaintexts come from L2; each ct word is loaded once per output tile.
+template <int OT>
+__global__ void __launch_bounds__(256, 2) mac_multi_kernel(u64* __restrict__ out, long long ostride, const MacMulti m,
+                                                        int nlimb, int logn, Limbs limbs,
+                                                        const PrimeInfo* __restrict__ pr, int accumulate) {
+    const int N = 1 << logn;
+    const long long LN = (long long)nlimb << logn;
+    const long long g = blockIdx.x;
+    const int n = blockIdx.y * blockDim.x + threadIdx.x;
+    const int t = blockIdx.z;
+    if (n >= N) return;
+    const PrimeInfo& P = pr[limbs.prime[t]];
+    const u64 q = P.q, qn = P.qinv_neg;
+    const long long off = (long long)t * N + n;
+    const long long cbase = g * 2 * LN + off;
+    Acc128 a0[OT], a1[OT];
+#pragma unroll
+    for (int o = 0; o < OT; o++) { a0[o].zero(); a1[o].zero(); }
+    // register double buffer: term k+1's words are in flight while term k multiplies
+    u64 nc0 = __ldg(m.ct[0] + cbase), nc1 = __ldg(m.ct[0] + cbase + LN), np_[OT];
+#pragma unroll
+    for (int o = 0; o < OT; o++) np_[o] = o < m.n_out ? __ldg(m.pt[o][0] + off) : 0ull;
+    for (int k = 0; k < m.n_terms; k++) {
+        const u64 c0 = nc0, c1 = nc1;
+        u64 p[OT];
+#pragma unroll
+        for (int o = 0; o < OT; o++) p[o] = np_[o];
+        if (k + 1 < m.n_terms) {
+            nc0 = __ldg(m.ct[k + 1] + cbase);
+            nc1 = __ldg(m.ct[k + 1] + cbase + LN);
+#pragma unroll
+            for (int o = 0; o < OT; o++) np_[o] = o < m.n_out ? __ldg(m.pt[o][k + 1] + off) : 0ull;
+        }
+#pragma unroll
+        for (int o = 0; o < OT; o++) {
+            a0[o].mac_nr(c0, p[o]);
+            a1[o].mac_nr(c1, p[o]);
+        }
+        if (k % 7 == 6) {
+#pragma unroll
+            for (int o = 0; o < OT; o++) { a0[o].fold(q); a1[o].fold(q); }
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < OT; o++) {
+        if (o >= m.n_out) break;
+        a0[o].fold(q);
+        a1[o].fold(q);
+        u64* po = out + o * ostride + cbase;
+        u64 r0 = a0[o].reduce(q, qn), r1 = a1[o].reduce(q, qn);
+        if (accumulate) { r0 = add_mod(r0, po[0], q); r1 = add_mod(r1, po[LN], q); }
+        po[0] = r0;
+        po[LN] = r1;
+    }
+}
+
+cudaError_t mac_multi_op(u64* out, long long out_stride, const MacMulti& m, int G, int nlimb, int logn,
+                         const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st) {
+    const int N = 1 << logn;
+    if (G <= 0 || m.n_terms <= 0 || m.n_out <= 0) return cudaSuccess;
+    const int tpb = N < 256 ? N : 256;
+    dim3 grid(G, (N + tpb - 1) / tpb, nlimb);
+    if (m.n_out <= 4) mac_multi_kernel<4><<<grid, tpb, 0, st>>>(out, out_stride, m, nlimb, logn, limbs, pr, accumulate);
+    else mac_multi_kernel<BCN_MAC_OUT><<<grid, tpb, 0, st>>>(out, out_stride, m, nlimb, logn, limbs, pr, accumulate);
+    return launched();
+}
+
 // ---------------------------------------------------------- tensor (K6)
 // d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1 for G ciphertext pairs.
 // a, b: [G][2][L][N] with strides; d: [G][3][L][N]

@@ -62,6 +62,18 @@ struct RotTerms {
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long key_digit_stride, long long key_comp_stride, const Limbs& ext,
                       const PrimeInfo* pr, int accumulate, cudaStream_t st);
+// Multi-output linear combination out_o = sum_k ct_k (x) pt_{o,k} for a tile of
+// up to BCN_MAC_OUT outputs sharing the same ct terms (conv output channels).
+#define BCN_MAC_OUT 8
+#define BCN_MULTI_TERMS 128
+struct MacMulti {
+    int n_terms;
+    int n_out;
+    const u64* ct[BCN_MULTI_TERMS];
+    const u64* pt[BCN_MAC_OUT][BCN_MULTI_TERMS];
+};
+cudaError_t mac_multi_op(u64* out, long long out_stride, const MacMulti& m, int G, int nlimb, int logn,
+                         const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
                          const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,

@@ -244,6 +244,18 @@ class Engine:
         _lib.call("bcn_rotsum", self._h, _ptr(out), n, Us, cts, gal, pts, bat, G, level, _stream())
         return out
 
+    def mac_multi(self, cts, pts, level: int, rescale: bool = True) -> torch.Tensor:
+        """out[o] = sum_k cts[k] (x) pts[o][k]; cts: K tensors u64[G,2,level+1,N];
+        pts: O lists of K Montgomery plaintexts u64[1,level+1,N] -> u64[O,G,2,l,N]."""
+        O, K = len(pts), len(cts)
+        G = cts[0].shape[0]
+        c_arr = (ctypes.c_uint64 * K)(*[c.data_ptr() for c in cts])
+        p_arr = (ctypes.c_uint64 * (O * K))(*[p.data_ptr() for row in pts for p in row])
+        nl = level if rescale else level + 1
+        out = torch.empty((O, G, 2, nl, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_mac_multi", self._h, _ptr(out), O, K, c_arr, p_arr, G, level, int(rescale), _stream())
+        return out
+
     def mac_terms_acc(self, out: torch.Tensor, terms, level: int) -> torch.Tensor:
         G = terms[0][0].shape[0]
         n = len(terms)

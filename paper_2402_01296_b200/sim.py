@@ -565,6 +565,32 @@ def he_rotate_mul(c: Ciphertext, r: int, plain, rec: OpRecorder, *, mask: bool =
     return _rot_times_plain(c, r, plain)
 
 
+def materialize_group(cts: list) -> None:
+    """Evaluate several lazy sums that share their ciphertext terms (the output
+    channels of one conv layer) with one multi-output MAC pass and one batched
+    rescale; anything that does not fit that pattern is materialised alone."""
+    lazy = [c for c in cts if c.pending]
+    if len(lazy) > 1:
+        first = lazy[0]
+        ref = [id(t[1]) for t in first._terms] if all(t[0] == "ct" for t in first._terms) else None
+        same = ref is not None and all(
+            c._scaled and c.level == first.level and len(c._terms) == len(ref)
+            and all(t[0] == "ct" and id(t[1]) == r and t[2].shape[0] == 1 for t, r in zip(c._terms, ref))
+            for c in lazy)
+        if same and first._scaled:
+            eng = first.ctx.engine
+            lvl = first.data_level
+            out = eng.mac_multi([t[1] for t in first._terms], [[t[2] for t in c._terms] for c in lazy], lvl)
+            STATS["mac_launch"] += 1
+            STATS["rescale"] += len(lazy)
+            for c, d in zip(lazy, out):
+                object.__setattr__(c, "_data", d)
+                object.__setattr__(c, "_terms", None)
+                object.__setattr__(c, "_data_scale", c.scale)
+    for c in cts:
+        c.materialize()
+
+
 def mark_reused(c: Ciphertext) -> None:
     """Rotations of c will be reused by several outputs (multi-channel conv):
     materialise and memoise them instead of deferring their ModDown."""

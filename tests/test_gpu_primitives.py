@@ -174,6 +174,31 @@ def test_rotsum_lazy_moddown_matches(N, L, dnum):
     _assert_ct(unit, [orc.rotsum([(oc[i], 2, None), (oc2[i], 7, None)], L) for i in range(2)])
 
 
+def test_mac_multi_matches_oracle_composition():
+    """Multi-output conv MAC + batched rescale == per-output oracle sums + rescale."""
+    N, L = 1024, 3
+    eng, orc, hp = _pair(N, L)
+    rng = np.random.default_rng(9)
+    K, n_out = 11, 10            # > one output tile of 8
+    vs = rng.standard_normal((K, N // 2))
+    cts = [eng.encrypt(vs[k][None], counter=40 + k) for k in range(K)]
+    octs = [orc.encrypt(vs[k], 40 + k) for k in range(K)]
+    ws = rng.standard_normal((n_out, K, N // 2))
+    ql = float(hp.q[L])
+    pts = [[eng.encode(ws[o, k], L, ql, montgomery=True) for k in range(K)] for o in range(n_out)]
+    got = eng.mac_multi(cts, pts, L, rescale=True)
+    qs = list(hp.q[:L + 1])
+    for o in range(n_out):
+        acc0 = np.zeros((L + 1, N), dtype=np.uint64)
+        acc1 = np.zeros_like(acc0)
+        for k in range(K):
+            pt = orc.encode(ws[o, k], L, ql)
+            acc0 = O.add(acc0, O.mul(octs[k].c0, pt, qs), qs)
+            acc1 = O.add(acc1, O.mul(octs[k].c1, pt, qs), qs)
+        exp = orc.rescale(O.Ct(acc0, acc1, L, hp.scale * ql))
+        _assert_ct(got[o], [exp])
+
+
 def test_mac_matches():
     N = 1024
     eng, orc, hp = _pair(N, 3, 60)
