@@ -413,12 +413,13 @@ cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int lo
 // of one limb of one slot set; blockIdx.x is the slot set, so the G CTAs that
 // read the same key slice run back to back and share it through L2.
 template <int BLK>
-__global__ void __launch_bounds__(256) rotsum_kernel(u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T,
-                                                     long long c0_gstride, int nq, int next, int ndig, int logn,
-                                                     long long kds, long long kcs, Limbs ext,
-                                                     const PrimeInfo* __restrict__ pr, int accumulate) {
-    constexpr int TPB = BLK < 256 ? BLK : 256;
-    constexpr int PPT = BLK / TPB;
+__global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
+        u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T, long long c0_gstride, int nq, int next,
+        int ndig, int logn, long long kds, long long kcs, Limbs ext, const PrimeInfo* __restrict__ pr,
+        int accumulate) {
+    // one thread per output word; term k+1's staging words, key words and
+    // multiplier are loaded into registers while term k is being multiplied
+    constexpr int MAXD = 3;
     extern __shared__ u64 sm[];
     const int N = 1 << logn;
     const int logb = __ffs(BLK) - 1;
@@ -431,63 +432,78 @@ __global__ void __launch_bounds__(256) rotsum_kernel(u64* __restrict__ B, u64* _
     const bool has_c0 = t < nq;
     const int dst0 = blk * BLK;
     const int tid = threadIdx.x;
-    Acc128 b0[PPT], b1[PPT], cc[PPT];
-#pragma unroll
-    for (int e = 0; e < PPT; e++) { b0[e].zero(); b1[e].zero(); cc[e].zero(); }
-    for (int k = 0; k < T.n; k++) {
+    const int n = dst0 + tid;
+    const int nd = ndig < MAXD ? ndig : MAXD;
+    Acc128 b0, b1, cc;
+    b0.zero(); b1.zero(); cc.zero();
+    u64 su[MAXD + 1], kv0[MAXD], kv1[MAXD], w = one_m;
+    auto fetch = [&](int k) {
         const u32 g = T.g[k];
         const int sblk = (int)(automorph_src((u32)dst0, g, logn) >> logb);
-        __syncthreads();
-        const u64* Uk = T.U[k] + ((p * ndig) * (long long)next + t) * N + (long long)sblk * BLK;
-        for (int j = 0; j < ndig; j++)
-            for (int i = tid; i < BLK; i += TPB) sm[j * BLK + i] = __ldg(Uk + (long long)j * next * N + i);
-        if (has_c0) {
-            const u64* c0k = T.c0[k] + p * c0_gstride + (long long)t * N + (long long)sblk * BLK;
-            for (int i = tid; i < BLK; i += TPB) sm[ndig * BLK + i] = __ldg(c0k + i);
-        }
-        __syncthreads();
+        const u64* Uk = T.U[k] + ((p * ndig) * (long long)next + t) * N + (long long)sblk * BLK + tid;
+#pragma unroll
+        for (int j = 0; j < MAXD; j++)
+            if (j < nd) su[j] = __ldg(Uk + (long long)j * next * N);
+        su[MAXD] = has_c0 ? __ldg(T.c0[k] + p * c0_gstride + (long long)t * N + (long long)sblk * BLK + tid) : 0ull;
+        const u64* kp = T.key[k] + (long long)kt * N + n;
+#pragma unroll
+        for (int j = 0; j < MAXD; j++)
+            if (j < nd) { kv0[j] = __ldg(kp + j * kds); kv1[j] = __ldg(kp + j * kds + kcs); }
         const u64* pk = T.pt[k];
-        const long long pbase = T.pt_batched[k] ? p * (long long)next * N : 0;
+        w = pk ? __ldg(pk + (T.pt_batched[k] ? p * (long long)next * N : 0) + (long long)t * N + n) : one_m;
+    };
+    fetch(0);
+    for (int k = 0; k < T.n; k++) {
+        __syncthreads();
 #pragma unroll
-        for (int e = 0; e < PPT; e++) {
-            const int i = tid + e * TPB;
-            const int n = dst0 + i;
-            const int s = (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
-            Acc128 a0, a1;
-            a0.zero(); a1.zero();
-            const u64* kp = T.key[k] + (long long)kt * N + n;
-            for (int j = 0; j < ndig; j++) {
+        for (int j = 0; j < MAXD; j++)
+            if (j < nd) sm[j * BLK + tid] = su[j];
+        for (int j = MAXD; j < ndig; j++) {           // (rare) more digits than prefetch slots
+            const int sblk = (int)(automorph_src((u32)dst0, T.g[k], logn) >> logb);
+            sm[j * BLK + tid] = __ldg(T.U[k] + ((p * ndig + j) * (long long)next + t) * N + (long long)sblk * BLK + tid);
+        }
+        if (has_c0) sm[ndig * BLK + tid] = su[MAXD];
+        const u64 wk = w;
+        const u32 g = T.g[k];
+        __syncthreads();
+        const int s = (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
+        Acc128 a0, a1;
+        a0.zero(); a1.zero();
+#pragma unroll
+        for (int j = 0; j < MAXD; j++) {
+            if (j < nd) {
                 const u64 u = sm[j * BLK + s];
-                a0.mac_nr(u, __ldg(kp + j * kds));
-                a1.mac_nr(u, __ldg(kp + j * kds + kcs));
-                if (j % 7 == 6) { a0.fold(q); a1.fold(q); }
+                a0.mac_nr(u, kv0[j]);
+                a1.mac_nr(u, kv1[j]);
             }
-            a0.fold(q);
-            a1.fold(q);
-            const u64 w = pk ? __ldg(pk + pbase + (long long)t * N + n) : one_m;
-            b0[e].mac_nr(a0.reduce(q, qn), w);
-            b1[e].mac_nr(a1.reduce(q, qn), w);
-            if (has_c0) cc[e].mac_nr(sm[ndig * BLK + s], w);
-            if (k % 7 == 6) { b0[e].fold(q); b1[e].fold(q); cc[e].fold(q); }
         }
+        for (int j = MAXD; j < ndig; j++) {
+            const u64 u = sm[j * BLK + s];
+            const u64* kp = T.key[k] + (long long)kt * N + n;
+            a0.fold(q); a1.fold(q);
+            a0.mac_nr(u, __ldg(kp + j * kds));
+            a1.mac_nr(u, __ldg(kp + j * kds + kcs));
+        }
+        a0.fold(q);
+        a1.fold(q);
+        b0.mac_nr(a0.reduce(q, qn), wk);
+        b1.mac_nr(a1.reduce(q, qn), wk);
+        if (has_c0) cc.mac_nr(sm[ndig * BLK + s], wk);
+        if (k % 7 == 6) { b0.fold(q); b1.fold(q); cc.fold(q); }
+        if (k + 1 < T.n) fetch(k + 1);   // other warps hide this latency
     }
-#pragma unroll
-    for (int e = 0; e < PPT; e++) { b0[e].fold(q); b1[e].fold(q); cc[e].fold(q); }
-#pragma unroll
-    for (int e = 0; e < PPT; e++) {
-        const int n = dst0 + tid + e * TPB;
-        u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
-        u64* o1 = o0 + (long long)next * N;
-        u64 r0 = b0[e].reduce(q, qn), r1 = b1[e].reduce(q, qn);
-        if (accumulate) { r0 = add_mod(r0, *o0, q); r1 = add_mod(r1, *o1, q); }
-        *o0 = r0;
-        *o1 = r1;
-        if (has_c0) {
-            u64* oc = C0 + p * (long long)nq * N + (long long)t * N + n;
-            u64 rc = cc[e].reduce(q, qn);
-            if (accumulate) rc = add_mod(rc, *oc, q);
-            *oc = rc;
-        }
+    b0.fold(q); b1.fold(q); cc.fold(q);
+    u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
+    u64* o1 = o0 + (long long)next * N;
+    u64 r0 = b0.reduce(q, qn), r1 = b1.reduce(q, qn);
+    if (accumulate) { r0 = add_mod(r0, *o0, q); r1 = add_mod(r1, *o1, q); }
+    *o0 = r0;
+    *o1 = r1;
+    if (has_c0) {
+        u64* oc = C0 + p * (long long)nq * N + (long long)t * N + n;
+        u64 rc = cc.reduce(q, qn);
+        if (accumulate) rc = add_mod(rc, *oc, q);
+        *oc = rc;
     }
 }
 
@@ -502,13 +518,13 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
         static bool cfg = false;
         if (!cfg) { cudaFuncSetAttribute(rotsum_kernel<BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
         dim3 grid(G, N / BLK, next);
-        rotsum_kernel<BLK><<<grid, 256, smem, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, kds, kcs, ext, pr,
+        rotsum_kernel<BLK><<<grid, BLK, smem, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, kds, kcs, ext, pr,
                                                     accumulate);
     } else {
         const size_t smem = (size_t)(ndig + 1) * N * sizeof(u64);
         dim3 grid(G, 1, next);
         switch (N) {
-#define BCN_RS(NN) case NN: rotsum_kernel<NN><<<grid, (NN < 256 ? NN : 256), smem, st>>>(B, C0, terms, c0_gstride, \
+#define BCN_RS(NN) case NN: rotsum_kernel<NN><<<grid, NN, smem, st>>>(B, C0, terms, c0_gstride, \
                         nq, next, ndig, logn, kds, kcs, ext, pr, accumulate); break;
             BCN_RS(8) BCN_RS(16) BCN_RS(32) BCN_RS(64) BCN_RS(128) BCN_RS(256) BCN_RS(512)
 #undef BCN_RS
