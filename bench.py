@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--images", type=int, default=4096, help="images per rank per step")
-    ap.add_argument("--chunk", type=int, default=32, help="slot sets per device batch")
+    ap.add_argument("--chunk", type=int, default=128, help="slot sets per device batch")
     ap.add_argument("--no-extras", action="store_true", help="skip latency / micro / cpu baseline")
     return ap.parse_args()
 

@@ -12,6 +12,8 @@
 // Ordering (the contract with oracle/ckks_oracle.c): forward output index k
 // holds a(psi^(2 brev(k) + 1)); the inverse takes that order back to
 // coefficients and folds N^-1 into its final stage.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ops.cuh"
 
@@ -216,8 +218,18 @@ static cudaError_t launch_one(bool inverse, const NttArgs& a, int nlimbs, int np
     return launched();
 }
 
+static int cluster_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("BCN_NTT_CLUSTER");
+        mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return mode;
+}
+
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
     if (nlimbs <= 0 || npolys <= 0) return cudaSuccess;
+    if ((logn == 13 || logn == 14) && cluster_mode()) return ntt_cluster_launch(inverse, logn, a, nlimbs, npolys, st);
     switch (logn) {
         case 3: return launch_one<3>(inverse, a, nlimbs, npolys, st);
         case 4: return launch_one<4>(inverse, a, nlimbs, npolys, st);

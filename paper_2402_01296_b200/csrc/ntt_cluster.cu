@@ -1,0 +1,291 @@
+// ntt_cluster.cu -- NTT / INTT for N = 2^13, 2^14 on a 2-CTA thread-block
+// cluster (sm_90+ clusters, distributed shared memory).
+//
+// The single-CTA kernel (ntt.cu) needs the whole limb-polynomial in SMEM
+// (128 KiB at N = 2^14), so only one CTA fits per SM and its global-load,
+// butterfly and store phases cannot overlap with another CTA.  Here the
+// polynomial is split over a cluster of two CTAs with N/2 words each:
+//   forward: pass A (the first R0 stages, blocks strided by N/2^R0) reads HBM
+//            directly, each CTA taking half of the blocks; its outputs are
+//            written to the SMEM of the CTA that owns their chunk (local or
+//            peer via DSMEM); one cluster barrier; the remaining passes only
+//            touch the CTA's own half; the last pass writes HBM.
+//   inverse: the mirror image -- local passes first, one cluster barrier,
+//            pass A reads half of its inputs from the peer's SMEM.
+// Butterflies, twiddle indexing, lazy bounds and output order are exactly
+// those of ntt.cu (same contract with the oracle).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace bcn {
+
+template <int LOGN> struct CCfg {
+    static constexpr int LOGE = 4;
+    static constexpr int N = 1 << LOGN;
+    static constexpr int HALF = N / 2;
+    static constexpr int E = 1 << LOGE;
+    static constexpr int T = N / (2 * E);                 // threads per CTA
+    static constexpr int R0 = (LOGN % LOGE) ? (LOGN % LOGE) : LOGE;
+    static constexpr int SWZ = 15;
+    static constexpr int MINB = 65536 / (64 * T);        // resident CTAs per SM at a 64-register budget
+};
+
+__device__ __forceinline__ int cswz(int j) { return j ^ ((j >> 4) & 15); }
+
+// owner CTA of global word j after pass A, and its local index
+template <int LOGN> __device__ __forceinline__ int owner(int j) { return j >> (LOGN - 1); }
+template <int LOGN> __device__ __forceinline__ int local_idx(int j) { return j & ((1 << (LOGN - 1)) - 1); }
+
+// ------------------------------------------------------------------ forward
+template <int LOGN>
+__device__ __forceinline__ void cfwd_passA(u64* x, const u64* __restrict__ g, u64* sm, u64* peer, int rank,
+                                           const ulonglong2* __restrict__ W, u64 q, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
+    const u64 q2 = 2 * q;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = rank * (TL / 2) + tid + i * C::T;    // gi == 0 for S0 == 0
+#pragma unroll
+        for (int k = 0; k < BS; k++) x[i * BS + k] = g[b + k * TL];
+#pragma unroll
+        for (int ls = 0; ls < R; ls++) {
+            const int h = BS >> (ls + 1);
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                if (k & h) continue;
+                const ulonglong2 w = W[(1 << ls) + (k >> (R - ls))];
+                u64 u = x[i * BS + k];
+                if (ls) u = csub(u, q2);
+                const u64 v = shoup_lazy(x[i * BS + k + h], w.x, w.y, q);
+                x[i * BS + k] = u + v;
+                x[i * BS + k + h] = u - v + q2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = b + k * TL;
+            u64* dst = owner<LOGN>(j) == rank ? sm : peer;
+            dst[cswz(local_idx<LOGN>(j))] = x[i * BS + k];
+        }
+    }
+}
+
+// one local radix-16 pass (S0 >= R0): this CTA's half only
+template <int LOGN, int S0, bool LAST>
+__device__ __forceinline__ void cfwd_pass(u64* x, u64* __restrict__ g, u64* sm, int rank,
+                                          const ulonglong2* __restrict__ W, u64 q, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
+    const u64 q2 = 2 * q;
+    const int b = rank * ((C::N >> R) / 2) + tid;
+    const int gi = b / TL;
+    const int base = gi * (C::N >> S0) + (b % TL);
+    const int lbase = base - rank * C::HALF;
+#pragma unroll
+    for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+#pragma unroll
+    for (int ls = 0; ls < R; ls++) {
+        const int h = BS >> (ls + 1);
+        const int s = S0 + ls;
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            if (k & h) continue;
+            const ulonglong2 w = W[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const u64 u = csub(x[k], q2);
+            const u64 v = shoup_lazy(x[k + h], w.x, w.y, q);
+            x[k] = u + v;
+            x[k + h] = u - v + q2;
+        }
+    }
+    if constexpr (LAST) {
+        static_assert(TL == 1, "last pass is contiguous");
+#pragma unroll
+        for (int k = 0; k < BS; k += 2) {
+            ulonglong2 v;
+            v.x = csub(csub(x[k], q2), q);
+            v.y = csub(csub(x[k + 1], q2), q);
+            *reinterpret_cast<ulonglong2*>(g + base + k) = v;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < BS; k++) sm[cswz(lbase + k * TL)] = x[k];
+    }
+}
+
+template <int LOGN, int S0>
+__device__ __forceinline__ void cfwd_rest(u64* x, u64* g, u64* sm, int rank, const ulonglong2* __restrict__ W,
+                                          u64 q, int tid) {
+    using C = CCfg<LOGN>;
+    if constexpr (S0 < LOGN) {
+        if constexpr (S0 > C::R0) __syncthreads();
+        cfwd_pass<LOGN, S0, (S0 + C::LOGE >= LOGN)>(x, g, sm, rank, W, q, tid);
+        cfwd_rest<LOGN, S0 + C::LOGE>(x, g, sm, rank, W, q, tid);
+    }
+}
+
+__device__ __forceinline__ bool cskip(const NttArgs& a, int t, int poly) {
+    if (a.skip_alpha <= 0) return false;
+    return t <= a.skip_level && t / a.skip_alpha == poly % a.skip_dnum;
+}
+
+template <int LOGN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<LOGN>::MINB) ntt_fwd_cluster(NttArgs a) {
+    using C = CCfg<LOGN>;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ u64 sm[];
+    const int rank = (int)cluster.block_rank();
+    const int t = blockIdx.x >> 1, poly = blockIdx.y;
+    if (cskip(a, t, poly)) return;          // both CTAs of the cluster skip together
+    u64* peer = cluster.map_shared_rank(sm, rank ^ 1);
+    const int pidx = a.limbs.prime[t];
+    const u64 q = a.pr[pidx].q;
+    const ulonglong2* W = a.tw + (size_t)pidx * 2 * C::N;
+    u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    u64 x[C::E];
+    const int tid = threadIdx.x;
+    cluster.sync();                          // peer SMEM is live before remote stores
+    cfwd_passA<LOGN>(x, g, sm, peer, rank, W, q, tid);
+    cluster.sync();                          // all chunks delivered
+    cfwd_rest<LOGN, C::R0>(x, g, sm, rank, W, q, tid);
+}
+
+// ------------------------------------------------------------------ inverse
+template <int LOGN, int S0, bool FIRST>
+__device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ g, u64* sm, int rank,
+                                          const ulonglong2* __restrict__ Wi, u64 q, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
+    const u64 q2 = 2 * q;
+    const int b = rank * ((C::N >> R) / 2) + tid;
+    const int gi = b / TL;
+    const int base = gi * (C::N >> S0) + (b % TL);
+    const int lbase = base - rank * C::HALF;
+    if constexpr (FIRST) {
+        static_assert(TL == 1, "first inverse pass is contiguous");
+#pragma unroll
+        for (int k = 0; k < BS; k += 2) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + base + k);
+            x[k] = v.x;
+            x[k + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+    }
+#pragma unroll
+    for (int ls = R - 1; ls >= 0; ls--) {
+        const int h = BS >> (ls + 1);
+        const int s = S0 + ls;
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            if (k & h) continue;
+            const ulonglong2 w = Wi[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const u64 u = x[k], v = x[k + h];
+            x[k] = csub(u + v, q2);
+            x[k + h] = shoup_lazy(u - v + q2, w.x, w.y, q);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < BS; k++) sm[cswz(lbase + k * TL)] = x[k];
+}
+
+template <int LOGN, int S0>
+__device__ __forceinline__ void cinv_rest(u64* x, const u64* g, u64* sm, int rank, const ulonglong2* __restrict__ Wi,
+                                          u64 q, int tid) {
+    using C = CCfg<LOGN>;
+    if constexpr (S0 >= C::R0) {
+        cinv_pass<LOGN, S0, (S0 == LOGN - C::LOGE)>(x, g, sm, rank, Wi, q, tid);
+        if constexpr (S0 - C::LOGE >= C::R0) __syncthreads();
+        cinv_rest<LOGN, S0 - C::LOGE>(x, g, sm, rank, Wi, q, tid);
+    }
+}
+
+template <int LOGN>
+__device__ __forceinline__ void cinv_passA(u64* x, u64* __restrict__ g, u64* sm, u64* peer, int rank,
+                                           const ulonglong2* __restrict__ Wi, u64 q, u64 ninv, u64 ninv_p, u64 wn,
+                                           u64 wn_p, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
+    const u64 q2 = 2 * q;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = rank * (TL / 2) + tid + i * C::T;
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = b + k * TL;
+            const u64* src = owner<LOGN>(j) == rank ? sm : peer;
+            x[i * BS + k] = src[cswz(local_idx<LOGN>(j))];
+        }
+#pragma unroll
+        for (int ls = R - 1; ls >= 0; ls--) {
+            const int h = BS >> (ls + 1);
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                if (k & h) continue;
+                const u64 u = x[i * BS + k], v = x[i * BS + k + h];
+                if (ls == 0) {
+                    x[i * BS + k] = shoup(u + v, ninv, ninv_p, q);
+                    x[i * BS + k + h] = shoup(u - v + q2, wn, wn_p, q);
+                } else {
+                    const ulonglong2 w = Wi[(1 << ls) + (k >> (R - ls))];
+                    x[i * BS + k] = csub(u + v, q2);
+                    x[i * BS + k + h] = shoup_lazy(u - v + q2, w.x, w.y, q);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BS; k++) g[b + k * TL] = x[i * BS + k];
+    }
+}
+
+template <int LOGN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<LOGN>::MINB) ntt_inv_cluster(NttArgs a) {
+    using C = CCfg<LOGN>;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ u64 sm[];
+    const int rank = (int)cluster.block_rank();
+    const int t = blockIdx.x >> 1, poly = blockIdx.y;
+    u64* peer = cluster.map_shared_rank(sm, rank ^ 1);
+    const int pidx = a.limbs.prime[t];
+    const PrimeInfo& P = a.pr[pidx];
+    const u64 q = P.q;
+    const ulonglong2* Wi = a.tw + (size_t)pidx * 2 * C::N + C::N;
+    u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    u64 x[C::E];
+    const int tid = threadIdx.x;
+    cinv_rest<LOGN, LOGN - C::LOGE>(x, g, sm, rank, Wi, q, tid);
+    cluster.sync();                          // both halves complete
+    const ulonglong2 wn = Wi[0];
+    cinv_passA<LOGN>(x, g, sm, peer, rank, Wi, q, P.pad[0], P.pad[1], wn.x, wn.y, tid);
+    cluster.sync();                          // peer finished reading our SMEM
+}
+
+template <int LOGN>
+static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
+    using C = CCfg<LOGN>;
+    const size_t smem = (size_t)C::HALF * sizeof(u64);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid(2 * nlimbs, npolys);
+    if (inverse) ntt_inv_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
+    else ntt_fwd_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
+    return launched();
+}
+
+cudaError_t ntt_cluster_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
+    if (nlimbs <= 0 || npolys <= 0) return cudaSuccess;
+    if (logn == 13) return launch_cluster<13>(inverse, a, nlimbs, npolys, st);
+    if (logn == 14) return launch_cluster<14>(inverse, a, nlimbs, npolys, st);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace bcn

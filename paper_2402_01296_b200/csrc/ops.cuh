@@ -30,6 +30,7 @@ struct NttArgs {
 };
 
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
+cudaError_t ntt_cluster_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
 
 cudaError_t binary_op(int op, u64* out, long long os, const u64* a, long long as, const u64* b, long long bs,
                       int npoly, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st);
