@@ -87,6 +87,12 @@ int bcn_encode_ext(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int 
 int bcn_encrypt(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int G, int level, double scale,
                 uint64_t counter0, uint64_t *ct_out, void *stream);
 
+/* same, with the Philox id base read from DEVICE memory (*counter_dev) when the
+ * kernels run -- lets a captured CUDA graph encrypt with fresh randomness on
+ * every replay */
+int bcn_encrypt_devctr(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int G, int level, double scale,
+                       const uint64_t *counter_dev, uint64_t *ct_out, void *stream);
+
 /* ---- K11: decrypt_vector (sim.py:192-196): c0 + c1 s, INTT, CRT, FFT.
  * out: f64[G][nout] real slot values (nout <= N/2). */
 int bcn_decrypt(bcn_ctx *ctx, const uint64_t *ct, int ct_nlimb, int G, int level, double scale, double *out,

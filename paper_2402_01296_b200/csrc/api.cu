@@ -425,8 +425,8 @@ int bcn_encode_ext(bcn_ctx* c, const double* vals, int vlen, int vstride, int np
     return BCN_OK;
 }
 
-int bcn_encrypt(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
-                uint64_t counter0, uint64_t* ct, void* stream) {
+static int encrypt_impl(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
+                        uint64_t counter0, const uint64_t* counter_dev, uint64_t* ct, void* stream) {
     int e = check_level(c, level);
     if (e) return e;
     if (vlen > c->N / 2) return fail(BCN_ERR_CAPACITY, "vector exceeds slot count");
@@ -435,10 +435,21 @@ int bcn_encrypt(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, in
     Limbs l = limbs_range(0, nl);
     const long long cs = 2LL * nl * c->N;
     CUDA_TRY(encode_op((u64*)ct, cs, vals, vlen, vstride, G, scale, c->logn, l, c->pr, fft_tab(c), 1, c->seed,
-                       counter0, st));
+                       counter0, st, (const u64*)counter_dev));
     CUDA_TRY(ntt_run(c, false, (u64*)ct, cs, l, G, st));
-    CUDA_TRY(encrypt_combine_op((u64*)ct, G, nl, c->logn, l, c->pr, c->s_mont, c->seed, counter0, st));
+    CUDA_TRY(encrypt_combine_op((u64*)ct, G, nl, c->logn, l, c->pr, c->s_mont, c->seed, counter0, st,
+                                (const u64*)counter_dev));
     return BCN_OK;
+}
+
+int bcn_encrypt(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
+                uint64_t counter0, uint64_t* ct, void* stream) {
+    return encrypt_impl(c, vals, vlen, vstride, G, level, scale, counter0, nullptr, ct, stream);
+}
+
+int bcn_encrypt_devctr(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
+                       const uint64_t* counter_dev, uint64_t* ct, void* stream) {
+    return encrypt_impl(c, vals, vlen, vstride, G, level, scale, 0, counter_dev, ct, stream);
 }
 
 static int decrypt_poly_impl(bcn_ctx* c, const uint64_t* ct, int ct_nlimb, int G, int level, u64* out,

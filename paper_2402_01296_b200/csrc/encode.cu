@@ -15,9 +15,10 @@ namespace bcn {
 // out[p][t][i] = round(scale * m_i) (+ e_i) mod q_t, coefficient domain.
 __global__ void encode_kernel(u64* __restrict__ out, long long os, const double* __restrict__ vals, int vlen,
                               long long vs, double scale, int logn, Limbs limbs, const PrimeInfo* __restrict__ pr,
-                              FftTab ft, int add_err, u64 seed, u64 id_base) {
+                              FftTab ft, int add_err, u64 seed, u64 id_base, const u64* __restrict__ id_dev) {
     extern __shared__ double fsm[];
     const int N = 1 << logn, S = N >> 1, M = N << 1, logs = logn - 1;
+    if (id_dev) id_base = *id_dev;   // graph replays: the encryption counter lives in device memory
     double* xr = fsm;
     double* xi = fsm + S;
     const int p = blockIdx.x;
@@ -65,7 +66,7 @@ __global__ void encode_kernel(u64* __restrict__ out, long long os, const double*
 
 cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long long vs, int nplain, double scale,
                       int logn, const Limbs& limbs, const PrimeInfo* pr, const FftTab& ft, int add_err, u64 seed,
-                      u64 id_base, cudaStream_t st) {
+                      u64 id_base, cudaStream_t st, const u64* id_dev) {
     if (!nplain) return cudaSuccess;
     const int N = 1 << logn;
     const size_t smem = (size_t)N * sizeof(double);
@@ -73,7 +74,7 @@ cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long
     if (!cfg) { cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
     int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
     encode_kernel<<<nplain, tpb, smem, st>>>(out, os, vals, vlen, vs, scale, logn, limbs, pr, ft, add_err, seed,
-                                             id_base);
+                                             id_base, id_dev);
     return launched();
 }
 
@@ -211,8 +212,9 @@ cudaError_t sample_small_op(u64* out, long long os, int npoly, int nlimb, int lo
 // ct: [G][2][L][N]; c0 holds NTT(m + e) on entry.  c1 = a, c0 -= a s.
 __global__ void encrypt_combine_kernel(u64* __restrict__ ct, int nlimb, int logn, Limbs limbs,
                                        const PrimeInfo* __restrict__ pr, const u64* __restrict__ s_mont, u64 seed,
-                                       u64 id_base, long long total) {
+                                       u64 id_base, long long total, const u64* __restrict__ id_dev) {
     const int N = 1 << logn;
+    if (id_dev) id_base = *id_dev;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const int n = (int)(idx & (N - 1));
@@ -230,11 +232,11 @@ __global__ void encrypt_combine_kernel(u64* __restrict__ ct, int nlimb, int logn
 }
 
 cudaError_t encrypt_combine_op(u64* ct, int G, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr,
-                               const u64* s_mont, u64 seed, u64 id_base, cudaStream_t st) {
+                               const u64* s_mont, u64 seed, u64 id_base, cudaStream_t st, const u64* id_dev) {
     long long total = (long long)G * nlimb << logn;
     if (!total) return cudaSuccess;
     encrypt_combine_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(ct, nlimb, logn, limbs, pr, s_mont, seed,
-                                                                       id_base, total);
+                                                                       id_base, total, id_dev);
     return launched();
 }
 

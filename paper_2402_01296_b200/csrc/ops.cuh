@@ -110,7 +110,7 @@ struct FftTab {
 };
 cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long long vs, int nplain, double scale,
                       int logn, const Limbs& limbs, const PrimeInfo* pr, const FftTab& ft, int add_err, u64 seed,
-                      u64 id_base, cudaStream_t st);
+                      u64 id_base, cudaStream_t st, const u64* id_dev = nullptr);
 cudaError_t decode_op(double* out, int nout, const u64* poly, long long ps, int k, int npoly, double scale, int logn,
                       const PrimeInfo* pr, const FftTab& ft, u64 q0inv_mod_q1, u64 q0inv_p, cudaStream_t st);
 cudaError_t sample_uniform_op(u64* out, long long os, int npoly, int nlimb, int logn, const Limbs& limbs,
@@ -119,7 +119,8 @@ cudaError_t sample_small_op(u64* out, long long os, int npoly, int nlimb, int lo
                             const PrimeInfo* pr, u64 seed, u32 domain, u64 id_base, u64 id_step, int ternary,
                             cudaStream_t st);
 cudaError_t encrypt_combine_op(u64* ct, int G, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr,
-                               const u64* s_mont, u64 seed, u64 id_base, cudaStream_t st);
+                               const u64* s_mont, u64 seed, u64 id_base, cudaStream_t st,
+                               const u64* id_dev = nullptr);
 cudaError_t ksk_digit_op(u64* b_out, u64* a_out, const u64* e_ntt, const u64* s_mont, const u64* sprime,
                          int nbasis, int d0, int d1, int logn, const PrimeInfo* pr, const u64* pmod, u64 seed,
                          u64 kid, cudaStream_t st);

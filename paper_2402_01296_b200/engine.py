@@ -53,6 +53,7 @@ class Engine:
         _lib.call("bcn_ctx_set_fft", h, re.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                   im.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
         self._counter = 1   # Philox id of the next encryption
+        self.graph_counter: torch.Tensor | None = None   # device-side id base (CUDA-graph replays)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -123,8 +124,13 @@ class Engine:
         if v.shape[1] > self.N // 2:
             raise CapacityError(f"vector of length {v.shape[1]} exceeds {self.N // 2} slots")
         G = v.shape[0]
-        counter = self.next_counter(G) if counter is None else counter
         ct = self.empty_ct(G, level)
+        if self.graph_counter is not None and counter is None:
+            # CUDA-graph mode: the Philox id base is read from device memory at run time
+            _lib.call("bcn_encrypt_devctr", self._h, _ptr(v), v.shape[1], v.shape[1], G, level, float(scale),
+                      _ptr(self.graph_counter), _ptr(ct), _stream())
+            return ct
+        counter = self.next_counter(G) if counter is None else counter
         _lib.call("bcn_encrypt", self._h, _ptr(v), v.shape[1], v.shape[1], G, level, float(scale), counter,
                   _ptr(ct), _stream())
         return ct

@@ -35,6 +35,30 @@ class WeightCache:
         return t
 
 
+_INDEX: dict = {}
+
+
+def index_tensor(key, make, device) -> torch.Tensor:
+    """Device copy of a static index vector (slot anchors), uploaded once --
+    keeps host->device copies out of steady-state forwards and CUDA graphs."""
+    k = (key, str(device))
+    t = _INDEX.get(k)
+    if t is None:
+        t = torch.as_tensor(np.asarray(make(), dtype=np.int64), device=device)
+        _INDEX[k] = t
+    return t
+
+
+def weight_cache(ctx, weights) -> "WeightCache":
+    """One WeightCache per (context, archive): weights are uploaded once."""
+    caches = ctx.__dict__.setdefault("_weight_caches", {})
+    wc = caches.get(id(weights))
+    if wc is None or wc.weights is not weights:
+        wc = WeightCache(weights, ctx.engine.device)
+        caches[id(weights)] = wc
+    return wc
+
+
 def to_device(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=torch.float64)

@@ -361,7 +361,8 @@ def encrypt_vector(v: PlainLike, ctx: HeContext) -> Ciphertext:
             raise ParameterError("plaintext vector must contain only finite values")
     else:
         import torch
-        if not bool(torch.isfinite(rows).all()):
+        # (no host sync while a CUDA graph is being captured; graph inputs are checked at replay)
+        if not torch.cuda.is_current_stream_capturing() and not bool(torch.isfinite(rows).all()):
             raise ParameterError("plaintext vector must contain only finite values")
     eng = ctx.engine
     data = eng.encrypt(rows, ctx.max_level, ctx.delta)

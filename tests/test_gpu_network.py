@@ -89,3 +89,25 @@ def test_cifar3_group_batching_equals_single_sets():
     logits = res.decrypt_logits()
     assert logits.shape == (7, 10)
     _check(logits, d["logits_ref"][:7])
+
+
+def test_graphed_single_image_forward_matches_reference():
+    """CUDA-graph replay of the cnn3 1-image forward (config 1): fresh
+    encryption randomness per replay, same logits as the reference."""
+    from paper_2402_01296_b200.graphs import GraphedForward
+
+    d, w, dec, meta = _load("cnn3_cfg1")
+    bundle = B.get("cnn3")
+    ctx = B.make_context(8192, B.required_levels(bundle) + 1, 2.0 ** 50)
+    gf = GraphedForward(bundle.bi, w, ctx, (1, 1, 14, 14), (1, 1, 28, 28), strategy="hw")
+    assert gf.recorder.snapshot() == meta["counts_hw"]
+    out1 = gf(d["sens"], d["full"])
+    _check(out1, d["logits_ref"])
+    d2, w2, dec2, _ = _load("cnn3_fixture")          # different inputs, same graph
+    sens2 = d2["sens"][:1]
+    full2 = d2["full"][:1]
+    ref2 = B.reference_forward(bundle.bi, [DecomposedInput(sens2[0], full2[0], (7, 7, 14, 14))], w)
+    _check(gf(sens2, full2), ref2)
+    out3 = gf(d["sens"], d["full"])
+    _check(out3, d["logits_ref"])
+    assert not np.array_equal(out1, out3)            # fresh encryption noise on every replay
