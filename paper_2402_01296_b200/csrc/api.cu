@@ -3,6 +3,7 @@
 // the native runtime behind paper_2402_01296_b200/sim.py; it never touches
 // host data on the hot path and never falls back to the CPU.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -67,6 +68,7 @@ struct LevelTables {
     ConvTable* moddown = nullptr;   // [1]
     u64* pinv = nullptr;            // [2 * (level+1)] Shoup pairs of P^-1 mod q_i
     u64* qlinv = nullptr;           // [2 * level] Shoup pairs of q_level^-1 mod q_i
+    u64* qtopmod = nullptr;         // [level] q_level mod q_i (fused rescale lift)
     int ndig = 0;
 };
 
@@ -145,7 +147,34 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.skip_alpha = 0;
     a.skip_dnum = 1;
     a.skip_level = 0;
+    a.src = nullptr;
+    a.src_poly_stride = 0;
+    a.src_limb_stride = 0;
+    a.pro = 0;
+    a.pro_src = nullptr;
+    a.pro_stride = 0;
+    a.pro_qtop = 0;
+    a.pro_tab = nullptr;
+    a.epi = 0;
+    a.epi_c = nullptr;
+    a.epi_cps = a.epi_cls = 0;
+    a.epi_tab = nullptr;
     return a;
+}
+
+static bool getenv_flag_off(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] == '0';
+}
+
+// out-of-place transform: read limb t of poly p at src + p*src_ps + t*src_ls, write dst (packed)
+static cudaError_t ntt_run_src(const bcn_ctx* c, bool inv, u64* dst, long long dst_ps, const u64* src, long long src_ps,
+                               long long src_ls, const Limbs& l, int npoly, cudaStream_t st) {
+    NttArgs a = ntt_args(c, dst, dst_ps, l);
+    a.src = src;
+    a.src_poly_stride = src_ps;
+    a.src_limb_stride = src_ls;
+    return ntt_launch(inv, c->logn, a, l.n, npoly, st);
 }
 
 static cudaError_t ntt_run(const bcn_ctx* c, bool inv, u64* data, long long poly_stride, const Limbs& l, int npoly,
@@ -218,6 +247,13 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
     CUDA_TRY(dmalloc((void**)&T.moddown, sizeof(ConvTable), &c->table_bytes));
     CUDA_TRY(dmalloc((void**)&T.pinv, sizeof(u64) * pinv.size(), &c->table_bytes));
     CUDA_TRY(dmalloc((void**)&T.qlinv, sizeof(u64) * qlinv.size(), &c->table_bytes));
+    std::vector<u64> qtm(2 * std::max(level, 1));
+    for (int i = 0; i < level; i++) {
+        qtm[2 * i] = c->primes[level] % c->primes[i];
+        qtm[2 * i + 1] = (u64)(((u128)1 << 64) / c->primes[i]);   // Shoup companion of 1
+    }
+    CUDA_TRY(dmalloc((void**)&T.qtopmod, sizeof(u64) * qtm.size(), &c->table_bytes));
+    CUDA_TRY(cudaMemcpy(T.qtopmod, qtm.data(), sizeof(u64) * qtm.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(T.modup, up.data(), sizeof(ConvTable) * ndig, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(T.moddown, &down, sizeof(ConvTable), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(T.pinv, pinv.data(), sizeof(u64) * pinv.size(), cudaMemcpyHostToDevice));
@@ -225,6 +261,38 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
     c->lt[level] = T;
     *out = &c->lt[level];
     return BCN_OK;
+}
+
+
+// rescale by q_level of npoly polys: in (poly stride in_ps, level+1 limbs) -> out
+// (poly stride level*N).  N = 2^13 / 2^14: INTT of the top limb + ONE fused
+// cluster NTT whose prologue does the centred lift and whose epilogue does
+// (c - x) * q_level^-1 (no intermediate in HBM); other N: the staged kernels.
+static cudaError_t rescale_tail(const bcn_ctx* c, u64* out, const u64* in, long long in_ps, int npoly, int level,
+                                u64* top, u64* W, const LevelTables* T, cudaStream_t st) {
+    const long long N = c->N;
+    cudaError_t e = ntt_run_src(c, true, top, N, in + (size_t)level * N, in_ps, N, limbs_range(level, 1), npoly, st);
+    if (e != cudaSuccess) return e;
+    Limbs ql = limbs_range(0, level);
+    if ((c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_RESCALE")) {
+        NttArgs a = ntt_args(c, out, (long long)level * N, ql);
+        a.pro = 1;
+        a.pro_src = top;
+        a.pro_stride = N;
+        a.pro_qtop = c->primes[level];
+        a.pro_tab = T->qtopmod;
+        a.epi = 1;
+        a.epi_c = in;
+        a.epi_cps = in_ps;
+        a.epi_cls = N;
+        a.epi_tab = T->qlinv;
+        return ntt_launch(false, c->logn, a, level, npoly, st);
+    }
+    e = rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st);
+    if (e != cudaSuccess) return e;
+    e = ntt_run(c, false, W, (long long)level * N, ql, npoly, st);
+    if (e != cudaSuccess) return e;
+    return rescale_combine_op(out, (long long)level * N, in, in_ps, W, npoly, level, c->logn, ql, c->pr, T->qlinv, st);
 }
 
 static int check_level(const bcn_ctx* c, int level) {
@@ -531,13 +599,7 @@ static int rescale_impl(bcn_ctx* c, u64* out, const u64* in, int in_nlimb, int G
     u64* top = scratch_get(c, (size_t)npoly * N * (1 + level), &err);
     if (!top) return err;
     u64* W = top + (size_t)npoly * N;
-    CUDA_TRY(gather_limb_op(top, in, (long long)in_nlimb * N, (long long)level * N, npoly, c->logn, st));
-    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
-    Limbs ql = limbs_range(0, level);
-    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
-    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
-    CUDA_TRY(rescale_combine_op(out, (long long)level * N, in, (long long)in_nlimb * N, W, npoly, level, c->logn, ql,
-                                c->pr, T->qlinv, st));
+    CUDA_TRY(rescale_tail(c, out, in, (long long)in_nlimb * N, npoly, level, top, W, T, st));
     return BCN_OK;
 }
 
@@ -575,13 +637,7 @@ static int mul_plain_impl(bcn_ctx* c, u64* out, const u64* ct, int ct_nlimb, con
     const int npoly = 2 * G;
     u64* top = prod + (size_t)G * 2 * nl * N;
     u64* W = top + (size_t)npoly * N;
-    CUDA_TRY(gather_limb_op(top, prod, nl * N, (long long)level * N, npoly, c->logn, st));
-    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
-    Limbs ql = limbs_range(0, level);
-    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
-    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
-    CUDA_TRY(rescale_combine_op(out, (long long)level * N, prod, nl * N, W, npoly, level, c->logn, ql, c->pr,
-                                T->qlinv, st));
+    CUDA_TRY(rescale_tail(c, out, prod, nl * N, npoly, level, top, W, T, st));
     return BCN_OK;
 }
 
@@ -642,13 +698,7 @@ int bcn_mac_multi(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint6
     const int npoly = 2 * n_out * G;
     u64* top = acc + (size_t)n_out * cw;
     u64* W = top + (size_t)npoly * N;
-    CUDA_TRY(gather_limb_op(top, acc, nl * N, (long long)level * N, npoly, c->logn, st));
-    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
-    Limbs ql = limbs_range(0, level);
-    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
-    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
-    CUDA_TRY(rescale_combine_op((u64*)out, (long long)level * N, acc, nl * N, W, npoly, level, c->logn, ql, c->pr,
-                                LT->qlinv, st));
+    CUDA_TRY(rescale_tail(c, (u64*)out, acc, nl * N, npoly, level, top, W, LT, st));
     return BCN_OK;
 }
 
@@ -691,13 +741,7 @@ static int mac_terms_impl(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t
     const int npoly = 2 * G;
     u64* top = acc + (size_t)G * 2 * nl * N;
     u64* W = top + (size_t)npoly * N;
-    CUDA_TRY(gather_limb_op(top, acc, nl * N, (long long)level * N, npoly, c->logn, st));
-    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
-    Limbs ql = limbs_range(0, level);
-    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
-    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
-    CUDA_TRY(rescale_combine_op((u64*)out, (long long)level * N, acc, nl * N, W, npoly, level, c->logn, ql, c->pr,
-                                LT->qlinv, st));
+    CUDA_TRY(rescale_tail(c, (u64*)out, acc, nl * N, npoly, level, top, W, LT, st));
     return BCN_OK;
 }
 
@@ -802,18 +846,9 @@ static int modup_impl(bcn_ctx* c, u64* U, const u64* x, long long x_stride, int 
     const int nl = level + 1, next = nl + c->K, ndig = T->ndig;
     Limbs ql = limbs_range(0, nl);
     // coefficient-domain copy of x
-    CUDA_TRY(copy_limbs_op(tmp, nl * N, x, x_stride, G, nl * N, st));
-    CUDA_TRY(ntt_run(c, true, tmp, nl * N, ql, G, st));
+    CUDA_TRY(ntt_run_src(c, true, tmp, nl * N, x, x_stride, N, ql, G, st));     // coefficient form of x
     Limbs ext = limbs_ext(c, level);
-    // x_ntt is read from x itself (stride x_stride); x_coef from tmp (stride nl*N): pass both with the same stride
-    // by staging: modup kernel takes one stride, so copy x_ntt next to tmp when strides differ.
-    const u64* xn = x;
-    if (x_stride != nl * N) {
-        u64* xn2 = tmp + (size_t)G * nl * N;
-        CUDA_TRY(copy_limbs_op(xn2, nl * N, x, x_stride, G, nl * N, st));
-        xn = xn2;
-    }
-    CUDA_TRY(modup_op(U, tmp, xn, nl * N, G, nl, next, c->alpha, ndig, c->logn, ext, c->pr, T->modup, st));
+    CUDA_TRY(modup_op(U, tmp, nl * N, x, x_stride, G, nl, next, c->alpha, ndig, c->logn, ext, c->pr, T->modup, st));
     NttArgs a = ntt_args(c, U, (long long)next * N, ext);
     a.skip_alpha = c->alpha;
     a.skip_dnum = ndig;
@@ -1008,13 +1043,7 @@ int bcn_mul_cc(bcn_ctx* c, uint64_t* out, const uint64_t* a, int a_nlimb, const 
     u64* top = tmp;
     u64* W = top + (size_t)2 * G * N;
     const int npoly = 2 * G;
-    CUDA_TRY(gather_limb_op(top, R, nl * N, (long long)level * N, npoly, c->logn, st));
-    CUDA_TRY(ntt_run(c, true, top, N, limbs_range(level, 1), npoly, st));
-    Limbs ql = limbs_range(0, level);
-    CUDA_TRY(rescale_lift_op(W, top, npoly, level, c->primes[level], c->logn, ql, c->pr, st));
-    CUDA_TRY(ntt_run(c, false, W, (long long)level * N, ql, npoly, st));
-    CUDA_TRY(rescale_combine_op((u64*)out, (long long)level * N, R, nl * N, W, npoly, level, c->logn, ql, c->pr,
-                                T->qlinv, st));
+    CUDA_TRY(rescale_tail(c, (u64*)out, R, nl * N, npoly, level, top, W, T, st));
     return BCN_OK;
 }
 

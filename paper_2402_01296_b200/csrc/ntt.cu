@@ -113,15 +113,16 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_fwd_kernel(NttArgs a) {
     const u64 q = a.pr[pidx].q;
     const ulonglong2* W = a.tw + (size_t)pidx * 2 * C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
     u64 x[C::E];
     const int tid = threadIdx.x;
-    fwd_pass<LOGN, 0, C::R0, true, (C::R0 >= LOGN)>(x, g, sm, W, q, tid);
+    fwd_pass<LOGN, 0, C::R0, true, (C::R0 >= LOGN)>(x, const_cast<u64*>(gin), sm, W, q, tid);
     fwd_rest<LOGN, C::R0>(x, g, sm, W, q, tid);
 }
 
 // ---------------------------------------------------------------- inverse
 template <int LOGN, int S0, int R, bool LAST, bool FIRST = false>
-__device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, u64* sm,
+__device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, const u64* __restrict__ gin, u64* sm,
                                          const ulonglong2* __restrict__ Wi, u64 q,
                                          u64 ninv, u64 ninv_p, u64 wn, u64 wn_p, int tid) {
     using C = NttCfg<LOGN>;
@@ -137,7 +138,7 @@ __device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, u64* sm,
         if constexpr (FIRST && TL == 1) {
 #pragma unroll
             for (int k = 0; k < BS; k += 2) {
-                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + base + k);
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + base + k);
                 x[i * BS + k] = v.x;
                 x[i * BS + k + 1] = v.y;
             }
@@ -174,13 +175,14 @@ __device__ __forceinline__ void inv_pass(u64* x, u64* __restrict__ g, u64* sm,
 }
 
 template <int LOGN, int S0>
-__device__ __forceinline__ void inv_rest(u64* x, u64* g, u64* sm, const ulonglong2* __restrict__ Wi, u64 q,
-                                         u64 ninv, u64 ninv_p, u64 wn, u64 wn_p, int tid) {
+__device__ __forceinline__ void inv_rest(u64* x, u64* g, const u64* gin, u64* sm, const ulonglong2* __restrict__ Wi,
+                                         u64 q, u64 ninv, u64 ninv_p, u64 wn, u64 wn_p, int tid) {
     using C = NttCfg<LOGN>;
     if constexpr (S0 >= C::R0) {
-        inv_pass<LOGN, S0, C::LOGE, false, (S0 == LOGN - C::LOGE)>(x, g, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
+        inv_pass<LOGN, S0, C::LOGE, false, (S0 == LOGN - C::LOGE)>(x, g, gin, sm, Wi, q, ninv, ninv_p, wn, wn_p,
+                                                                    tid);
         __syncthreads();
-        inv_rest<LOGN, S0 - C::LOGE>(x, g, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
+        inv_rest<LOGN, S0 - C::LOGE>(x, g, gin, sm, Wi, q, ninv, ninv_p, wn, wn_p, tid);
     }
 }
 
@@ -194,12 +196,13 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_inv_kernel(NttArgs a) {
     const u64 q = P.q;
     const ulonglong2* Wi = a.tw + (size_t)pidx * 2 * C::N + C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
     const int tid = threadIdx.x;
     u64 x[C::E];
     const u64 ninv = P.pad[0], ninv_p = P.pad[1];
     const ulonglong2 wn = Wi[0];   // slot 0 of the inverse table holds {w1 n^-1, shoup}
-    inv_rest<LOGN, LOGN - C::LOGE>(x, g, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
-    inv_pass<LOGN, 0, C::R0, true>(x, g, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
+    inv_rest<LOGN, LOGN - C::LOGE>(x, g, gin, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
+    inv_pass<LOGN, 0, C::R0, true>(x, g, gin, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
 }
 
 template <int LOGN>

@@ -40,9 +40,35 @@ __device__ __forceinline__ int cswz(int j) { return j ^ ((j >> 4) & 15); }
 template <int LOGN> __device__ __forceinline__ int owner(int j) { return j >> (LOGN - 1); }
 template <int LOGN> __device__ __forceinline__ int local_idx(int j) { return j & ((1 << (LOGN - 1)) - 1); }
 
+// fused prologue: the value the forward transform reads at position j
+template <int MODE>
+struct Prologue {             // MODE 0 plain, 1 rescale lift
+    const u64* src;           // mode 0: the limb; mode 1: the coefficient-form top limb of this poly
+    u64 q, qtop, qtop_mod_q, inv_p;   // inv_p = floor(2^64 / q): v mod q by a Shoup multiply by 1
+    __device__ __forceinline__ u64 operator()(int j) const {
+        if constexpr (MODE == 0) return src[j];
+        const u64 v = src[j];                       // canonical mod qtop, centred lift -> mod q
+        u64 r = shoup(v, 1ull, inv_p, q);
+        if (v > (qtop >> 1)) r = sub_mod(r, qtop_mod_q, q);
+        return r;
+    }
+};
+
+// fused epilogue: what the forward transform writes for canonical result v at j
+template <int MODE>
+struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top^-1
+    u64* out;
+    const u64* c;
+    u64 q, w, wp;
+    __device__ __forceinline__ u64 operator()(int j, u64 v) const {
+        if constexpr (MODE == 0) return v;
+        else return shoup(c[j] + q - v, w, wp, q);
+    }
+};
+
 // ------------------------------------------------------------------ forward
-template <int LOGN>
-__device__ __forceinline__ void cfwd_passA(u64* x, const u64* __restrict__ g, u64* sm, u64* peer, int rank,
+template <int LOGN, class PRO>
+__device__ __forceinline__ void cfwd_passA(u64* x, const PRO& pro, u64* sm, u64* peer, int rank,
                                            const ulonglong2* __restrict__ W, u64 q, int tid) {
     using C = CCfg<LOGN>;
     constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
@@ -51,7 +77,7 @@ __device__ __forceinline__ void cfwd_passA(u64* x, const u64* __restrict__ g, u6
     for (int i = 0; i < NB; i++) {
         const int b = rank * (TL / 2) + tid + i * C::T;    // gi == 0 for S0 == 0
 #pragma unroll
-        for (int k = 0; k < BS; k++) x[i * BS + k] = g[b + k * TL];
+        for (int k = 0; k < BS; k++) x[i * BS + k] = pro(b + k * TL);
 #pragma unroll
         for (int ls = 0; ls < R; ls++) {
             const int h = BS >> (ls + 1);
@@ -76,8 +102,8 @@ __device__ __forceinline__ void cfwd_passA(u64* x, const u64* __restrict__ g, u6
 }
 
 // one local radix-16 pass (S0 >= R0): this CTA's half only
-template <int LOGN, int S0, bool LAST>
-__device__ __forceinline__ void cfwd_pass(u64* x, u64* __restrict__ g, u64* sm, int rank,
+template <int LOGN, int S0, bool LAST, class EPI>
+__device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int rank,
                                           const ulonglong2* __restrict__ W, u64 q, int tid) {
     using C = CCfg<LOGN>;
     constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
@@ -107,9 +133,9 @@ __device__ __forceinline__ void cfwd_pass(u64* x, u64* __restrict__ g, u64* sm, 
 #pragma unroll
         for (int k = 0; k < BS; k += 2) {
             ulonglong2 v;
-            v.x = csub(csub(x[k], q2), q);
-            v.y = csub(csub(x[k + 1], q2), q);
-            *reinterpret_cast<ulonglong2*>(g + base + k) = v;
+            v.x = epi(base + k, csub(csub(x[k], q2), q));
+            v.y = epi(base + k + 1, csub(csub(x[k + 1], q2), q));
+            *reinterpret_cast<ulonglong2*>(epi.out + base + k) = v;
         }
     } else {
 #pragma unroll
@@ -117,14 +143,14 @@ __device__ __forceinline__ void cfwd_pass(u64* x, u64* __restrict__ g, u64* sm, 
     }
 }
 
-template <int LOGN, int S0>
-__device__ __forceinline__ void cfwd_rest(u64* x, u64* g, u64* sm, int rank, const ulonglong2* __restrict__ W,
-                                          u64 q, int tid) {
+template <int LOGN, int S0, class EPI>
+__device__ __forceinline__ void cfwd_rest(u64* x, const EPI& epi, u64* sm, int rank,
+                                          const ulonglong2* __restrict__ W, u64 q, int tid) {
     using C = CCfg<LOGN>;
     if constexpr (S0 < LOGN) {
         if constexpr (S0 > C::R0) __syncthreads();
-        cfwd_pass<LOGN, S0, (S0 + C::LOGE >= LOGN)>(x, g, sm, rank, W, q, tid);
-        cfwd_rest<LOGN, S0 + C::LOGE>(x, g, sm, rank, W, q, tid);
+        cfwd_pass<LOGN, S0, (S0 + C::LOGE >= LOGN), EPI>(x, epi, sm, rank, W, q, tid);
+        cfwd_rest<LOGN, S0 + C::LOGE, EPI>(x, epi, sm, rank, W, q, tid);
     }
 }
 
@@ -133,7 +159,7 @@ __device__ __forceinline__ bool cskip(const NttArgs& a, int t, int poly) {
     return t <= a.skip_level && t / a.skip_alpha == poly % a.skip_dnum;
 }
 
-template <int LOGN>
+template <int LOGN, int PM, int EM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<LOGN>::MINB) ntt_fwd_cluster(NttArgs a) {
     using C = CCfg<LOGN>;
     cg::cluster_group cluster = cg::this_cluster();
@@ -146,17 +172,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
     const u64 q = a.pr[pidx].q;
     const ulonglong2* W = a.tw + (size_t)pidx * 2 * C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
+    Prologue<PM> pro;
+    pro.q = q;
+    if constexpr (PM == 1) {
+        pro.src = a.pro_src + (size_t)poly * a.pro_stride;
+        pro.qtop = a.pro_qtop;
+        pro.qtop_mod_q = a.pro_tab[2 * t];
+        pro.inv_p = a.pro_tab[2 * t + 1];
+    } else {
+        pro.src = gin;
+        pro.qtop = pro.qtop_mod_q = pro.inv_p = 0;
+    }
+    Epilogue<EM> epi;
+    epi.out = g;
+    epi.q = q;
+    if constexpr (EM == 1) {
+        epi.c = a.epi_c + (size_t)poly * a.epi_cps + (size_t)t * a.epi_cls;
+        epi.w = a.epi_tab[2 * t];
+        epi.wp = a.epi_tab[2 * t + 1];
+    } else {
+        epi.c = nullptr;
+        epi.w = epi.wp = 0;
+    }
     u64 x[C::E];
     const int tid = threadIdx.x;
     cluster.sync();                          // peer SMEM is live before remote stores
-    cfwd_passA<LOGN>(x, g, sm, peer, rank, W, q, tid);
+    cfwd_passA<LOGN, Prologue<PM>>(x, pro, sm, peer, rank, W, q, tid);
     cluster.sync();                          // all chunks delivered
-    cfwd_rest<LOGN, C::R0>(x, g, sm, rank, W, q, tid);
+    cfwd_rest<LOGN, C::R0, Epilogue<EM>>(x, epi, sm, rank, W, q, tid);
 }
 
 // ------------------------------------------------------------------ inverse
 template <int LOGN, int S0, bool FIRST>
-__device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ g, u64* sm, int rank,
+__device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ gin, u64* sm, int rank,
                                           const ulonglong2* __restrict__ Wi, u64 q, int tid) {
     using C = CCfg<LOGN>;
     constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
@@ -169,7 +218,7 @@ __device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ g, u64
         static_assert(TL == 1, "first inverse pass is contiguous");
 #pragma unroll
         for (int k = 0; k < BS; k += 2) {
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(g + base + k);
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + base + k);
             x[k] = v.x;
             x[k + 1] = v.y;
         }
@@ -195,13 +244,13 @@ __device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ g, u64
 }
 
 template <int LOGN, int S0>
-__device__ __forceinline__ void cinv_rest(u64* x, const u64* g, u64* sm, int rank, const ulonglong2* __restrict__ Wi,
+__device__ __forceinline__ void cinv_rest(u64* x, const u64* gin, u64* sm, int rank, const ulonglong2* __restrict__ Wi,
                                           u64 q, int tid) {
     using C = CCfg<LOGN>;
     if constexpr (S0 >= C::R0) {
-        cinv_pass<LOGN, S0, (S0 == LOGN - C::LOGE)>(x, g, sm, rank, Wi, q, tid);
+        cinv_pass<LOGN, S0, (S0 == LOGN - C::LOGE)>(x, gin, sm, rank, Wi, q, tid);
         if constexpr (S0 - C::LOGE >= C::R0) __syncthreads();
-        cinv_rest<LOGN, S0 - C::LOGE>(x, g, sm, rank, Wi, q, tid);
+        cinv_rest<LOGN, S0 - C::LOGE>(x, gin, sm, rank, Wi, q, tid);
     }
 }
 
@@ -256,9 +305,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
     const u64 q = P.q;
     const ulonglong2* Wi = a.tw + (size_t)pidx * 2 * C::N + C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
+    const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
     u64 x[C::E];
     const int tid = threadIdx.x;
-    cinv_rest<LOGN, LOGN - C::LOGE>(x, g, sm, rank, Wi, q, tid);
+    cinv_rest<LOGN, LOGN - C::LOGE>(x, gin, sm, rank, Wi, q, tid);
     cluster.sync();                          // both halves complete
     const ulonglong2 wn = Wi[0];
     cinv_passA<LOGN>(x, g, sm, peer, rank, Wi, q, P.pad[0], P.pad[1], wn.x, wn.y, tid);
@@ -271,13 +321,15 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     const size_t smem = (size_t)C::HALF * sizeof(u64);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     dim3 grid(2 * nlimbs, npolys);
     if (inverse) ntt_inv_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
-    else ntt_fwd_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
+    else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(a);
+    else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(a);
     return launched();
 }
 

@@ -292,8 +292,9 @@ cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, in
 // the digit's limbs, then U[p][j][t] = REDC(sum_i y_i * hat_m[i][t]) for
 // every extended limb t outside the digit (coefficient domain; NTT'd by the
 // caller), and U[p][j][t] = x_ntt[t] (already NTT domain) inside it.
-__global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, const u64* __restrict__ xn,
-                             long long x_stride, int nq, int next, int alpha, int ndig, int logn,
+__global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, long long xc_stride,
+                             const u64* __restrict__ xn, long long x_stride, int nq, int next, int alpha, int ndig,
+                             int logn,
                              Limbs ext, const PrimeInfo* __restrict__ pr, const ConvTable* __restrict__ tab) {
     const int N = 1 << logn;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -304,7 +305,7 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, co
     const int i0 = j * alpha;
     const int na = T.n_src;
     u64 y[BCN_MAX_ALPHA];
-    const u64* xcp = xc + p * x_stride + n;
+    const u64* xcp = xc + p * xc_stride + n;
     const u64* xnp = xn + p * x_stride + n;
     u64* Up = U + (p * ndig + j) * (long long)next * N + n;
 #pragma unroll 4
@@ -323,13 +324,13 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, co
     (void)nq;
 }
 
-cudaError_t modup_op(u64* U, const u64* xc, const u64* xn, long long x_stride, int npoly, int nq, int next,
-                     int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab,
-                     cudaStream_t st) {
+cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, long long x_stride, int npoly, int nq,
+                     int next, int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr,
+                     const ConvTable* tab, cudaStream_t st) {
     const int N = 1 << logn;
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, npoly, ndig);
-    modup_kernel<<<grid, tpb, 0, st>>>(U, xc, xn, x_stride, nq, next, alpha, ndig, logn, ext, pr, tab);
+    modup_kernel<<<grid, tpb, 0, st>>>(U, xc, xc_stride, xn, x_stride, nq, next, alpha, ndig, logn, ext, pr, tab);
     return launched();
 }
 

@@ -27,6 +27,19 @@ struct NttArgs {
     int skip_alpha;          // ModUp: skip limb t of digit d when t/alpha == d and t <= skip_level
     int skip_dnum;
     int skip_level;
+    const u64* src;          // out-of-place input (nullptr: in place); same limb layout
+    long long src_poly_stride;
+    long long src_limb_stride;   // words between limbs of one input poly (N when packed)
+    // fused prologue / epilogue of the forward cluster NTT (ntt_cluster.cu)
+    int pro;                 // 0: read input; 1: rescale lift of pro_src (one coef limb per poly)
+    const u64* pro_src;
+    long long pro_stride;
+    u64 pro_qtop;            // lift: the dropped prime
+    const u64* pro_tab;      // lift: [limb] q_top mod q_t
+    int epi;                 // 0: store; 1: rescale combine out = (c - x) * q_top^-1
+    const u64* epi_c;        // c[poly * epi_cps + t * epi_cls + n]
+    long long epi_cps, epi_cls;
+    const u64* epi_tab;      // Shoup pairs per limb
 };
 
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
@@ -81,9 +94,9 @@ cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long lon
                       int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st);
 cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, int npoly, int nlimb, int logn,
                          u32 g, cudaStream_t st);
-cudaError_t modup_op(u64* U, const u64* xc, const u64* xn, long long x_stride, int npoly, int nq, int next,
-                     int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab,
-                     cudaStream_t st);
+cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, long long x_stride, int npoly, int nq,
+                     int next, int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr,
+                     const ConvTable* tab, cudaStream_t st);
 cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
                      long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
                      const PrimeInfo* pr, cudaStream_t st);
