@@ -92,6 +92,7 @@ struct bcn_ctx {
     size_t scratch_bytes = 0;
     size_t table_bytes = 0, key_bytes = 0;
     u64 q0inv_q1 = 0, q0inv_q1_p = 0;
+    u64* md_scale = nullptr;  // [4K] {n^-1 h_k, shoup, w1 n^-1 h_k, shoup}: ModDown INTT outputs y_k directly
 
     size_t key_words() const { return (size_t)dnum * 2 * nbasis * N; }
 };
@@ -159,6 +160,13 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.epi_c = nullptr;
     a.epi_cps = a.epi_cls = 0;
     a.epi_tab = nullptr;
+    a.pro_conv = nullptr;
+    a.pro_K = 0;
+    a.epi_add = nullptr;
+    a.epi_aps = 0;
+    a.epi_add_c1 = 0;
+    a.epi_g = 1;
+    a.inv_scale = nullptr;
     return a;
 }
 
@@ -396,6 +404,21 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
     }
     CUDA_TRY(dmalloc((void**)&c->pmod, sizeof(u64) * pmod.size(), &c->table_bytes));
     CUDA_TRY(cudaMemcpy(c->pmod, pmod.data(), sizeof(u64) * pmod.size(), cudaMemcpyHostToDevice));
+    {
+        std::vector<u64> ms(4 * n_special);
+        for (int k = 0; k < n_special; k++) {
+            const u64 pk = c->primes[nq + k];
+            u64 prod = 1;
+            for (int k2 = 0; k2 < n_special; k2++) if (k2 != k) prod = mulmod_h(prod, c->primes[nq + k2] % pk, pk);
+            const u64 h = inv_h(prod, pk);                                 // (P/p_k)^-1 mod p_k
+            const u64 a = mulmod_h(c->hpr[nq + k].pad[0], h, pk);          // n^-1 h
+            const u64 b = mulmod_h(tw[(size_t)(nq + k) * 2 * N + N + 1].x, a, pk);   // w1 n^-1 h
+            ms[4 * k] = a; ms[4 * k + 1] = shoup_h(a, pk);
+            ms[4 * k + 2] = b; ms[4 * k + 3] = shoup_h(b, pk);
+        }
+        CUDA_TRY(dmalloc((void**)&c->md_scale, sizeof(u64) * ms.size(), &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(c->md_scale, ms.data(), sizeof(u64) * ms.size(), cudaMemcpyHostToDevice));
+    }
     if (nq >= 2) {
         c->q0inv_q1 = inv_h(c->primes[0] % c->primes[1], c->primes[1]);
         c->q0inv_q1_p = shoup_h(c->q0inv_q1, c->primes[1]);
@@ -431,7 +454,7 @@ int bcn_ctx_destroy(bcn_ctx* c) {
     }
     for (auto& kv : c->keys) cudaFree(kv.second);
     cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
-    cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod);
+    cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod); cudaFree(c->md_scale);
     if (c->scratch) cudaFree(c->scratch);
     delete c;
     return BCN_OK;
@@ -869,6 +892,50 @@ int bcn_modup(bcn_ctx* c, uint64_t* U, const uint64_t* ct, int ct_nlimb, int G, 
                       (cudaStream_t)stream);
 }
 
+
+// out (packed ct layout, poly stride nl*N for the 2G component polys) =
+//   addend' + (A - conv_P->Q(INTT(A_P))) * P^-1 over the extended-basis pair A.
+// N = 2^13 / 2^14: the INTT of the special limbs folds (P/p_k)^-1 into its last
+// stage (outputs y_k), then ONE fused cluster NTT converts y -> q_t in its
+// prologue and applies the combine + addend in its epilogue; other N: staged.
+static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int level, const u64* addend,
+                        long long as, int add_c1, u32 g, const LevelTables* T, u64* Z, cudaStream_t st) {
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K;
+    Limbs ext = limbs_ext(c, level);
+    Limbs pl;
+    pl.n = c->K;
+    for (int k = 0; k < c->K; k++) pl.prime[k] = (short)(c->nq + k);
+    Limbs ql = limbs_range(0, nl);
+    if ((c->logn == 13 || c->logn == 14) && os == 2LL * nl * N && !getenv_flag_off("BCN_FUSED_MODDOWN")) {
+        NttArgs ia = ntt_args(c, A + (size_t)nl * N, (long long)next * N, pl);
+        ia.inv_scale = c->md_scale;
+        CUDA_TRY(ntt_launch(true, c->logn, ia, c->K, 2 * G, st));
+        NttArgs a = ntt_args(c, out, (long long)nl * N, ql);
+        a.pro = 2;
+        a.pro_src = A + (size_t)nl * N;
+        a.pro_stride = (long long)next * N;
+        a.pro_conv = T->moddown;
+        a.pro_K = c->K;
+        a.epi = 2;
+        a.epi_c = A;
+        a.epi_cps = (long long)next * N;
+        a.epi_cls = N;
+        a.epi_tab = T->pinv;
+        a.epi_add = addend;
+        a.epi_aps = as;
+        a.epi_add_c1 = add_c1;
+        a.epi_g = g;
+        CUDA_TRY(ntt_launch(false, c->logn, a, nl, 2 * G, st));
+        return BCN_OK;
+    }
+    CUDA_TRY(ntt_run(c, true, A + (size_t)nl * N, (long long)next * N, pl, 2 * G, st));
+    CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st));
+    CUDA_TRY(ntt_run(c, false, Z, (long long)nl * N, ql, 2 * G, st));
+    CUDA_TRY(moddown_combine_op(out, os, A, next, Z, addend, as, add_c1, g, G, nl, c->logn, ql, c->pr, T->pinv, st));
+    return BCN_OK;
+}
+
 // out = addend (+ permuted c0) + ModDown(sum_j U_j (x) key_j)
 static int keyswitch_tail(bcn_ctx* c, u64* out, long long os, const u64* U, int G, int level, u64 g, const u64* key,
                           const u64* addend, long long as, int add_c1, u64* tmp, cudaStream_t st) {
@@ -883,16 +950,7 @@ static int keyswitch_tail(bcn_ctx* c, u64* out, long long os, const u64* U, int 
     CUDA_TRY(inner_op(A, U, G, next, ndig, c->logn, (u32)g, key, 2LL * c->nbasis * N, (long long)c->nbasis * N, ext,
                       ext, c->pr, st));
     // INTT of the special limbs of both components
-    Limbs pl;
-    pl.n = c->K;
-    for (int k = 0; k < c->K; k++) pl.prime[k] = (short)(c->nq + k);
-    CUDA_TRY(ntt_run(c, true, A + (size_t)nl * N, (long long)next * N, pl, 2 * G, st));
-    CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st));
-    Limbs ql = limbs_range(0, nl);
-    CUDA_TRY(ntt_run(c, false, Z, (long long)nl * N, ql, 2 * G, st));
-    CUDA_TRY(moddown_combine_op(out, os, A, next, Z, addend, as, add_c1, (u32)g, G, nl, c->logn, ql, c->pr, T->pinv,
-                                st));
-    return BCN_OK;
+    return moddown_tail(c, out, os, A, G, level, addend, as, add_c1, (u32)g, T, Z, st);
 }
 
 static size_t tail_words(const bcn_ctx* c, int G, int level) {
@@ -940,16 +998,7 @@ int bcn_rotsum(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* U,
         CUDA_TRY(rotsum_op(B, C0, R, 2LL * nl * N, G, nl, next, ndig, c->logn, 2LL * c->nbasis * N,
                            (long long)c->nbasis * N, ext, c->pr, t0 > 0, st));
     }
-    Limbs pl;
-    pl.n = c->K;
-    for (int k = 0; k < c->K; k++) pl.prime[k] = (short)(c->nq + k);
-    CUDA_TRY(ntt_run(c, true, B + (size_t)nl * N, (long long)next * N, pl, 2 * G, st));
-    CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st));
-    Limbs ql = limbs_range(0, nl);
-    CUDA_TRY(ntt_run(c, false, Z, (long long)nl * N, ql, 2 * G, st));
-    CUDA_TRY(moddown_combine_op((u64*)out, 2LL * nl * N, B, next, Z, C0, (long long)nl * N, 0, 1u, G, nl, c->logn,
-                                ql, c->pr, T->pinv, st));
-    return BCN_OK;
+    return moddown_tail(c, (u64*)out, 2LL * nl * N, B, G, level, C0, (long long)nl * N, 0, 1u, T, Z, st);
 }
 
 int bcn_rotate_hoisted(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, const uint64_t* U, int G,

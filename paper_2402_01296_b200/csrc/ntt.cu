@@ -199,8 +199,12 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_inv_kernel(NttArgs a) {
     const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
     const int tid = threadIdx.x;
     u64 x[C::E];
-    const u64 ninv = P.pad[0], ninv_p = P.pad[1];
-    const ulonglong2 wn = Wi[0];   // slot 0 of the inverse table holds {w1 n^-1, shoup}
+    u64 ninv = P.pad[0], ninv_p = P.pad[1];
+    ulonglong2 wn = Wi[0];   // slot 0 of the inverse table holds {w1 n^-1, shoup}
+    if (a.inv_scale) {       // per-limb extra factor folded into the final stage (ModDown)
+        const u64* sc = a.inv_scale + 4 * t;
+        ninv = sc[0]; ninv_p = sc[1]; wn.x = sc[2]; wn.y = sc[3];
+    }
     inv_rest<LOGN, LOGN - C::LOGE>(x, g, gin, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
     inv_pass<LOGN, 0, C::R0, true>(x, g, gin, sm, Wi, q, ninv, ninv_p, wn.x, wn.y, tid);
 }

@@ -42,27 +42,53 @@ template <int LOGN> __device__ __forceinline__ int local_idx(int j) { return j &
 
 // fused prologue: the value the forward transform reads at position j
 template <int MODE>
-struct Prologue {             // MODE 0 plain, 1 rescale lift
+struct Prologue {             // MODE 0 plain, 1 rescale lift, 2 ModDown base conversion
     const u64* src;           // mode 0: the limb; mode 1: the coefficient-form top limb of this poly
     u64 q, qtop, qtop_mod_q, inv_p;   // inv_p = floor(2^64 / q): v mod q by a Shoup multiply by 1
     __device__ __forceinline__ u64 operator()(int j) const {
-        if constexpr (MODE == 0) return src[j];
-        const u64 v = src[j];                       // canonical mod qtop, centred lift -> mod q
-        u64 r = shoup(v, 1ull, inv_p, q);
-        if (v > (qtop >> 1)) r = sub_mod(r, qtop_mod_q, q);
-        return r;
+        if constexpr (MODE == 0) {
+            return src[j];
+        } else if constexpr (MODE == 1) {
+            const u64 v = src[j];                   // canonical mod qtop, centred lift -> mod q
+            u64 r = shoup(v, 1ull, inv_p, q);
+            if (v > (qtop >> 1)) r = sub_mod(r, qtop_mod_q, q);
+            return r;
+        } else {                                    // sum_k y_k[j] * [P/p_k]_q (Montgomery table)
+            Acc128 acc;
+            acc.zero();
+            for (int k = 0; k < K; k++) {
+                acc.mac_nr(src[(size_t)k * nstride + j], hat[k * BCN_MAX_LIMBS]);
+                if (k % 7 == 6) acc.fold(q);
+            }
+            acc.fold(q);
+            return acc.reduce(q, qinv_neg);
+        }
     }
+    int K = 0;
+    long long nstride = 0;
+    const u64* hat = nullptr;   // &conv.hat_m[t]
+    u64 qinv_neg = 0;
 };
 
 // fused epilogue: what the forward transform writes for canonical result v at j
 template <int MODE>
-struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top^-1
+struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top^-1, 2 ModDown combine
     u64* out;
     const u64* c;
     u64 q, w, wp;
+    const u64* add = nullptr;   // ModDown addend for this (ct, component, limb), or null
+    u32 g = 1;
+    int logn = 0;
     __device__ __forceinline__ u64 operator()(int j, u64 v) const {
-        if constexpr (MODE == 0) return v;
-        else return shoup(c[j] + q - v, w, wp, q);
+        if constexpr (MODE == 0) {
+            return v;
+        } else {
+            u64 r = shoup(c[j] + q - v, w, wp, q);
+            if constexpr (MODE == 2) {
+                if (add) r = add_mod(r, add[g == 1u ? j : (int)automorph_src((u32)j, g, logn)], q);
+            }
+            return r;
+        }
     }
 };
 
@@ -180,6 +206,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
         pro.qtop = a.pro_qtop;
         pro.qtop_mod_q = a.pro_tab[2 * t];
         pro.inv_p = a.pro_tab[2 * t + 1];
+    } else if constexpr (PM == 2) {
+        pro.src = a.pro_src + (size_t)poly * a.pro_stride;
+        pro.K = a.pro_K;
+        pro.nstride = C::N;
+        pro.hat = a.pro_conv->hat_m + t;
+        pro.qinv_neg = a.pr[pidx].qinv_neg;
+        pro.qtop = pro.qtop_mod_q = pro.inv_p = 0;
     } else {
         pro.src = gin;
         pro.qtop = pro.qtop_mod_q = pro.inv_p = 0;
@@ -187,10 +220,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
     Epilogue<EM> epi;
     epi.out = g;
     epi.q = q;
-    if constexpr (EM == 1) {
+    if constexpr (EM == 1 || EM == 2) {
         epi.c = a.epi_c + (size_t)poly * a.epi_cps + (size_t)t * a.epi_cls;
         epi.w = a.epi_tab[2 * t];
         epi.wp = a.epi_tab[2 * t + 1];
+        if constexpr (EM == 2) {
+            const int comp = poly & 1;
+            epi.add = (a.epi_add && (comp == 0 || a.epi_add_c1))
+                          ? a.epi_add + (size_t)(poly >> 1) * a.epi_aps + (size_t)comp * a.limbs.n * C::N +
+                                (size_t)t * C::N
+                          : nullptr;
+            epi.g = a.epi_g;
+            epi.logn = LOGN;
+        }
     } else {
         epi.c = nullptr;
         epi.w = epi.wp = 0;
@@ -311,7 +353,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
     cinv_rest<LOGN, LOGN - C::LOGE>(x, gin, sm, rank, Wi, q, tid);
     cluster.sync();                          // both halves complete
     const ulonglong2 wn = Wi[0];
-    cinv_passA<LOGN>(x, g, sm, peer, rank, Wi, q, P.pad[0], P.pad[1], wn.x, wn.y, tid);
+    if (a.inv_scale) {
+        const u64* sc = a.inv_scale + 4 * t;
+        cinv_passA<LOGN>(x, g, sm, peer, rank, Wi, q, sc[0], sc[1], sc[2], sc[3], tid);
+    } else {
+        cinv_passA<LOGN>(x, g, sm, peer, rank, Wi, q, P.pad[0], P.pad[1], wn.x, wn.y, tid);
+    }
     cluster.sync();                          // peer finished reading our SMEM
 }
 
@@ -323,12 +370,14 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     if (!configured) {
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     dim3 grid(2 * nlimbs, npolys);
     if (inverse) ntt_inv_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(a);
+    else if (a.pro == 2 && a.epi == 2) ntt_fwd_cluster<LOGN, 2, 2><<<grid, C::T, smem, st>>>(a);
     else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(a);
     return launched();
 }

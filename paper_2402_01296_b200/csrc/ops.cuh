@@ -36,10 +36,24 @@ struct NttArgs {
     long long pro_stride;
     u64 pro_qtop;            // lift: the dropped prime
     const u64* pro_tab;      // lift: [limb] q_top mod q_t
-    int epi;                 // 0: store; 1: rescale combine out = (c - x) * q_top^-1
+    int epi;                 // 0: store; 1: rescale combine out = (c - x) * q_top^-1;
+                             // 2: ModDown combine out = (A - x) * P^-1 (+ addend)
     const u64* epi_c;        // c[poly * epi_cps + t * epi_cls + n]
     long long epi_cps, epi_cls;
     const u64* epi_tab;      // Shoup pairs per limb
+    // ModDown: prologue 2 converts the INTT'd, pre-scaled special limbs
+    // (y_k at pro_src + poly * pro_stride + k * N) to limb t; epilogue 2 adds
+    // addend[(poly/2) * epi_aps + (poly%2) * nl * N + t * N + perm_g(n)] to
+    // component 0 (and component 1 when epi_add_c1).
+    const ConvTable* pro_conv;
+    int pro_K;
+    const u64* epi_add;
+    long long epi_aps;
+    int epi_add_c1;
+    u32 epi_g;
+    // inverse: per-limb replacement of the folded n^-1 constants
+    // {n^-1 s_t, shoup, w1 n^-1 s_t, shoup} (s_t = hatinv of that special prime)
+    const u64* inv_scale;
 };
 
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
