@@ -566,6 +566,69 @@ def he_rotate_mul(c: Ciphertext, r: int, plain, rec: OpRecorder, *, mask: bool =
     return _rot_times_plain(c, r, plain)
 
 
+def linear_bsgs(parts, rec: OpRecorder) -> Ciphertext:
+    """sum over parts and generalised diagonals d of rot_d(x) * v_d, by
+    baby-step / giant-step (Halevi-Shoup): with D diagonals per part and
+    b = ceil(sqrt(D)) baby steps,
+        sum_d v_d rot_d(x) = sum_j rot_{R_j}( sum_i roll(v_{R_j+i}, R_j) * rot_i(x) ),
+    R_j = d_min + j b.  Key switches per part: b - 1 hoisted baby rotations +
+    ~D/b giant rotations, all giant rotations sharing ONE lazy ModDown, and one
+    rescale -- instead of D key switches.  The caller bumps the reference's
+    per-diagonal counts (layers.py:275-314); depth semantics are he_rotate_mul's.
+
+    parts: [(x Ciphertext, [(d, vector, key)])]."""
+    import math
+    ctx = parts[0][0].ctx
+    eng = ctx.engine
+    S = ctx.slot_count
+    x0 = parts[0][0]
+    if x0.level < 1:
+        raise _depth_error(rec, ctx)
+    giants = []          # (P_j data, R_j)
+    level = None
+    for x, diags in parts:
+        x.materialize()
+        level = x.level if level is None else level
+        if x.level != level:
+            raise UsageError("FC blocks must share one level")
+        mark_reused(x)
+        dmin = min(d for d, _, _ in diags)
+        D = max(d for d, _, _ in diags) - dmin + 1
+        b = max(1, math.isqrt(D - 1) + 1) if D > 1 else 1
+        by_d = {d: (v, key) for d, v, key in diags}
+        ql = ctx.q(level)
+        for j in range(-(-D // b)):
+            R = dmin + j * b
+            pairs = []
+            for i in range(b):
+                d = R + i
+                if d not in by_d:
+                    continue
+                v, key = by_d[d]
+                pv = KeyedPlain(np.roll(v, R % S), key + ("bsgs", R)) if key is not None else np.roll(v, R % S)
+                pt = _encode(ctx, pv, level, float(ql), True, x.batch)
+                pairs.append((_rotated(x, i % S)._data, pt))
+            if pairs:
+                giants.append((eng.mac_terms(pairs, level, rescale=False), R % S))
+                STATS["mac_launch"] += 1
+    rot_terms = []
+    out = None
+    for data, R in giants:
+        if R == 0:
+            out = data if out is None else eng.add(out, data, level)
+        else:
+            rot_terms.append((data, eng.modup(data, level), galois_element(R, ctx.poly_degree), None))
+            STATS["modup"] += 1
+    if rot_terms:
+        rs = eng.rotsum(rot_terms, level)
+        STATS["moddown"] += 1
+        STATS["keyswitch_lazy"] += len(rot_terms)
+        out = rs if out is None else eng.add(out, rs, level)
+    out = eng.rescale(out, level)
+    STATS["rescale"] += 1
+    return Ciphertext(out, level - 1, x0.scale, ctx)
+
+
 def materialize_group(cts: list) -> None:
     """Evaluate several lazy sums that share their ciphertext terms (the output
     channels of one conv layer) with one multi-output MAC pass and one batched

@@ -111,3 +111,34 @@ def test_graphed_single_image_forward_matches_reference():
     out3 = gf(d["sens"], d["full"])
     _check(out3, d["logits_ref"])
     assert not np.array_equal(out1, out3)            # fresh encryption noise on every replay
+
+
+@pytest.mark.parametrize("n1,n2,tiles", [(4, 2, 1), (30, 7, 1), (125, 50, 1), (40, 10, 4)])
+def test_fc_bsgs_matches_direct_and_plain(n1, n2, tiles, monkeypatch):
+    """fc_forward (layers.py:275-324) by baby-step/giant-step vs the direct
+    per-diagonal lazy sum: same reference counts, same values (to CKKS noise)."""
+    rng = np.random.default_rng(n1 * 31 + n2)
+    ctx = B.make_context(2048, 3, 2.0 ** 50)
+    S = ctx.slot_count
+    step = 256 if tiles > 1 else 0
+    xs = rng.standard_normal((tiles, n1))
+    slots = np.zeros(S)
+    for tt in range(tiles):
+        slots[tt * step:tt * step + n1] = xs[tt]
+    W = rng.standard_normal((n1, n2)) / np.sqrt(n1)
+    kb = rng.standard_normal(n2)
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BCN_FC_BSGS", mode)
+        rec = B.OpRecorder()
+        ct = B.encrypt_vector(slots, ctx)
+        out = B.fc_forward(ct, W, kb, ctx, rec, tiles=tiles, tile_step=step)
+        dec = B.decrypt_vector(out, ctx)
+        res[mode] = (np.stack([dec[tt * step:tt * step + n2] for tt in range(tiles)]), rec.snapshot(), out.level)
+    want = xs @ W + kb
+    for mode, (got, counts, level) in res.items():
+        assert np.abs(got - want).max() < 1e-8, mode
+        assert counts["Rot"] == counts["Mul_PC"] == n1 + n2 - 1
+        assert counts["Add_CC"] == n1 + n2 - 2 and counts["Add_PC"] == 1
+        assert level == ctx.max_level - 1
+    assert res["1"][1] == res["0"][1]
