@@ -37,7 +37,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(HERE, "..", "include"), *sources(), "-o", LIB + ".tmp"]
+    extra = os.environ.get("BCN_NVCC_EXTRA", "").split()   # experiments: e.g. -DBCN_CNTT_MINB=1
+    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"), *sources(), "-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -366,6 +366,7 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
         const u64 ninv = inv_h(N % qi, qi);
         P.pad[0] = ninv;
         P.pad[1] = shoup_h(ninv, qi);
+        P.pad[2] = shoup_h(1, qi);      // floor(2^64 / q): Barrett reduction of a 64-bit word
         const u64 psi = primitive_root_2n(qi, N), psi_inv = inv_h(psi, qi);
         u64 a = 1, b = 1;
         for (u64 k = 0; k < N; k++) { pw[k] = a; pwi[k] = b; a = mulmod_h(a, psi, qi); b = mulmod_h(b, psi_inv, qi); }

@@ -25,7 +25,7 @@ struct PrimeInfo {
     u64 r2;         // 2^128 mod q         (to-Montgomery)
     u64 r1;         // 2^64 mod q
     u64 r1_shoup;   // floor(r1 * 2^64 / q)
-    u64 pad[3];
+    u64 pad[3];     // [0] n^-1, [1] its Shoup companion, [2] floor(2^64 / q)
 };
 
 // limb t of a buffer lives modulo prime[t] (index into the context's basis)
@@ -148,6 +148,75 @@ __device__ __forceinline__ i64 cbd21(uint4 o) {
 __device__ __forceinline__ u64 signed_to_residue(i64 v, u64 q) {
     i64 r = v % (i64)q;
     return r < 0 ? (u64)(r + (i64)q) : (u64)r;
+}
+
+// ---- exact u128 multiply-accumulate (4 x 32-bit words, no reduction) ----
+// acc += a*b for a, b < 2^61: four IMAD.WIDE.U32 (a0b0 and a1b1 straight into
+// the aligned word pairs, the two cross products summed into one 64-bit word
+// first) plus a 3-word carry add.  Products are < 2^122, so 32 of them fit
+// on top of a state whose high half is < q before fold_hi() must run.
+struct Acc4 {
+    u64 lo, hi;            // kept as aligned register pairs: no moves between MACs
+    __device__ __forceinline__ void zero() { lo = hi = 0ull; }
+    __device__ __forceinline__ void mac(u32 a0, u32 a1, u32 b0, u32 b1) {
+        u64 x;
+        asm("mul.wide.u32 %0, %1, %2;\n\tmad.wide.u32 %0, %3, %4, %0;" : "=l"(x) : "r"(a0), "r"(b1), "r"(a1), "r"(b0));
+        asm("{\n\t.reg .u32 w0, w1, w2, w3, x0, x1;\n\t"
+            "mov.b64 {w0, w1}, %0;\n\t"
+            "mov.b64 {w2, w3}, %1;\n\t"
+            "mov.b64 {x0, x1}, %6;\n\t"
+            "mad.lo.cc.u32 w0, %2, %4, w0;\n\t"
+            "madc.hi.cc.u32 w1, %2, %4, w1;\n\t"
+            "madc.lo.cc.u32 w2, %3, %5, w2;\n\t"
+            "madc.hi.u32 w3, %3, %5, w3;\n\t"
+            "add.cc.u32 w1, w1, x0;\n\t"
+            "addc.cc.u32 w2, w2, x1;\n\t"
+            "addc.u32 w3, w3, 0;\n\t"
+            "mov.b64 %0, {w0, w1};\n\t"
+            "mov.b64 %1, {w2, w3};\n\t}"
+            : "+l"(lo), "+l"(hi)
+            : "r"(a0), "r"(a1), "r"(b0), "r"(b1), "l"(x));
+    }
+    __device__ __forceinline__ void mac(u64 a, u64 b) { mac((u32)a, (u32)(a >> 32), (u32)b, (u32)(b >> 32)); }
+    // high half -> [0, q) (value changes by a multiple of q 2^64); inv1 = floor(2^64 / q)
+    __device__ __forceinline__ void fold_hi(u64 q, u64 inv1) {
+        u64 h = hi - umulhi(hi, inv1) * q;
+        hi = h >= q ? h - q : h;
+    }
+    // REDC of the (folded) value: sum a*b * 2^-64 mod q
+    __device__ __forceinline__ u64 reduce(u64 q, u64 qinv_neg, u64 inv1) {
+        fold_hi(q, inv1);
+        return redc(hi, lo, q, qinv_neg);
+    }
+};
+
+// ---- bulk async copies (TMA engine, 1-D) completing on an mbarrier ----
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, u32 bytes, u64* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+    u32 done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
 }
 
 #define BCN_CHECK_LAUNCH() do { cudaError_t _e = cudaGetLastError(); if (_e != cudaSuccess) return _e; } while (0)

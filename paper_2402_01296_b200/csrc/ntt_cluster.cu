@@ -31,7 +31,11 @@ template <int LOGN> struct CCfg {
     static constexpr int T = N / (2 * E);                 // threads per CTA
     static constexpr int R0 = (LOGN % LOGE) ? (LOGN % LOGE) : LOGE;
     static constexpr int SWZ = 15;
+#ifdef BCN_CNTT_MINB
+    static constexpr int MINB = BCN_CNTT_MINB;
+#else
     static constexpr int MINB = 65536 / (64 * T);        // resident CTAs per SM at a 64-register budget
+#endif
 };
 
 __device__ __forceinline__ int cswz(int j) { return j ^ ((j >> 4) & 15); }
@@ -54,20 +58,17 @@ struct Prologue {             // MODE 0 plain, 1 rescale lift, 2 ModDown base co
             if (v > (qtop >> 1)) r = sub_mod(r, qtop_mod_q, q);
             return r;
         } else {                                    // sum_k y_k[j] * [P/p_k]_q (Montgomery table)
-            Acc128 acc;
+            Acc4 acc;                               // K <= 16 products: no intermediate fold
             acc.zero();
-            for (int k = 0; k < K; k++) {
-                acc.mac_nr(src[(size_t)k * nstride + j], hat[k * BCN_MAX_LIMBS]);
-                if (k % 7 == 6) acc.fold(q);
-            }
-            acc.fold(q);
-            return acc.reduce(q, qinv_neg);
+            for (int k = 0; k < K; k++) acc.mac(src[(size_t)k * nstride + j], hat[k * BCN_MAX_LIMBS]);
+            return acc.reduce(q, qinv_neg, inv1);
         }
     }
     int K = 0;
     long long nstride = 0;
     const u64* hat = nullptr;   // &conv.hat_m[t]
     u64 qinv_neg = 0;
+    u64 inv1 = 0;               // floor(2^64 / q)
 };
 
 // fused epilogue: what the forward transform writes for canonical result v at j
@@ -93,6 +94,23 @@ struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top
 };
 
 // ------------------------------------------------------------------ forward
+// Lazy bounds of the forward butterflies (q < 2^61, so 8q < 2^64).  Default:
+// stage 0 reads canonical input; from stage 2 on, even stages fold the upper
+// input into [0, 4q) with one conditional subtraction of 4q and odd stages
+// skip it (invariant: inputs < 8q, u < 4q, v < 2q, outputs < 6q / 8q), so
+// half of the stages save a 64-bit compare-select.  BCN_NTT_FULL_CSUB keeps
+// the classic Harvey schedule (inputs < 4q, csub 2q every stage).  Results
+// are canonical either way (identical outputs).
+#ifdef BCN_NTT_FULL_CSUB
+__device__ __forceinline__ constexpr bool fwd_reduce(int s) { return s > 0; }
+__device__ __forceinline__ u64 fwd_rbound(u64 q) { return 2 * q; }
+__device__ __forceinline__ u64 fwd_final(u64 x, u64 q) { return csub(csub(x, 2 * q), q); }
+#else
+__device__ __forceinline__ constexpr bool fwd_reduce(int s) { return s >= 2 && (s & 1) == 0; }
+__device__ __forceinline__ u64 fwd_rbound(u64 q) { return 4 * q; }
+__device__ __forceinline__ u64 fwd_final(u64 x, u64 q) { return csub(csub(csub(x, 4 * q), 2 * q), q); }
+#endif
+
 template <int LOGN, class PRO>
 __device__ __forceinline__ void cfwd_passA(u64* x, const PRO& pro, u64* sm, u64* peer, int rank,
                                            const ulonglong2* __restrict__ W, u64 q, int tid) {
@@ -112,7 +130,7 @@ __device__ __forceinline__ void cfwd_passA(u64* x, const PRO& pro, u64* sm, u64*
                 if (k & h) continue;
                 const ulonglong2 w = W[(1 << ls) + (k >> (R - ls))];
                 u64 u = x[i * BS + k];
-                if (ls) u = csub(u, q2);
+                if (fwd_reduce(ls)) u = csub(u, fwd_rbound(q));
                 const u64 v = shoup_lazy(x[i * BS + k + h], w.x, w.y, q);
                 x[i * BS + k] = u + v;
                 x[i * BS + k + h] = u - v + q2;
@@ -148,7 +166,7 @@ __device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int r
         for (int k = 0; k < BS; k++) {
             if (k & h) continue;
             const ulonglong2 w = W[(1 << s) + (gi << ls) + (k >> (R - ls))];
-            const u64 u = csub(x[k], q2);
+            const u64 u = fwd_reduce(s) ? csub(x[k], fwd_rbound(q)) : x[k];
             const u64 v = shoup_lazy(x[k + h], w.x, w.y, q);
             x[k] = u + v;
             x[k + h] = u - v + q2;
@@ -159,8 +177,8 @@ __device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int r
 #pragma unroll
         for (int k = 0; k < BS; k += 2) {
             ulonglong2 v;
-            v.x = epi(base + k, csub(csub(x[k], q2), q));
-            v.y = epi(base + k + 1, csub(csub(x[k + 1], q2), q));
+            v.x = epi(base + k, fwd_final(x[k], q));
+            v.y = epi(base + k + 1, fwd_final(x[k + 1], q));
             *reinterpret_cast<ulonglong2*>(epi.out + base + k) = v;
         }
     } else {
@@ -212,6 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
         pro.nstride = C::N;
         pro.hat = a.pro_conv->hat_m + t;
         pro.qinv_neg = a.pr[pidx].qinv_neg;
+        pro.inv1 = a.pr[pidx].pad[2];
         pro.qtop = pro.qtop_mod_q = pro.inv_p = 0;
     } else {
         pro.src = gin;

@@ -126,20 +126,18 @@ __global__ void __launch_bounds__(256) mac_terms_kernel(u64* __restrict__ out, c
         const int t = (int)(off >> logn);
         const PrimeInfo& P = pr[limbs.prime[t]];
         const u64 q = P.q;
-        Acc128 a0, a1;
+        Acc4 a0, a1;
         a0.zero(); a1.zero();
         const long long cbase = g * 2 * LN + off;
         const long long pbase = g * LN + off;
         for (int k = 0; k < terms.n; k++) {
             const u64 p = __ldg(terms.pt[k] + (terms.pt_batched[k] ? pbase : off));
             const u64* c = terms.ct[k] + cbase;
-            a0.mac_nr(__ldg(c), p);
-            a1.mac_nr(__ldg(c + LN), p);
-            if (k % 7 == 6) { a0.fold(q); a1.fold(q); }
+            a0.mac(__ldg(c), p);
+            a1.mac(__ldg(c + LN), p);
+            if ((k & 31) == 31) { a0.fold_hi(q, P.pad[2]); a1.fold_hi(q, P.pad[2]); }
         }
-        a0.fold(q);
-        a1.fold(q);
-        u64 r0 = a0.reduce(q, P.qinv_neg), r1 = a1.reduce(q, P.qinv_neg);
+        u64 r0 = a0.reduce(q, P.qinv_neg, P.pad[2]), r1 = a1.reduce(q, P.qinv_neg, P.pad[2]);
         u64* o = out + cbase;
         if (accumulate) {
             r0 = add_mod(r0, o[0], q);
@@ -219,10 +217,117 @@ __global__ void __launch_bounds__(256, 2) mac_multi_kernel(u64* __restrict__ out
     }
 }
 
+// Staged variant for N >= 128 (the production path).  CTA = (slot set g,
+// 128-coefficient block, limb t), 256 threads: threads 0-127 own component 0,
+// 128-255 component 1, one coefficient each, OT output accumulators.  Per
+// term k, thread 0 issues 1-KiB bulk async copies (TMA engine) of the two
+// ct slices and the OT plaintext slices into an S-deep shared-memory ring
+// (completion on one mbarrier per stage), so the loads of term k+S overlap
+// the multiplies of term k without holding prefetch registers.  The MAC is
+// exact u128 (Acc4: 4 IMAD.WIDE + carry add, no per-term reduction); the high
+// half is Barrett-folded every 32 terms and one REDC finishes each output.
+#define MM_NB 128
+template <int OT, int S, bool FULL>
+__global__ void __launch_bounds__(2 * MM_NB, 2)
+    mac_multi_tma_kernel(u64* __restrict__ out, long long ostride, const MacMulti m, int nlimb, int logn, Limbs limbs,
+                         const PrimeInfo* __restrict__ pr, int accumulate) {
+    extern __shared__ __align__(128) u64 ring[];     // [S][2 + OT][MM_NB]
+    __shared__ __align__(8) u64 full[S];
+    const int N = 1 << logn;
+    const long long LN = (long long)nlimb << logn;
+    const long long g = blockIdx.x;
+    const int n0 = blockIdx.y * MM_NB;
+    const int t = blockIdx.z;
+    const int tid = threadIdx.x, comp = tid / MM_NB, n = tid % MM_NB;
+    const int n_out = m.n_out, nt = m.n_terms;
+    const long long off = (long long)t * N + n0;
+    const long long cbase = g * 2 * LN + off;
+    constexpr int SW = (2 + OT) * MM_NB;             // words per stage
+    const u32 bytes = (u32)((2 + n_out) * MM_NB * sizeof(u64));
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    // the 2 + n_out copies of a stage are spread over the 8 warps (lane 0 of
+    // warp w issues copies w, w + 8, ...); warp 0 also arms the barrier.  A
+    // copy may land before the arm: tx-count may dip below zero, and the
+    // phase cannot complete before warp 0's arrival.
+    const int warp = tid >> 5;
+    auto issue = [&](int k) {
+        const int s = k % S;
+        u64* dst = ring + s * SW;
+        if (warp == 0) mbar_expect_tx(&full[s], bytes);
+        for (int c = warp; c < 2 + n_out; c += 2 * MM_NB / 32) {
+            const u64* src = c < 2 ? m.ct[k] + cbase + c * LN : m.pt[c - 2][k] + off;
+            bulk_load(dst + c * MM_NB, src, MM_NB * 8, &full[s]);
+        }
+    };
+    if ((tid & 31) == 0)
+        for (int k = 0; k < S && k < nt; k++) issue(k);
+    const PrimeInfo& P = pr[limbs.prime[t]];
+    Acc4 acc[OT];
+#pragma unroll
+    for (int o = 0; o < OT; o++) acc[o].zero();
+    for (int k = 0; k < nt; k++) {
+        const int s = k % S;
+        mbar_wait(&full[s], (u32)((k / S) & 1));
+        const u64* st = ring + s * SW;
+        const u64 c = st[comp * MM_NB + n];
+        const u32 c0 = (u32)c, c1 = (u32)(c >> 32);
+#pragma unroll
+        for (int o = 0; o < OT; o++) {
+            if (FULL || o < n_out) {
+                const u64 p = st[(2 + o) * MM_NB + n];
+                acc[o].mac(c0, c1, (u32)p, (u32)(p >> 32));
+            }
+        }
+        if ((k & 31) == 31) {
+#pragma unroll
+            for (int o = 0; o < OT; o++) acc[o].fold_hi(P.q, P.pad[2]);
+        }
+        __syncthreads();                             // stage s fully consumed
+        if ((tid & 31) == 0 && k + S < nt) issue(k + S);
+    }
+    const u64 q = P.q;
+    u64* po = out + cbase + (long long)comp * LN + n;
+#pragma unroll
+    for (int o = 0; o < OT; o++) {
+        if (FULL || o < n_out) {
+            u64 r = acc[o].reduce(q, P.qinv_neg, P.pad[2]);
+            if (accumulate) r = add_mod(r, po[o * ostride], q);
+            po[o * ostride] = r;
+        }
+    }
+}
+
+template <int OT, int S, bool FULL>
+static cudaError_t launch_mac_multi_tma(u64* out, long long out_stride, const MacMulti& m, int G, int nlimb, int logn,
+                                        const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st) {
+    const size_t smem = (size_t)S * (2 + OT) * MM_NB * sizeof(u64);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(mac_multi_tma_kernel<OT, S, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    dim3 grid(G, (1 << logn) / MM_NB, nlimb);
+    mac_multi_tma_kernel<OT, S, FULL>
+        <<<grid, 2 * MM_NB, smem, st>>>(out, out_stride, m, nlimb, logn, limbs, pr, accumulate);
+    return launched();
+}
+
 cudaError_t mac_multi_op(u64* out, long long out_stride, const MacMulti& m, int G, int nlimb, int logn,
                          const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st) {
     const int N = 1 << logn;
     if (G <= 0 || m.n_terms <= 0 || m.n_out <= 0) return cudaSuccess;
+    if (N >= MM_NB) {
+        const int no = m.n_out;
+        if (no == BCN_MAC_OUT)
+            return launch_mac_multi_tma<BCN_MAC_OUT, 6, true>(out, out_stride, m, G, nlimb, logn, limbs, pr, accumulate, st);
+        if (no == 8) return launch_mac_multi_tma<8, 8, true>(out, out_stride, m, G, nlimb, logn, limbs, pr, accumulate, st);
+        if (no < 8) return launch_mac_multi_tma<8, 8, false>(out, out_stride, m, G, nlimb, logn, limbs, pr, accumulate, st);
+        return launch_mac_multi_tma<BCN_MAC_OUT, 6, false>(out, out_stride, m, G, nlimb, logn, limbs, pr, accumulate, st);
+    }
     const int tpb = N < 256 ? N : 256;
     dim3 grid(G, (N + tpb - 1) / tpb, nlimb);
     if (m.n_out <= 4) mac_multi_kernel<4><<<grid, tpb, 0, st>>>(out, out_stride, m, nlimb, logn, limbs, pr, accumulate);
@@ -317,9 +422,9 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, lo
     for (int t = 0; t < next; t++) {
         if (t >= i0 && t < i0 + na) continue;
         const PrimeInfo& P = pr[ext.prime[t]];
-        Acc128 acc; acc.zero();
-        for (int i = 0; i < na; i++) acc.mac(y[i], T.hat_m[i * BCN_MAX_LIMBS + t], P.q);
-        Up[(long long)t * N] = acc.reduce(P.q, P.qinv_neg);
+        Acc4 acc; acc.zero();                          // na <= 16 products
+        for (int i = 0; i < na; i++) acc.mac(y[i], T.hat_m[i * BCN_MAX_LIMBS + t]);
+        Up[(long long)t * N] = acc.reduce(P.q, P.qinv_neg, P.pad[2]);
     }
     (void)nq;
 }
@@ -364,17 +469,17 @@ __global__ void __launch_bounds__(256) inner_kernel(u64* __restrict__ A, const u
     for (int i = threadIdx.x; i < BLK; i += blockDim.x) {
         const int n = dst0 + i;
         const int s = (g == 1u) ? i : (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
-        Acc128 a0, a1;
+        Acc4 a0, a1;                                   // ndig <= 32 products
         a0.zero(); a1.zero();
         for (int j = 0; j < ndig; j++) {
             const u64 u = sm[j * BLK + s];
             const u64* kp = key + j * key_digit_stride + (long long)kt * N + n;
-            a0.mac(u, __ldg(kp), q);
-            a1.mac(u, __ldg(kp + key_comp_stride), q);
+            a0.mac(u, __ldg(kp));
+            a1.mac(u, __ldg(kp + key_comp_stride));
         }
         u64* o = A + (p * 2 * next + t) * (long long)N + n;
-        o[0] = a0.reduce(q, P.qinv_neg);
-        o[(long long)next * N] = a1.reduce(q, P.qinv_neg);
+        o[0] = a0.reduce(q, P.qinv_neg, P.pad[2]);
+        o[(long long)next * N] = a1.reduce(q, P.qinv_neg, P.pad[2]);
     }
 }
 
@@ -435,7 +540,8 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
     const int tid = threadIdx.x;
     const int n = dst0 + tid;
     const int nd = ndig < MAXD ? ndig : MAXD;
-    Acc128 b0, b1, cc;
+    const u64 inv1 = P.pad[2];
+    Acc4 b0, b1, cc;
     b0.zero(); b1.zero(); cc.zero();
     u64 su[MAXD + 1], kv0[MAXD], kv1[MAXD], w = one_m;
     auto fetch = [&](int k) {
@@ -468,41 +574,37 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
         const u32 g = T.g[k];
         __syncthreads();
         const int s = (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
-        Acc128 a0, a1;
+        Acc4 a0, a1;                                   // ndig <= 32 products
         a0.zero(); a1.zero();
 #pragma unroll
         for (int j = 0; j < MAXD; j++) {
             if (j < nd) {
                 const u64 u = sm[j * BLK + s];
-                a0.mac_nr(u, kv0[j]);
-                a1.mac_nr(u, kv1[j]);
+                a0.mac(u, kv0[j]);
+                a1.mac(u, kv1[j]);
             }
         }
         for (int j = MAXD; j < ndig; j++) {
             const u64 u = sm[j * BLK + s];
             const u64* kp = T.key[k] + (long long)kt * N + n;
-            a0.fold(q); a1.fold(q);
-            a0.mac_nr(u, __ldg(kp + j * kds));
-            a1.mac_nr(u, __ldg(kp + j * kds + kcs));
+            a0.mac(u, __ldg(kp + j * kds));
+            a1.mac(u, __ldg(kp + j * kds + kcs));
         }
-        a0.fold(q);
-        a1.fold(q);
-        b0.mac_nr(a0.reduce(q, qn), wk);
-        b1.mac_nr(a1.reduce(q, qn), wk);
-        if (has_c0) cc.mac_nr(sm[ndig * BLK + s], wk);
-        if (k % 7 == 6) { b0.fold(q); b1.fold(q); cc.fold(q); }
+        b0.mac(a0.reduce(q, qn, inv1), wk);
+        b1.mac(a1.reduce(q, qn, inv1), wk);
+        if (has_c0) cc.mac(sm[ndig * BLK + s], wk);
+        if ((k & 31) == 31) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); cc.fold_hi(q, inv1); }
         if (k + 1 < T.n) fetch(k + 1);   // other warps hide this latency
     }
-    b0.fold(q); b1.fold(q); cc.fold(q);
     u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
     u64* o1 = o0 + (long long)next * N;
-    u64 r0 = b0.reduce(q, qn), r1 = b1.reduce(q, qn);
+    u64 r0 = b0.reduce(q, qn, inv1), r1 = b1.reduce(q, qn, inv1);
     if (accumulate) { r0 = add_mod(r0, *o0, q); r1 = add_mod(r1, *o1, q); }
     *o0 = r0;
     *o1 = r1;
     if (has_c0) {
         u64* oc = C0 + p * (long long)nq * N + (long long)t * N + n;
-        u64 rc = cc.reduce(q, qn);
+        u64 rc = cc.reduce(q, qn, inv1);
         if (accumulate) rc = add_mod(rc, *oc, q);
         *oc = rc;
     }
@@ -555,9 +657,9 @@ __global__ void moddown_conv_kernel(u64* __restrict__ Z, const u64* __restrict__
     u64* zp = Z + p * (long long)nq * N + n;
     for (int i = 0; i < nq; i++) {
         const PrimeInfo& P = pr[ext.prime[i]];
-        Acc128 acc; acc.zero();
-        for (int k = 0; k < K; k++) acc.mac(y[k], T.hat_m[k * BCN_MAX_LIMBS + i], P.q);
-        zp[(long long)i * N] = acc.reduce(P.q, P.qinv_neg);
+        Acc4 acc; acc.zero();                          // K <= 16 products
+        for (int k = 0; k < K; k++) acc.mac(y[k], T.hat_m[k * BCN_MAX_LIMBS + i]);
+        zp[(long long)i * N] = acc.reduce(P.q, P.qinv_neg, P.pad[2]);
     }
 }
 

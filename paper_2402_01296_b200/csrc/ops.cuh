@@ -92,7 +92,7 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
                       const PrimeInfo* pr, int accumulate, cudaStream_t st);
 // Multi-output linear combination out_o = sum_k ct_k (x) pt_{o,k} for a tile of
 // up to BCN_MAC_OUT outputs sharing the same ct terms (conv output channels).
-#define BCN_MAC_OUT 8
+#define BCN_MAC_OUT 16
 #define BCN_MULTI_TERMS 128
 struct MacMulti {
     int n_terms;
