@@ -128,6 +128,15 @@ int bcn_mac_terms(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *cons
  * o < n_out; out u64[n_out][G][2][level or level+1][N] (rescaled or not). */
 int bcn_mac_multi(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *cts,
                   const uint64_t *const *pts, int G, int level, int rescale, void *stream);
+/* Tensor-core form of bcn_mac_multi (IMMA u8 byte-plane products, bit-exact
+ * with it).  The plaintexts of a layer are packed once into byte planes
+ * (bcn_planes_bytes bytes, device memory owned by the caller) and reused by
+ * every call: pts as for bcn_mac_multi (n_terms <= 256). */
+int bcn_planes_bytes(bcn_ctx *ctx, int n_out, int n_terms, int level, uint64_t *bytes);
+int bcn_pack_planes(bcn_ctx *ctx, uint8_t *planes, int n_out, int n_terms, const uint64_t *const *pts, int level,
+                    void *stream);
+int bcn_mac_multi_planes(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *cts,
+                         const uint8_t *planes, int G, int level, int rescale, void *stream);
 /* same, accumulating into an existing unrescaled out u64[G][2][level+1][N] */
 int bcn_mac_terms_acc(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts,
                       const uint64_t *const *pts, const int *pt_batched, int G, int level, void *stream);

@@ -56,6 +56,9 @@ SIGNATURES = {
     "bcn_mac": [_P, _P, _P, _P, _I, _I, _I, _P],
     "bcn_mac_terms": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _I, _P],
     "bcn_mac_multi": [_P, _P, _I, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), _I, _I, _I, _P],
+    "bcn_planes_bytes": [_P, _I, _I, _I, ctypes.POINTER(_U64)],
+    "bcn_pack_planes": [_P, _P, _I, _I, ctypes.POINTER(_U64), _I, _P],
+    "bcn_mac_multi_planes": [_P, _P, _I, _I, ctypes.POINTER(_U64), _P, _I, _I, _I, _P],
     "bcn_mac_terms_acc": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],
     "bcn_rotsum": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64),
                    ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],

@@ -90,6 +90,8 @@ struct bcn_ctx {
     std::map<u64, u64*> keys;
     u64* scratch = nullptr;
     size_t scratch_bytes = 0;
+    void* ptr_dev = nullptr;  // device copy of a host pointer table (plane packing)
+    size_t ptr_cap = 0;
     size_t table_bytes = 0, key_bytes = 0;
     u64 q0inv_q1 = 0, q0inv_q1_p = 0;
     u64* md_scale = nullptr;  // [4K] {n^-1 h_k, shoup, w1 n^-1 h_k, shoup}: ModDown INTT outputs y_k directly
@@ -457,6 +459,7 @@ int bcn_ctx_destroy(bcn_ctx* c) {
     cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
     cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod); cudaFree(c->md_scale);
     if (c->scratch) cudaFree(c->scratch);
+    if (c->ptr_dev) cudaFree(c->ptr_dev);
     delete c;
     return BCN_OK;
 }
@@ -715,6 +718,83 @@ int bcn_mac_multi(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint6
             CUDA_TRY(mac_multi_op(acc + o0 * cw, cw, M, G, nl, c->logn, l, c->pr, k0 > 0, st));
         }
     }
+    if (!rescale) return BCN_OK;
+    LevelTables* LT;
+    e = build_level(c, level, &LT);
+    if (e) return e;
+    const int npoly = 2 * n_out * G;
+    u64* top = acc + (size_t)n_out * cw;
+    u64* W = top + (size_t)npoly * N;
+    CUDA_TRY(rescale_tail(c, (u64*)out, acc, nl * N, npoly, level, top, W, LT, st));
+    return BCN_OK;
+}
+
+// ---- tensor-core multi-output MAC (mac_imma.cu) ----
+static int planes_geometry(int n_out, int n_terms, int* opad, int* nch) {
+    if (n_out < 1 || n_terms < 1) return fail(BCN_ERR_PARAM, "no outputs / terms");
+    if (n_terms > BCN_IMMA_TERMS) return fail(BCN_ERR_PARAM, "more than 256 terms per plane pack");
+    *opad = n_out <= 16 ? 16 : (n_out + 31) / 32 * 32;
+    *nch = (n_terms + 31) / 32;
+    return BCN_OK;
+}
+
+int bcn_planes_bytes(bcn_ctx* c, int n_out, int n_terms, int level, uint64_t* bytes) {
+    int e = check_level(c, level);
+    if (e) return e;
+    int opad, nch;
+    e = planes_geometry(n_out, n_terms, &opad, &nch);
+    if (e) return e;
+    *bytes = (uint64_t)(level + 1) * c->N * nch * 8 * opad * 32;
+    return BCN_OK;
+}
+
+int bcn_pack_planes(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const uint64_t* const* pts, int level,
+                    void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    int opad, nch;
+    e = planes_geometry(n_out, n_terms, &opad, &nch);
+    if (e) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t np = (size_t)n_out * n_terms;
+    if (np > c->ptr_cap) {
+        if (c->ptr_dev) cudaFree(c->ptr_dev);
+        c->ptr_dev = nullptr;
+        c->ptr_cap = 0;
+        if (cudaMalloc(&c->ptr_dev, np * sizeof(u64*)) != cudaSuccess) return fail(BCN_ERR_CUDA, "pointer table");
+        c->ptr_cap = np;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->ptr_dev, pts, np * sizeof(u64*), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(pack_planes_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch, level + 1, c->logn,
+                            st));
+    CUDA_TRY(cudaStreamSynchronize(st));          // the host pointer table may go away after return
+    return BCN_OK;
+}
+
+int bcn_mac_multi_planes(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* cts,
+                         const uint8_t* planes, int G, int level, int rescale, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    int opad, nch;
+    e = planes_geometry(n_out, n_terms, &opad, &nch);
+    if (e) return e;
+    if (rescale && level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nl = level + 1;
+    const long long N = c->N;
+    const long long cw = (long long)G * 2 * nl * N;
+    Limbs l = limbs_range(0, nl);
+    u64* acc = (u64*)out;
+    int err = 0;
+    if (rescale) {
+        acc = scratch_get(c, (size_t)n_out * cw + (size_t)2 * n_out * G * N * (1 + level), &err);
+        if (!acc) return err;
+    }
+    MacImma M;
+    M.n_terms = n_terms;
+    M.n_out = n_out;
+    for (int k = 0; k < n_terms; k++) M.ct[k] = (const u64*)cts[k];
+    CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, opad, G, nl, c->logn, l, c->pr, 0, st));
     if (!rescale) return BCN_OK;
     LevelTables* LT;
     e = build_level(c, level, &LT);

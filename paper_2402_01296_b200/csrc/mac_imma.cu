@@ -1,0 +1,256 @@
+// mac_imma.cu -- multi-output ciphertext x plaintext MAC (the conv-layer
+// linear combination out_o = sum_k ct_k (x) pt_{o,k}) on the integer tensor
+// cores.
+//
+// For one coefficient slot b = (limb t, coefficient n) the op is a small
+// matrix product over Z: D[o][gc] = sum_k P[o][k] * C[k][gc] with P the
+// (Montgomery) plaintext words, C the ciphertext words of all slot sets and
+// components (gc = 2g + c), every entry < q < 2^61.  Splitting both operands
+// into bytes, P = sum_i 2^(8i) P_i and C = sum_j 2^(8j) C_j, gives
+//     D = sum_s 2^(8s) D_s,   D_s = sum_{i+j=s} P_i C_j   (s = 0..14),
+// fifteen u8 x u8 -> s32 matrix products with exact int32 accumulation
+// (<= 8 pairs x 256 terms x 255^2 < 2^31).  Each D_s is computed on the
+// tensor cores with mma.sync m16n8k32 (IMMA); the epilogue recombines the
+// fifteen partials into the 128-bit value, reduces it mod q (one REDC, which
+// also strips the Montgomery factor of P) and writes the canonical word.
+// Bit-exact with the CUDA-core kernel (mac_multi_op) by construction.
+//
+// Operands:
+//  * P is constant per layer, so it is packed ONCE (pack_planes_kernel) into
+//    byte planes laid out exactly as the A fragments want them:
+//      planes[((b * nch + c) * 8 + i) * opad * 32 + o * 32 + kperm(kk)]
+//    = byte i of pt[o][32c + kk] at slot b  (zero-padded to opad rows and
+//    nch * 32 terms), where kperm interleaves k so that a thread's two A
+//    registers (k = 4tq.. and 16 + 4tq..) are one 8-byte load.
+//  * C is the fresh rotated ciphertexts: each CTA gathers the words of its
+//    slot (one word per (k, gc), cp.async 8 B) into shared memory, and every
+//    thread byte-transposes its four k-consecutive words into the eight B
+//    fragments (j = 0..7) with 16 PRMTs.
+// One CTA = one slot b x one block of up to 32 slot-set columns x one block
+// of up to 32 outputs; warp w owns M-tile (16 outputs) x N-tile (8 columns)
+// and keeps its 15 partial accumulators (60 registers) over the whole term
+// loop, which runs in chunks of 32 terms, double-buffered with cp.async.
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace bcn {
+
+typedef unsigned char u8;
+
+__device__ __forceinline__ int kperm(int kk) { return ((kk & 15) >> 2) * 8 + (kk >> 4) * 4 + (kk & 3); }
+
+// one thread per (o, chunk c, limb t, coefficient n); n fastest -> the 32
+// plaintext reads of a warp are coalesced, each thread writes 8 x 32 bytes
+__global__ void pack_planes_kernel(u8* __restrict__ planes, const u64* const* __restrict__ pts, int n_out,
+                                   int n_terms, int opad, int nch, int logn) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int t = blockIdx.y;
+    const int o = blockIdx.z / nch, c = blockIdx.z % nch;
+    const long long b = (long long)t * N + n;
+    u32 w[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int d = 0; d < 8; d++) w[i][d] = 0u;
+#pragma unroll
+    for (int kk = 0; kk < 32; kk++) {
+        const int k = c * 32 + kk;
+        const u64 v = (o < n_out && k < n_terms) ? __ldg(pts[(size_t)o * n_terms + k] + b) : 0ull;
+        const int pos = kperm(kk), d = pos >> 2, sh = (pos & 3) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; i++) w[i][d] |= (u32)((v >> (8 * i)) & 0xffull) << sh;
+    }
+    u8* dst = planes + ((b * nch + c) * 8) * (long long)opad * 32 + (long long)o * 32;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint4* p = reinterpret_cast<uint4*>(dst + (long long)i * opad * 32);
+        p[0] = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+        p[1] = make_uint4(w[i][4], w[i][5], w[i][6], w[i][7]);
+    }
+}
+
+cudaError_t pack_planes_op(u8* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad, int nch, int nl,
+                           int logn, cudaStream_t st) {
+    const int N = 1 << logn;
+    const int tpb = N < 128 ? N : 128;
+    dim3 grid((N + tpb - 1) / tpb, nl, opad * nch);
+    pack_planes_kernel<<<grid, tpb, 0, st>>>(planes, pts_dev, n_out, n_terms, opad, nch, logn);
+    return launched();
+}
+
+// ---------------------------------------------------------------- kernel
+#define IM_BP 66          // B tile row pitch in words (2-way = conflict-optimal LDS.64)
+#define IM_GC 64          // max slot-set columns per CTA (32 slot sets x 2 components)
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ void imma(int* d, u32 a0, u32 a1, u32 a2, u32 a3, u32 b0, u32 b1) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// bytes j of four k-consecutive words -> b[j] = {w0.bj, w1.bj, w2.bj, w3.bj}
+__device__ __forceinline__ void transpose4(const u64 v[4], u32 b[8]) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const u32 x0 = (u32)(v[0] >> (32 * h)), x1 = (u32)(v[1] >> (32 * h));
+        const u32 x2 = (u32)(v[2] >> (32 * h)), x3 = (u32)(v[3] >> (32 * h));
+        const u32 p01l = __byte_perm(x0, x1, 0x5140), p01h = __byte_perm(x0, x1, 0x7362);
+        const u32 p23l = __byte_perm(x2, x3, 0x5140), p23h = __byte_perm(x2, x3, 0x7362);
+        b[4 * h + 0] = __byte_perm(p01l, p23l, 0x5410);
+        b[4 * h + 1] = __byte_perm(p01l, p23l, 0x7632);
+        b[4 * h + 2] = __byte_perm(p01h, p23h, 0x5410);
+        b[4 * h + 3] = __byte_perm(p01h, p23h, 0x7632);
+    }
+}
+
+__global__ void __launch_bounds__(512, 1)
+    mac_imma_kernel(u64* __restrict__ out, long long ostride, const MacImma m, const u8* __restrict__ planes,
+                    int opad, int nch, int G, int nlimb, int logn, Limbs limbs, const PrimeInfo* __restrict__ pr,
+                    int accumulate) {
+    extern __shared__ __align__(128) unsigned char im_smem[];
+    const int N = 1 << logn;
+    const long long LN = (long long)nlimb << logn;
+    const long long b = blockIdx.x;                      // slot: t * N + n
+    const int t = (int)(b >> logn), n = (int)(b & (N - 1));
+    const int g0 = blockIdx.y * (IM_GC / 2);
+    const int ngc = min(IM_GC, 2 * (G - g0));            // columns in this CTA
+    const int o0 = blockIdx.z * 32;
+    const int MT = (opad - o0) >= 32 ? 2 : 1;            // M-tiles of 16 outputs
+    const int NT = (ngc + 7) >> 3;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const int mt = warp % MT, nt = warp / MT;
+    constexpr int ABYTES = 8 * 32 * 32;                  // 8 planes x 32 rows x 32 bytes
+    constexpr int BBYTES = 32 * IM_BP * 8;
+    u8* Abuf[2] = {im_smem, im_smem + ABYTES + BBYTES};
+    u64* Bbuf[2] = {reinterpret_cast<u64*>(im_smem + ABYTES),
+                    reinterpret_cast<u64*>(im_smem + 2 * ABYTES + BBYTES)};
+    const int arow = MT * 16;                            // A rows this CTA reads per plane
+    const long long coff = (long long)t * N + n;
+
+    auto load_chunk = [&](int c, int buf) {
+        // A: 8 planes x arow rows x 32 bytes, contiguous per plane
+        const u8* asrc = planes + ((b * nch + c) * 8) * (long long)opad * 32 + (long long)o0 * 32;
+        const int a16 = 8 * arow * 2;                    // 16-byte pieces
+        for (int x = tid; x < a16; x += nthr) {
+            const int i = x / (arow * 2), r = x % (arow * 2);
+            cp_async16(Abuf[buf] + i * 32 * 32 + r * 16, asrc + (long long)i * opad * 32 + r * 16);
+        }
+        // B: one word per (k, column), k < n_terms only (A rows are zero past it)
+        const int kmax = min(32, m.n_terms - c * 32);
+        for (int x = tid; x < kmax * ngc; x += nthr) {
+            const int kk = x / ngc, col = x % ngc;
+            const int g = g0 + (col >> 1), cc = col & 1;
+            cp_async8(Bbuf[buf] + kk * IM_BP + col, m.ct[c * 32 + kk] + (long long)g * 2 * LN + cc * LN + coff);
+        }
+        cp_async_commit();
+    };
+
+    int acc[15][4];
+#pragma unroll
+    for (int s = 0; s < 15; s++) acc[s][0] = acc[s][1] = acc[s][2] = acc[s][3] = 0;
+
+    load_chunk(0, 0);
+    if (nch > 1) load_chunk(1, 1);
+    else cp_async_commit();
+    const bool active = warp < MT * NT;
+    for (int c = 0; c < nch; c++) {
+        const int buf = c & 1;
+        cp_async_wait1();
+        __syncthreads();
+        if (active) {
+            const u64* Bs = Bbuf[buf];
+            const int col = nt * 8 + gq;
+            u64 v[8];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                v[r] = Bs[(4 * tq + r) * IM_BP + col];
+                v[4 + r] = Bs[(16 + 4 * tq + r) * IM_BP + col];
+            }
+            u32 b0[8], b1[8];
+            transpose4(v, b0);
+            transpose4(v + 4, b1);
+            const u8* As = Abuf[buf] + (mt * 16 + gq) * 32 + tq * 8;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const uint2 lo = *reinterpret_cast<const uint2*>(As + i * 32 * 32);
+                const uint2 hi = *reinterpret_cast<const uint2*>(As + i * 32 * 32 + 8 * 32);
+#pragma unroll
+                for (int j = 0; j < 8; j++) imma(acc[i + j], lo.x, hi.x, lo.y, hi.y, b0[j], b1[j]);
+            }
+        }
+        __syncthreads();                                 // buffer consumed
+        if (c + 2 < nch) load_chunk(c + 2, buf);
+        else cp_async_commit();
+    }
+    if (!active) return;
+
+    // epilogue: value = sum_s 2^(8s) D_s = V_lo + 2^64 V_hi; result = REDC(value)
+    const PrimeInfo& P = pr[limbs.prime[t]];
+    const u64 q = P.q;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const int o = o0 + mt * 16 + gq + 8 * (e >> 1);
+        const int col = nt * 8 + 2 * tq + (e & 1);
+        if (o >= m.n_out || col >= ngc) continue;
+        unsigned __int128 lo128 = 0, hi128 = 0;
+#pragma unroll
+        for (int s = 0; s < 8; s++) lo128 += (unsigned __int128)(u32)acc[s][e] << (8 * s);
+#pragma unroll
+        for (int s = 8; s < 15; s++) hi128 += (unsigned __int128)(u32)acc[s][e] << (8 * (s - 8));
+        u64 l = (u64)hi128;                              // V_hi = 2^64 h + l, h < 2^16
+        const u64 h = (u64)(hi128 >> 64);
+        l = l - umulhi(l, P.pad[2]) * q;                 // l mod q
+        l = l >= q ? l - q : l;
+        const u64 hr = shoup(h, P.r1, P.r1_shoup, q);    // h 2^64 mod q
+        const u64 xl = (u64)lo128;
+        const u64 xh = (u64)(lo128 >> 64) + l + hr;      // < 2^24 + 2q < 3q
+        const u64 mq = xl * P.qinv_neg;
+        u64 r = xh + umulhi(mq, q) + (xl != 0ull ? 1ull : 0ull);   // < 4q
+        r = csub(r, 2 * q);
+        r = csub(r, q);
+        const int g = g0 + (col >> 1), cc = col & 1;
+        u64* po = out + (long long)o * ostride + (long long)g * 2 * LN + cc * LN + coff;
+        if (accumulate) r = add_mod(r, *po, q);
+        *po = r;
+    }
+}
+
+size_t mac_imma_smem() { return 2 * (8 * 32 * 32 + 32 * IM_BP * 8); }
+
+cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const u8* planes, int opad, int G,
+                        int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, int accumulate,
+                        cudaStream_t st) {
+    const int N = 1 << logn;
+    if (G <= 0 || m.n_terms <= 0 || m.n_out <= 0) return cudaSuccess;
+    const int nch = (m.n_terms + 31) / 32;
+    const size_t smem = mac_imma_smem();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(mac_imma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const int gblocks = (G + IM_GC / 2 - 1) / (IM_GC / 2);
+    const int oblocks = (opad + 31) / 32;
+    const int gcols = G < IM_GC / 2 ? 2 * G : IM_GC;
+    const int mt = opad >= 32 ? 2 : 1;
+    const int threads = 32 * mt * ((gcols + 7) / 8);
+    dim3 grid((unsigned)((long long)nlimb * N), gblocks, oblocks);
+    mac_imma_kernel<<<grid, threads, smem, st>>>(out, out_stride, m, planes, opad, nch, G, nlimb, logn, limbs, pr,
+                                                 accumulate);
+    return launched();
+}
+
+}  // namespace bcn

@@ -102,6 +102,19 @@ struct MacMulti {
 };
 cudaError_t mac_multi_op(u64* out, long long out_stride, const MacMulti& m, int G, int nlimb, int logn,
                          const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st);
+// Tensor-core multi-output MAC (mac_imma.cu): ct words gathered per slot,
+// plaintexts pre-packed into byte planes by pack_planes_op.
+#define BCN_IMMA_TERMS 256
+struct MacImma {
+    int n_terms;
+    int n_out;
+    const u64* ct[BCN_IMMA_TERMS];
+};
+cudaError_t pack_planes_op(unsigned char* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad,
+                           int nch, int nl, int logn, cudaStream_t st);
+cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const unsigned char* planes, int opad,
+                        int G, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, int accumulate,
+                        cudaStream_t st);
 cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
                          const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,

@@ -262,6 +262,29 @@ class Engine:
         _lib.call("bcn_mac_multi", self._h, _ptr(out), O, K, c_arr, p_arr, G, level, int(rescale), _stream())
         return out
 
+    def pack_planes(self, pts, level: int) -> torch.Tensor:
+        """Byte-plane pack of an O x K plaintext matrix (Montgomery u64[1,level+1,N]
+        each) for mac_multi_planes; K <= 256.  Done once per layer."""
+        O, K = len(pts), len(pts[0])
+        nb = ctypes.c_uint64()
+        _lib.call("bcn_planes_bytes", self._h, O, K, level, ctypes.byref(nb))
+        planes = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
+        p_arr = (ctypes.c_uint64 * (O * K))(*[p.data_ptr() for row in pts for p in row])
+        _lib.call("bcn_pack_planes", self._h, _ptr(planes), O, K, p_arr, level, _stream())
+        return planes
+
+    def mac_multi_planes(self, cts, planes: torch.Tensor, n_out: int, level: int, rescale: bool = True) -> torch.Tensor:
+        """Tensor-core mac_multi: out[o] = sum_k cts[k] (x) pt[o][k] with the
+        plaintexts given as pack_planes(...) output; bit-identical to mac_multi."""
+        K = len(cts)
+        G = cts[0].shape[0]
+        c_arr = (ctypes.c_uint64 * K)(*[c.data_ptr() for c in cts])
+        nl = level if rescale else level + 1
+        out = torch.empty((n_out, G, 2, nl, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_mac_multi_planes", self._h, _ptr(out), n_out, K, c_arr, _ptr(planes), G, level, int(rescale),
+                  _stream())
+        return out
+
     def mac_terms_acc(self, out: torch.Tensor, terms, level: int) -> torch.Tensor:
         G = terms[0][0].shape[0]
         n = len(terms)

@@ -50,7 +50,7 @@ MAX_RING = 1 << 14
 # device work actually issued (after hoisting / memoisation / lazy rescale);
 # the recorder keeps the reference's logical counts separately.
 STATS = {"modup": 0, "keyswitch": 0, "keyswitch_lazy": 0, "moddown": 0, "rescale": 0, "encode": 0,
-         "encode_hit": 0, "mac_launch": 0}
+         "encode_hit": 0, "mac_launch": 0, "plane_pack": 0}
 
 
 def _term_batch(term) -> int:
@@ -424,13 +424,41 @@ def _encode(ctx: HeContext, plain, level: int, scale: float, montgomery: bool, b
                                                                                   montgomery=montgomery)
     STATS["encode"] += 1
     if key is not None:
-        nb = pt.numel() * 8
-        ctx._pt_cache[k] = pt
-        ctx._pt_bytes += nb
-        while ctx._pt_bytes > ctx.pt_cache_budget and len(ctx._pt_cache) > 1:
-            _, old = ctx._pt_cache.popitem(last=False)
-            ctx._pt_bytes -= old.numel() * 8
+        _cache_put(ctx, k, pt)
     return pt
+
+
+def _entry_bytes(v) -> int:
+    t = v[0] if isinstance(v, tuple) else v
+    return t.numel() * t.element_size()
+
+
+def _cache_put(ctx: HeContext, k, v) -> None:
+    """LRU insert into the HBM plaintext cache (budget BCN_PT_CACHE_GB)."""
+    ctx._pt_cache[k] = v
+    ctx._pt_bytes += _entry_bytes(v)
+    while ctx._pt_bytes > ctx.pt_cache_budget and len(ctx._pt_cache) > 1:
+        _, old = ctx._pt_cache.popitem(last=False)
+        ctx._pt_bytes -= _entry_bytes(old)
+
+
+def _use_imma() -> bool:
+    return os.environ.get("BCN_MAC_IMMA", "1") != "0"
+
+
+def _planes_for(ctx: HeContext, pts: list, level: int):
+    """Byte planes of an O x K plaintext matrix for the tensor-core MAC, packed
+    once and cached next to the plaintexts.  The entry keeps the plaintext
+    tensors alive and is only reused for the very same objects."""
+    key = ("planes", level, tuple(id(p) for row in pts for p in row))
+    hit = ctx._pt_cache.get(key)
+    if hit is not None and all(a is b for a, b in zip(hit[1], (p for row in pts for p in row))):
+        ctx._pt_cache.move_to_end(key)
+        return hit[0]
+    planes = ctx.engine.pack_planes(pts, level)
+    STATS["plane_pack"] += 1
+    _cache_put(ctx, key, (planes, [p for row in pts for p in row]))
+    return planes
 
 
 def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
@@ -644,7 +672,12 @@ def materialize_group(cts: list) -> None:
         if same and first._scaled:
             eng = first.ctx.engine
             lvl = first.data_level
-            out = eng.mac_multi([t[1] for t in first._terms], [[t[2] for t in c._terms] for c in lazy], lvl)
+            cts_k = [t[1] for t in first._terms]
+            pts_ok = [[t[2] for t in c._terms] for c in lazy]
+            if _use_imma() and len(cts_k) <= 256:
+                out = eng.mac_multi_planes(cts_k, _planes_for(first.ctx, pts_ok, lvl), len(lazy), lvl)
+            else:
+                out = eng.mac_multi(cts_k, pts_ok, lvl)
             STATS["mac_launch"] += 1
             STATS["rescale"] += len(lazy)
             for c, d in zip(lazy, out):

@@ -220,3 +220,55 @@ def test_mac_matches():
                 O.lib().orc_mac(O._p(np.ascontiguousarray(ct[lo:hi, c, i])), O._p(np.ascontiguousarray(pt[lo:hi, i])),
                                 O._p(exp), hi - lo, N, q)
                 np.testing.assert_array_equal(got[g, c, i], exp)
+
+
+def test_mac_multi_planes_matches_oracle_composition():
+    """Tensor-core (IMMA byte-plane) multi-output MAC + rescale == oracle sums + rescale."""
+    N, L = 1024, 3
+    eng, orc, hp = _pair(N, L)
+    rng = np.random.default_rng(19)
+    K, n_out = 13, 18            # two output blocks of 16 rows, one partial term chunk
+    vs = rng.standard_normal((K, N // 2))
+    cts = [eng.encrypt(vs[k][None], counter=80 + k) for k in range(K)]
+    octs = [orc.encrypt(vs[k], 80 + k) for k in range(K)]
+    ws = rng.standard_normal((n_out, K, N // 2))
+    ql = float(hp.q[L])
+    pts = [[eng.encode(ws[o, k], L, ql, montgomery=True) for k in range(K)] for o in range(n_out)]
+    got = eng.mac_multi_planes(cts, eng.pack_planes(pts, L), n_out, L, rescale=True)
+    qs = list(hp.q[:L + 1])
+    for o in range(n_out):
+        acc0 = np.zeros((L + 1, N), dtype=np.uint64)
+        acc1 = np.zeros_like(acc0)
+        for k in range(K):
+            pt = orc.encode(ws[o, k], L, ql)
+            acc0 = O.add(acc0, O.mul(octs[k].c0, pt, qs), qs)
+            acc1 = O.add(acc1, O.mul(octs[k].c1, pt, qs), qs)
+        exp = orc.rescale(O.Ct(acc0, acc1, L, hp.scale * ql))
+        _assert_ct(got[o], [exp])
+
+
+@pytest.mark.parametrize("n_out,K,G,extreme", [(5, 7, 3, False), (16, 33, 1, False), (40, 144, 33, False),
+                                               (32, 256, 4, True)])
+def test_mac_multi_planes_bitexact(n_out, K, G, extreme):
+    """IMMA path == CUDA-core path bit for bit on uniform residues (60-bit
+    primes: all eight bytes live), several output / slot-set blocks, the
+    256-term maximum, and the all-(q-1) worst case of the int32 partials."""
+    N, L = 4096, 2
+    hp = make_params(N, L, 60, dnum=1, n_special=1)
+    eng = Engine(hp)
+    nl = L + 1
+    cts = [eng.sample_uniform(2 * G, nl, 0, seed=1000 + k).view(G, 2, nl, N) for k in range(K)]
+    pts = [[eng.to_montgomery(eng.sample_uniform(1, nl, 0, seed=5000 + 300 * o + k)) for k in range(K)]
+           for o in range(n_out)]
+    if extreme:
+        for t in range(nl):
+            qm1 = int(hp.q[t]) - 1
+            qm1 = qm1 - (1 << 64) if qm1 >= (1 << 63) else qm1
+            for c in cts:
+                c[:, :, t, :] = qm1
+            for row in pts:
+                for p in row:
+                    p[:, t, :] = qm1
+    want = to_numpy_u64(eng.mac_multi(cts, pts, L, rescale=False))
+    got = to_numpy_u64(eng.mac_multi_planes(cts, eng.pack_planes(pts, L), n_out, L, rescale=False))
+    np.testing.assert_array_equal(got, want)
