@@ -29,7 +29,7 @@
 // One CTA = one slot b x one block of up to 32 slot-set columns x one block
 // of up to 32 outputs; warp w owns M-tile (16 outputs) x N-tile (8 columns)
 // and keeps its 15 partial accumulators (60 registers) over the whole term
-// loop, which runs in chunks of 32 terms, double-buffered with cp.async.
+// loop, which runs in chunks of 32 terms through a 3-stage cp.async ring.
 #include "common.cuh"
 #include "ops.cuh"
 
@@ -91,7 +91,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int K> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
+}
+#define IM_ST 3           // pipeline stages
 
 __device__ __forceinline__ void imma(int* d, u32 a0, u32 a1, u32 a2, u32 a3, u32 b0, u32 b1) {
     asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -131,47 +134,52 @@ __global__ void __launch_bounds__(512, 1)
     const int NT = (ngc + 7) >> 3;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-    const int mt = warp % MT, nt = warp / MT;
+    const int mt = MT == 2 ? (warp & 1) : 0, nt = MT == 2 ? (warp >> 1) : warp;
     constexpr int ABYTES = 8 * 32 * 32;                  // 8 planes x 32 rows x 32 bytes
     constexpr int BBYTES = 32 * IM_BP * 8;
-    u8* Abuf[2] = {im_smem, im_smem + ABYTES + BBYTES};
-    u64* Bbuf[2] = {reinterpret_cast<u64*>(im_smem + ABYTES),
-                    reinterpret_cast<u64*>(im_smem + 2 * ABYTES + BBYTES)};
+    constexpr int SBYTES = ABYTES + BBYTES;              // one pipeline stage
     const int arow = MT * 16;                            // A rows this CTA reads per plane
+    const int lg_pieces = MT == 2 ? 6 : 5;               // log2(16-byte pieces per plane)
     const long long coff = (long long)t * N + n;
+    const int nwarps = nthr >> 5;
 
-    auto load_chunk = [&](int c, int buf) {
+    auto load_chunk = [&](int c, int stage) {
+        u8* As = im_smem + stage * SBYTES;
+        u64* Bs = reinterpret_cast<u64*>(As + ABYTES);
         // A: 8 planes x arow rows x 32 bytes, contiguous per plane
         const u8* asrc = planes + ((b * nch + c) * 8) * (long long)opad * 32 + (long long)o0 * 32;
-        const int a16 = 8 * arow * 2;                    // 16-byte pieces
-        for (int x = tid; x < a16; x += nthr) {
-            const int i = x / (arow * 2), r = x % (arow * 2);
-            cp_async16(Abuf[buf] + i * 32 * 32 + r * 16, asrc + (long long)i * opad * 32 + r * 16);
+        for (int x = tid; x < (8 << lg_pieces); x += nthr) {
+            const int i = x >> lg_pieces, r = x & ((1 << lg_pieces) - 1);
+            cp_async16(As + i * 32 * 32 + r * 16, asrc + (long long)i * opad * 32 + r * 16);
         }
         // B: one word per (k, column), k < n_terms only (A rows are zero past it)
         const int kmax = min(32, m.n_terms - c * 32);
-        for (int x = tid; x < kmax * ngc; x += nthr) {
-            const int kk = x / ngc, col = x % ngc;
-            const int g = g0 + (col >> 1), cc = col & 1;
-            cp_async8(Bbuf[buf] + kk * IM_BP + col, m.ct[c * 32 + kk] + (long long)g * 2 * LN + cc * LN + coff);
+        for (int kk = warp; kk < kmax; kk += nwarps) {
+            const u64* src = m.ct[c * 32 + kk] + coff;
+            for (int col = lane; col < ngc; col += 32)
+                cp_async8(Bs + kk * IM_BP + col, src + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN);
         }
         cp_async_commit();
     };
+    (void)arow;
 
     int acc[15][4];
 #pragma unroll
     for (int s = 0; s < 15; s++) acc[s][0] = acc[s][1] = acc[s][2] = acc[s][3] = 0;
 
-    load_chunk(0, 0);
-    if (nch > 1) load_chunk(1, 1);
-    else cp_async_commit();
+    // IM_ST-stage cp.async ring: chunks c+1 .. c+IM_ST-1 load while c multiplies
+    for (int c = 0; c < IM_ST - 1; c++) {
+        if (c < nch) load_chunk(c, c);
+        else cp_async_commit();
+    }
     const bool active = warp < MT * NT;
     for (int c = 0; c < nch; c++) {
-        const int buf = c & 1;
-        cp_async_wait1();
+        const int stage = c % IM_ST;
+        cp_async_wait<IM_ST - 2>();
         __syncthreads();
         if (active) {
-            const u64* Bs = Bbuf[buf];
+            const u8* Ab = im_smem + stage * SBYTES;
+            const u64* Bs = reinterpret_cast<const u64*>(Ab + ABYTES);
             const int col = nt * 8 + gq;
             u64 v[8];
 #pragma unroll
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(512, 1)
             u32 b0[8], b1[8];
             transpose4(v, b0);
             transpose4(v + 4, b1);
-            const u8* As = Abuf[buf] + (mt * 16 + gq) * 32 + tq * 8;
+            const u8* As = Ab + (mt * 16 + gq) * 32 + tq * 8;
 #pragma unroll
             for (int i = 0; i < 8; i++) {
                 const uint2 lo = *reinterpret_cast<const uint2*>(As + i * 32 * 32);
@@ -191,8 +199,8 @@ __global__ void __launch_bounds__(512, 1)
                 for (int j = 0; j < 8; j++) imma(acc[i + j], lo.x, hi.x, lo.y, hi.y, b0[j], b1[j]);
             }
         }
-        __syncthreads();                                 // buffer consumed
-        if (c + 2 < nch) load_chunk(c + 2, buf);
+        __syncthreads();                                 // stage consumed
+        if (c + IM_ST - 1 < nch) load_chunk(c + IM_ST - 1, (c + IM_ST - 1) % IM_ST);
         else cp_async_commit();
     }
     if (!active) return;
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
-size_t mac_imma_smem() { return 2 * (8 * 32 * 32 + 32 * IM_BP * 8); }
+size_t mac_imma_smem() { return IM_ST * (8 * 32 * 32 + 32 * IM_BP * 8); }
 
 cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const u8* planes, int opad, int G,
                         int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, int accumulate,

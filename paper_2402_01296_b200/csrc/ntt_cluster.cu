@@ -1,17 +1,20 @@
-// ntt_cluster.cu -- NTT / INTT for N = 2^13, 2^14 on a 2-CTA thread-block
-// cluster (sm_90+ clusters, distributed shared memory).
+// ntt_cluster.cu -- NTT / INTT for N = 2^13, 2^14 on a thread-block cluster
+// (distributed shared memory): 2 CTAs x 32 KiB at N = 2^13, 4 CTAs x 32 KiB
+// at N = 2^14 (BCN_CLUSTER2 builds the 2 x 64 KiB variant for comparison).
 //
 // The single-CTA kernel (ntt.cu) needs the whole limb-polynomial in SMEM
 // (128 KiB at N = 2^14), so only one CTA fits per SM and its global-load,
 // butterfly and store phases cannot overlap with another CTA.  Here the
-// polynomial is split over a cluster of two CTAs with N/2 words each:
-//   forward: pass A (the first R0 stages, blocks strided by N/2^R0) reads HBM
-//            directly, each CTA taking half of the blocks; its outputs are
-//            written to the SMEM of the CTA that owns their chunk (local or
-//            peer via DSMEM); one cluster barrier; the remaining passes only
-//            touch the CTA's own half; the last pass writes HBM.
+// polynomial is split over a cluster of CS CTAs with N/CS words each, so
+// 4 independent CTAs share an SM and hide each other's barriers:
+//   forward: pass A (the first R0 >= log2 CS stages, blocks strided by
+//            N/2^R0) reads HBM directly, each CTA taking 1/CS of the blocks;
+//            its outputs are written to the SMEM of the CTA that owns their
+//            part (local or peer via DSMEM); one cluster barrier; the
+//            remaining radix-16 passes only touch the CTA's own part; the
+//            last pass writes HBM.
 //   inverse: the mirror image -- local passes first, one cluster barrier,
-//            pass A reads half of its inputs from the peer's SMEM.
+//            pass A reads its inputs from the owners' SMEM.
 // Butterflies, twiddle indexing, lazy bounds and output order are exactly
 // those of ntt.cu (same contract with the oracle).
 #include <cooperative_groups.h>
@@ -26,10 +29,17 @@ namespace bcn {
 template <int LOGN> struct CCfg {
     static constexpr int LOGE = 4;
     static constexpr int N = 1 << LOGN;
-    static constexpr int HALF = N / 2;
+#ifdef BCN_CLUSTER2
+    static constexpr int LOGCS = 1;
+#else
+    static constexpr int LOGCS = LOGN >= 14 ? 2 : 1;     // 4 CTAs x 32 KiB at N = 2^14, 2 x 32 KiB at 2^13
+#endif
+    static constexpr int CS = 1 << LOGCS;                // CTAs per cluster
+    static constexpr int PART = N / CS;                  // words owned by one CTA
     static constexpr int E = 1 << LOGE;
-    static constexpr int T = N / (2 * E);                 // threads per CTA
+    static constexpr int T = N / (CS * E);               // threads per CTA
     static constexpr int R0 = (LOGN % LOGE) ? (LOGN % LOGE) : LOGE;
+    static_assert(R0 >= LOGCS, "pass A must cover the cross-CTA stages");
     static constexpr int SWZ = 15;
 #ifdef BCN_CNTT_MINB
     static constexpr int MINB = BCN_CNTT_MINB;
@@ -40,9 +50,8 @@ template <int LOGN> struct CCfg {
 
 __device__ __forceinline__ int cswz(int j) { return j ^ ((j >> 4) & 15); }
 
-// owner CTA of global word j after pass A, and its local index
-template <int LOGN> __device__ __forceinline__ int owner(int j) { return j >> (LOGN - 1); }
-template <int LOGN> __device__ __forceinline__ int local_idx(int j) { return j & ((1 << (LOGN - 1)) - 1); }
+// local index of global word j in its owner CTA (owner = j / PART)
+template <int LOGN> __device__ __forceinline__ int local_idx(int j) { return j & (CCfg<LOGN>::PART - 1); }
 
 // fused prologue: the value the forward transform reads at position j
 template <int MODE>
@@ -112,14 +121,14 @@ __device__ __forceinline__ u64 fwd_final(u64 x, u64 q) { return csub(csub(csub(x
 #endif
 
 template <int LOGN, class PRO>
-__device__ __forceinline__ void cfwd_passA(u64* x, const PRO& pro, u64* sm, u64* peer, int rank,
+__device__ __forceinline__ void cfwd_passA(u64* x, const PRO& pro, u64* const* peers, int rank,
                                            const ulonglong2* __restrict__ W, u64 q, int tid) {
     using C = CCfg<LOGN>;
     constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
     const u64 q2 = 2 * q;
 #pragma unroll
     for (int i = 0; i < NB; i++) {
-        const int b = rank * (TL / 2) + tid + i * C::T;    // gi == 0 for S0 == 0
+        const int b = rank * (TL / C::CS) + tid + i * C::T;    // gi == 0 for S0 == 0
 #pragma unroll
         for (int k = 0; k < BS; k++) x[i * BS + k] = pro(b + k * TL);
 #pragma unroll
@@ -137,10 +146,9 @@ __device__ __forceinline__ void cfwd_passA(u64* x, const PRO& pro, u64* sm, u64*
             }
         }
 #pragma unroll
-        for (int k = 0; k < BS; k++) {
+        for (int k = 0; k < BS; k++) {          // word b + k TL belongs to CTA k >> (R0 - LOGCS)
             const int j = b + k * TL;
-            u64* dst = owner<LOGN>(j) == rank ? sm : peer;
-            dst[cswz(local_idx<LOGN>(j))] = x[i * BS + k];
+            peers[k >> (R - C::LOGCS)][cswz(local_idx<LOGN>(j))] = x[i * BS + k];
         }
     }
 }
@@ -152,10 +160,10 @@ __device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int r
     using C = CCfg<LOGN>;
     constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
     const u64 q2 = 2 * q;
-    const int b = rank * ((C::N >> R) / 2) + tid;
+    const int b = rank * ((C::N >> R) / C::CS) + tid;
     const int gi = b / TL;
     const int base = gi * (C::N >> S0) + (b % TL);
-    const int lbase = base - rank * C::HALF;
+    const int lbase = base - rank * C::PART;
 #pragma unroll
     for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
 #pragma unroll
@@ -204,14 +212,17 @@ __device__ __forceinline__ bool cskip(const NttArgs& a, int t, int poly) {
 }
 
 template <int LOGN, int PM, int EM>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<LOGN>::MINB) ntt_fwd_cluster(NttArgs a) {
+__global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<LOGN>::MINB)
+    ntt_fwd_cluster(NttArgs a) {
     using C = CCfg<LOGN>;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ u64 sm[];
     const int rank = (int)cluster.block_rank();
-    const int t = blockIdx.x >> 1, poly = blockIdx.y;
-    if (cskip(a, t, poly)) return;          // both CTAs of the cluster skip together
-    u64* peer = cluster.map_shared_rank(sm, rank ^ 1);
+    const int t = blockIdx.x >> C::LOGCS, poly = blockIdx.y;
+    if (cskip(a, t, poly)) return;          // all CTAs of the cluster skip together
+    u64* peers[C::CS];
+#pragma unroll
+    for (int r = 0; r < C::CS; r++) peers[r] = cluster.map_shared_rank(sm, r);
     const int pidx = a.limbs.prime[t];
     const u64 q = a.pr[pidx].q;
     const ulonglong2* W = a.tw + (size_t)pidx * 2 * C::N;
@@ -259,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
     u64 x[C::E];
     const int tid = threadIdx.x;
     cluster.sync();                          // peer SMEM is live before remote stores
-    cfwd_passA<LOGN, Prologue<PM>>(x, pro, sm, peer, rank, W, q, tid);
+    cfwd_passA<LOGN, Prologue<PM>>(x, pro, peers, rank, W, q, tid);
     cluster.sync();                          // all chunks delivered
     cfwd_rest<LOGN, C::R0, Epilogue<EM>>(x, epi, sm, rank, W, q, tid);
 }
@@ -271,10 +282,10 @@ __device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ gin, u
     using C = CCfg<LOGN>;
     constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
     const u64 q2 = 2 * q;
-    const int b = rank * ((C::N >> R) / 2) + tid;
+    const int b = rank * ((C::N >> R) / C::CS) + tid;
     const int gi = b / TL;
     const int base = gi * (C::N >> S0) + (b % TL);
-    const int lbase = base - rank * C::HALF;
+    const int lbase = base - rank * C::PART;
     if constexpr (FIRST) {
         static_assert(TL == 1, "first inverse pass is contiguous");
 #pragma unroll
@@ -316,7 +327,7 @@ __device__ __forceinline__ void cinv_rest(u64* x, const u64* gin, u64* sm, int r
 }
 
 template <int LOGN>
-__device__ __forceinline__ void cinv_passA(u64* x, u64* __restrict__ g, u64* sm, u64* peer, int rank,
+__device__ __forceinline__ void cinv_passA(u64* x, u64* __restrict__ g, u64* const* peers, int rank,
                                            const ulonglong2* __restrict__ Wi, u64 q, u64 ninv, u64 ninv_p, u64 wn,
                                            u64 wn_p, int tid) {
     using C = CCfg<LOGN>;
@@ -324,12 +335,11 @@ __device__ __forceinline__ void cinv_passA(u64* x, u64* __restrict__ g, u64* sm,
     const u64 q2 = 2 * q;
 #pragma unroll
     for (int i = 0; i < NB; i++) {
-        const int b = rank * (TL / 2) + tid + i * C::T;
+        const int b = rank * (TL / C::CS) + tid + i * C::T;
 #pragma unroll
         for (int k = 0; k < BS; k++) {
             const int j = b + k * TL;
-            const u64* src = owner<LOGN>(j) == rank ? sm : peer;
-            x[i * BS + k] = src[cswz(local_idx<LOGN>(j))];
+            x[i * BS + k] = peers[k >> (R - C::LOGCS)][cswz(local_idx<LOGN>(j))];
         }
 #pragma unroll
         for (int ls = R - 1; ls >= 0; ls--) {
@@ -354,13 +364,16 @@ __device__ __forceinline__ void cinv_passA(u64* x, u64* __restrict__ g, u64* sm,
 }
 
 template <int LOGN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<LOGN>::MINB) ntt_inv_cluster(NttArgs a) {
+__global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<LOGN>::MINB)
+    ntt_inv_cluster(NttArgs a) {
     using C = CCfg<LOGN>;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ u64 sm[];
     const int rank = (int)cluster.block_rank();
-    const int t = blockIdx.x >> 1, poly = blockIdx.y;
-    u64* peer = cluster.map_shared_rank(sm, rank ^ 1);
+    const int t = blockIdx.x >> C::LOGCS, poly = blockIdx.y;
+    u64* peers[C::CS];
+#pragma unroll
+    for (int r = 0; r < C::CS; r++) peers[r] = cluster.map_shared_rank(sm, r);
     const int pidx = a.limbs.prime[t];
     const PrimeInfo& P = a.pr[pidx];
     const u64 q = P.q;
@@ -374,9 +387,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
     const ulonglong2 wn = Wi[0];
     if (a.inv_scale) {
         const u64* sc = a.inv_scale + 4 * t;
-        cinv_passA<LOGN>(x, g, sm, peer, rank, Wi, q, sc[0], sc[1], sc[2], sc[3], tid);
+        cinv_passA<LOGN>(x, g, peers, rank, Wi, q, sc[0], sc[1], sc[2], sc[3], tid);
     } else {
-        cinv_passA<LOGN>(x, g, sm, peer, rank, Wi, q, P.pad[0], P.pad[1], wn.x, wn.y, tid);
+        cinv_passA<LOGN>(x, g, peers, rank, Wi, q, P.pad[0], P.pad[1], wn.x, wn.y, tid);
     }
     cluster.sync();                          // peer finished reading our SMEM
 }
@@ -384,7 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CCfg<LOGN>::T, CCfg<
 template <int LOGN>
 static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
     using C = CCfg<LOGN>;
-    const size_t smem = (size_t)C::HALF * sizeof(u64);
+    const size_t smem = (size_t)C::PART * sizeof(u64);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -393,7 +406,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    dim3 grid(2 * nlimbs, npolys);
+    dim3 grid(C::CS * nlimbs, npolys);
     if (inverse) ntt_inv_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 2 && a.epi == 2) ntt_fwd_cluster<LOGN, 2, 2><<<grid, C::T, smem, st>>>(a);

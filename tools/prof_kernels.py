@@ -48,12 +48,17 @@ elif what == "multi":
     # conv2-like multi-output MAC: 144 rotated cts x 16 outputs, level 12, G = 8
     hp = make_params(16384, 14, 50, dnum=3)
     eng = Engine(hp)
-    lvl, G, K = 12, 8, 144
+    lvl, G, K = 12, int(os.environ.get('PROF_G', '8')), 144
     cts = [eng.sample_uniform(2 * G, lvl + 1, 0, seed=7 + k).view(G, 2, lvl + 1, 16384) for k in range(K)]
     pts = [[eng.to_montgomery(eng.sample_uniform(1, lvl + 1, 0, seed=1000 + 200 * o + k)) for k in range(K)]
            for o in range(16)]
-    for _ in range(2):
-        eng.mac_multi(cts, pts, lvl)
+    if os.environ.get("PROF_IMMA", "0") == "1":
+        planes = eng.pack_planes(pts, lvl)
+        for _ in range(2):
+            eng.mac_multi_planes(cts, planes, 16, lvl)
+    else:
+        for _ in range(2):
+            eng.mac_multi(cts, pts, lvl)
     torch.cuda.synchronize()
 else:
     hp = make_params(16384, 7, 50, dnum=2, n_special=1)
