@@ -69,6 +69,7 @@ struct LevelTables {
     u64* pinv = nullptr;            // [2 * (level+1)] Shoup pairs of P^-1 mod q_i
     u64* qlinv = nullptr;           // [2 * level] Shoup pairs of q_level^-1 mod q_i
     u64* qtopmod = nullptr;         // [level] q_level mod q_i (fused rescale lift)
+    u64* upscale = nullptr;         // [4 (level+1)] ModUp INTT constants {n^-1 h_i, sh, w1 n^-1 h_i, sh}
     int ndig = 0;
 };
 
@@ -78,6 +79,7 @@ struct bcn_ctx {
     u64 seed = 0;
     std::vector<u64> primes;
     std::vector<PrimeInfo> hpr;
+    std::vector<u64> wn_host;     // per prime: w1 n^-1 (inverse-table entry 0), for folded INTT scales
     PrimeInfo* pr = nullptr;
     ulonglong2* tw = nullptr;
     double* ksi_re = nullptr;
@@ -90,6 +92,8 @@ struct bcn_ctx {
     std::map<u64, u64*> keys;
     u64* scratch = nullptr;
     size_t scratch_bytes = 0;
+    u64* scratch2 = nullptr;
+    size_t scratch2_bytes = 0;
     void* ptr_dev = nullptr;  // device copy of a host pointer table (plane packing)
     size_t ptr_cap = 0;
     size_t table_bytes = 0, key_bytes = 0;
@@ -119,6 +123,22 @@ static u64* scratch_get(bcn_ctx* c, size_t words, int* err) {
         c->scratch_bytes = nb;
     }
     return c->scratch;
+}
+
+// second arena for operands that live alongside scratch (slot-major MAC staging)
+static u64* scratch2_get(bcn_ctx* c, size_t words, int* err) {
+    size_t bytes = words * sizeof(u64);
+    if (bytes > c->scratch2_bytes) {
+        if (c->scratch2) cudaFree(c->scratch2);
+        c->scratch2 = nullptr;
+        if (cudaMalloc(&c->scratch2, bytes) != cudaSuccess) {
+            c->scratch2_bytes = 0;
+            *err = fail(BCN_ERR_CUDA, "scratch allocation of " + std::to_string(bytes) + " bytes failed");
+            return nullptr;
+        }
+        c->scratch2_bytes = bytes;
+    }
+    return c->scratch2;
 }
 
 static Limbs limbs_range(int prime0, int n) {
@@ -169,7 +189,16 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.epi_add_c1 = 0;
     a.epi_g = 1;
     a.inv_scale = nullptr;
+    a.pro_dnum = 0;
+    a.pro_dstride = 0;
+    a.copy_src = nullptr;
+    a.copy_stride = 0;
     return a;
+}
+
+static bool getenv_flag_on(const char* name) {
+    const char* v = getenv(name);
+    return v && v[0] == '1';
 }
 
 static bool getenv_flag_off(const char* name) {
@@ -262,6 +291,19 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
         qtm[2 * i] = c->primes[level] % c->primes[i];
         qtm[2 * i + 1] = (u64)(((u128)1 << 64) / c->primes[i]);   // Shoup companion of 1
     }
+    std::vector<u64> ups(4 * (level + 1));
+    for (int j = 0; j < ndig; j++) {
+        const int i0 = j * c->alpha;
+        for (int i = i0; i < i0 + up[j].n_src; i++) {
+            const u64 qi = c->primes[i];
+            const u64 h = up[j].hatinv[i - i0];
+            const u64 a = mulmod_h(c->hpr[i].pad[0], h, qi), b = mulmod_h(c->wn_host[i], h, qi);
+            ups[4 * i] = a; ups[4 * i + 1] = shoup_h(a, qi);
+            ups[4 * i + 2] = b; ups[4 * i + 3] = shoup_h(b, qi);
+        }
+    }
+    CUDA_TRY(dmalloc((void**)&T.upscale, sizeof(u64) * ups.size(), &c->table_bytes));
+    CUDA_TRY(cudaMemcpy(T.upscale, ups.data(), sizeof(u64) * ups.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(dmalloc((void**)&T.qtopmod, sizeof(u64) * qtm.size(), &c->table_bytes));
     CUDA_TRY(cudaMemcpy(T.qtopmod, qtm.data(), sizeof(u64) * qtm.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(T.modup, up.data(), sizeof(ConvTable) * ndig, cudaMemcpyHostToDevice));
@@ -381,6 +423,7 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
         }
         const u64 wn = mulmod_h(I[1].x, ninv, qi);
         I[0] = make_ulonglong2(wn, shoup_h(wn, qi));
+        c->wn_host.push_back(wn);
     }
     CUDA_TRY(dmalloc((void**)&c->pr, sizeof(PrimeInfo) * nb, &c->table_bytes));
     CUDA_TRY(cudaMemcpy(c->pr, c->hpr.data(), sizeof(PrimeInfo) * nb, cudaMemcpyHostToDevice));
@@ -454,25 +497,31 @@ int bcn_ctx_destroy(bcn_ctx* c) {
     for (auto& kv : c->lt) {
         cudaFree(kv.second.modup); cudaFree(kv.second.moddown);
         cudaFree(kv.second.pinv); cudaFree(kv.second.qlinv);
+        cudaFree(kv.second.qtopmod); cudaFree(kv.second.upscale);
     }
     for (auto& kv : c->keys) cudaFree(kv.second);
     cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
     cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod); cudaFree(c->md_scale);
     if (c->scratch) cudaFree(c->scratch);
     if (c->ptr_dev) cudaFree(c->ptr_dev);
+    if (c->scratch2) cudaFree(c->scratch2);
     delete c;
     return BCN_OK;
 }
 
 int bcn_ctx_memory(bcn_ctx* c, uint64_t* bytes) {
-    *bytes = c->table_bytes + c->key_bytes + c->scratch_bytes;
+    *bytes = c->table_bytes + c->key_bytes + c->scratch_bytes + c->scratch2_bytes;
     return BCN_OK;
 }
 
 int bcn_ctx_trim(bcn_ctx* c) {
-    if (c->scratch) { cudaDeviceSynchronize(); cudaFree(c->scratch); }
+    if (c->scratch || c->scratch2) cudaDeviceSynchronize();
+    if (c->scratch) cudaFree(c->scratch);
+    if (c->scratch2) cudaFree(c->scratch2);
     c->scratch = nullptr;
     c->scratch_bytes = 0;
+    c->scratch2 = nullptr;
+    c->scratch2_bytes = 0;
     return BCN_OK;
 }
 
@@ -794,7 +843,20 @@ int bcn_mac_multi_planes(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, cons
     M.n_terms = n_terms;
     M.n_out = n_out;
     for (int k = 0; k < n_terms; k++) M.ct[k] = (const u64*)cts[k];
-    CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, opad, G, nl, c->logn, l, c->pr, 0, st));
+    // stage blocks of <= 32 slot sets x tcnt limbs slot-major (<= ~4 GiB), then multiply
+    const size_t per_limb = (size_t)N * n_terms * 64 * sizeof(u64);
+    const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(nl, ((size_t)4 << 30) / per_limb));
+    u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * 64, &err);
+    if (!S) return err;
+    for (int g0 = 0; g0 < G; g0 += 32) {
+        const int gcnt = std::min(32, G - g0);
+        for (int t0 = 0; t0 < nl; t0 += tcnt) {
+            const int tc = std::min(tcnt, nl - t0);
+            CUDA_TRY(slot_major_op(S, M, g0, gcnt, t0, tc, nl, c->logn, st));
+            CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, nl, c->logn,
+                                 l, c->pr, 0, st));
+        }
+    }
     if (!rescale) return BCN_OK;
     LevelTables* LT;
     e = build_level(c, level, &LT);
@@ -949,9 +1011,34 @@ static int modup_impl(bcn_ctx* c, u64* U, const u64* x, long long x_stride, int 
     const long long N = c->N;
     const int nl = level + 1, next = nl + c->K, ndig = T->ndig;
     Limbs ql = limbs_range(0, nl);
+    Limbs ext = limbs_ext(c, level);
+    if ((c->logn == 13 || c->logn == 14) && getenv_flag_on("BCN_FUSED_MODUP")) {   // opt-in: measured no faster
+        // INTT with hatinv_i folded into its last stage -> y_i; then ONE forward
+        // NTT whose prologue base-converts each digit's y to the other limbs and
+        // whose skipped (own-digit) CTAs copy the NTT-domain input limbs
+        NttArgs ia = ntt_args(c, tmp, nl * N, ql);
+        ia.src = x;
+        ia.src_poly_stride = x_stride;
+        ia.src_limb_stride = N;
+        ia.inv_scale = T->upscale;
+        CUDA_TRY(ntt_launch(true, c->logn, ia, nl, G, st));
+        NttArgs a = ntt_args(c, U, (long long)next * N, ext);
+        a.skip_alpha = c->alpha;
+        a.skip_dnum = ndig;
+        a.skip_level = level;
+        a.copy_src = x;
+        a.copy_stride = x_stride;
+        a.pro = 2;
+        a.pro_src = tmp;
+        a.pro_stride = nl * N;
+        a.pro_dnum = ndig;
+        a.pro_dstride = (long long)c->alpha * N;
+        a.pro_conv = T->modup;
+        CUDA_TRY(ntt_launch(false, c->logn, a, next, G * ndig, st));
+        return BCN_OK;
+    }
     // coefficient-domain copy of x
     CUDA_TRY(ntt_run_src(c, true, tmp, nl * N, x, x_stride, N, ql, G, st));     // coefficient form of x
-    Limbs ext = limbs_ext(c, level);
     CUDA_TRY(modup_op(U, tmp, nl * N, x, x_stride, G, nl, next, c->alpha, ndig, c->logn, ext, c->pr, T->modup, st));
     NttArgs a = ntt_args(c, U, (long long)next * N, ext);
     a.skip_alpha = c->alpha;

@@ -80,6 +80,32 @@ cudaError_t pack_planes_op(u8* planes, const u64* const* pts_dev, int n_out, int
     return launched();
 }
 
+// -------------------------------------------------- slot-major transpose
+// S[((tl * N + n) * K + k) * 64 + col] = ct_k[g0 + col/2][col%2][t0 + tl][n]
+// for col < 2 * gcnt: every slot's K x 64 word matrix becomes one contiguous
+// run, so the MAC kernel streams it instead of gathering 8-byte words.  One
+// CTA = (k, limb, 32 coefficients): 64 coalesced 256-byte row reads, 32
+// coalesced 512-byte row writes through a padded SMEM tile.
+__global__ void __launch_bounds__(256) slot_major_kernel(u64* __restrict__ S, const MacImma m, int g0, int gcnt,
+                                                         int t0, int nlimb, int logn) {
+    __shared__ u64 tile[64][33];
+    const int N = 1 << logn;
+    const long long LN = (long long)nlimb << logn;
+    const int n0 = blockIdx.x * 32, tl = blockIdx.y, k = blockIdx.z;
+    const int ncol = 2 * gcnt;
+    const u64* src = m.ct[k] + (long long)(t0 + tl) * N + n0;
+    for (int x = threadIdx.x; x < ncol * 32; x += blockDim.x) {
+        const int col = x >> 5, nn = x & 31;
+        tile[col][nn] = __ldg(src + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN + nn);
+    }
+    __syncthreads();
+    u64* dst = S + (((long long)tl * N + n0) * m.n_terms + k) * 64;
+    for (int x = threadIdx.x; x < 32 * ncol; x += blockDim.x) {
+        const int nn = x / ncol, col = x - nn * ncol;
+        dst[(long long)nn * m.n_terms * 64 + col] = tile[col][nn];
+    }
+}
+
 // ---------------------------------------------------------------- kernel
 #define IM_BP 66          // B tile row pitch in words (2-way = conflict-optimal LDS.64)
 #define IM_GC 64          // max slot-set columns per CTA (32 slot sets x 2 components)
@@ -120,15 +146,15 @@ __device__ __forceinline__ void transpose4(const u64 v[4], u32 b[8]) {
 
 __global__ void __launch_bounds__(512, 1)
     mac_imma_kernel(u64* __restrict__ out, long long ostride, const MacImma m, const u8* __restrict__ planes,
-                    int opad, int nch, int G, int nlimb, int logn, Limbs limbs, const PrimeInfo* __restrict__ pr,
-                    int accumulate) {
+                    const u64* __restrict__ S, int g0, int gcnt, int t0, int opad, int nch, int nlimb, int logn,
+                    Limbs limbs, const PrimeInfo* __restrict__ pr, int accumulate) {
     extern __shared__ __align__(128) unsigned char im_smem[];
     const int N = 1 << logn;
     const long long LN = (long long)nlimb << logn;
-    const long long b = blockIdx.x;                      // slot: t * N + n
+    const long long bl = blockIdx.x;                     // slot within the limb block
+    const long long b = bl + (long long)t0 * N;          // slot: t * N + n
     const int t = (int)(b >> logn), n = (int)(b & (N - 1));
-    const int g0 = blockIdx.y * (IM_GC / 2);
-    const int ngc = min(IM_GC, 2 * (G - g0));            // columns in this CTA
+    const int ngc = 2 * gcnt;                            // columns in this CTA (<= 64)
     const int o0 = blockIdx.z * 32;
     const int MT = (opad - o0) >= 32 ? 2 : 1;            // M-tiles of 16 outputs
     const int NT = (ngc + 7) >> 3;
@@ -152,16 +178,19 @@ __global__ void __launch_bounds__(512, 1)
             const int i = x >> lg_pieces, r = x & ((1 << lg_pieces) - 1);
             cp_async16(As + i * 32 * 32 + r * 16, asrc + (long long)i * opad * 32 + r * 16);
         }
-        // B: one word per (k, column), k < n_terms only (A rows are zero past it)
+        // B: rows k < n_terms of this slot's contiguous K x 64 block (A rows are zero past it)
         const int kmax = min(32, m.n_terms - c * 32);
-        for (int kk = warp; kk < kmax; kk += nwarps) {
-            const u64* src = m.ct[c * 32 + kk] + coff;
-            for (int col = lane; col < ngc; col += 32)
-                cp_async8(Bs + kk * IM_BP + col, src + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN);
+        const u64* bsrc = S + (bl * m.n_terms + c * 32) * 64;
+        const int pieces = ngc >> 1;                     // 16-byte pieces per row
+        for (int x = tid; x < kmax * pieces; x += nthr) {
+            const int kk = x / pieces, pc = x - kk * pieces;
+            cp_async16(Bs + kk * IM_BP + 2 * pc, bsrc + kk * 64 + 2 * pc);
         }
         cp_async_commit();
     };
     (void)arow;
+    (void)LN;
+    (void)nwarps;
 
     int acc[15][4];
 #pragma unroll
@@ -238,11 +267,19 @@ __global__ void __launch_bounds__(512, 1)
 
 size_t mac_imma_smem() { return IM_ST * (8 * 32 * 32 + 32 * IM_BP * 8); }
 
-cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const u8* planes, int opad, int G,
-                        int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, int accumulate,
-                        cudaStream_t st) {
+cudaError_t slot_major_op(u64* S, const MacImma& m, int g0, int gcnt, int t0, int tcnt, int nlimb, int logn,
+                          cudaStream_t st) {
     const int N = 1 << logn;
-    if (G <= 0 || m.n_terms <= 0 || m.n_out <= 0) return cudaSuccess;
+    dim3 grid(N / 32, tcnt, m.n_terms);
+    slot_major_kernel<<<grid, 256, 0, st>>>(S, m, g0, gcnt, t0, nlimb, logn);
+    return launched();
+}
+
+cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const u8* planes, const u64* S, int g0,
+                        int gcnt, int t0, int tcnt, int opad, int nlimb, int logn, const Limbs& limbs,
+                        const PrimeInfo* pr, int accumulate, cudaStream_t st) {
+    const int N = 1 << logn;
+    if (gcnt <= 0 || m.n_terms <= 0 || m.n_out <= 0) return cudaSuccess;
     const int nch = (m.n_terms + 31) / 32;
     const size_t smem = mac_imma_smem();
     static bool configured = false;
@@ -250,14 +287,12 @@ cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const 
         cudaFuncSetAttribute(mac_imma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    const int gblocks = (G + IM_GC / 2 - 1) / (IM_GC / 2);
     const int oblocks = (opad + 31) / 32;
-    const int gcols = G < IM_GC / 2 ? 2 * G : IM_GC;
     const int mt = opad >= 32 ? 2 : 1;
-    const int threads = 32 * mt * ((gcols + 7) / 8);
-    dim3 grid((unsigned)((long long)nlimb * N), gblocks, oblocks);
-    mac_imma_kernel<<<grid, threads, smem, st>>>(out, out_stride, m, planes, opad, nch, G, nlimb, logn, limbs, pr,
-                                                 accumulate);
+    const int threads = 32 * mt * ((2 * gcnt + 7) / 8);
+    dim3 grid((unsigned)((long long)tcnt * N), 1, oblocks);
+    mac_imma_kernel<<<grid, threads, smem, st>>>(out, out_stride, m, planes, S, g0, gcnt, t0, opad, nch, nlimb, logn,
+                                                 limbs, pr, accumulate);
     return launched();
 }
 

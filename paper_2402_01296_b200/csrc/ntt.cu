@@ -236,7 +236,10 @@ static int cluster_mode() {
 
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
     if (nlimbs <= 0 || npolys <= 0) return cudaSuccess;
-    if ((logn == 13 || logn == 14) && cluster_mode()) return ntt_cluster_launch(inverse, logn, a, nlimbs, npolys, st);
+    // fused prologue / epilogue / copy forms exist only in the cluster kernels
+    const bool fused = a.pro || a.epi || a.copy_src || a.inv_scale;
+    if ((logn == 13 || logn == 14) && (cluster_mode() || fused))
+        return ntt_cluster_launch(inverse, logn, a, nlimbs, npolys, st);
     switch (logn) {
         case 3: return launch_one<3>(inverse, a, nlimbs, npolys, st);
         case 4: return launch_one<4>(inverse, a, nlimbs, npolys, st);

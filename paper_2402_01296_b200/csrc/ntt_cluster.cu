@@ -219,7 +219,16 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     extern __shared__ u64 sm[];
     const int rank = (int)cluster.block_rank();
     const int t = blockIdx.x >> C::LOGCS, poly = blockIdx.y;
-    if (cskip(a, t, poly)) return;          // all CTAs of the cluster skip together
+    if (cskip(a, t, poly)) {                // all CTAs of the cluster skip together
+        if (a.copy_src) {                    // ModUp: the digit's own limb, already in NTT form
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
+                a.copy_src + (size_t)(poly / a.skip_dnum) * a.copy_stride + (size_t)t * C::N + rank * C::PART);
+            ulonglong2* dst = reinterpret_cast<ulonglong2*>(
+                a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N + rank * C::PART);
+            for (int i = threadIdx.x; i < C::PART / 2; i += C::T) dst[i] = src[i];
+        }
+        return;
+    }
     u64* peers[C::CS];
 #pragma unroll
     for (int r = 0; r < C::CS; r++) peers[r] = cluster.map_shared_rank(sm, r);
@@ -236,10 +245,18 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
         pro.qtop_mod_q = a.pro_tab[2 * t];
         pro.inv_p = a.pro_tab[2 * t + 1];
     } else if constexpr (PM == 2) {
-        pro.src = a.pro_src + (size_t)poly * a.pro_stride;
-        pro.K = a.pro_K;
+        if (a.pro_dnum > 0) {                // ModUp: digit poly % dnum of entry poly / dnum
+            const int d = poly % a.pro_dnum;
+            const ConvTable* tab = a.pro_conv + d;
+            pro.src = a.pro_src + (size_t)(poly / a.pro_dnum) * a.pro_stride + (size_t)d * a.pro_dstride;
+            pro.K = tab->n_src;
+            pro.hat = tab->hat_m + t;
+        } else {                             // ModDown: the special limbs of poly
+            pro.src = a.pro_src + (size_t)poly * a.pro_stride;
+            pro.K = a.pro_K;
+            pro.hat = a.pro_conv->hat_m + t;
+        }
         pro.nstride = C::N;
-        pro.hat = a.pro_conv->hat_m + t;
         pro.qinv_neg = a.pr[pidx].qinv_neg;
         pro.inv1 = a.pr[pidx].pad[2];
         pro.qtop = pro.qtop_mod_q = pro.inv_p = 0;
@@ -403,6 +420,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
@@ -410,6 +428,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     if (inverse) ntt_inv_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 2 && a.epi == 2) ntt_fwd_cluster<LOGN, 2, 2><<<grid, C::T, smem, st>>>(a);
+    else if (a.pro == 2 && a.epi == 0) ntt_fwd_cluster<LOGN, 2, 0><<<grid, C::T, smem, st>>>(a);
     else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(a);
     return launched();
 }

@@ -54,6 +54,15 @@ struct NttArgs {
     // inverse: per-limb replacement of the folded n^-1 constants
     // {n^-1 s_t, shoup, w1 n^-1 s_t, shoup} (s_t = hatinv of that special prime)
     const u64* inv_scale;
+    // ModUp form of prologue 2: poly = entry * pro_dnum + digit; digit d converts
+    // its own source limbs pro_src + entry * pro_stride + d * pro_dstride with
+    // table pro_conv[d] (pro_K ignored).  0 = ModDown form.
+    int pro_dnum;
+    long long pro_dstride;
+    // skipped limbs (skip_alpha) copy copy_src[(poly / skip_dnum) * copy_stride + t * N + n]
+    // instead of being left untouched (ModUp: the digit's own NTT-domain limbs)
+    const u64* copy_src;
+    long long copy_stride;
 };
 
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
@@ -112,9 +121,12 @@ struct MacImma {
 };
 cudaError_t pack_planes_op(unsigned char* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad,
                            int nch, int nl, int logn, cudaStream_t st);
-cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const unsigned char* planes, int opad,
-                        int G, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, int accumulate,
-                        cudaStream_t st);
+// slot-major staging of a g-block x limb-block of the ct terms: S[(tl N + n) K + k][64]
+cudaError_t slot_major_op(u64* S, const MacImma& m, int g0, int gcnt, int t0, int tcnt, int nlimb, int logn,
+                          cudaStream_t st);
+cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const unsigned char* planes, const u64* S,
+                        int g0, int gcnt, int t0, int tcnt, int opad, int nlimb, int logn, const Limbs& limbs,
+                        const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
                          const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,
