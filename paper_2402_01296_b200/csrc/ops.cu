@@ -543,21 +543,32 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
     const u64 inv1 = P.pad[2];
     Acc4 b0, b1, cc;
     b0.zero(); b1.zero(); cc.zero();
+    // loop-invariant offsets (words): only the term's base pointers and its
+    // source block change from term to term
+    // (32-bit: every operand of one launch is < 2^32 words, checked by the launcher)
+    const u32 dstr = (u32)next * (u32)N;                                // digit stride of U
+    const u32 uoff = (((u32)p * ndig) * (u32)next + t) * (u32)N + tid;
+    const u32 coff = (u32)(p * c0_gstride) + (u32)t * N + tid;
+    const u32 koff = (u32)kt * N + n;
+    const u32 poff_b = ((u32)p * next + t) * (u32)N + n, poff_1 = (u32)t * N + n;
     u64 su[MAXD + 1], kv0[MAXD], kv1[MAXD], w = one_m;
+    int s_next = 0;
     auto fetch = [&](int k) {
         const u32 g = T.g[k];
         const int sblk = (int)(automorph_src((u32)dst0, g, logn) >> logb);
-        const u64* Uk = T.U[k] + ((p * ndig) * (long long)next + t) * N + (long long)sblk * BLK + tid;
+        const u32 so = (u32)sblk * BLK;
+        const u64* Uk = T.U[k] + uoff + so;
 #pragma unroll
         for (int j = 0; j < MAXD; j++)
-            if (j < nd) su[j] = __ldg(Uk + (long long)j * next * N);
-        su[MAXD] = has_c0 ? __ldg(T.c0[k] + p * c0_gstride + (long long)t * N + (long long)sblk * BLK + tid) : 0ull;
-        const u64* kp = T.key[k] + (long long)kt * N + n;
+            if (j < nd) su[j] = __ldg(Uk + j * dstr);
+        su[MAXD] = has_c0 ? __ldg(T.c0[k] + coff + so) : 0ull;
+        const u64* kp = T.key[k] + koff;
 #pragma unroll
         for (int j = 0; j < MAXD; j++)
             if (j < nd) { kv0[j] = __ldg(kp + j * kds); kv1[j] = __ldg(kp + j * kds + kcs); }
         const u64* pk = T.pt[k];
-        w = pk ? __ldg(pk + (T.pt_batched[k] ? p * (long long)next * N : 0) + (long long)t * N + n) : one_m;
+        w = pk ? __ldg(pk + (T.pt_batched[k] ? poff_b : poff_1)) : one_m;
+        s_next = (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
     };
     fetch(0);
     for (int k = 0; k < T.n; k++) {
@@ -567,13 +578,12 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
             if (j < nd) sm[j * BLK + tid] = su[j];
         for (int j = MAXD; j < ndig; j++) {           // (rare) more digits than prefetch slots
             const int sblk = (int)(automorph_src((u32)dst0, T.g[k], logn) >> logb);
-            sm[j * BLK + tid] = __ldg(T.U[k] + ((p * ndig + j) * (long long)next + t) * N + (long long)sblk * BLK + tid);
+            sm[j * BLK + tid] = __ldg(T.U[k] + uoff + (u32)sblk * BLK + (u32)j * dstr);
         }
         if (has_c0) sm[ndig * BLK + tid] = su[MAXD];
         const u64 wk = w;
-        const u32 g = T.g[k];
+        const int s = s_next;
         __syncthreads();
-        const int s = (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
         Acc4 a0, a1;                                   // ndig <= 32 products
         a0.zero(); a1.zero();
 #pragma unroll
@@ -586,7 +596,7 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
         }
         for (int j = MAXD; j < ndig; j++) {
             const u64 u = sm[j * BLK + s];
-            const u64* kp = T.key[k] + (long long)kt * N + n;
+            const u64* kp = T.key[k] + koff;
             a0.mac(u, __ldg(kp + j * kds));
             a1.mac(u, __ldg(kp + j * kds + kcs));
         }
@@ -615,6 +625,8 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
                       int accumulate, cudaStream_t st) {
     const int N = 1 << logn;
     if (terms.n <= 0 || G <= 0) return cudaSuccess;
+    if ((long long)G * (ndig + 2) * next * N >= (1LL << 32) || (long long)G * c0_gstride >= (1LL << 32))
+        return cudaErrorInvalidValue;                 // kernel offsets are 32-bit
     if (N >= 1024) {
         constexpr int BLK = 1024;
         const size_t smem = (size_t)(ndig + 1) * BLK * sizeof(u64);

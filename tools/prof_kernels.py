@@ -27,6 +27,19 @@ elif what == "ntt14":
         eng.ntt(data, 0)
         eng.ntt(data, 0, inverse=True)
     torch.cuda.synchronize()
+elif what == "rotsum3":
+    # pooling / compaction shape of cifar3: 3 rotations of one source at level 7, G = 32
+    from paper_2402_01296_b200.params import galois_element as ge
+    hp = make_params(16384, 14, 50, dnum=3)
+    eng = Engine(hp)
+    lvl, G = 7, 32
+    ct = eng.sample_uniform(2 * G, lvl + 1, 0, seed=5).view(G, 2, lvl + 1, 16384)
+    U = eng.modup(ct, lvl)
+    pts = [eng.to_montgomery(eng.sample_uniform(1, lvl + 1 + hp.K, 0, seed=100 + i)) for i in range(3)]
+    terms = [(ct, U, ge(r, 16384), pts[i]) for i, r in enumerate((1, 16, 17))]
+    for _ in range(3):
+        eng.rotsum(terms, lvl)
+    torch.cuda.synchronize()
 elif what in ("rotsum", "mac"):
     # fc1-like: one level-5 source (cifar3 chain), 96 rotate-multiply terms, G = 32 slot sets
     from paper_2402_01296_b200.params import galois_element as ge
