@@ -63,6 +63,24 @@ def config2(steps=10, warmup=3, n_ct=4096, limbs=4, N=8192):
     return res
 
 
+def ntt14(steps=10, warmup=3, npoly=128, limbs=12):
+    """The workload's NTT: N = 2^14 cluster kernels (ntt_fwd_cluster<14,0,0> /
+    ntt_inv_cluster<14>) over a ModDown-shaped batch of 128 polys x 12 limbs of
+    cifar3's 50-bit primes; one launch each, in place."""
+    hp = make_params(16384, 14, 50, dnum=3)
+    eng = Engine(hp)
+    data = eng.sample_uniform(npoly, limbs, 0, seed=1)
+    nbytes = 2 * data.numel() * 8
+    fwd_ms = time_region(lambda: eng.ntt(data, 0), steps, warmup)
+    inv_ms = time_region(lambda: eng.ntt(data, 0, inverse=True), steps, warmup)
+    res = {"fwd": {"ms": fwd_ms, "bytes": nbytes, "GBps": nbytes / fwd_ms / 1e6},
+           "inv": {"ms": inv_ms, "bytes": nbytes, "GBps": nbytes / inv_ms / 1e6},
+           "limb_polys": npoly * limbs}
+    del eng, data
+    torch.cuda.empty_cache()
+    return res
+
+
 def config3(steps=3, warmup=1, n_ct=1024, N=16384, limbs=8, batch=128):
     """Keyswitch microbench, processed in batches of `batch` ciphertexts."""
     hp = make_params(N, limbs - 1, 50, dnum=2, n_special=1)

@@ -19,10 +19,10 @@ if what == "ntt":
         eng.mac(data.view(4096, 2, 4, 8192), pts, 25)
     torch.cuda.synchronize()
 elif what == "ntt14":
-    # ModDown-shaped batch: 64 polys x 12 limbs of N = 2^14, 50-bit primes
+    # bench_micro.ntt14 launch: 128 polys x 12 limbs of N = 2^14, 50-bit primes
     hp = make_params(16384, 14, 50, dnum=3)
     eng = Engine(hp)
-    data = eng.sample_uniform(64, 12, 0, seed=1)
+    data = eng.sample_uniform(128, 12, 0, seed=1)
     for _ in range(2):
         eng.ntt(data, 0)
         eng.ntt(data, 0, inverse=True)
