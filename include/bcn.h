@@ -151,6 +151,16 @@ int bcn_mac_terms_acc(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *
 int bcn_rotsum(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *U, const uint64_t *const *cts,
                const uint64_t *gal, const uint64_t *const *pts, const int *pt_batched, int G, int level,
                void *stream);
+/* same, with optional per-term key overrides keys[t] (NULL array or entry =
+ * the context's Galois key): an override must be bcn_premul_key(g_t, pt_t),
+ * i.e. the multiplier folded into the key, which saves the per-term REDC and
+ * second product (pt_t must then be unbatched; it still multiplies c0). */
+int bcn_rotsum_keys(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *U, const uint64_t *const *cts,
+                    const uint64_t *gal, const uint64_t *const *pts, const int *pt_batched,
+                    const uint64_t *const *keys, int G, int level, void *stream);
+/* out u64[dnum][2][nbasis][N] (the Galois key layout) = key_g (x) pt over the
+ * extended limbs of `level`; pt Montgomery u64[1][level+1+K][N]. */
+int bcn_premul_key(bcn_ctx *ctx, uint64_t *out, uint64_t g, const uint64_t *pt, int level, void *stream);
 /* K4 microbenchmark form: out[g] = sum_{t in [g*group, min((g+1)*group, n_items))} ct[t] (x) pt[t] */
 int bcn_mac(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, const uint64_t *pt_mont, int n_items, int group,
             int nlimb, void *stream);

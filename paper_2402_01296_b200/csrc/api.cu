@@ -1127,9 +1127,33 @@ static size_t tail_words(const bcn_ctx* c, int G, int level) {
 }
 
 // out = C0 + ModDown(B) with B = sum_t pt_t sum_j sigma_t(U_t,j) key_t,j (lazy ModDown)
+int bcn_premul_key(bcn_ctx* c, uint64_t* out, uint64_t g, const uint64_t* pt, int level, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (g == 1 || (g & 1) == 0) return fail(BCN_ERR_PARAM, "premultiplied keys need odd Galois elements != 1");
+    if (!key_ptr(c, g)) {
+        e = bcn_keygen_galois(c, g, stream);
+        if (e) return e;
+    }
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    CUDA_TRY(premul_key_op((u64*)out, key_ptr(c, g), (const u64*)pt, T->ndig, level + 1 + c->K, c->logn,
+                           2LL * c->nbasis * N, (long long)c->nbasis * N, limbs_ext(c, level), c->pr,
+                           (cudaStream_t)stream));
+    return BCN_OK;
+}
+
 int bcn_rotsum(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* U, const uint64_t* const* cts,
                const uint64_t* gal, const uint64_t* const* pts, const int* pt_batched, int G, int level,
                void* stream) {
+    return bcn_rotsum_keys(c, out, n_terms, U, cts, gal, pts, pt_batched, nullptr, G, level, stream);
+}
+
+int bcn_rotsum_keys(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* U, const uint64_t* const* cts,
+                    const uint64_t* gal, const uint64_t* const* pts, const int* pt_batched,
+                    const uint64_t* const* keys, int G, int level, void* stream) {
     int e = check_level(c, level);
     if (e) return e;
     if (n_terms < 1) return fail(BCN_ERR_PARAM, "no terms");
@@ -1157,11 +1181,14 @@ int bcn_rotsum(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* U,
         R.n = std::min(BCN_ROT_TERMS, n_terms - t0);
         for (int k = 0; k < R.n; k++) {
             R.U[k] = (const u64*)U[t0 + k];
-            R.key[k] = key_ptr(c, gal[t0 + k]);
+            const u64* pk = keys ? (const u64*)keys[t0 + k] : nullptr;
+            R.key[k] = pk ? pk : key_ptr(c, gal[t0 + k]);
             R.c0[k] = (const u64*)cts[t0 + k];
             R.pt[k] = (const u64*)pts[t0 + k];
             R.g[k] = (u32)gal[t0 + k];
             R.pt_batched[k] = (unsigned char)(pt_batched[t0 + k] != 0);
+            if (pk && R.pt_batched[k]) return fail(BCN_ERR_PARAM, "premultiplied keys need a shared (unbatched) pt");
+            R.fused[k] = (unsigned char)(pk != nullptr || R.pt[k] == nullptr);
         }
         CUDA_TRY(rotsum_op(B, C0, R, 2LL * nl * N, G, nl, next, ndig, c->logn, 2LL * c->nbasis * N,
                            (long long)c->nbasis * N, ext, c->pr, t0 > 0, st));

@@ -571,6 +571,7 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
         s_next = (int)(automorph_src((u32)n, g, logn) & (BLK - 1));
     };
     fetch(0);
+    int np = 0;                                       // products in b0/b1 since the last fold
     for (int k = 0; k < T.n; k++) {
         __syncthreads();
 #pragma unroll
@@ -584,26 +585,49 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
         const u64 wk = w;
         const int s = s_next;
         __syncthreads();
-        Acc4 a0, a1;                                   // ndig <= 32 products
-        a0.zero(); a1.zero();
+        if (T.fused[k]) {
+            // multiplier folded into the key (or absent): products go straight
+            // into the output sums -- ndig MACs per component, no REDC
+            if (np + ndig > 32) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); np = 0; }
 #pragma unroll
-        for (int j = 0; j < MAXD; j++) {
-            if (j < nd) {
-                const u64 u = sm[j * BLK + s];
-                a0.mac(u, kv0[j]);
-                a1.mac(u, kv1[j]);
+            for (int j = 0; j < MAXD; j++) {
+                if (j < nd) {
+                    const u64 u = sm[j * BLK + s];
+                    b0.mac(u, kv0[j]);
+                    b1.mac(u, kv1[j]);
+                }
             }
+            for (int j = MAXD; j < ndig; j++) {
+                const u64 u = sm[j * BLK + s];
+                const u64* kp = T.key[k] + koff;
+                b0.mac(u, __ldg(kp + j * kds));
+                b1.mac(u, __ldg(kp + j * kds + kcs));
+            }
+            np += ndig;
+        } else {
+            Acc4 a0, a1;                               // ndig <= 32 products
+            a0.zero(); a1.zero();
+#pragma unroll
+            for (int j = 0; j < MAXD; j++) {
+                if (j < nd) {
+                    const u64 u = sm[j * BLK + s];
+                    a0.mac(u, kv0[j]);
+                    a1.mac(u, kv1[j]);
+                }
+            }
+            for (int j = MAXD; j < ndig; j++) {
+                const u64 u = sm[j * BLK + s];
+                const u64* kp = T.key[k] + koff;
+                a0.mac(u, __ldg(kp + j * kds));
+                a1.mac(u, __ldg(kp + j * kds + kcs));
+            }
+            if (np + 1 > 32) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); np = 0; }
+            b0.mac(a0.reduce(q, qn, inv1), wk);
+            b1.mac(a1.reduce(q, qn, inv1), wk);
+            np += 1;
         }
-        for (int j = MAXD; j < ndig; j++) {
-            const u64 u = sm[j * BLK + s];
-            const u64* kp = T.key[k] + koff;
-            a0.mac(u, __ldg(kp + j * kds));
-            a1.mac(u, __ldg(kp + j * kds + kcs));
-        }
-        b0.mac(a0.reduce(q, qn, inv1), wk);
-        b1.mac(a1.reduce(q, qn, inv1), wk);
         if (has_c0) cc.mac(sm[ndig * BLK + s], wk);
-        if ((k & 31) == 31) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); cc.fold_hi(q, inv1); }
+        if ((k & 31) == 31) cc.fold_hi(q, inv1);
         if (k + 1 < T.n) fetch(k + 1);   // other warps hide this latency
     }
     u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
@@ -618,6 +642,28 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
         if (accumulate) rc = add_mod(rc, *oc, q);
         *oc = rc;
     }
+}
+
+__global__ void premul_key_kernel(u64* __restrict__ out, const u64* __restrict__ key, const u64* __restrict__ pt,
+                                  int next, int logn, long long kds, long long kcs, Limbs ext,
+                                  const PrimeInfo* __restrict__ pr) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y, jc = blockIdx.z, j = jc >> 1, c = jc & 1;
+    if (n >= N) return;
+    const int kt = ext.prime[t];
+    const PrimeInfo& P = pr[kt];
+    const long long o = j * kds + c * kcs + (long long)kt * N + n;
+    out[o] = mont_mul(__ldg(key + o), __ldg(pt + (long long)t * N + n), P.q, P.qinv_neg);
+}
+
+cudaError_t premul_key_op(u64* out, const u64* key, const u64* pt, int ndig, int next, int logn, long long kds,
+                          long long kcs, const Limbs& ext, const PrimeInfo* pr, cudaStream_t st) {
+    const int N = 1 << logn;
+    const int tpb = N < 256 ? N : 256;
+    dim3 grid((N + tpb - 1) / tpb, next, 2 * ndig);
+    premul_key_kernel<<<grid, tpb, 0, st>>>(out, key, pt, next, logn, kds, kcs, ext, pr);
+    return launched();
 }
 
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,

@@ -95,7 +95,14 @@ struct RotTerms {
     const u64* pt[BCN_ROT_TERMS];    // Montgomery, ext basis [G|1][ext][N]; null = 1
     u32 g[BCN_ROT_TERMS];
     unsigned char pt_batched[BCN_ROT_TERMS];
+    // 1: key already carries the multiplier (pt (x) key, bcn_premul_key) or
+    // there is none -- the digit products go straight into the output sums
+    // (no per-term REDC and no second product); pt still multiplies c0
+    unsigned char fused[BCN_ROT_TERMS];
 };
+// out[j][c][kt][n] = key[j][c][kt][n] (x) pt[t][n] over the extended limbs t of a level
+cudaError_t premul_key_op(u64* out, const u64* key, const u64* pt, int ndig, int next, int logn,
+                          long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr, cudaStream_t st);
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long key_digit_stride, long long key_comp_stride, const Limbs& ext,
                       const PrimeInfo* pr, int accumulate, cudaStream_t st);

@@ -235,9 +235,10 @@ class Engine:
                   _ptr(out), _stream())
         return out
 
-    def rotsum(self, terms, level: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    def rotsum(self, terms, level: int, out: torch.Tensor | None = None, keys=None) -> torch.Tensor:
         """sum_t pt_t (x) rot_{g_t}(ct_t) with ONE ModDown (unrescaled, at `level`).
-        terms: [(ct u64[G,2,level+1,N], U from modup(ct), g, pt_ext or None)]."""
+        terms: [(ct u64[G,2,level+1,N], U from modup(ct), g, pt_ext or None)];
+        keys: optional per-term premul_key(g_t, pt_t, level) tensors (or None)."""
         G = terms[0][0].shape[0]
         n = len(terms)
         Us = (ctypes.c_uint64 * n)(*[t[1].data_ptr() for t in terms])
@@ -247,7 +248,18 @@ class Engine:
         bat = (ctypes.c_int * n)(*[int(t[3] is not None and t[3].shape[0] != 1) for t in terms])
         if out is None:
             out = self.empty_ct(G, level)
-        _lib.call("bcn_rotsum", self._h, _ptr(out), n, Us, cts, gal, pts, bat, G, level, _stream())
+        if keys is None:
+            _lib.call("bcn_rotsum", self._h, _ptr(out), n, Us, cts, gal, pts, bat, G, level, _stream())
+        else:
+            ks = (ctypes.c_uint64 * n)(*[0 if k is None else k.data_ptr() for k in keys])
+            _lib.call("bcn_rotsum_keys", self._h, _ptr(out), n, Us, cts, gal, pts, bat, ks, G, level, _stream())
+        return out
+
+    def premul_key(self, g: int, pt: torch.Tensor, level: int) -> torch.Tensor:
+        """Galois key g with the (unbatched, ext-basis Montgomery) multiplier pt
+        folded in, for rotsum(keys=...): u64[dnum,2,nbasis,N]."""
+        out = torch.empty((self.params.dnum, 2, self.nbasis, self.N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_premul_key", self._h, _ptr(out), int(g), _ptr(pt), level, _stream())
         return out
 
     def mac_multi(self, cts, pts, level: int, rescale: bool = True) -> torch.Tensor:

@@ -50,7 +50,7 @@ MAX_RING = 1 << 14
 # device work actually issued (after hoisting / memoisation / lazy rescale);
 # the recorder keeps the reference's logical counts separately.
 STATS = {"modup": 0, "keyswitch": 0, "keyswitch_lazy": 0, "moddown": 0, "rescale": 0, "encode": 0,
-         "encode_hit": 0, "mac_launch": 0, "plane_pack": 0}
+         "encode_hit": 0, "mac_launch": 0, "plane_pack": 0, "key_fold": 0}
 
 
 def _term_batch(term) -> int:
@@ -254,7 +254,10 @@ class Ciphertext:
                 if src._modup is None:
                     object.__setattr__(src, "_modup", eng.modup(src._data, src.level))
                     STATS["modup"] += 1
-            out = eng.rotsum([(t[1]._data, t[1]._modup, t[2], t[3]) for t in rots], lvl)
+            keys = [_premul_key(self.ctx, t[2], t[3], lvl) if _fold_keys() and t[3] is not None
+                    and t[3].shape[0] == 1 else None for t in rots]
+            out = eng.rotsum([(t[1]._data, t[1]._modup, t[2], t[3]) for t in rots], lvl,
+                             keys=keys if any(k is not None for k in keys) else None)
             STATS["moddown"] += 1
             STATS["keyswitch_lazy"] += len(rots)
         if cts:
@@ -444,6 +447,24 @@ def _cache_put(ctx: HeContext, k, v) -> None:
 
 def _use_imma() -> bool:
     return os.environ.get("BCN_MAC_IMMA", "1") != "0"
+
+
+def _fold_keys() -> bool:
+    return os.environ.get("BCN_FOLD_KEYS", "1") != "0"
+
+
+def _premul_key(ctx: HeContext, g: int, pt, level: int):
+    """Galois key with a constant multiplier folded in (rotsum), cached next
+    to the plaintexts; the entry pins the plaintext object it was made from."""
+    key = ("premul", int(g), id(pt), level)
+    hit = ctx._pt_cache.get(key)
+    if hit is not None and hit[1][0] is pt:
+        ctx._pt_cache.move_to_end(key)
+        return hit[0]
+    k = ctx.engine.premul_key(g, pt, level)
+    STATS["key_fold"] += 1
+    _cache_put(ctx, key, (k, [pt]))
+    return k
 
 
 def _planes_for(ctx: HeContext, pts: list, level: int):

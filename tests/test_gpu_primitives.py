@@ -172,6 +172,14 @@ def test_rotsum_lazy_moddown_matches(N, L, dnum):
     assert np.abs(dec - want).max() < 1e-5
     unit = eng.rotsum([(ct, Ua, ge(2, N), None), (ct2, Ub, ge(7, N), None)], L)
     _assert_ct(unit, [orc.rotsum([(oc[i], 2, None), (oc2[i], 7, None)], L) for i in range(2)])
+    # multipliers folded into the keys (bcn_premul_key): same ciphertext bit for bit
+    keys = [eng.premul_key(t[2], t[3], L) for t in terms]
+    _assert_ct(eng.rotsum(terms, L, keys=keys), [orc.rotsum([(oc[i], 1, p1), (oc[i], 5, p2), (oc2[i], 3, p3)], L)
+                                                 for i in range(2)])
+    mixed = terms + [(ct2, Ub, ge(7, N), None)]
+    _assert_ct(eng.rotsum(mixed, L, keys=[keys[0], None, keys[2], None]),
+               [orc.rotsum([(oc[i], 1, p1), (oc[i], 5, p2), (oc2[i], 3, p3), (oc2[i], 7, None)], L)
+                for i in range(2)])
 
 
 def test_mac_multi_matches_oracle_composition():
