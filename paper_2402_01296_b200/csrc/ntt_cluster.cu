@@ -48,6 +48,17 @@ template <int LOGN> struct CCfg {
 #endif
 };
 
+// grid order: consecutive clusters transform the same limb (same prime, same
+// twiddle table) of consecutive polys, so the twiddles stay hot in L1/L2
+// (BCN_NTT_LIMB_MAJOR restores limb-fastest order for comparison)
+#ifdef BCN_NTT_LIMB_MAJOR
+template <int LOGCS> __device__ __forceinline__ int ntt_limb() { return blockIdx.x >> LOGCS; }
+template <int LOGCS> __device__ __forceinline__ int ntt_poly() { return blockIdx.y; }
+#else
+template <int LOGCS> __device__ __forceinline__ int ntt_limb() { return blockIdx.y; }
+template <int LOGCS> __device__ __forceinline__ int ntt_poly() { return blockIdx.x >> LOGCS; }
+#endif
+
 __device__ __forceinline__ int cswz(int j) { return j ^ ((j >> 4) & 15); }
 
 // local index of global word j in its owner CTA (owner = j / PART)
@@ -218,7 +229,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ u64 sm[];
     const int rank = (int)cluster.block_rank();
-    const int t = blockIdx.x >> C::LOGCS, poly = blockIdx.y;
+    const int t = ntt_limb<C::LOGCS>(), poly = ntt_poly<C::LOGCS>();
     if (cskip(a, t, poly)) {                // all CTAs of the cluster skip together
         if (a.copy_src) {                    // ModUp: the digit's own limb, already in NTT form
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
@@ -387,7 +398,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ u64 sm[];
     const int rank = (int)cluster.block_rank();
-    const int t = blockIdx.x >> C::LOGCS, poly = blockIdx.y;
+    const int t = ntt_limb<C::LOGCS>(), poly = ntt_poly<C::LOGCS>();
     u64* peers[C::CS];
 #pragma unroll
     for (int r = 0; r < C::CS; r++) peers[r] = cluster.map_shared_rank(sm, r);
@@ -424,7 +435,11 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
+#ifdef BCN_NTT_LIMB_MAJOR
     dim3 grid(C::CS * nlimbs, npolys);
+#else
+    dim3 grid(C::CS * npolys, nlimbs);
+#endif
     if (inverse) ntt_inv_cluster<LOGN><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 2 && a.epi == 2) ntt_fwd_cluster<LOGN, 2, 2><<<grid, C::T, smem, st>>>(a);
