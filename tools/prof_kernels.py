@@ -37,8 +37,9 @@ elif what == "rotsum3":
     U = eng.modup(ct, lvl)
     pts = [eng.to_montgomery(eng.sample_uniform(1, lvl + 1 + hp.K, 0, seed=100 + i)) for i in range(3)]
     terms = [(ct, U, ge(r, 16384), pts[i]) for i, r in enumerate((1, 16, 17))]
+    keys = [eng.premul_key(t[2], t[3], lvl) for t in terms]
     for _ in range(3):
-        eng.rotsum(terms, lvl)
+        eng.rotsum(terms, lvl, keys=keys)
     torch.cuda.synchronize()
 elif what in ("rotsum", "mac"):
     # fc1-like: one level-5 source (cifar3 chain), 96 rotate-multiply terms, G = 32 slot sets
