@@ -158,6 +158,16 @@ int bcn_rotsum(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *
 int bcn_rotsum_keys(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *U, const uint64_t *const *cts,
                     const uint64_t *gal, const uint64_t *const *pts, const int *pt_batched,
                     const uint64_t *const *keys, int G, int level, void *stream);
+/* Lazy rotation sum (as bcn_rotsum_keys) plus n_ct ciphertext x plaintext terms
+ * (ct u64[G][2][level+1][N], Montgomery pt u64[G or 1][level+1][N]), evaluated
+ * with ONE merged ModDown + rescale per component: the extended-basis sum B
+ * and the q-basis sum C become (B + P C) / (P q_level) through a single base
+ * conversion from {q_level, p_*}.  out u64[G][2][level][N]
+ * at level-1 (multipliers encoded at q_level keep the scale). */
+int bcn_rotsum_rescale(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *U,
+                       const uint64_t *const *cts, const uint64_t *gal, const uint64_t *const *pts,
+                       const int *pt_batched, const uint64_t *const *keys, int n_ct, const uint64_t *const *ct_cts,
+                       const uint64_t *const *ct_pts, const int *ct_batched, int G, int level, void *stream);
 /* out u64[dnum][2][nbasis][N] (the Galois key layout) = key_g (x) pt over the
  * extended limbs of `level`; pt Montgomery u64[1][level+1+K][N]. */
 int bcn_premul_key(bcn_ctx *ctx, uint64_t *out, uint64_t g, const uint64_t *pt, int level, void *stream);

@@ -65,6 +65,9 @@ SIGNATURES = {
     "bcn_rotsum_keys": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64),
                         ctypes.POINTER(_U64), ctypes.POINTER(_I), ctypes.POINTER(_U64), _I, _I, _P],
     "bcn_premul_key": [_P, _P, _U64, _P, _I, _P],
+    "bcn_rotsum_rescale": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64),
+                           ctypes.POINTER(_U64), ctypes.POINTER(_I), ctypes.POINTER(_U64), _I,
+                           ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],
     "bcn_encode_ext": [_P, _P, _I, _I, _I, _D, _I, _P, _P],
     "bcn_rescale": [_P, _P, _P, _I, _I, _I, _P],
     "bcn_mul_cc": [_P, _P, _P, _I, _P, _I, _I, _I, _I, _P],

@@ -70,6 +70,10 @@ struct LevelTables {
     u64* qlinv = nullptr;           // [2 * level] Shoup pairs of q_level^-1 mod q_i
     u64* qtopmod = nullptr;         // [level] q_level mod q_i (fused rescale lift)
     u64* upscale = nullptr;         // [4 (level+1)] ModUp INTT constants {n^-1 h_i, sh, w1 n^-1 h_i, sh}
+    // merged ModDown + rescale (P' = q_level * P, sources {q_level, p_0..p_{K-1}}, targets q_0..q_{level-1})
+    ConvTable* mdr = nullptr;       // [1]
+    u64* mdr_scale = nullptr;       // [4 (K+1)] INTT constants with (P'/s)^-1 folded in
+    u64* pqinv = nullptr;           // [2 level] Shoup pairs of (P q_level)^-1 mod q_i
     int ndig = 0;
 };
 
@@ -80,6 +84,7 @@ struct bcn_ctx {
     std::vector<u64> primes;
     std::vector<PrimeInfo> hpr;
     std::vector<u64> wn_host;     // per prime: w1 n^-1 (inverse-table entry 0), for folded INTT scales
+    std::vector<u64> pmod_host;   // [2 nq] Shoup pairs of P mod q_i
     PrimeInfo* pr = nullptr;
     ulonglong2* tw = nullptr;
     double* ksi_re = nullptr;
@@ -193,6 +198,8 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.pro_dstride = 0;
     a.copy_src = nullptr;
     a.copy_stride = 0;
+    a.epi_tab2 = nullptr;
+    a.epi_acs = 0;
     return a;
 }
 
@@ -290,6 +297,49 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
     for (int i = 0; i < level; i++) {
         qtm[2 * i] = c->primes[level] % c->primes[i];
         qtm[2 * i + 1] = (u64)(((u128)1 << 64) / c->primes[i]);   // Shoup companion of 1
+    }
+    if (level >= 1) {
+        // sources s = {q_level, p_0..p_{K-1}} (prime indices), P' = prod s
+        const int ns = c->K + 1;
+        std::vector<int> sp(ns);
+        sp[0] = level;
+        for (int k = 0; k < c->K; k++) sp[1 + k] = c->nq + k;
+        ConvTable m;
+        memset(&m, 0, sizeof(m));
+        m.n_src = ns;
+        std::vector<u64> msc(4 * ns);
+        for (int a = 0; a < ns; a++) {
+            const u64 sa = c->primes[sp[a]];
+            u64 prod = 1;
+            for (int b = 0; b < ns; b++) if (b != a) prod = mulmod_h(prod, c->primes[sp[b]] % sa, sa);
+            const u64 hinv = inv_h(prod, sa);
+            m.hatinv[a] = hinv;
+            m.hatinv_p[a] = shoup_h(hinv, sa);
+            for (int i = 0; i < level; i++) {
+                const u64 qi = c->primes[i];
+                u64 pm = 1;
+                for (int b = 0; b < ns; b++) if (b != a) pm = mulmod_h(pm, c->primes[sp[b]] % qi, qi);
+                m.hat_m[a * BCN_MAX_LIMBS + i] = mont_h(pm, qi);
+            }
+            const u64 x = mulmod_h(c->hpr[sp[a]].pad[0], hinv, sa), y = mulmod_h(c->wn_host[sp[a]], hinv, sa);
+            msc[4 * a] = x; msc[4 * a + 1] = shoup_h(x, sa);
+            msc[4 * a + 2] = y; msc[4 * a + 3] = shoup_h(y, sa);
+        }
+        std::vector<u64> pq(2 * level);
+        for (int i = 0; i < level; i++) {
+            const u64 qi = c->primes[i];
+            u64 v = c->primes[level] % qi;
+            for (int k = 0; k < c->K; k++) v = mulmod_h(v, c->primes[c->nq + k] % qi, qi);
+            const u64 vi = inv_h(v, qi);
+            pq[2 * i] = vi;
+            pq[2 * i + 1] = shoup_h(vi, qi);
+        }
+        CUDA_TRY(dmalloc((void**)&T.mdr, sizeof(ConvTable), &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(T.mdr, &m, sizeof(ConvTable), cudaMemcpyHostToDevice));
+        CUDA_TRY(dmalloc((void**)&T.mdr_scale, sizeof(u64) * msc.size(), &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(T.mdr_scale, msc.data(), sizeof(u64) * msc.size(), cudaMemcpyHostToDevice));
+        CUDA_TRY(dmalloc((void**)&T.pqinv, sizeof(u64) * pq.size(), &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(T.pqinv, pq.data(), sizeof(u64) * pq.size(), cudaMemcpyHostToDevice));
     }
     std::vector<u64> ups(4 * (level + 1));
     for (int j = 0; j < ndig; j++) {
@@ -448,6 +498,7 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
         pmod[2 * i] = P;
         pmod[2 * i + 1] = shoup_h(P, qi);
     }
+    c->pmod_host = pmod;
     CUDA_TRY(dmalloc((void**)&c->pmod, sizeof(u64) * pmod.size(), &c->table_bytes));
     CUDA_TRY(cudaMemcpy(c->pmod, pmod.data(), sizeof(u64) * pmod.size(), cudaMemcpyHostToDevice));
     {
@@ -498,6 +549,7 @@ int bcn_ctx_destroy(bcn_ctx* c) {
         cudaFree(kv.second.modup); cudaFree(kv.second.moddown);
         cudaFree(kv.second.pinv); cudaFree(kv.second.qlinv);
         cudaFree(kv.second.qtopmod); cudaFree(kv.second.upscale);
+        cudaFree(kv.second.mdr); cudaFree(kv.second.mdr_scale); cudaFree(kv.second.pqinv);
     }
     for (auto& kv : c->keys) cudaFree(kv.second);
     cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
@@ -1194,6 +1246,117 @@ int bcn_rotsum_keys(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* cons
                            (long long)c->nbasis * N, ext, c->pr, t0 > 0, st));
     }
     return moddown_tail(c, (u64*)out, 2LL * nl * N, B, G, level, C0, (long long)nl * N, 0, 1u, T, Z, st);
+}
+
+// merged ModDown + rescale: out (level-1, [G][2][level][N]) =
+// (B + P C) / (P q_level) for B [G][2][level+1+K][N] (consumed) and the
+// optional addend C [G][2][level+1][N] (component 1 only when add_c1).
+static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int G, int level, const LevelTables* T,
+                    u64* Z, cudaStream_t st) {
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K;
+    Limbs sl;
+    sl.n = c->K + 1;
+    sl.prime[0] = (short)level;
+    for (int k = 0; k < c->K; k++) sl.prime[1 + k] = (short)(c->nq + k);
+    if (C) {   // Y_top = B_top + P C_top (component 0, and 1 when add_c1)
+        const int npoly = add_c1 ? 2 * G : G;
+        const long long ds = add_c1 ? (long long)next * N : 2LL * next * N;
+        const long long ss = add_c1 ? (long long)nl * N : 2LL * nl * N;
+        CUDA_TRY(axpy_limb_op(B + (size_t)level * N, ds, C + (size_t)level * N, ss, npoly, c->pmod_host[2 * level],
+                              c->pmod_host[2 * level + 1], c->primes[level], c->logn, st));
+    }
+    Limbs ql = limbs_range(0, level);
+    if ((c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_MODDOWN")) {
+        NttArgs ia = ntt_args(c, B + (size_t)level * N, (long long)next * N, sl);
+        ia.inv_scale = T->mdr_scale;
+        CUDA_TRY(ntt_launch(true, c->logn, ia, sl.n, 2 * G, st));
+        NttArgs a = ntt_args(c, out, (long long)level * N, ql);
+        a.pro = 2;
+        a.pro_src = B + (size_t)level * N;
+        a.pro_stride = (long long)next * N;
+        a.pro_conv = T->mdr;
+        a.pro_K = sl.n;
+        a.epi = 3;
+        a.epi_c = B;
+        a.epi_cps = (long long)next * N;
+        a.epi_cls = N;
+        a.epi_tab = T->pqinv;
+        a.epi_tab2 = T->qlinv;
+        a.epi_add = C;
+        a.epi_aps = 2LL * nl * N;
+        a.epi_acs = (long long)nl * N;
+        a.epi_add_c1 = add_c1;
+        CUDA_TRY(ntt_launch(false, c->logn, a, level, 2 * G, st));
+        return BCN_OK;
+    }
+    CUDA_TRY(ntt_run(c, true, B + (size_t)level * N, (long long)next * N, sl, 2 * G, st));
+    Limbs ext = limbs_ext(c, level);
+    CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st));
+    CUDA_TRY(ntt_run(c, false, Z, (long long)level * N, ql, 2 * G, st));
+    CUDA_TRY(mdr_combine_op(out, B, (long long)next * N, Z, C, 2LL * nl * N, add_c1, 2 * G, level, c->logn, ql, c->pr,
+                            T->pqinv, T->qlinv, st));
+    return BCN_OK;
+}
+
+int bcn_rotsum_rescale(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* const* U, const uint64_t* const* cts,
+                       const uint64_t* gal, const uint64_t* const* pts, const int* pt_batched,
+                       const uint64_t* const* keys, int n_ct, const uint64_t* const* ct_cts,
+                       const uint64_t* const* ct_pts, const int* ct_batched, int G, int level, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (n_terms < 1) return fail(BCN_ERR_PARAM, "no rotation terms");
+    if (level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int k = 0; k < n_terms; k++) {
+        if (gal[k] == 1 || (gal[k] & 1) == 0) return fail(BCN_ERR_PARAM, "rotation sum needs odd Galois elements != 1");
+        if (!key_ptr(c, gal[k])) {
+            e = bcn_keygen_galois(c, gal[k], stream);
+            if (e) return e;
+        }
+    }
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K, ndig = T->ndig;
+    Limbs ext = limbs_ext(c, level);
+    int err = 0;
+    u64* B = scratch_get(c, (size_t)G * 2 * next * N + (size_t)G * 2 * nl * N + (size_t)G * 2 * level * N, &err);
+    if (!B) return err;
+    u64* Cf = B + (size_t)G * 2 * next * N;
+    u64* Z = Cf + (size_t)G * 2 * nl * N;
+    if (n_ct > 0) {   // ct x pt terms -> both components of the addend
+        MacTerms M;
+        Limbs l = limbs_range(0, nl);
+        for (int t0 = 0; t0 < n_ct; t0 += BCN_MAC_TERMS) {
+            M.n = std::min(BCN_MAC_TERMS, n_ct - t0);
+            for (int k = 0; k < M.n; k++) {
+                M.ct[k] = (const u64*)ct_cts[t0 + k];
+                M.pt[k] = (const u64*)ct_pts[t0 + k];
+                M.pt_batched[k] = (unsigned char)(ct_batched[t0 + k] != 0);
+            }
+            CUDA_TRY(mac_terms_op(Cf, M, G, nl, c->logn, l, c->pr, t0 > 0, st));
+        }
+    }
+    RotTerms R;
+    for (int t0 = 0; t0 < n_terms; t0 += BCN_ROT_TERMS) {
+        R.n = std::min(BCN_ROT_TERMS, n_terms - t0);
+        for (int k = 0; k < R.n; k++) {
+            const u64* pk = keys ? (const u64*)keys[t0 + k] : nullptr;
+            R.key[k] = pk ? pk : key_ptr(c, gal[t0 + k]);
+            R.U[k] = (const u64*)U[t0 + k];
+            R.c0[k] = (const u64*)cts[t0 + k];
+            R.pt[k] = (const u64*)pts[t0 + k];
+            R.g[k] = (u32)gal[t0 + k];
+            R.pt_batched[k] = (unsigned char)(pt_batched[t0 + k] != 0);
+            if (pk && R.pt_batched[k]) return fail(BCN_ERR_PARAM, "premultiplied keys need a shared (unbatched) pt");
+            R.fused[k] = (unsigned char)(pk != nullptr || R.pt[k] == nullptr);
+        }
+        CUDA_TRY(rotsum_op(B, Cf, R, 2LL * nl * N, G, nl, next, ndig, c->logn, 2LL * c->nbasis * N,
+                           (long long)c->nbasis * N, ext, c->pr, t0 > 0, st, 2LL * nl * N, (t0 > 0) || (n_ct > 0)));
+    }
+    return mdr_tail(c, (u64*)out, B, Cf, n_ct > 0, G, level, T, Z, st);
 }
 
 int bcn_rotate_hoisted(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, const uint64_t* U, int G,

@@ -93,13 +93,15 @@ struct Prologue {             // MODE 0 plain, 1 rescale lift, 2 ModDown base co
 
 // fused epilogue: what the forward transform writes for canonical result v at j
 template <int MODE>
-struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top^-1, 2 ModDown combine
+struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top^-1, 2 ModDown combine,
+                              // 3 merged ModDown + rescale: (c - v) (P q_l)^-1 + addend q_l^-1
     u64* out;
     const u64* c;
     u64 q, w, wp;
     const u64* add = nullptr;   // ModDown addend for this (ct, component, limb), or null
     u32 g = 1;
     int logn = 0;
+    u64 w2 = 0, wp2 = 0;
     __device__ __forceinline__ u64 operator()(int j, u64 v) const {
         if constexpr (MODE == 0) {
             return v;
@@ -107,6 +109,8 @@ struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top
             u64 r = shoup(c[j] + q - v, w, wp, q);
             if constexpr (MODE == 2) {
                 if (add) r = add_mod(r, add[g == 1u ? j : (int)automorph_src((u32)j, g, logn)], q);
+            } else if constexpr (MODE == 3) {
+                if (add) r = add_mod(r, shoup(add[j], w2, wp2, q), q);
             }
             return r;
         }
@@ -278,18 +282,22 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     Epilogue<EM> epi;
     epi.out = g;
     epi.q = q;
-    if constexpr (EM == 1 || EM == 2) {
+    if constexpr (EM == 1 || EM == 2 || EM == 3) {
         epi.c = a.epi_c + (size_t)poly * a.epi_cps + (size_t)t * a.epi_cls;
         epi.w = a.epi_tab[2 * t];
         epi.wp = a.epi_tab[2 * t + 1];
-        if constexpr (EM == 2) {
+        if constexpr (EM == 2 || EM == 3) {
             const int comp = poly & 1;
+            const long long acs = a.epi_acs ? a.epi_acs : (long long)a.limbs.n * C::N;
             epi.add = (a.epi_add && (comp == 0 || a.epi_add_c1))
-                          ? a.epi_add + (size_t)(poly >> 1) * a.epi_aps + (size_t)comp * a.limbs.n * C::N +
-                                (size_t)t * C::N
+                          ? a.epi_add + (size_t)(poly >> 1) * a.epi_aps + (size_t)comp * acs + (size_t)t * C::N
                           : nullptr;
             epi.g = a.epi_g;
             epi.logn = LOGN;
+            if constexpr (EM == 3) {
+                epi.w2 = a.epi_tab2[2 * t];
+                epi.wp2 = a.epi_tab2[2 * t + 1];
+            }
         }
     } else {
         epi.c = nullptr;
@@ -432,6 +440,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
@@ -444,6 +453,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 2 && a.epi == 2) ntt_fwd_cluster<LOGN, 2, 2><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 2 && a.epi == 0) ntt_fwd_cluster<LOGN, 2, 0><<<grid, C::T, smem, st>>>(a);
+    else if (a.pro == 2 && a.epi == 3) ntt_fwd_cluster<LOGN, 2, 3><<<grid, C::T, smem, st>>>(a);
     else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(a);
     return launched();
 }

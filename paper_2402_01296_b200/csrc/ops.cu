@@ -522,7 +522,9 @@ template <int BLK>
 __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
         u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T, long long c0_gstride, int nq, int next,
         int ndig, int logn, long long kds, long long kcs, Limbs ext, const PrimeInfo* __restrict__ pr,
-        int accumulate) {
+        int acc_flags, long long c0_ostride) {
+    const int accumulate = acc_flags & 1;             // add onto B
+    const int c0_acc = (acc_flags >> 1) & 1;          // add onto C0
     // one thread per output word; term k+1's staging words, key words and
     // multiplier are loaded into registers while term k is being multiplied
     constexpr int MAXD = 3;
@@ -637,9 +639,9 @@ __global__ void __launch_bounds__(BLK < 1024 ? BLK : 1024) rotsum_kernel(
     *o0 = r0;
     *o1 = r1;
     if (has_c0) {
-        u64* oc = C0 + p * (long long)nq * N + (long long)t * N + n;
+        u64* oc = C0 + p * c0_ostride + (long long)t * N + n;
         u64 rc = cc.reduce(q, qn, inv1);
-        if (accumulate) rc = add_mod(rc, *oc, q);
+        if (c0_acc) rc = add_mod(rc, *oc, q);
         *oc = rc;
     }
 }
@@ -668,9 +670,12 @@ cudaError_t premul_key_op(u64* out, const u64* key, const u64* pt, int ndig, int
 
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
-                      int accumulate, cudaStream_t st) {
+                      int accumulate, cudaStream_t st, long long c0_ostride, int c0_accumulate) {
     const int N = 1 << logn;
     if (terms.n <= 0 || G <= 0) return cudaSuccess;
+    if (c0_ostride < 0) c0_ostride = (long long)nq * N;
+    if (c0_accumulate < 0) c0_accumulate = accumulate;
+    const int flags = (accumulate ? 1 : 0) | (c0_accumulate ? 2 : 0);
     if ((long long)G * (ndig + 2) * next * N >= (1LL << 32) || (long long)G * c0_gstride >= (1LL << 32))
         return cudaErrorInvalidValue;                 // kernel offsets are 32-bit
     if (N >= 1024) {
@@ -680,18 +685,71 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
         if (!cfg) { cudaFuncSetAttribute(rotsum_kernel<BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
         dim3 grid(G, N / BLK, next);
         rotsum_kernel<BLK><<<grid, BLK, smem, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, kds, kcs, ext, pr,
-                                                    accumulate);
+                                                    flags, c0_ostride);
     } else {
         const size_t smem = (size_t)(ndig + 1) * N * sizeof(u64);
         dim3 grid(G, 1, next);
         switch (N) {
 #define BCN_RS(NN) case NN: rotsum_kernel<NN><<<grid, NN, smem, st>>>(B, C0, terms, c0_gstride, \
-                        nq, next, ndig, logn, kds, kcs, ext, pr, accumulate); break;
+                        nq, next, ndig, logn, kds, kcs, ext, pr, flags, c0_ostride); break;
             BCN_RS(8) BCN_RS(16) BCN_RS(32) BCN_RS(64) BCN_RS(128) BCN_RS(256) BCN_RS(512)
 #undef BCN_RS
             default: return cudaErrorInvalidValue;
         }
     }
+    return launched();
+}
+
+// dst[p][n] += src[p][n] * w mod q  (merged ModDown + rescale: Y_top = B_top + P C_top)
+__global__ void axpy_limb_kernel(u64* __restrict__ dst, long long ds, const u64* __restrict__ src, long long ss,
+                                 u64 w, u64 wp, u64 q, int logn, long long total) {
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long p = idx >> logn;
+        const int n = (int)(idx & ((1 << logn) - 1));
+        u64* d = dst + p * ds + n;
+        *d = add_mod(*d, shoup(src[p * ss + n], w, wp, q), q);
+    }
+}
+
+cudaError_t axpy_limb_op(u64* dst, long long ds, const u64* src, long long ss, int npoly, u64 w, u64 wp, u64 q,
+                         int logn, cudaStream_t st) {
+    const long long total = (long long)npoly << logn;
+    if (!total) return cudaSuccess;
+    axpy_limb_kernel<<<blocks_for(total, 256), 256, 0, st>>>(dst, ds, src, ss, w, wp, q, logn, total);
+    return launched();
+}
+
+// out[p][i] = (B[p][i] - Z[p][i]) * pq_i + C[(p/2)][(p%2)][i] * ql_i for i < nout (staged merged ModDown+rescale)
+__global__ void mdr_combine_kernel(u64* __restrict__ out, const u64* __restrict__ B, long long bps,
+                                   const u64* __restrict__ Z, const u64* __restrict__ C, long long cps, int add_c1,
+                                   int nout, int logn, Limbs ql, const PrimeInfo* __restrict__ pr,
+                                   const u64* __restrict__ pqinv, const u64* __restrict__ qlinv, long long total) {
+    const int N = 1 << logn;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int n = (int)(idx & (N - 1));
+        const long long rest = idx >> logn;
+        const int i = (int)(rest % nout);
+        const long long p = rest / nout;
+        const u64 q = pr[ql.prime[i]].q;
+        u64 r = shoup(B[p * bps + (long long)i * N + n] + q - Z[(p * nout + i) * N + n], pqinv[2 * i],
+                      pqinv[2 * i + 1], q);
+        const int comp = (int)(p & 1);
+        if (C && (comp == 0 || add_c1))
+            r = add_mod(r, shoup(C[(p >> 1) * cps + (long long)comp * (nout + 1) * N + (long long)i * N + n],
+                                 qlinv[2 * i], qlinv[2 * i + 1], q), q);
+        out[(p * nout + i) * N + n] = r;
+    }
+}
+
+cudaError_t mdr_combine_op(u64* out, const u64* B, long long bps, const u64* Z, const u64* C, long long cps,
+                           int add_c1, int npoly, int nout, int logn, const Limbs& ql, const PrimeInfo* pr,
+                           const u64* pqinv, const u64* qlinv, cudaStream_t st) {
+    const long long total = (long long)npoly * nout << logn;
+    if (!total) return cudaSuccess;
+    mdr_combine_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, B, bps, Z, C, cps, add_c1, nout, logn, ql, pr,
+                                                              pqinv, qlinv, total);
     return launched();
 }
 

@@ -59,6 +59,10 @@ struct NttArgs {
     // table pro_conv[d] (pro_K ignored).  0 = ModDown form.
     int pro_dnum;
     long long pro_dstride;
+    // epilogue 3 (merged ModDown + rescale): out = (c - v) * epi_tab + addend * epi_tab2,
+    // addend component stride epi_acs (0: limbs.n * N)
+    const u64* epi_tab2;
+    long long epi_acs;
     // skipped limbs (skip_alpha) copy copy_src[(poly / skip_dnum) * copy_stride + t * N + n]
     // instead of being left untouched (ModUp: the digit's own NTT-domain limbs)
     const u64* copy_src;
@@ -103,9 +107,18 @@ struct RotTerms {
 // out[j][c][kt][n] = key[j][c][kt][n] (x) pt[t][n] over the extended limbs t of a level
 cudaError_t premul_key_op(u64* out, const u64* key, const u64* pt, int ndig, int next, int logn,
                           long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr, cudaStream_t st);
+// C0 output: slot set p at C0 + p * c0_ostride (nq limbs); c0_accumulate adds onto it
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long key_digit_stride, long long key_comp_stride, const Limbs& ext,
-                      const PrimeInfo* pr, int accumulate, cudaStream_t st);
+                      const PrimeInfo* pr, int accumulate, cudaStream_t st, long long c0_ostride = -1,
+                      int c0_accumulate = -1);
+// dst[p][n] = dst[p][n] + src[p][n] * w (mod q) on one limb (Shoup pair w, wp)
+cudaError_t axpy_limb_op(u64* dst, long long ds, const u64* src, long long ss, int npoly, u64 w, u64 wp, u64 q,
+                         int logn, cudaStream_t st);
+// merged ModDown + rescale combine (staged form): out_i = (B_i - Z_i) * pq_i + C_i * ql_i
+cudaError_t mdr_combine_op(u64* out, const u64* B, long long bps, const u64* Z, const u64* C, long long cps,
+                           int add_c1, int npoly, int nout, int logn, const Limbs& ql, const PrimeInfo* pr,
+                           const u64* pqinv, const u64* qlinv, cudaStream_t st);
 // Multi-output linear combination out_o = sum_k ct_k (x) pt_{o,k} for a tile of
 // up to BCN_MAC_OUT outputs sharing the same ct terms (conv output channels).
 #define BCN_MAC_OUT 16

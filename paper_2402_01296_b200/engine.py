@@ -255,6 +255,26 @@ class Engine:
             _lib.call("bcn_rotsum_keys", self._h, _ptr(out), n, Us, cts, gal, pts, bat, ks, G, level, _stream())
         return out
 
+    def rotsum_rescale(self, terms, level: int, keys=None, ct_terms=()) -> torch.Tensor:
+        """Rescaled lazy sum: rotation terms as in rotsum plus (ct, pt) terms, with
+        ONE merged ModDown + rescale per component -> u64[G,2,level,N] at level-1."""
+        G = terms[0][0].shape[0]
+        n = len(terms)
+        Us = (ctypes.c_uint64 * n)(*[t[1].data_ptr() for t in terms])
+        cts = (ctypes.c_uint64 * n)(*[t[0].data_ptr() for t in terms])
+        gal = (ctypes.c_uint64 * n)(*[int(t[2]) for t in terms])
+        pts = (ctypes.c_uint64 * n)(*[0 if t[3] is None else t[3].data_ptr() for t in terms])
+        bat = (ctypes.c_int * n)(*[int(t[3] is not None and t[3].shape[0] != 1) for t in terms])
+        ks = None if keys is None else (ctypes.c_uint64 * n)(*[0 if k is None else k.data_ptr() for k in keys])
+        m = len(ct_terms)
+        c_c = (ctypes.c_uint64 * max(m, 1))(*[t[0].data_ptr() for t in ct_terms])
+        c_p = (ctypes.c_uint64 * max(m, 1))(*[t[1].data_ptr() for t in ct_terms])
+        c_b = (ctypes.c_int * max(m, 1))(*[int(t[1].shape[0] != 1) for t in ct_terms])
+        out = self.empty_ct(G, level - 1)
+        _lib.call("bcn_rotsum_rescale", self._h, _ptr(out), n, Us, cts, gal, pts, bat, ks, m, c_c, c_p, c_b, G,
+                  level, _stream())
+        return out
+
     def premul_key(self, g: int, pt: torch.Tensor, level: int) -> torch.Tensor:
         """Galois key g with the (unbatched, ext-basis Montgomery) multiplier pt
         folded in, for rotsum(keys=...): u64[dnum,2,nbasis,N]."""

@@ -256,6 +256,19 @@ class Ciphertext:
                     STATS["modup"] += 1
             keys = [_premul_key(self.ctx, t[2], t[3], lvl) if _fold_keys() and t[3] is not None
                     and t[3].shape[0] == 1 else None for t in rots]
+            if self._scaled and _merged_rescale():
+                # ModDown and rescale in one base conversion
+                out = eng.rotsum_rescale([(t[1]._data, t[1]._modup, t[2], t[3]) for t in rots], lvl,
+                                         keys=keys if any(k is not None for k in keys) else None,
+                                         ct_terms=[(t[1], t[2]) for t in cts])
+                STATS["moddown"] += 1
+                STATS["keyswitch_lazy"] += len(rots)
+                STATS["rescale"] += 1
+                STATS["mac_launch"] += 1 if cts else 0
+                object.__setattr__(self, "_data", out)
+                object.__setattr__(self, "_terms", None)
+                object.__setattr__(self, "_data_scale", self.scale)
+                return self
             out = eng.rotsum([(t[1]._data, t[1]._modup, t[2], t[3]) for t in rots], lvl,
                              keys=keys if any(k is not None for k in keys) else None)
             STATS["moddown"] += 1
@@ -447,6 +460,10 @@ def _cache_put(ctx: HeContext, k, v) -> None:
 
 def _use_imma() -> bool:
     return os.environ.get("BCN_MAC_IMMA", "1") != "0"
+
+
+def _merged_rescale() -> bool:
+    return os.environ.get("BCN_MERGED_RESCALE", "1") != "0"
 
 
 def _fold_keys() -> bool:

@@ -280,3 +280,35 @@ def test_mac_multi_planes_bitexact(n_out, K, G, extreme):
     want = to_numpy_u64(eng.mac_multi(cts, pts, L, rescale=False))
     got = to_numpy_u64(eng.mac_multi_planes(cts, eng.pack_planes(pts, L), n_out, L, rescale=False))
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("N,L", [(1024, 3), (8192, 3)])
+def test_rotsum_rescale_merged_matches_oracle(N, L):
+    """Rotation sum + ct x pt terms with ONE merged ModDown + rescale
+    (bcn_rotsum_rescale; staged at N=1024, fused cluster NTT at N=8192) ==
+    Oracle.rotsum_rescale bit for bit, with and without premultiplied keys;
+    decrypts to the slot-wise expectation."""
+    eng, orc, hp = _pair(N, L, dnum=2)
+    rng = np.random.default_rng(31)
+    v, ct, oc = _enc2(eng, orc, N, rng)
+    w, ct2, oc2 = _enc2(eng, orc, N, rng, counter=41)
+    Ua, Ub = eng.modup(ct, L), eng.modup(ct2, L)
+    from paper_2402_01296_b200.params import galois_element as ge
+    p1, p2, p3, p4 = rng.standard_normal((4, N // 2))
+    ql = float(hp.q[L])
+    terms = [(ct, Ua, ge(1, N), eng.encode_ext(p1, L, ql)), (ct2, Ub, ge(3, N), eng.encode_ext(p2, L, ql)),
+             (ct, Ua, ge(9, N), None)]
+    cterms = [(ct2, eng.encode(p3, L, ql, montgomery=True)), (ct, eng.encode(p4, L, ql, montgomery=True))]
+    want = [orc.rotsum_rescale([(oc[i], 1, p1), (oc2[i], 3, p2), (oc[i], 9, None)],
+                               [(oc2[i], p3), (oc[i], p4)], L) for i in range(2)]
+    got = eng.rotsum_rescale(terms, L, ct_terms=cterms)
+    _assert_ct(got, want)
+    keys = [eng.premul_key(t[2], t[3], L) if t[3] is not None else None for t in terms]
+    _assert_ct(eng.rotsum_rescale(terms, L, keys=keys, ct_terms=cterms), want)
+    # without ct terms (addend on component 0 only)
+    want0 = [orc.rotsum_rescale([(oc[i], 1, p1), (oc2[i], 3, p2)], [], L) for i in range(2)]
+    _assert_ct(eng.rotsum_rescale(terms[:2], L), want0)
+    scaled = eng.rotsum_rescale(terms[:2], L, ct_terms=cterms)     # every term carries a multiplier
+    dec = eng.decrypt(scaled, L - 1, hp.scale).cpu().numpy()
+    exp = np.roll(v, -1, axis=1) * p1 + np.roll(w, -3, axis=1) * p2 + w * p3 + v * p4
+    assert np.abs(dec - exp).max() < 1e-4

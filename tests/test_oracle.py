@@ -141,6 +141,21 @@ def test_oracle_fc_4_to_2_matches_reference_pin(orc):
     assert np.abs(orc.decrypt(acc)[:2] - np.array([40.0, 50.0])).max() < 1e-6
 
 
+def test_merged_moddown_rescale_equals_separate_evaluation(orc):
+    """rotsum_rescale (ONE base conversion from {q_l, P}) decrypts to the same
+    slots as rescale(rotsum + ct terms) (ModDown, then rescale), to CKKS noise."""
+    rng = np.random.default_rng(12)
+    x, y, p1, p2, p3 = rng.standard_normal((5, 32))
+    cx, cy = orc.encrypt(x, 21), orc.encrypt(y, 22)
+    L = cx.level
+    merged = orc.rotsum_rescale([(cx, 1, p1), (cy, 5, p2)], [(cy, p3)], L)
+    assert merged.level == L - 1
+    want = np.roll(x, -1) * p1 + np.roll(y, -5) * p2 + y * p3
+    assert np.abs(orc.decrypt(merged)[:32] - want).max() < 1e-6
+    sep = orc.add_cc(orc.add_cc(orc.rotate_mul(cx, 1, p1), orc.rotate_mul(cy, 5, p2)), orc.mul_plain(cy, p3))
+    assert np.abs(orc.decrypt(merged)[:32] - orc.decrypt(sep)[:32]).max() < 1e-6
+
+
 def test_hoisted_rotation_equals_fresh_modup(orc):
     rng = np.random.default_rng(5)
     ct = orc.encrypt(rng.standard_normal(32), 9)
