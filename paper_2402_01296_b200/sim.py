@@ -537,6 +537,34 @@ def _times_plain(x: Ciphertext, plain) -> Ciphertext:
     return Ciphertext(None, level - 1, x.scale, ctx, terms=(("ct", x._data, pt),), data_scale=x.scale * float(ql))
 
 
+def _distributes(a: Ciphertext) -> bool:
+    """An unscaled lazy sum whose terms all sit at its level (sum_pool's
+    rotations + identity) can take a multiplier term by term."""
+    if os.environ.get("BCN_DISTRIBUTE_MUL", "1") == "0":
+        return False
+    for t in a._terms:
+        if t[0] == "ct" and t[1].shape[2] != a.level + 1:
+            return False
+        if t[0] == "rot" and t[1].level != a.level:
+            return False
+    return True
+
+
+def _lazy_times_plain(a: Ciphertext, plain) -> Ciphertext:
+    """(sum_t term_t) * plain as the scaled lazy sum sum_t term_t * plain: the
+    rotations keep their deferred ModDown, which the later materialisation
+    merges with the rescale (one base conversion)."""
+    ctx = a.ctx
+    level = a.level
+    ql = float(ctx.q(level))
+    has_ct = any(t[0] == "ct" for t in a._terms)
+    has_rot = any(t[0] == "rot" for t in a._terms)
+    pt = _encode(ctx, plain, level, ql, True, a.batch) if has_ct else None
+    pt_ext = _encode(ctx, plain, level, ql, True, a.batch, ext=True) if has_rot else None
+    terms = tuple(("ct", t[1], pt) if t[0] == "ct" else ("rot", t[1], t[2], pt_ext) for t in a._terms)
+    return Ciphertext(None, level - 1, a.scale, ctx, terms=terms, data_scale=a.scale * ql)
+
+
 def _rot_times_plain(c: Ciphertext, r: int, plain) -> Ciphertext:
     """rotate(c, r) * plain as a lazy rotation term (ModDown deferred to the sum)."""
     ctx = c.ctx
@@ -564,6 +592,8 @@ def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Cipherte
         rec.bump("Mul_PC")
         if mask:
             rec.bump("Mul_PC_mask")
+    if not is_cc and a.pending and not a._scaled and _distributes(a):
+        return _lazy_times_plain(a, b)
     a.materialize()
     if not is_cc:
         return _times_plain(a, b)
