@@ -137,6 +137,20 @@ int bcn_pack_planes(bcn_ctx *ctx, uint8_t *planes, int n_out, int n_terms, const
                     void *stream);
 int bcn_mac_multi_planes(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *cts,
                          const uint8_t *planes, int G, int level, int rescale, void *stream);
+/* Conv layer with lazy ModDown: out[o] = Rescale(sum_k pt[o][k]
+ * (x) rot_{g_k}(src_k)) with the key-switch inner products computed on the
+ * fly into the tensor-core MAC over the extended basis and ONE merged
+ * ModDown + rescale per output (no per-rotation ModDown).  srcs/Us: per term
+ * the source ct u64[G][2][level+1][N] and its bcn_modup (ignored for g = 1);
+ * planes: bcn_pack_planes_ext of the extended-basis plaintexts (rotation
+ * terms from bcn_encode_ext, identity terms level+1 limbs).
+ * out u64[n_out][G][2][level][N] at level-1. */
+int bcn_planes_ext_bytes(bcn_ctx *ctx, int n_out, int n_terms, int level, uint64_t *bytes);
+int bcn_pack_planes_ext(bcn_ctx *ctx, uint8_t *planes, int n_out, int n_terms, const uint64_t *const *pts,
+                        const int *term_limbs, int level, void *stream);
+int bcn_conv_ks_mac(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *srcs,
+                    const uint64_t *const *Us, const uint64_t *gal, const uint8_t *planes, int G, int level,
+                    void *stream);
 /* same, accumulating into an existing unrescaled out u64[G][2][level+1][N] */
 int bcn_mac_terms_acc(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts,
                       const uint64_t *const *pts, const int *pt_batched, int G, int level, void *stream);

@@ -872,6 +872,111 @@ int bcn_pack_planes(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const u
     return BCN_OK;
 }
 
+// extended-basis planes (conv with lazy ModDown): term k's plaintexts have
+// term_limbs[k] limbs (level+1+K for rotation terms, level+1 for identity
+// terms, whose special limbs multiply zeros); packed over level+1+K limbs
+int bcn_planes_ext_bytes(bcn_ctx* c, int n_out, int n_terms, int level, uint64_t* bytes) {
+    int e = check_level(c, level);
+    if (e) return e;
+    int opad, nch;
+    e = planes_geometry(n_out, n_terms, &opad, &nch);
+    if (e) return e;
+    *bytes = (uint64_t)(level + 1 + c->K) * c->N * nch * 8 * opad * 32;
+    return BCN_OK;
+}
+
+int bcn_pack_planes_ext(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const uint64_t* const* pts,
+                        const int* term_limbs, int level, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    int opad, nch;
+    e = planes_geometry(n_out, n_terms, &opad, &nch);
+    if (e) return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t np = (size_t)n_out * n_terms;
+    const size_t bytes = np * sizeof(u64*) + (size_t)n_terms * sizeof(int);
+    if (bytes > c->ptr_cap * sizeof(u64*)) {
+        if (c->ptr_dev) cudaFree(c->ptr_dev);
+        c->ptr_dev = nullptr;
+        c->ptr_cap = 0;
+        if (cudaMalloc(&c->ptr_dev, bytes) != cudaSuccess) return fail(BCN_ERR_CUDA, "pointer table");
+        c->ptr_cap = (bytes + sizeof(u64*) - 1) / sizeof(u64*);
+    }
+    std::vector<unsigned char> host(bytes);
+    memcpy(host.data(), pts, np * sizeof(u64*));
+    memcpy(host.data() + np * sizeof(u64*), term_limbs, (size_t)n_terms * sizeof(int));
+    CUDA_TRY(cudaMemcpyAsync(c->ptr_dev, host.data(), bytes, cudaMemcpyHostToDevice, st));
+    const int* tl = (const int*)((const unsigned char*)c->ptr_dev + np * sizeof(u64*));
+    CUDA_TRY(pack_planes_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch, level + 1 + c->K,
+                            c->logn, st, tl));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return BCN_OK;
+}
+
+static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int G, int level, const LevelTables* T,
+                    u64* Z, cudaStream_t st);
+static u64* key_ptr(bcn_ctx* c, u64 id);
+
+int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* srcs,
+                    const uint64_t* const* Us, const uint64_t* gal, const uint8_t* planes, int G, int level,
+                    void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    int opad, nch;
+    e = planes_geometry(n_out, n_terms, &opad, &nch);
+    if (e) return e;
+    if (level < 1) return fail(BCN_ERR_DEPTH, "multiplicative depth exhausted: level is 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int k = 0; k < n_terms; k++) {
+        if (gal[k] == 1) continue;
+        if ((gal[k] & 1) == 0) return fail(BCN_ERR_PARAM, "Galois elements must be odd");
+        if (!key_ptr(c, gal[k])) {
+            e = bcn_keygen_galois(c, gal[k], stream);
+            if (e) return e;
+        }
+    }
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K;
+    Limbs ext = limbs_ext(c, level);
+    KsTerms KT;
+    KT.n = n_terms;
+    MacImma M;
+    M.n_terms = n_terms;
+    M.n_out = n_out;
+    for (int k = 0; k < n_terms; k++) {
+        KT.src[k] = (const u64*)srcs[k];
+        KT.U[k] = (const u64*)Us[k];
+        KT.key[k] = gal[k] == 1 ? nullptr : key_ptr(c, gal[k]);
+        KT.g[k] = (u32)gal[k];
+        M.ct[k] = nullptr;
+    }
+    const long long cw = (long long)G * 2 * next * N;    // one output's extended-basis sum
+    const bool fused = (c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_MODDOWN");
+    int err = 0;
+    u64* acc = scratch_get(c, (size_t)n_out * cw + (fused ? 0 : (size_t)n_out * G * 2 * level * N), &err);
+    if (!acc) return err;
+    u64* Z = acc + (size_t)n_out * cw;
+    const size_t per_limb = (size_t)N * n_terms * 64 * sizeof(u64);
+    const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(next, ((size_t)4 << 30) / per_limb));
+    u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * 64, &err);
+    if (!S) return err;
+    for (int g0 = 0; g0 < G; g0 += 32) {
+        const int gcnt = std::min(32, G - g0);
+        for (int t0 = 0; t0 < next; t0 += tcnt) {
+            const int tc = std::min(tcnt, next - t0);
+            CUDA_TRY(slot_major_ks_op(S, KT, g0, gcnt, t0, tc, nl, next, T->ndig, c->logn, 2LL * c->nbasis * N,
+                                      (long long)c->nbasis * N, ext, c->pr, c->pmod, st));
+            CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, next, c->logn,
+                                 ext, c->pr, 0, st));
+        }
+    }
+    // the O x G extended-basis sums -> one merged ModDown + rescale each
+    return mdr_tail(c, (u64*)out, acc, nullptr, 0, n_out * G, level, T, Z, st);
+}
+
 int bcn_mac_multi_planes(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* cts,
                          const uint8_t* planes, int G, int level, int rescale, void* stream) {
     int e = check_level(c, level);

@@ -42,7 +42,7 @@ __device__ __forceinline__ int kperm(int kk) { return ((kk & 15) >> 2) * 8 + (kk
 // one thread per (o, chunk c, limb t, coefficient n); n fastest -> the 32
 // plaintext reads of a warp are coalesced, each thread writes 8 x 32 bytes
 __global__ void pack_planes_kernel(u8* __restrict__ planes, const u64* const* __restrict__ pts, int n_out,
-                                   int n_terms, int opad, int nch, int logn) {
+                                   int n_terms, int opad, int nch, int logn, const int* __restrict__ tlimbs) {
     const int N = 1 << logn;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
@@ -57,7 +57,8 @@ __global__ void pack_planes_kernel(u8* __restrict__ planes, const u64* const* __
 #pragma unroll
     for (int kk = 0; kk < 32; kk++) {
         const int k = c * 32 + kk;
-        const u64 v = (o < n_out && k < n_terms) ? __ldg(pts[(size_t)o * n_terms + k] + b) : 0ull;
+        const bool live = o < n_out && k < n_terms && (!tlimbs || t < tlimbs[k]);   // short plaintexts: 0 above
+        const u64 v = live ? __ldg(pts[(size_t)o * n_terms + k] + (tlimbs ? (long long)t * N + n : b)) : 0ull;
         const int pos = kperm(kk), d = pos >> 2, sh = (pos & 3) * 8;
 #pragma unroll
         for (int i = 0; i < 8; i++) w[i][d] |= (u32)((v >> (8 * i)) & 0xffull) << sh;
@@ -72,11 +73,93 @@ __global__ void pack_planes_kernel(u8* __restrict__ planes, const u64* const* __
 }
 
 cudaError_t pack_planes_op(u8* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad, int nch, int nl,
-                           int logn, cudaStream_t st) {
+                           int logn, cudaStream_t st, const int* tlimbs_dev) {
     const int N = 1 << logn;
     const int tpb = N < 128 ? N : 128;
     dim3 grid((N + tpb - 1) / tpb, nl, opad * nch);
-    pack_planes_kernel<<<grid, tpb, 0, st>>>(planes, pts_dev, n_out, n_terms, opad, nch, logn);
+    pack_planes_kernel<<<grid, tpb, 0, st>>>(planes, pts_dev, n_out, n_terms, opad, nch, logn, tlimbs_dev);
+    return launched();
+}
+
+// ------------------------------------- fused key switch + slot-major staging
+// Conv layer with lazy ModDown: term k is the source ciphertext x_k rotated
+// by g_k (g_k = 1: x_k itself).  Instead of materialising rot_k(x_k) (one
+// ModDown per rotation) the MAC runs on the extended basis over
+//   B'_k,c = sum_j sigma_k(U_k,j) (x) key_k,j,c  +  [c = 0] P sigma_k(c0_k)   (g_k != 1)
+//   B'_k,c = P x_k,c  on q_0..q_l, 0 on p_*                                   (g_k = 1)
+// so that ModDown(B'_k) = rot_k(x_k) exactly in value, and the conv outputs
+// need one merged ModDown+rescale each.  This kernel computes B'_k for a
+// block of slot sets and extended limbs and writes it slot-major
+// (S[(tl N + n) K + k][64]) for mac_imma_kernel; the key inner product never
+// touches HBM.  One CTA = (32 coefficients, limb, term).  Under X -> X^g an
+// aligned 32-block is the image of one aligned 32-block, so the gathers stay
+// inside one 256-byte segment.
+__global__ void __launch_bounds__(256, 3) slot_major_ks_kernel(u64* __restrict__ S, const KsTerms T, int g0, int gcnt,
+                                                            int t0, int nq, int next, int ndig, int logn,
+                                                            long long kds, long long kcs, Limbs ext,
+                                                            const PrimeInfo* __restrict__ pr,
+                                                            const u64* __restrict__ pmod) {
+    __shared__ u64 tile[64][33];
+    constexpr int MAXD = 4;                                       // key words kept in registers
+    const int N = 1 << logn;
+    const int n0 = blockIdx.x * 32, tl = blockIdx.y, k = blockIdx.z;
+    const int t = t0 + tl;
+    const int ncol = 2 * gcnt;
+    const int kt = ext.prime[t];
+    const PrimeInfo& P = pr[kt];
+    const u64 q = P.q;
+    const u32 g = T.g[k];
+    const long long LNs = (long long)nq * N;                      // source ct: [G][2][nq][N]
+    // lane = coefficient, warp = a strided set of (slot set, component) columns:
+    // the permutation, the key words and the P-multiplier are per lane only
+    const int nn = threadIdx.x & 31, w0 = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int n = n0 + nn;
+    const u64* src = T.src[k] + (long long)t * N;
+    if (g == 1u) {
+        const u64 pw = t < nq ? pmod[2 * t] : 0ull, pwp = t < nq ? pmod[2 * t + 1] : 0ull;
+#pragma unroll 4
+        for (int col = w0; col < ncol; col += nw) {
+            const int gs = g0 + (col >> 1), c = col & 1;
+            tile[col][nn] = t < nq ? shoup(__ldg(src + (long long)gs * 2 * LNs + c * LNs + n), pw, pwp, q) : 0ull;
+        }
+    } else {
+        const int sn = (int)automorph_src((u32)n, g, logn);
+        const int nd = ndig < MAXD ? ndig : MAXD;
+        u64 k0[MAXD], k1[MAXD];
+        const u64* kp = T.key[k] + (long long)kt * N + n;
+#pragma unroll
+        for (int j = 0; j < MAXD; j++)
+            if (j < nd) { k0[j] = __ldg(kp + j * kds); k1[j] = __ldg(kp + j * kds + kcs); }
+        const u64 pw = t < nq ? pmod[2 * t] : 0ull, pwp = t < nq ? pmod[2 * t + 1] : 0ull;
+        const long long dstr = (long long)next * N;
+        const u64* Ub = T.U[k] + (long long)t * N + sn;
+#pragma unroll 2
+        for (int col = w0; col < ncol; col += nw) {
+            const int gs = g0 + (col >> 1), c = col & 1;
+            const u64* Up = Ub + (long long)gs * ndig * dstr;
+            Acc4 a;
+            a.zero();
+#pragma unroll
+            for (int j = 0; j < MAXD; j++)
+                if (j < nd) a.mac(__ldg(Up + j * dstr), c ? k1[j] : k0[j]);
+            for (int j = MAXD; j < ndig; j++) a.mac(__ldg(Up + j * dstr), __ldg(kp + j * kds + c * kcs));
+            u64 v = a.reduce(q, P.qinv_neg, P.pad[2]);
+            if (c == 0 && t < nq) v = add_mod(v, shoup(__ldg(src + (long long)gs * 2 * LNs + sn), pw, pwp, q), q);
+            tile[col][nn] = v;
+        }
+    }
+    __syncthreads();
+    u64* dst = S + (((long long)tl * N + n0) * T.n + k) * 64;
+    for (int r = w0; r < 32; r += nw)                      // row r: this slot's 512-byte run
+        for (int col = nn; col < ncol; col += 32) dst[(long long)r * T.n * 64 + col] = tile[col][r];
+}
+
+cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,
+                             int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
+                             const u64* pmod, cudaStream_t st) {
+    const int N = 1 << logn;
+    dim3 grid(N / 32, tcnt, T.n);
+    slot_major_ks_kernel<<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, kds, kcs, ext, pr, pmod);
     return launched();
 }
 
@@ -100,10 +183,9 @@ __global__ void __launch_bounds__(256) slot_major_kernel(u64* __restrict__ S, co
     }
     __syncthreads();
     u64* dst = S + (((long long)tl * N + n0) * m.n_terms + k) * 64;
-    for (int x = threadIdx.x; x < 32 * ncol; x += blockDim.x) {
-        const int nn = x / ncol, col = x - nn * ncol;
-        dst[(long long)nn * m.n_terms * 64 + col] = tile[col][nn];
-    }
+    const int lane = threadIdx.x & 31;
+    for (int r = threadIdx.x >> 5; r < 32; r += blockDim.x >> 5)
+        for (int col = lane; col < ncol; col += 32) dst[(long long)r * m.n_terms * 64 + col] = tile[col][r];
 }
 
 // ---------------------------------------------------------------- kernel

@@ -140,7 +140,18 @@ struct MacImma {
     const u64* ct[BCN_IMMA_TERMS];
 };
 cudaError_t pack_planes_op(unsigned char* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad,
-                           int nch, int nl, int logn, cudaStream_t st);
+                           int nch, int nl, int logn, cudaStream_t st, const int* tlimbs_dev = nullptr);
+// conv terms with lazy ModDown (mac_imma.cu: slot_major_ks_kernel)
+struct KsTerms {
+    int n;
+    const u64* src[BCN_IMMA_TERMS];   // source ct u64[G][2][level+1][N]
+    const u64* U[BCN_IMMA_TERMS];     // its ModUp u64[G][ndig][ext][N] (g != 1)
+    const u64* key[BCN_IMMA_TERMS];   // Galois key (g != 1)
+    u32 g[BCN_IMMA_TERMS];            // 1: the source itself
+};
+cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,
+                             int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
+                             const u64* pmod, cudaStream_t st);
 // slot-major staging of a g-block x limb-block of the ct terms: S[(tl N + n) K + k][64]
 cudaError_t slot_major_op(u64* S, const MacImma& m, int g0, int gcnt, int t0, int tcnt, int nlimb, int logn,
                           cudaStream_t st);

@@ -484,16 +484,16 @@ def _premul_key(ctx: HeContext, g: int, pt, level: int):
     return k
 
 
-def _planes_for(ctx: HeContext, pts: list, level: int):
+def _planes_for(ctx: HeContext, pts: list, level: int, ext: bool = False):
     """Byte planes of an O x K plaintext matrix for the tensor-core MAC, packed
     once and cached next to the plaintexts.  The entry keeps the plaintext
     tensors alive and is only reused for the very same objects."""
-    key = ("planes", level, tuple(id(p) for row in pts for p in row))
+    key = ("planes_ext" if ext else "planes", level, tuple(id(p) for row in pts for p in row))
     hit = ctx._pt_cache.get(key)
     if hit is not None and all(a is b for a, b in zip(hit[1], (p for row in pts for p in row))):
         ctx._pt_cache.move_to_end(key)
         return hit[0]
-    planes = ctx.engine.pack_planes(pts, level)
+    planes = ctx.engine.pack_planes_ext(pts, level) if ext else ctx.engine.pack_planes(pts, level)
     STATS["plane_pack"] += 1
     _cache_put(ctx, key, (planes, [p for row in pts for p in row]))
     return planes
@@ -754,6 +754,69 @@ def materialize_group(cts: list) -> None:
                 object.__setattr__(c, "_data_scale", c.scale)
     for c in cts:
         c.materialize()
+
+
+def lazy_conv_enabled() -> bool:
+    return os.environ.get("BCN_LAZY_CONV", "1") != "0"
+
+
+def materialize_conv(accs: list) -> bool:
+    """Evaluate the output channels of a conv layer whose taps are lazy
+    rotation terms ("rot", x, g, pt_ext) and identity terms ("ct", x, pt) over
+    the same (source, rotation) list: key-switch inner products fused into the
+    tensor-core MAC over the extended basis, then ONE merged ModDown+rescale
+    per output (bcn_conv_ks_mac) -- no ModDown per rotation.
+    Returns False (nothing done) when the sums do not have that shape."""
+    lazy = [c for c in accs if c.pending]
+    if len(lazy) != len(accs) or len(lazy) < 2:
+        return False
+    first = lazy[0]
+    if not first._scaled or len(first._terms) > 256:
+        return False
+
+    def sig(t):
+        return (id(t[1]), t[2]) if t[0] == "rot" else (id(t[1]), 1)
+
+    ref = [sig(t) for t in first._terms]
+    for c in lazy:
+        if not c._scaled or c.level != first.level or len(c._terms) != len(ref):
+            return False
+        for t, r in zip(c._terms, ref):
+            if sig(t) != r or (t[0] == "rot" and (t[3] is None or t[3].shape[0] != 1)) or \
+                    (t[0] == "ct" and t[2].shape[0] != 1):
+                return False
+    ctx = first.ctx
+    eng = ctx.engine
+    lvl = first.data_level
+    srcs, Us, gals = [], [], []
+    for t in first._terms:
+        if t[0] == "rot":
+            src = t[1]
+            if src.level != lvl:
+                return False
+            if src._modup is None:
+                object.__setattr__(src, "_modup", eng.modup(src._data, src.level))
+                STATS["modup"] += 1
+            srcs.append(src._data)
+            Us.append(src._modup)
+            gals.append(int(t[2]))
+        else:
+            if t[1].shape[2] != lvl + 1:
+                return False
+            srcs.append(t[1])
+            Us.append(None)
+            gals.append(1)
+    pts = [[t[3] if t[0] == "rot" else t[2] for t in c._terms] for c in lazy]
+    out = eng.conv_ks_mac(srcs, Us, gals, _planes_for(ctx, pts, lvl, ext=True), len(lazy), lvl)
+    STATS["mac_launch"] += 1
+    STATS["moddown"] += len(lazy)
+    STATS["keyswitch_lazy"] += sum(g != 1 for g in gals)
+    STATS["rescale"] += len(lazy)
+    for c, d in zip(lazy, out):
+        object.__setattr__(c, "_data", d)
+        object.__setattr__(c, "_terms", None)
+        object.__setattr__(c, "_data_scale", c.scale)
+    return True
 
 
 def mark_reused(c: Ciphertext) -> None:

@@ -312,3 +312,37 @@ def test_rotsum_rescale_merged_matches_oracle(N, L):
     dec = eng.decrypt(scaled, L - 1, hp.scale).cpu().numpy()
     exp = np.roll(v, -1, axis=1) * p1 + np.roll(w, -3, axis=1) * p2 + w * p3 + v * p4
     assert np.abs(dec - exp).max() < 1e-4
+
+
+@pytest.mark.parametrize("N,L", [(1024, 3), (8192, 3)])
+def test_conv_ks_mac_matches_oracle(N, L):
+    """Conv layer with lazy ModDown (bcn_conv_ks_mac: key-switch inner products
+    fused into the slot-major staging, tensor-core MAC over the extended
+    basis, one merged ModDown+rescale per output) == Oracle.rotsum_rescale of
+    each output bit for bit (identity taps enter as P*x, rotations as
+    inner product + P*sigma(c0))."""
+    eng, orc, hp = _pair(N, L, dnum=2)
+    rng = np.random.default_rng(37)
+    v, ct, oc = _enc2(eng, orc, N, rng)
+    w, ct2, oc2 = _enc2(eng, orc, N, rng, counter=51)
+    Ua, Ub = eng.modup(ct, L), eng.modup(ct2, L)
+    from paper_2402_01296_b200.params import galois_element as ge
+    ql = float(hp.q[L])
+    taps = [(ct, Ua, 1, 0), (ct, Ua, 0, 0), (ct2, Ub, 3, 1), (ct2, Ub, 0, 1), (ct, Ua, 7, 0)]   # (src, U, r, which)
+    n_out = 3
+    vals = rng.standard_normal((n_out, len(taps), N // 2))
+    pts = [[eng.encode_ext(vals[o, k], L, ql) if r else eng.encode(vals[o, k], L, ql, montgomery=True)
+            for k, (_, _, r, _) in enumerate(taps)] for o in range(n_out)]
+    planes = eng.pack_planes_ext(pts, L)
+    got = eng.conv_ks_mac([t[0] for t in taps], [t[1] if t[2] else None for t in taps],
+                          [ge(t[2], N) if t[2] else 1 for t in taps], planes, n_out, L)
+    srcs = [oc, oc, oc2, oc2, oc]
+    for o in range(n_out):
+        want = [orc.rotsum_rescale([(srcs[k][i], r, vals[o, k]) for k, (_, _, r, _) in enumerate(taps) if r],
+                                   [(srcs[k][i], vals[o, k]) for k, (_, _, r, _) in enumerate(taps) if not r], L)
+                for i in range(2)]
+        _assert_ct(got[o], want)
+    dec = eng.decrypt(got[1], L - 1, hp.scale).cpu().numpy()
+    x = [v, v, w, w, v]
+    exp = sum(np.roll(x[k], -r, axis=1) * vals[1, k] for k, (_, _, r, _) in enumerate(taps))
+    assert np.abs(dec - exp).max() < 1e-4
