@@ -831,6 +831,12 @@ int bcn_mac_multi(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint6
 }
 
 // ---- tensor-core multi-output MAC (mac_imma.cu) ----
+static int imma_gblock() {
+    const char* v = getenv("BCN_IMMA_GB");
+    const int g = v ? atoi(v) : 16;
+    return g >= 1 && g <= 32 ? g : 16;
+}
+
 static int planes_geometry(int n_out, int n_terms, int* opad, int* nch) {
     if (n_out < 1 || n_terms < 1) return fail(BCN_ERR_PARAM, "no outputs / terms");
     if (n_terms > BCN_IMMA_TERMS) return fail(BCN_ERR_PARAM, "more than 256 terms per plane pack");
@@ -963,8 +969,11 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
     const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(next, ((size_t)4 << 30) / per_limb));
     u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * 64, &err);
     if (!S) return err;
-    for (int g0 = 0; g0 < G; g0 += 32) {
-        const int gcnt = std::min(32, G - g0);
+    // blocks of IMMA_GB slot sets: 16 -> 8-warp CTAs, two resident per SM, so one CTA's
+    // pipeline fill overlaps the other's MMAs (32 -> 16-warp CTAs, one per SM)
+    const int GB = imma_gblock();
+    for (int g0 = 0; g0 < G; g0 += GB) {
+        const int gcnt = std::min(GB, G - g0);
         for (int t0 = 0; t0 < next; t0 += tcnt) {
             const int tc = std::min(tcnt, next - t0);
             CUDA_TRY(slot_major_ks_op(S, KT, g0, gcnt, t0, tc, nl, next, T->ndig, c->logn, 2LL * c->nbasis * N,
@@ -1005,8 +1014,9 @@ int bcn_mac_multi_planes(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, cons
     const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(nl, ((size_t)4 << 30) / per_limb));
     u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * 64, &err);
     if (!S) return err;
-    for (int g0 = 0; g0 < G; g0 += 32) {
-        const int gcnt = std::min(32, G - g0);
+    const int GB = imma_gblock();
+    for (int g0 = 0; g0 < G; g0 += GB) {
+        const int gcnt = std::min(GB, G - g0);
         for (int t0 = 0; t0 < nl; t0 += tcnt) {
             const int tc = std::min(tcnt, nl - t0);
             CUDA_TRY(slot_major_op(S, M, g0, gcnt, t0, tc, nl, c->logn, st));

@@ -37,10 +37,12 @@ namespace bcn {
 
 typedef unsigned char u8;
 
-__device__ __forceinline__ int kperm(int kk) { return ((kk & 15) >> 2) * 8 + (kk >> 4) * 4 + (kk & 3); }
-
 // one thread per (o, chunk c, limb t, coefficient n); n fastest -> the 32
-// plaintext reads of a warp are coalesced, each thread writes 8 x 32 bytes
+// plaintext reads of a warp are coalesced.  Within a plane, each 16-row
+// M-tile is stored in mma.m16n8k32 A-fragment order: the 16 bytes a lane
+// (gq, tq) needs -- {row gq, row gq+8} x {k 4tq.., k 16+4tq..} -- are one
+// contiguous LDS.128 in the MAC kernel:
+//   offset(o, kk) = (o/16)*512 + ((o%8)*4 + (kk%16)/4)*16 + ((kk/16)*2 + (o%16)/8)*4 + kk%4
 __global__ void pack_planes_kernel(u8* __restrict__ planes, const u64* const* __restrict__ pts, int n_out,
                                    int n_terms, int opad, int nch, int logn, const int* __restrict__ tlimbs) {
     const int N = 1 << logn;
@@ -49,7 +51,7 @@ __global__ void pack_planes_kernel(u8* __restrict__ planes, const u64* const* __
     const int t = blockIdx.y;
     const int o = blockIdx.z / nch, c = blockIdx.z % nch;
     const long long b = (long long)t * N + n;
-    u32 w[8][8];
+    u32 w[8][8];                                          // [plane i][hi * 4 + tq]
 #pragma unroll
     for (int i = 0; i < 8; i++)
 #pragma unroll
@@ -58,17 +60,18 @@ __global__ void pack_planes_kernel(u8* __restrict__ planes, const u64* const* __
     for (int kk = 0; kk < 32; kk++) {
         const int k = c * 32 + kk;
         const bool live = o < n_out && k < n_terms && (!tlimbs || t < tlimbs[k]);   // short plaintexts: 0 above
-        const u64 v = live ? __ldg(pts[(size_t)o * n_terms + k] + (tlimbs ? (long long)t * N + n : b)) : 0ull;
-        const int pos = kperm(kk), d = pos >> 2, sh = (pos & 3) * 8;
+        const u64 v = live ? __ldg(pts[(size_t)o * n_terms + k] + b) : 0ull;
+        const int d = (kk >> 4) * 4 + ((kk & 15) >> 2), sh = (kk & 3) * 8;
 #pragma unroll
         for (int i = 0; i < 8; i++) w[i][d] |= (u32)((v >> (8 * i)) & 0xffull) << sh;
     }
-    u8* dst = planes + ((b * nch + c) * 8) * (long long)opad * 32 + (long long)o * 32;
+    const int m = o >> 4, g = o & 7, half = (o >> 3) & 1;
+    u8* base = planes + ((b * nch + c) * 8) * (long long)opad * 32 + (long long)m * 512 + g * 64 + half * 4;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-        uint4* p = reinterpret_cast<uint4*>(dst + (long long)i * opad * 32);
-        p[0] = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
-        p[1] = make_uint4(w[i][4], w[i][5], w[i][6], w[i][7]);
+        u32* p = reinterpret_cast<u32*>(base + (long long)i * opad * 32);
+#pragma unroll
+        for (int d = 0; d < 8; d++) p[((d & 3) * 16 + (d >> 2) * 8) / 4] = w[i][d];   // tq*16 + hi*8
     }
 }
 
@@ -263,16 +266,13 @@ __global__ void __launch_bounds__(512, 1)
         // B: rows k < n_terms of this slot's contiguous K x 64 block (A rows are zero past it)
         const int kmax = min(32, m.n_terms - c * 32);
         const u64* bsrc = S + (bl * m.n_terms + c * 32) * 64;
-        const int pieces = ngc >> 1;                     // 16-byte pieces per row
-        for (int x = tid; x < kmax * pieces; x += nthr) {
-            const int kk = x / pieces, pc = x - kk * pieces;
-            cp_async16(Bs + kk * IM_BP + 2 * pc, bsrc + kk * 64 + 2 * pc);
-        }
+        const int pieces = ngc >> 1;                     // 16-byte pieces per row (<= 32)
+        for (int kk = warp; kk < kmax; kk += nwarps)      // a row per warp, a piece per lane
+            if (lane < pieces) cp_async16(Bs + kk * IM_BP + 2 * lane, bsrc + kk * 64 + 2 * lane);
         cp_async_commit();
     };
     (void)arow;
     (void)LN;
-    (void)nwarps;
 
     int acc[15][4];
 #pragma unroll
@@ -301,13 +301,12 @@ __global__ void __launch_bounds__(512, 1)
             u32 b0[8], b1[8];
             transpose4(v, b0);
             transpose4(v + 4, b1);
-            const u8* As = Ab + (mt * 16 + gq) * 32 + tq * 8;
+            const u8* As = Ab + mt * 512 + (gq * 4 + tq) * 16;   // fragment-ordered M-tile
 #pragma unroll
             for (int i = 0; i < 8; i++) {
-                const uint2 lo = *reinterpret_cast<const uint2*>(As + i * 32 * 32);
-                const uint2 hi = *reinterpret_cast<const uint2*>(As + i * 32 * 32 + 8 * 32);
+                const uint4 a = *reinterpret_cast<const uint4*>(As + i * 32 * 32);
 #pragma unroll
-                for (int j = 0; j < 8; j++) imma(acc[i + j], lo.x, hi.x, lo.y, hi.y, b0[j], b1[j]);
+                for (int j = 0; j < 8; j++) imma(acc[i + j], a.x, a.y, a.z, a.w, b0[j], b1[j]);
             }
         }
         __syncthreads();                                 // stage consumed
@@ -324,18 +323,25 @@ __global__ void __launch_bounds__(512, 1)
         const int o = o0 + mt * 16 + gq + 8 * (e >> 1);
         const int col = nt * 8 + 2 * tq + (e & 1);
         if (o >= m.n_out || col >= ngc) continue;
-        unsigned __int128 lo128 = 0, hi128 = 0;
+        // partials D_s < 2^31: four consecutive ones fit a 64-bit word (< 2^56)
+        auto quad = [&](int s0, int cnt) {
+            u64 v = 0;
 #pragma unroll
-        for (int s = 0; s < 8; s++) lo128 += (unsigned __int128)(u32)acc[s][e] << (8 * s);
-#pragma unroll
-        for (int s = 8; s < 15; s++) hi128 += (unsigned __int128)(u32)acc[s][e] << (8 * (s - 8));
-        u64 l = (u64)hi128;                              // V_hi = 2^64 h + l, h < 2^16
-        const u64 h = (u64)(hi128 >> 64);
-        l = l - umulhi(l, P.pad[2]) * q;                 // l mod q
+            for (int d = 0; d < 4; d++)
+                if (d < cnt) v += (u64)(u32)acc[s0 + d][e] << (8 * d);
+            return v;
+        };
+        const u64 A = quad(0, 4), B = quad(4, 4), C = quad(8, 4), D = quad(12, 3);
+        // V_lo = A + 2^32 B (< 2^89), V_hi = C + 2^32 D (< 2^81)
+        const u64 bl = B << 32, cl = C + (D << 32);
+        const u64 lo = A + bl;
+        u64 hi = (B >> 32) + (lo < A ? 1ull : 0ull);
+        const u64 h = (D >> 32) + (cl < C ? 1ull : 0ull); // V_hi = 2^64 h + cl, h < 2^17
+        u64 l = cl - umulhi(cl, P.pad[2]) * q;           // cl mod q
         l = l >= q ? l - q : l;
         const u64 hr = shoup(h, P.r1, P.r1_shoup, q);    // h 2^64 mod q
-        const u64 xl = (u64)lo128;
-        const u64 xh = (u64)(lo128 >> 64) + l + hr;      // < 2^24 + 2q < 3q
+        const u64 xl = lo;
+        const u64 xh = hi + l + hr;                      // < 2^25 + 2q < 3q
         const u64 mq = xl * P.qinv_neg;
         u64 r = xh + umulhi(mq, q) + (xl != 0ull ? 1ull : 0ull);   // < 4q
         r = csub(r, 2 * q);

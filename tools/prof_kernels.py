@@ -27,6 +27,25 @@ elif what == "ntt14":
         eng.ntt(data, 0)
         eng.ntt(data, 0, inverse=True)
     torch.cuda.synchronize()
+elif what == "convks":
+    # cifar3 conv2 shape: 16 sources x 9 taps = 144 terms, 32 outputs, level 11, G = 32
+    from paper_2402_01296_b200.params import galois_element as ge
+    import ctypes
+    from paper_2402_01296_b200 import _lib
+    hp = make_params(16384, 14, 50, dnum=3)
+    eng = Engine(hp)
+    lvl, G, O = 11, int(os.environ.get("PROF_G", "32")), 32
+    srcs = [eng.sample_uniform(2 * G, lvl + 1, 0, seed=9 + i).view(G, 2, lvl + 1, 16384) for i in range(16)]
+    Us = [eng.modup(x, lvl) for x in srcs]
+    rots = [0, 1, 2, 16, 17, 18, 32, 33, 34]
+    terms = [(srcs[c], Us[c], ge(r, 16384) if r else 1) for c in range(16) for r in rots]
+    nb = ctypes.c_uint64()
+    _lib.call("bcn_planes_ext_bytes", eng._h, O, len(terms), lvl, ctypes.byref(nb))
+    planes = torch.randint(0, 256, (int(nb.value),), dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        eng.conv_ks_mac([t[0] for t in terms], [t[1] if t[2] != 1 else None for t in terms], [t[2] for t in terms],
+                        planes, O, lvl)
+    torch.cuda.synchronize()
 elif what == "rotsum3":
     # pooling / compaction shape of cifar3: 3 rotations of one source at level 7, G = 32
     from paper_2402_01296_b200.params import galois_element as ge
