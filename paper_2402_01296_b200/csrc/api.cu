@@ -920,7 +920,7 @@ int bcn_pack_planes_ext(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, con
 }
 
 static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int G, int level, const LevelTables* T,
-                    u64* Z, cudaStream_t st);
+                    u64* Z, cudaStream_t st, long long c_gstride = 0);
 static u64* key_ptr(bcn_ctx* c, u64 id);
 
 int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* srcs,
@@ -1367,19 +1367,23 @@ int bcn_rotsum_keys(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* cons
 // (B + P C) / (P q_level) for B [G][2][level+1+K][N] (consumed) and the
 // optional addend C [G][2][level+1][N] (component 1 only when add_c1).
 static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int G, int level, const LevelTables* T,
-                    u64* Z, cudaStream_t st) {
+                    u64* Z, cudaStream_t st, long long c_gstride) {
     const long long N = c->N;
     const int nl = level + 1, next = nl + c->K;
+    if (c_gstride <= 0) c_gstride = 2LL * nl * N;       // addend: [G][2][nl][N] unless given
     Limbs sl;
     sl.n = c->K + 1;
     sl.prime[0] = (short)level;
     for (int k = 0; k < c->K; k++) sl.prime[1 + k] = (short)(c->nq + k);
     if (C) {   // Y_top = B_top + P C_top (component 0, and 1 when add_c1)
         const int npoly = add_c1 ? 2 * G : G;
-        const long long ds = add_c1 ? (long long)next * N : 2LL * next * N;
-        const long long ss = add_c1 ? (long long)nl * N : 2LL * nl * N;
-        CUDA_TRY(axpy_limb_op(B + (size_t)level * N, ds, C + (size_t)level * N, ss, npoly, c->pmod_host[2 * level],
-                              c->pmod_host[2 * level + 1], c->primes[level], c->logn, st));
+        // polys of component 0 (and 1): B poly p = 2g + comp, C at g * c_gstride + comp * nl * N
+        for (int comp = 0; comp < (add_c1 ? 2 : 1); comp++)
+            CUDA_TRY(axpy_limb_op(B + (size_t)comp * next * N + (size_t)level * N, 2LL * next * N,
+                                  C + (size_t)comp * nl * N + (size_t)level * N, c_gstride, G,
+                                  c->pmod_host[2 * level], c->pmod_host[2 * level + 1], c->primes[level], c->logn,
+                                  st));
+        (void)npoly;
     }
     Limbs ql = limbs_range(0, level);
     if ((c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_MODDOWN")) {
@@ -1399,7 +1403,7 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
         a.epi_tab = T->pqinv;
         a.epi_tab2 = T->qlinv;
         a.epi_add = C;
-        a.epi_aps = 2LL * nl * N;
+        a.epi_aps = c_gstride;
         a.epi_acs = (long long)nl * N;
         a.epi_add_c1 = add_c1;
         CUDA_TRY(ntt_launch(false, c->logn, a, level, 2 * G, st));
@@ -1409,7 +1413,7 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
     Limbs ext = limbs_ext(c, level);
     CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st));
     CUDA_TRY(ntt_run(c, false, Z, (long long)level * N, ql, 2 * G, st));
-    CUDA_TRY(mdr_combine_op(out, B, (long long)next * N, Z, C, 2LL * nl * N, add_c1, 2 * G, level, c->logn, ql, c->pr,
+    CUDA_TRY(mdr_combine_op(out, B, (long long)next * N, Z, C, c_gstride, add_c1, 2 * G, level, c->logn, ql, c->pr,
                             T->pqinv, T->qlinv, st));
     return BCN_OK;
 }
@@ -1557,6 +1561,15 @@ int bcn_mul_cc(bcn_ctx* c, uint64_t* out, const uint64_t* a, int a_nlimb, const 
                        limbs_range(0, nl), c->pr, st));
     e = modup_impl(c, U, d + 2 * nl * N, 3LL * nl * N, G, level, tmp, st);
     if (e) return e;
+    if (rescale && !getenv_flag_off("BCN_MERGED_RESCALE")) {
+        // relinearise + rescale in one base conversion: (ModDown(A) + (d0, d1)) / q_l
+        const int next = nl + c->K;
+        u64* A = tmp;                                   // [G][2][next][N]
+        u64* Z = A + (size_t)G * 2 * next * N;          // staged path only
+        CUDA_TRY(inner_op(A, U, G, next, T->ndig, c->logn, 1u, key_ptr(c, 2), 2LL * c->nbasis * N,
+                          (long long)c->nbasis * N, limbs_ext(c, level), limbs_ext(c, level), c->pr, st));
+        return mdr_tail(c, (u64*)out, A, d, 1, G, level, T, Z, st, 3LL * nl * N);
+    }
     u64* dst = rescale ? R : (u64*)out;
     e = keyswitch_tail(c, dst, 2LL * nl * N, U, G, level, 1, key_ptr(c, 2), d, 3LL * nl * N, 1, tmp, st);
     if (e) return e;
