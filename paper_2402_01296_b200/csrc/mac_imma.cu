@@ -97,13 +97,13 @@ cudaError_t pack_planes_op(u8* planes, const u64* const* pts_dev, int n_out, int
 // touches HBM.  One CTA = (32 coefficients, limb, term).  Under X -> X^g an
 // aligned 32-block is the image of one aligned 32-block, so the gathers stay
 // inside one 256-byte segment.
+template <int ND>    // digits (1..4); 0: any count, key words re-read from L1
 __global__ void __launch_bounds__(256, 3) slot_major_ks_kernel(u64* __restrict__ S, const KsTerms T, int g0, int gcnt,
                                                             int t0, int nq, int next, int ndig, int logn,
                                                             long long kds, long long kcs, Limbs ext,
                                                             const PrimeInfo* __restrict__ pr,
                                                             const u64* __restrict__ pmod) {
     __shared__ u64 tile[64][33];
-    constexpr int MAXD = 4;                                       // key words kept in registers
     const int N = 1 << logn;
     const int n0 = blockIdx.x * 32, tl = blockIdx.y, k = blockIdx.z;
     const int t = t0 + tl;
@@ -113,42 +113,57 @@ __global__ void __launch_bounds__(256, 3) slot_major_ks_kernel(u64* __restrict__
     const u64 q = P.q;
     const u32 g = T.g[k];
     const long long LNs = (long long)nq * N;                      // source ct: [G][2][nq][N]
-    // lane = coefficient, warp = a strided set of (slot set, component) columns:
-    // the permutation, the key words and the P-multiplier are per lane only
+    // lane = coefficient, warp = a strided set of slot sets (both components:
+    // one set of U loads feeds the two key products); the permutation, the
+    // key words and the P multiplier are per lane only
     const int nn = threadIdx.x & 31, w0 = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int n = n0 + nn;
     const u64* src = T.src[k] + (long long)t * N;
+    const bool qlimb = t < nq;
+    const u64 pw = qlimb ? pmod[2 * t] : 0ull, pwp = qlimb ? pmod[2 * t + 1] : 0ull;
     if (g == 1u) {
-        const u64 pw = t < nq ? pmod[2 * t] : 0ull, pwp = t < nq ? pmod[2 * t + 1] : 0ull;
 #pragma unroll 4
         for (int col = w0; col < ncol; col += nw) {
             const int gs = g0 + (col >> 1), c = col & 1;
-            tile[col][nn] = t < nq ? shoup(__ldg(src + (long long)gs * 2 * LNs + c * LNs + n), pw, pwp, q) : 0ull;
+            tile[col][nn] = qlimb ? shoup(__ldg(src + (long long)gs * 2 * LNs + c * LNs + n), pw, pwp, q) : 0ull;
         }
     } else {
         const int sn = (int)automorph_src((u32)n, g, logn);
-        const int nd = ndig < MAXD ? ndig : MAXD;
-        u64 k0[MAXD], k1[MAXD];
+        constexpr int KD = ND > 0 ? ND : 1;
+        u64 k0[KD], k1[KD];
         const u64* kp = T.key[k] + (long long)kt * N + n;
+        if constexpr (ND > 0) {
 #pragma unroll
-        for (int j = 0; j < MAXD; j++)
-            if (j < nd) { k0[j] = __ldg(kp + j * kds); k1[j] = __ldg(kp + j * kds + kcs); }
-        const u64 pw = t < nq ? pmod[2 * t] : 0ull, pwp = t < nq ? pmod[2 * t + 1] : 0ull;
+            for (int j = 0; j < ND; j++) { k0[j] = __ldg(kp + j * kds); k1[j] = __ldg(kp + j * kds + kcs); }
+        }
+        const int nd = ND > 0 ? ND : ndig;
         const long long dstr = (long long)next * N;
         const u64* Ub = T.U[k] + (long long)t * N + sn;
 #pragma unroll 2
-        for (int col = w0; col < ncol; col += nw) {
-            const int gs = g0 + (col >> 1), c = col & 1;
-            const u64* Up = Ub + (long long)gs * ndig * dstr;
-            Acc4 a;
-            a.zero();
+        for (int gi = w0; gi < gcnt; gi += nw) {
+            const int gs = g0 + gi;
+            const u64* Up = Ub + (long long)gs * nd * dstr;
+            Acc4 a0, a1;
+            a0.zero();
+            a1.zero();
+            if constexpr (ND > 0) {
 #pragma unroll
-            for (int j = 0; j < MAXD; j++)
-                if (j < nd) a.mac(__ldg(Up + j * dstr), c ? k1[j] : k0[j]);
-            for (int j = MAXD; j < ndig; j++) a.mac(__ldg(Up + j * dstr), __ldg(kp + j * kds + c * kcs));
-            u64 v = a.reduce(q, P.qinv_neg, P.pad[2]);
-            if (c == 0 && t < nq) v = add_mod(v, shoup(__ldg(src + (long long)gs * 2 * LNs + sn), pw, pwp, q), q);
-            tile[col][nn] = v;
+                for (int j = 0; j < ND; j++) {
+                    const u64 u = __ldg(Up + j * dstr);
+                    a0.mac(u, k0[j]);
+                    a1.mac(u, k1[j]);
+                }
+            } else {
+                for (int j = 0; j < nd; j++) {
+                    const u64 u = __ldg(Up + j * dstr);
+                    a0.mac(u, __ldg(kp + j * kds));
+                    a1.mac(u, __ldg(kp + j * kds + kcs));
+                }
+            }
+            u64 v0 = a0.reduce(q, P.qinv_neg, P.pad[2]);
+            if (qlimb) v0 = add_mod(v0, shoup(__ldg(src + (long long)gs * 2 * LNs + sn), pw, pwp, q), q);
+            tile[2 * gi][nn] = v0;
+            tile[2 * gi + 1][nn] = a1.reduce(q, P.qinv_neg, P.pad[2]);
         }
     }
     __syncthreads();
@@ -162,7 +177,15 @@ cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0,
                              const u64* pmod, cudaStream_t st) {
     const int N = 1 << logn;
     dim3 grid(N / 32, tcnt, T.n);
-    slot_major_ks_kernel<<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, kds, kcs, ext, pr, pmod);
+    switch (ndig) {
+#define BCN_SMK(D) case D: slot_major_ks_kernel<D><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, \
+                                                   kds, kcs, ext, pr, pmod); break;
+        BCN_SMK(1) BCN_SMK(2) BCN_SMK(3) BCN_SMK(4)
+#undef BCN_SMK
+        default:
+            slot_major_ks_kernel<0><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, kds, kcs, ext, pr,
+                                                          pmod);
+    }
     return launched();
 }
 
