@@ -668,6 +668,88 @@ cudaError_t premul_key_op(u64* out, const u64* key, const u64* pt, int ndig, int
     return launched();
 }
 
+// Direct-gather rotation sum: one thread per output word (slot set, limb,
+// coefficient).  Under X -> X^g an aligned 32-block of the bit-reversed NTT
+// domain is the image of one aligned 32-block (tests/test_oracle.py), so the
+// 32 gathers of a warp hit one 256-byte run -- coalesced without the SMEM
+// staging and the two barriers per term of rotsum_kernel.
+template <int ND>    // digits (1..4); 0: runtime count
+__global__ void __launch_bounds__(256, 4) rotsum2_kernel(
+        u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T, long long c0_gstride, int nq, int next,
+        int ndig, int logn, long long kds, long long kcs, Limbs ext, const PrimeInfo* __restrict__ pr,
+        int acc_flags, long long c0_ostride) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * 256 + threadIdx.x;
+    const int t = blockIdx.y;
+    const long long p = blockIdx.z;
+    const int kt = ext.prime[t];
+    const PrimeInfo& P = pr[kt];
+    const u64 q = P.q, qn = P.qinv_neg, one_m = P.r1, inv1 = P.pad[2];
+    const bool has_c0 = t < nq;
+    const int nd = ND > 0 ? ND : ndig;
+    const long long dstr = (long long)next * N;
+    const long long uoff = (p * nd * next + t) * (long long)N;
+    const long long coff = p * c0_gstride + (long long)t * N;
+    const long long koff = (long long)kt * N + n;
+    const long long poff_b = (p * next + t) * (long long)N + n, poff_1 = (long long)t * N + n;
+    Acc4 b0, b1, cc;
+    b0.zero(); b1.zero(); cc.zero();
+    int np = 0;                                       // products in b0/b1 since the last fold
+    for (int k = 0; k < T.n; k++) {
+        const int sn = (int)automorph_src((u32)n, T.g[k], logn);
+        const u64* Uk = T.U[k] + uoff + sn;
+        const u64* kp = T.key[k] + koff;
+        const u64* pk = T.pt[k];
+        const u64 w = pk ? __ldg(pk + (T.pt_batched[k] ? poff_b : poff_1)) : one_m;
+        if (T.fused[k]) {
+            if (np + nd > 32) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); np = 0; }
+#pragma unroll
+            for (int j = 0; j < (ND > 0 ? ND : 1); j++) {
+                if (ND == 0) break;
+                const u64 u = __ldg(Uk + j * dstr);
+                b0.mac(u, __ldg(kp + j * kds));
+                b1.mac(u, __ldg(kp + j * kds + kcs));
+            }
+            if (ND == 0)
+                for (int j = 0; j < nd; j++) {
+                    const u64 u = __ldg(Uk + j * dstr);
+                    b0.mac(u, __ldg(kp + j * kds));
+                    b1.mac(u, __ldg(kp + j * kds + kcs));
+                }
+            np += nd;
+        } else {
+            Acc4 a0, a1;
+            a0.zero(); a1.zero();
+            for (int j = 0; j < nd; j++) {
+                const u64 u = __ldg(Uk + j * dstr);
+                a0.mac(u, __ldg(kp + j * kds));
+                a1.mac(u, __ldg(kp + j * kds + kcs));
+            }
+            if (np + 1 > 32) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); np = 0; }
+            b0.mac(a0.reduce(q, qn, inv1), w);
+            b1.mac(a1.reduce(q, qn, inv1), w);
+            np += 1;
+        }
+        if (has_c0) {
+            cc.mac(__ldg(T.c0[k] + coff + sn), w);
+            if ((k & 31) == 31) cc.fold_hi(q, inv1);
+        }
+    }
+    const int accumulate = acc_flags & 1, c0_acc = (acc_flags >> 1) & 1;
+    u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
+    u64* o1 = o0 + (long long)next * N;
+    u64 r0 = b0.reduce(q, qn, inv1), r1 = b1.reduce(q, qn, inv1);
+    if (accumulate) { r0 = add_mod(r0, *o0, q); r1 = add_mod(r1, *o1, q); }
+    *o0 = r0;
+    *o1 = r1;
+    if (has_c0) {
+        u64* oc = C0 + p * c0_ostride + (long long)t * N + n;
+        u64 rc = cc.reduce(q, qn, inv1);
+        if (c0_acc) rc = add_mod(rc, *oc, q);
+        *oc = rc;
+    }
+}
+
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
                       int accumulate, cudaStream_t st, long long c0_ostride, int c0_accumulate) {
@@ -676,6 +758,19 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
     if (c0_ostride < 0) c0_ostride = (long long)nq * N;
     if (c0_accumulate < 0) c0_accumulate = accumulate;
     const int flags = (accumulate ? 1 : 0) | (c0_accumulate ? 2 : 0);
+    if (N >= 256 && !getenv("BCN_ROTSUM_STAGED")) {
+        dim3 grid(N / 256, next, G);
+        switch (ndig) {
+#define BCN_RS2(D) case D: rotsum2_kernel<D><<<grid, 256, 0, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, \
+                                                                 kds, kcs, ext, pr, flags, c0_ostride); break;
+            BCN_RS2(1) BCN_RS2(2) BCN_RS2(3) BCN_RS2(4)
+#undef BCN_RS2
+            default:
+                rotsum2_kernel<0><<<grid, 256, 0, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, kds, kcs, ext,
+                                                        pr, flags, c0_ostride);
+        }
+        return launched();
+    }
     if ((long long)G * (ndig + 2) * next * N >= (1LL << 32) || (long long)G * c0_gstride >= (1LL << 32))
         return cudaErrorInvalidValue;                 // kernel offsets are 32-bit
     if (N >= 1024) {

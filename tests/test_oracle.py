@@ -79,7 +79,7 @@ def test_automorphism_maps_aligned_blocks_to_aligned_blocks():
     idx = np.arange(N, dtype=np.uint64)
     for r in (1, 2, 100, 2047):
         perm = from_(idx[None], O.galois_elt(r, N))[0].astype(np.int64)
-        for blk in (256, 1024):
+        for blk in (32, 256, 1024):
             src = perm.reshape(-1, blk) // blk
             assert (src == src[:, :1]).all()
 
