@@ -397,10 +397,12 @@ cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, in
 // the digit's limbs, then U[p][j][t] = REDC(sum_i y_i * hat_m[i][t]) for
 // every extended limb t outside the digit (coefficient domain; NTT'd by the
 // caller), and U[p][j][t] = x_ntt[t] (already NTT domain) inside it.
+template <int A>     // A >= digit size, compile time: y[] stays in registers (0: runtime, local array)
 __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, long long xc_stride,
                              const u64* __restrict__ xn, long long x_stride, int nq, int next, int alpha, int ndig,
                              int logn,
                              Limbs ext, const PrimeInfo* __restrict__ pr, const ConvTable* __restrict__ tab) {
+    constexpr int YA = A > 0 ? A : BCN_MAX_ALPHA;
     const int N = 1 << logn;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
@@ -409,21 +411,27 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, lo
     const ConvTable& T = tab[j];
     const int i0 = j * alpha;
     const int na = T.n_src;
-    u64 y[BCN_MAX_ALPHA];
+    u64 y[YA];
     const u64* xcp = xc + p * xc_stride + n;
     const u64* xnp = xn + p * x_stride + n;
     u64* Up = U + (p * ndig + j) * (long long)next * N + n;
-#pragma unroll 4
-    for (int i = 0; i < na; i++) {
-        const PrimeInfo& P = pr[ext.prime[i0 + i]];
-        y[i] = shoup(__ldg(xcp + (long long)(i0 + i) * N), T.hatinv[i], T.hatinv_p[i], P.q);
-        Up[(long long)(i0 + i) * N] = __ldg(xnp + (long long)(i0 + i) * N);
+#pragma unroll
+    for (int i = 0; i < YA; i++) {
+        if (i < na) {
+            const PrimeInfo& P = pr[ext.prime[i0 + i]];
+            y[i] = shoup(__ldg(xcp + (long long)(i0 + i) * N), T.hatinv[i], T.hatinv_p[i], P.q);
+            Up[(long long)(i0 + i) * N] = __ldg(xnp + (long long)(i0 + i) * N);
+        } else {
+            y[i] = 0ull;
+        }
     }
     for (int t = 0; t < next; t++) {
         if (t >= i0 && t < i0 + na) continue;
         const PrimeInfo& P = pr[ext.prime[t]];
         Acc4 acc; acc.zero();                          // na <= 16 products
-        for (int i = 0; i < na; i++) acc.mac(y[i], T.hat_m[i * BCN_MAX_LIMBS + t]);
+#pragma unroll
+        for (int i = 0; i < YA; i++)
+            if (i < na) acc.mac(y[i], T.hat_m[i * BCN_MAX_LIMBS + t]);
         Up[(long long)t * N] = acc.reduce(P.q, P.qinv_neg, P.pad[2]);
     }
     (void)nq;
@@ -435,7 +443,15 @@ cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, 
     const int N = 1 << logn;
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, npoly, ndig);
-    modup_kernel<<<grid, tpb, 0, st>>>(U, xc, xc_stride, xn, x_stride, nq, next, alpha, ndig, logn, ext, pr, tab);
+    switch (alpha) {
+#define BCN_MU(AA) case AA: modup_kernel<AA><<<grid, tpb, 0, st>>>(U, xc, xc_stride, xn, x_stride, nq, next, alpha, \
+                                                                  ndig, logn, ext, pr, tab); break;
+        BCN_MU(1) BCN_MU(2) BCN_MU(3) BCN_MU(4) BCN_MU(5) BCN_MU(6) BCN_MU(7) BCN_MU(8)
+#undef BCN_MU
+        default:
+            modup_kernel<0><<<grid, tpb, 0, st>>>(U, xc, xc_stride, xn, x_stride, nq, next, alpha, ndig, logn, ext, pr,
+                                                  tab);
+    }
     return launched();
 }
 
