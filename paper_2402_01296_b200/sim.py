@@ -422,6 +422,31 @@ def _batch_of(a: Ciphertext, b: Ciphertext) -> None:
         raise UsageError(f"ciphertext batches differ ({a.batch} vs {b.batch})")
 
 
+def he_add_plain_many(cts: list, vecs, rec: OpRecorder) -> list:
+    """[he_add(ct_c, vecs[c])] (one Add_PC per channel, sim.py:208-218) with all
+    channels' input-dependent plaintexts encoded by ONE batched launch when
+    the ciphertexts share level and scale (vecs: (C, G, S) slots)."""
+    import torch
+    if not cts:
+        return []
+    for c in cts:
+        c.materialize()
+    same = isinstance(vecs, torch.Tensor) and all(c.level == cts[0].level and c.scale == cts[0].scale
+                                                 and c.batch == cts[0].batch for c in cts)
+    if not same or len(cts) == 1:
+        return [he_add(ct, vecs[c], rec) for c, ct in enumerate(cts)]
+    ctx, lvl, G = cts[0].ctx, cts[0].level, cts[0].batch
+    if tuple(vecs.shape[:2]) != (len(cts), G):
+        raise UsageError(f"plain batch {tuple(vecs.shape[:2])} does not match ({len(cts)}, {G})")
+    pts = ctx.engine.encode(vecs.reshape(len(cts) * G, -1), lvl, cts[0].scale)
+    STATS["encode"] += 1
+    out = []
+    for c, ct in enumerate(cts):
+        rec.bump("Add_PC")
+        out.append(Ciphertext(ctx.engine.add_plain(ct._data, pts[c * G:(c + 1) * G], lvl), lvl, ct.scale, ctx))
+    return out
+
+
 def _encode(ctx: HeContext, plain, level: int, scale: float, montgomery: bool, batch: int, ext: bool = False):
     """Encode a plain vector; keyed (weight-derived) vectors are cached in HBM.
     ext=True: Montgomery multiplier over the extended basis (rotsum terms)."""

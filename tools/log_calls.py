@@ -13,7 +13,8 @@ from paper_2402_01296_b200.engine import Engine  # noqa: E402
 
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 log = collections.Counter()
-for name in ("rotsum", "mac_terms", "mac_multi_planes", "modup", "rotate", "rescale", "mul_cc", "mac_terms_acc"):
+for name in ("rotsum", "mac_terms", "mac_multi_planes", "modup", "rotate", "rescale", "mul_cc", "mac_terms_acc",
+             "encode", "encode_ext", "encrypt", "rotsum_rescale", "conv_ks_mac", "add", "add_plain"):
     fn = getattr(Engine, name)
 
     def wrap(self, *a, _fn=fn, _name=name, **k):
@@ -23,6 +24,10 @@ for name in ("rotsum", "mac_terms", "mac_multi_planes", "modup", "rotate", "resc
             key = (len(a[0] if _name == "mac_terms" else a[1]), a[1] if _name == "mac_terms" else a[2])
         elif _name == "mac_multi_planes":
             key = (len(a[0]), a[2], a[3])
+        elif _name in ("encode", "encode_ext", "encrypt"):
+            import traceback
+            st = traceback.extract_stack(limit=6)
+            key = (tuple(getattr(a[0], "shape", ())), "/".join(f"{f.name}" for f in st[-5:-1]))
         else:
             key = tuple(x for x in a[1:3] if isinstance(x, int))
         log[(_name,) + tuple(key)] += 1
