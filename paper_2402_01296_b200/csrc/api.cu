@@ -962,7 +962,8 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
     const long long cw = (long long)G * 2 * next * N;    // one output's extended-basis sum
     const bool fused = (c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_MODDOWN");
     int err = 0;
-    u64* acc = scratch_get(c, (size_t)n_out * cw + (fused ? 0 : (size_t)n_out * G * 2 * level * N), &err);
+    (void)fused;
+    u64* acc = scratch_get(c, (size_t)n_out * cw + (size_t)n_out * G * 2 * level * N, &err);
     if (!acc) return err;
     u64* Z = acc + (size_t)n_out * cw;
     const size_t per_limb = (size_t)N * n_terms * 64 * sizeof(u64);
@@ -1243,15 +1244,27 @@ static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int l
     for (int k = 0; k < c->K; k++) pl.prime[k] = (short)(c->nq + k);
     Limbs ql = limbs_range(0, nl);
     if ((c->logn == 13 || c->logn == 14) && os == 2LL * nl * N && !getenv_flag_off("BCN_FUSED_MODDOWN")) {
+        const bool split = Z && !getenv_flag_off("BCN_SPLIT_CONV");
         NttArgs ia = ntt_args(c, A + (size_t)nl * N, (long long)next * N, pl);
-        ia.inv_scale = c->md_scale;
+        if (!split) ia.inv_scale = c->md_scale;
         CUDA_TRY(ntt_launch(true, c->logn, ia, c->K, 2 * G, st));
         NttArgs a = ntt_args(c, out, (long long)nl * N, ql);
-        a.pro = 2;
-        a.pro_src = A + (size_t)nl * N;
-        a.pro_stride = (long long)next * N;
-        a.pro_conv = T->moddown;
-        a.pro_K = c->K;
+        if (split) {
+            // base conversion once per coefficient (sources read once, in registers), then
+            // a plain-prologue NTT with the fused combine: the prologue form re-reads the
+            // sources for every output limb and stalls on their latency
+            CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown,
+                                     st));
+            a.src = Z;
+            a.src_poly_stride = (long long)nl * N;
+            a.src_limb_stride = N;
+        } else {
+            a.pro = 2;
+            a.pro_src = A + (size_t)nl * N;
+            a.pro_stride = (long long)next * N;
+            a.pro_conv = T->moddown;
+            a.pro_K = c->K;
+        }
         a.epi = 2;
         a.epi_c = A;
         a.epi_cps = (long long)next * N;
@@ -1387,15 +1400,24 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
     }
     Limbs ql = limbs_range(0, level);
     if ((c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_MODDOWN")) {
+        const bool split = Z && !getenv_flag_off("BCN_SPLIT_CONV");
         NttArgs ia = ntt_args(c, B + (size_t)level * N, (long long)next * N, sl);
-        ia.inv_scale = T->mdr_scale;
+        if (!split) ia.inv_scale = T->mdr_scale;
         CUDA_TRY(ntt_launch(true, c->logn, ia, sl.n, 2 * G, st));
         NttArgs a = ntt_args(c, out, (long long)level * N, ql);
-        a.pro = 2;
-        a.pro_src = B + (size_t)level * N;
-        a.pro_stride = (long long)next * N;
-        a.pro_conv = T->mdr;
-        a.pro_K = sl.n;
+        if (split) {   // conversion once per coefficient, then plain-prologue NTT + fused combine
+            Limbs ext = limbs_ext(c, level);
+            CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st));
+            a.src = Z;
+            a.src_poly_stride = (long long)level * N;
+            a.src_limb_stride = N;
+        } else {
+            a.pro = 2;
+            a.pro_src = B + (size_t)level * N;
+            a.pro_stride = (long long)next * N;
+            a.pro_conv = T->mdr;
+            a.pro_K = sl.n;
+        }
         a.epi = 3;
         a.epi_c = B;
         a.epi_cps = (long long)next * N;

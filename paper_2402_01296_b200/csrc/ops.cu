@@ -867,25 +867,33 @@ cudaError_t mdr_combine_op(u64* out, const u64* B, long long bps, const u64* Z, 
 // -------------------------------------------------------- ModDown (K7)
 // Z[p][i] = REDC(sum_k [xP_k * phatinv_k]_{p_k} * phat_m[k][i]) for i <= level
 // (coefficient domain), from the INTT'd special limbs of A.
+template <int KK>    // source count at compile time: y[] in registers (0: runtime count, local array)
 __global__ void moddown_conv_kernel(u64* __restrict__ Z, const u64* __restrict__ A, long long a_stride,
                                     int nq, int K, int logn, Limbs ext, const PrimeInfo* __restrict__ pr,
                                     const ConvTable* __restrict__ tab) {
+    constexpr int YK = KK > 0 ? KK : BCN_MAX_ALPHA;
     const int N = 1 << logn;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     const long long p = blockIdx.y;
     const ConvTable& T = *tab;
-    u64 y[BCN_MAX_ALPHA];
+    const int nk = KK > 0 ? KK : K;
+    u64 y[YK];
     const u64* ap = A + p * a_stride + (long long)nq * N + n;
-    for (int k = 0; k < K; k++) {
-        const PrimeInfo& P = pr[ext.prime[nq + k]];
-        y[k] = shoup(__ldg(ap + (long long)k * N), T.hatinv[k], T.hatinv_p[k], P.q);
+#pragma unroll
+    for (int k = 0; k < YK; k++) {
+        if (k < nk) {
+            const PrimeInfo& P = pr[ext.prime[nq + k]];
+            y[k] = shoup(__ldg(ap + (long long)k * N), T.hatinv[k], T.hatinv_p[k], P.q);
+        }
     }
     u64* zp = Z + p * (long long)nq * N + n;
     for (int i = 0; i < nq; i++) {
         const PrimeInfo& P = pr[ext.prime[i]];
         Acc4 acc; acc.zero();                          // K <= 16 products
-        for (int k = 0; k < K; k++) acc.mac(y[k], T.hat_m[k * BCN_MAX_LIMBS + i]);
+#pragma unroll
+        for (int k = 0; k < YK; k++)
+            if (k < nk) acc.mac(y[k], T.hat_m[k * BCN_MAX_LIMBS + i]);
         zp[(long long)i * N] = acc.reduce(P.q, P.qinv_neg, P.pad[2]);
     }
 }
@@ -895,7 +903,12 @@ cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly,
     const int N = 1 << logn;
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, npoly);
-    moddown_conv_kernel<<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab);
+    switch (K) {
+#define BCN_MC(KV) case KV: moddown_conv_kernel<KV><<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab); break;
+        BCN_MC(1) BCN_MC(2) BCN_MC(3) BCN_MC(4) BCN_MC(5) BCN_MC(6) BCN_MC(7) BCN_MC(8) BCN_MC(9)
+#undef BCN_MC
+        default: moddown_conv_kernel<0><<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab);
+    }
     return launched();
 }
 
