@@ -312,9 +312,44 @@ def oracle_images_per_s(t: dict, counts: dict, work: dict) -> float:
 CIFAR3_COUNTS = {"Add_PC": 98, "Add_CC": 5857, "Mul_PC": 5925, "Mul_CC": 50, "Rot": 6003}
 
 
+_REF = {}
+
+
+def _ref_init():
+    """Per-process oracle context (keys generated once, reused by every step)."""
+    os.environ["OMP_NUM_THREADS"] = "1"        # one core per process: no oversubscription
+    from oracle import ckks as O
+    p = O.make_params(1 << 14, 14, 50, dnum=3, seed=0)
+    orc = O.Oracle(p)
+    orc.galois_key(O.galois_elt(1, p.N))
+    orc.relin_key()
+    _REF["O"], _REF["orc"] = O, orc
+
+
 def _ref_worker(args):
     seed, work = args
-    t = oracle_op_times(seed=seed)
+    O, orc = _REF["O"], _REF["orc"]
+    level = 10
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(8192) * 0.1
+    ct = orc.encrypt(v, 1 + seed, level=level)
+    g = O.galois_elt(1, orc.P.N)
+    t = {}
+    t0 = time.perf_counter()
+    U = orc.modup(ct.c1, level)
+    t["modup"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.keyswitch_from_modup(U, level, orc.galois_key(g), g)
+    t["keyswitch"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.mul_plain(ct, v)
+    t["mul_pc"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.add_cc(ct, ct)
+    t["add"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.mul_cc(ct, ct)
+    t["mul_cc"] = time.perf_counter() - t0
     return oracle_images_per_s(t, CIFAR3_COUNTS, work)
 
 
@@ -328,8 +363,9 @@ def run_reference(args) -> None:
     cores = len(os.sched_getaffinity(0))
     work = {"modup": 1300, "keyswitch": 1016 + 50}
     per_step = []
+    os.environ["OMP_NUM_THREADS"] = "1"        # set before any worker loads the OpenMP oracle library
     ctxm = mp.get_context("fork")
-    with ctxm.Pool(cores) as pool:
+    with ctxm.Pool(cores, initializer=_ref_init) as pool:
         for i in range(args.warmup + args.steps):
             rates = pool.map(_ref_worker, [(i * cores + c, work) for c in range(cores)])
             if i >= args.warmup:
