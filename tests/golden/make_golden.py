@@ -116,7 +116,27 @@ def cifar3_cfg4(n=8):
           meta=json.dumps(meta), **{f"w::{k}": v for k, v in w.items()})
 
 
+def cnn3_backbone():
+    """The single-chain cnn3 run fully encrypted by the reference's
+    forward_backbone (network.py:510-582) on one whole image (the reference's
+    own test recipe, pkg/tests/test_network.py:247-256): counts (1952 HE ops),
+    per-layer table, simulator logits and reference_backbone logits."""
+    bundle = RC.get("cnn3")
+    w = fixture_weights("cnn3", seed=0)
+    imgs, _ = digit_images(8, seed=2)
+    dec = R.decompose_batch(imgs, noise_sigma=0.1, seed=5)
+    img = dec[0].plain_full.copy()
+    r0, c0, hs, ws = dec[0].region
+    img[:, r0:r0 + hs, c0:c0 + ws] = dec[0].sensitive
+    ctx = R.make_context(**RC.default_context_params(bundle))
+    res = R.forward_backbone(bundle.backbone, img[None], w, ctx, strategy="hw")
+    ref = R.reference_backbone(bundle.backbone, img[None], w)
+    meta = {"counts_hw": res.recorder.snapshot(), "layer_table": res.recorder.layer_table()}
+    _pack(os.path.join(HERE, "cnn3_backbone.npz"), image=img, logits_ref=ref, logits_sim=res.decrypt_logits(),
+          meta=json.dumps(meta), **_weights_arrays(w))
+
+
 if __name__ == "__main__":
-    cnn3_fixture()
-    cnn3_cfg1()
-    cifar3_cfg4()
+    which = sys.argv[1:] or ["cnn3_fixture", "cnn3_cfg1", "cifar3_cfg4", "cnn3_backbone"]
+    for name in which:
+        globals()[name]()

@@ -51,6 +51,25 @@ def test_cnn3_fixture_bhw_matches_reference():
     assert B.taint_check(bundle.bi, res.recorder).passed
 
 
+def test_cnn3_backbone_fully_encrypted_matches_reference():
+    """forward_backbone (the fully-encrypted single-chain baseline, SURVEY 8(f)
+    item 3): the reference's counts (1952 HE ops) and per-layer table as
+    integers, logits vs reference_backbone, and taint_check failing on every
+    op-bearing layer as in the reference (pkg/tests/test_network.py:247-256, 325-333)."""
+    d = np.load(os.path.join(GOLD, "cnn3_backbone.npz"))
+    meta = json.loads(str(d["meta"]))
+    w = TensorArchive({k[3:]: d[k] for k in d.files if k.startswith("w::")})
+    bundle = B.get("cnn3")
+    ctx = B.make_context(1 << 14, B.required_levels(bundle) + 1, 2.0 ** 50)
+    res = B.forward_backbone(bundle.backbone, d["image"][None], w, ctx, strategy="hw")
+    c = res.recorder.snapshot()
+    assert c == meta["counts_hw"]
+    assert c["Add_PC"] + c["Add_CC"] + c["Mul_PC"] + c["Mul_CC"] == 1952
+    assert [list(x) for x in res.recorder.layer_table()] == meta["layer_table"]
+    _check(res.decrypt_logits(), d["logits_ref"])
+    assert not B.taint_check(bundle.backbone, res.recorder).passed
+
+
 def test_cnn3_hw_single_image_counts():
     d, w, dec, meta = _load("cnn3_fixture")
     bundle = B.get("cnn3")

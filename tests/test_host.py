@@ -140,6 +140,16 @@ def test_clear_forward_matches_reference_golden():
         assert np.abs(got - d["logits_ref"]).max() <= 1e-12 * max(1.0, np.abs(d["logits_ref"]).max())
 
 
+def test_clear_backbone_matches_reference_golden():
+    """reference_backbone (single-chain clear forward, network.py:585-604) ==
+    the reference's logits on the golden image."""
+    d = np.load(os.path.join(GOLD, "cnn3_backbone.npz"))
+    from paper_2402_01296_b200.archive import TensorArchive
+    w = TensorArchive({k[3:]: d[k] for k in d.files if k.startswith("w::")})
+    got = B.reference_backbone(catalog.get("cnn3").backbone, d["image"][None], w)
+    assert np.abs(got - d["logits_ref"]).max() <= 1e-12 * max(1.0, np.abs(d["logits_ref"]).max())
+
+
 def test_decompose_and_crop_semantics():
     img = np.arange(16.0).reshape(1, 4, 4)
     d = B.decompose_input(img, noise_sigma=0.0, seed=0)

@@ -35,15 +35,16 @@ int main() {
     const int iters = 256;
     cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
     cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
-    for (int mode = 0; mode < 2; mode++) for (int wpb : {8, 16}) {
-        const int blocks = 148 * 4, tpb = 32 * wpb;
+    for (int mode = 0; mode < 2; mode++) for (int cfg = 0; cfg < 4; cfg++) {
+        const int wpb = cfg < 2 ? 8 : 16;
+        const int blocks = 148 * (cfg == 0 ? 2 : cfg == 1 ? 4 : cfg == 2 ? 1 : 2), tpb = 32 * wpb;
         for (int rep = 0; rep < 3; rep++) {
             cudaEventRecord(e0);
             if (mode) k<1><<<blocks, tpb, 16384>>>(out, iters, 77u); else k<0><<<blocks, tpb, 16384>>>(out, iters, 77u);
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);
             double ops = 2.0 * blocks * wpb * (double)iters * 64 * 16 * 8 * 32;
-            if (rep == 2) printf("mode %d (A %s) warps/block %d: %.1f TOPS\n", mode, mode ? "LDS.128" : "const", wpb, ops / ms / 1e9);
+            if (rep == 2) printf("mode %d (A %s) warps/block %d blocks/SM %d: %.1f TOPS\n", mode, mode ? "LDS.128" : "const", wpb, blocks / 148, ops / ms / 1e9);
         }
     }
     return 0;
