@@ -237,3 +237,15 @@ def test_sharded_gather_world2_gloo(n_items):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert np.array_equal(got[:, 0, 0], np.arange(n_items, dtype=float))
+
+
+def test_latency_table_has_the_reference_cost_model_format():
+    """profiles/latency_table_b200.json (tools/latency_table.py) follows the
+    BIBRANCH_LATENCY_TABLE override format of the reference's cost model
+    (costs.py:22-47): {scheme: {op: ms}} with every HE op positive."""
+    path = os.path.join(ROOT, "profiles", "latency_table_b200.json")
+    tab = json.load(open(path))
+    for scheme in ("CKKS_B200", "CKKS_B200_G128"):
+        ops = tab[scheme]
+        for k in ("Add_PC", "Add_CC", "Mul_PC", "Mul_CC", "Rot"):
+            assert ops[k] > 0
