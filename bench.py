@@ -192,6 +192,17 @@ def run_ours(args, rank: int, world: int, dist_on: bool):
                                             for s, f in zip(sens_np[:8], full_np[:8])], w)
     max_err = float(np.abs(rec_res.decrypt_logits()[:8] - ref).max())
 
+    keys_agree = None
+    if dist_on:
+        # keys are regenerated on every rank from the shared seed (no broadcast);
+        # check it once with a key-checksum all-gather
+        k = ctx.engine.export_key(2)
+        h = torch.stack([k.sum(), (k * torch.arange(1, k.shape[-1] + 1, device=k.device)).sum()])
+        hs = [torch.empty_like(h) for _ in range(world)]
+        torch.distributed.all_gather(hs, h)
+        keys_agree = all(bool((x == hs[0]).all()) for x in hs)
+        if not keys_agree:
+            raise RuntimeError("switching keys differ across ranks")
     ms, launches, clocks, _ = timed(True, False, args.steps, args.warmup, True)
     total_images = args.images * world
     value = total_images / (ms / 1e3)
@@ -202,7 +213,7 @@ def run_ours(args, rank: int, world: int, dist_on: bool):
     return {
         "value": value, "ms_per_step": ms, "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": h2d,
                                                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "gpu_launches": launches, "clocks": clocks, "counts_per_forward": counts,
+        "gpu_launches": launches, "clocks": clocks, "counts_per_forward": counts, "keys_agree_across_ranks": keys_agree,
         "device_work_per_forward": dev_work, "max_abs_logit_err_vs_reference": max_err, "ctx": ctx,
         "logits_shape": list(logits.shape) if logits is not None else None,
     }
@@ -444,7 +455,8 @@ def main():
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
             "parity": {"max_abs_logit_err_vs_reference_forward": res["max_abs_logit_err_vs_reference"],
-                       "counts_per_forward": res["counts_per_forward"]},
+                       "counts_per_forward": res["counts_per_forward"],
+                       "keys_agree_across_ranks": res["keys_agree_across_ranks"]},
             "device_work_per_forward": res["device_work_per_forward"],
         }
         line.update(extras)
