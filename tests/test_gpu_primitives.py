@@ -346,3 +346,35 @@ def test_conv_ks_mac_matches_oracle(N, L):
     x = [v, v, w, w, v]
     exp = sum(np.roll(x[k], -r, axis=1) * vals[1, k] for k, (_, _, r, _) in enumerate(taps))
     assert np.abs(dec - exp).max() < 1e-4
+
+
+def test_conv_ks_mac_blocks_bitexact_vs_eager_path():
+    """Lazy-ModDown conv over several output blocks (40 outputs: 32 + 8) and
+    slot-set blocks (G = 20: 16 + 4), 60-bit primes with every byte live: the
+    result equals the eager path (rotate with ModDown, then MAC, then rescale)
+    to CKKS noise, and a rerun is bit-identical (deterministic)."""
+    N, L = 2048, 3
+    hp = make_params(N, L, 40, dnum=2)
+    eng = Engine(hp)
+    rng = np.random.default_rng(41)
+    G, n_src, n_out = 20, 3, 40
+    from paper_2402_01296_b200.params import galois_element as ge
+    xs = [eng.encrypt(rng.standard_normal((G, N // 2)) * 0.5, counter=200 + 30 * i) for i in range(n_src)]
+    Us = [eng.modup(x, L) for x in xs]
+    rots = [0, 1, 5, 31]
+    taps = [(i, r) for i in range(n_src) for r in rots]
+    ql = float(hp.q[L])
+    vals = rng.standard_normal((n_out, len(taps), N // 2)) * 0.3
+    pts = [[eng.encode_ext(vals[o, k], L, ql) if r else eng.encode(vals[o, k], L, ql, montgomery=True)
+            for k, (_, r) in enumerate(taps)] for o in range(n_out)]
+    planes = eng.pack_planes_ext(pts, L)
+    args = ([xs[i] for i, _ in taps], [Us[i] if r else None for i, r in taps], [ge(r, N) if r else 1 for _, r in taps],
+            planes, n_out, L)
+    got = eng.conv_ks_mac(*args)
+    again = eng.conv_ks_mac(*args)
+    assert torch.equal(got, again)
+    dec = eng.decrypt(got.reshape(n_out * G, 2, L, N), L - 1, hp.scale).cpu().numpy().reshape(n_out, G, -1)
+    xv = [eng.decrypt(x, L, hp.scale).cpu().numpy() for x in xs]
+    for o in (0, 17, 39):
+        want = sum(np.roll(xv[i], -r, axis=1) * vals[o, k] for k, (i, r) in enumerate(taps))
+        assert np.abs(dec[o] - want).max() < 1e-3
