@@ -703,17 +703,19 @@ __global__ void __launch_bounds__(256, 4) rotsum2_kernel(
     const u64 q = P.q, qn = P.qinv_neg, one_m = P.r1, inv1 = P.pad[2];
     const bool has_c0 = t < nq;
     const int nd = ND > 0 ? ND : ndig;
-    const long long dstr = (long long)next * N;
-    const long long uoff = (p * nd * next + t) * (long long)N;
-    const long long coff = p * c0_gstride + (long long)t * N;
-    const long long koff = (long long)kt * N + n;
-    const long long poff_b = (p * next + t) * (long long)N + n, poff_1 = (long long)t * N + n;
+    // 32-bit word offsets (the launcher checks every operand stays below 2^32 words)
+    const u32 dstr = (u32)next * (u32)N;
+    const u32 uoff = ((u32)p * nd * next + t) * (u32)N;
+    const u32 coff = (u32)(p * c0_gstride) + (u32)t * N;
+    const u32 koff = (u32)kt * N + n;
+    const u32 poff_b = ((u32)p * next + t) * (u32)N + n, poff_1 = (u32)t * N + n;
+    const u32 kds32 = (u32)kds, kcs32 = (u32)kcs;
     Acc4 b0, b1, cc;
     b0.zero(); b1.zero(); cc.zero();
     int np = 0;                                       // products in b0/b1 since the last fold
     for (int k = 0; k < T.n; k++) {
-        const int sn = (int)automorph_src((u32)n, T.g[k], logn);
-        const u64* Uk = T.U[k] + uoff + sn;
+        const u32 sn = automorph_src((u32)n, T.g[k], logn);
+        const u64* Uk = T.U[k] + (uoff + sn);
         const u64* kp = T.key[k] + koff;
         const u64* pk = T.pt[k];
         const u64 w = pk ? __ldg(pk + (T.pt_batched[k] ? poff_b : poff_1)) : one_m;
@@ -723,23 +725,23 @@ __global__ void __launch_bounds__(256, 4) rotsum2_kernel(
             for (int j = 0; j < (ND > 0 ? ND : 1); j++) {
                 if (ND == 0) break;
                 const u64 u = __ldg(Uk + j * dstr);
-                b0.mac(u, __ldg(kp + j * kds));
-                b1.mac(u, __ldg(kp + j * kds + kcs));
+                b0.mac(u, __ldg(kp + j * kds32));
+                b1.mac(u, __ldg(kp + j * kds32 + kcs32));
             }
             if (ND == 0)
                 for (int j = 0; j < nd; j++) {
-                    const u64 u = __ldg(Uk + j * dstr);
-                    b0.mac(u, __ldg(kp + j * kds));
-                    b1.mac(u, __ldg(kp + j * kds + kcs));
+                    const u64 u = __ldg(Uk + (u32)j * dstr);
+                    b0.mac(u, __ldg(kp + (u32)j * kds32));
+                    b1.mac(u, __ldg(kp + (u32)j * kds32 + kcs32));
                 }
             np += nd;
         } else {
             Acc4 a0, a1;
             a0.zero(); a1.zero();
             for (int j = 0; j < nd; j++) {
-                const u64 u = __ldg(Uk + j * dstr);
-                a0.mac(u, __ldg(kp + j * kds));
-                a1.mac(u, __ldg(kp + j * kds + kcs));
+                const u64 u = __ldg(Uk + (u32)j * dstr);
+                a0.mac(u, __ldg(kp + (u32)j * kds32));
+                a1.mac(u, __ldg(kp + (u32)j * kds32 + kcs32));
             }
             if (np + 1 > 32) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); np = 0; }
             b0.mac(a0.reduce(q, qn, inv1), w);
@@ -747,7 +749,7 @@ __global__ void __launch_bounds__(256, 4) rotsum2_kernel(
             np += 1;
         }
         if (has_c0) {
-            cc.mac(__ldg(T.c0[k] + coff + sn), w);
+            cc.mac(__ldg(T.c0[k] + (coff + sn)), w);
             if ((k & 31) == 31) cc.fold_hi(q, inv1);
         }
     }
@@ -774,6 +776,9 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
     if (c0_ostride < 0) c0_ostride = (long long)nq * N;
     if (c0_accumulate < 0) c0_accumulate = accumulate;
     const int flags = (accumulate ? 1 : 0) | (c0_accumulate ? 2 : 0);
+    if ((long long)G * (ndig + 2) * next * N >= (1LL << 32) || (long long)G * c0_gstride >= (1LL << 32) ||
+        2LL * kds >= (1LL << 32))
+        return cudaErrorInvalidValue;                 // kernel offsets are 32-bit
     if (N >= 256 && !getenv("BCN_ROTSUM_STAGED")) {
         dim3 grid(N / 256, next, G);
         switch (ndig) {
