@@ -689,8 +689,11 @@ cudaError_t premul_key_op(u64* out, const u64* key, const u64* pt, int ndig, int
 // domain is the image of one aligned 32-block (tests/test_oracle.py), so the
 // 32 gathers of a warp hit one 256-byte run -- coalesced without the SMEM
 // staging and the two barriers per term of rotsum_kernel.
+#ifndef BCN_RS2_MINB
+#define BCN_RS2_MINB 6
+#endif
 template <int ND>    // digits (1..4); 0: runtime count
-__global__ void __launch_bounds__(256, 4) rotsum2_kernel(
+__global__ void __launch_bounds__(256, BCN_RS2_MINB) rotsum2_kernel(
         u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T, long long c0_gstride, int nq, int next,
         int ndig, int logn, long long kds, long long kcs, Limbs ext, const PrimeInfo* __restrict__ pr,
         int acc_flags, long long c0_ostride) {
