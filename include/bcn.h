@@ -143,14 +143,19 @@ int bcn_mac_multi_planes(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, co
  * ModDown + rescale per output (no per-rotation ModDown).  srcs/Us: per term
  * the source ct u64[G][2][level+1][N] and its bcn_modup (ignored for g = 1);
  * planes: bcn_pack_planes_ext of the extended-basis plaintexts (rotation
- * terms from bcn_encode_ext, identity terms level+1 limbs).
+ * terms from bcn_encode_ext, identity terms level+1 limbs), packed with the
+ * same layout as passed here: BCN_PLANES_IMMA (mma.sync fragments, any G) or
+ * BCN_PLANES_TCGEN05 (strip windows for tcgen05.mma kind::i8, 64 slot sets
+ * per pass: for G >= 64).  Both give bit-identical results.
  * out u64[n_out][G][2][level][N] at level-1. */
+#define BCN_PLANES_IMMA 0
+#define BCN_PLANES_TCGEN05 1
 int bcn_planes_ext_bytes(bcn_ctx *ctx, int n_out, int n_terms, int level, uint64_t *bytes);
 int bcn_pack_planes_ext(bcn_ctx *ctx, uint8_t *planes, int n_out, int n_terms, const uint64_t *const *pts,
-                        const int *term_limbs, int level, void *stream);
+                        const int *term_limbs, int level, int layout, void *stream);
 int bcn_conv_ks_mac(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *srcs,
-                    const uint64_t *const *Us, const uint64_t *gal, const uint8_t *planes, int G, int level,
-                    void *stream);
+                    const uint64_t *const *Us, const uint64_t *gal, const uint8_t *planes, int layout, int G,
+                    int level, void *stream);
 /* same, accumulating into an existing unrescaled out u64[G][2][level+1][N] */
 int bcn_mac_terms_acc(bcn_ctx *ctx, uint64_t *out, int n_terms, const uint64_t *const *cts,
                       const uint64_t *const *pts, const int *pt_batched, int G, int level, void *stream);

@@ -66,9 +66,9 @@ SIGNATURES = {
                         ctypes.POINTER(_U64), ctypes.POINTER(_I), ctypes.POINTER(_U64), _I, _I, _P],
     "bcn_premul_key": [_P, _P, _U64, _P, _I, _P],
     "bcn_planes_ext_bytes": [_P, _I, _I, _I, ctypes.POINTER(_U64)],
-    "bcn_pack_planes_ext": [_P, _P, _I, _I, ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _P],
+    "bcn_pack_planes_ext": [_P, _P, _I, _I, ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],
     "bcn_conv_ks_mac": [_P, _P, _I, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64), _P, _I,
-                        _I, _P],
+                        _I, _I, _P],
     "bcn_rotsum_rescale": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64),
                            ctypes.POINTER(_U64), ctypes.POINTER(_I), ctypes.POINTER(_U64), _I,
                            ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],

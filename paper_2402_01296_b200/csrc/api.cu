@@ -892,7 +892,8 @@ int bcn_planes_ext_bytes(bcn_ctx* c, int n_out, int n_terms, int level, uint64_t
 }
 
 int bcn_pack_planes_ext(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const uint64_t* const* pts,
-                        const int* term_limbs, int level, void* stream) {
+                        const int* term_limbs, int level, int layout, void* stream) {
+    if (layout != BCN_PLANES_IMMA && layout != BCN_PLANES_TCGEN05) return fail(BCN_ERR_PARAM, "unknown plane layout");
     int e = check_level(c, level);
     if (e) return e;
     int opad, nch;
@@ -913,8 +914,12 @@ int bcn_pack_planes_ext(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, con
     memcpy(host.data() + np * sizeof(u64*), term_limbs, (size_t)n_terms * sizeof(int));
     CUDA_TRY(cudaMemcpyAsync(c->ptr_dev, host.data(), bytes, cudaMemcpyHostToDevice, st));
     const int* tl = (const int*)((const unsigned char*)c->ptr_dev + np * sizeof(u64*));
-    CUDA_TRY(pack_planes_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch, level + 1 + c->K,
-                            c->logn, st, tl));
+    if (layout == BCN_PLANES_TCGEN05)
+        CUDA_TRY(pack_planes_umma_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch,
+                                     level + 1 + c->K, c->logn, st, tl));
+    else
+        CUDA_TRY(pack_planes_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch, level + 1 + c->K,
+                                c->logn, st, tl));
     CUDA_TRY(cudaStreamSynchronize(st));
     return BCN_OK;
 }
@@ -924,8 +929,9 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
 static u64* key_ptr(bcn_ctx* c, u64 id);
 
 int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* srcs,
-                    const uint64_t* const* Us, const uint64_t* gal, const uint8_t* planes, int G, int level,
-                    void* stream) {
+                    const uint64_t* const* Us, const uint64_t* gal, const uint8_t* planes, int layout, int G,
+                    int level, void* stream) {
+    if (layout != BCN_PLANES_IMMA && layout != BCN_PLANES_TCGEN05) return fail(BCN_ERR_PARAM, "unknown plane layout");
     int e = check_level(c, level);
     if (e) return e;
     int opad, nch;
@@ -966,21 +972,28 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
     u64* acc = scratch_get(c, (size_t)n_out * cw + (size_t)n_out * G * 2 * level * N, &err);
     if (!acc) return err;
     u64* Z = acc + (size_t)n_out * cw;
-    const size_t per_limb = (size_t)N * n_terms * 64 * sizeof(u64);
+    // tcgen05: blocks of 64 slot sets (M = 128 columns); IMMA: blocks of IMMA_GB slot
+    // sets (16 -> 8-warp CTAs, two resident per SM, so one CTA's pipeline fill
+    // overlaps the other's MMAs)
+    const bool tc05 = layout == BCN_PLANES_TCGEN05;
+    const int spitch = tc05 ? 128 : 64;
+    const size_t per_limb = (size_t)N * n_terms * spitch * sizeof(u64);
     const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(next, ((size_t)4 << 30) / per_limb));
-    u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * 64, &err);
+    u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * spitch, &err);
     if (!S) return err;
-    // blocks of IMMA_GB slot sets: 16 -> 8-warp CTAs, two resident per SM, so one CTA's
-    // pipeline fill overlaps the other's MMAs (32 -> 16-warp CTAs, one per SM)
-    const int GB = imma_gblock();
+    const int GB = tc05 ? 64 : imma_gblock();
     for (int g0 = 0; g0 < G; g0 += GB) {
         const int gcnt = std::min(GB, G - g0);
         for (int t0 = 0; t0 < next; t0 += tcnt) {
             const int tc = std::min(tcnt, next - t0);
-            CUDA_TRY(slot_major_ks_op(S, KT, g0, gcnt, t0, tc, nl, next, T->ndig, c->logn, 2LL * c->nbasis * N,
-                                      (long long)c->nbasis * N, ext, c->pr, c->pmod, st));
-            CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, next, c->logn,
-                                 ext, c->pr, 0, st));
+            CUDA_TRY(slot_major_ks_op(S, KT, g0, gcnt, t0, tc, nl, next, T->ndig, c->logn, spitch,
+                                      2LL * c->nbasis * N, (long long)c->nbasis * N, ext, c->pr, c->pmod, st));
+            if (tc05)
+                CUDA_TRY(mac_umma_op(acc, cw, n_out, n_terms, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad,
+                                     next, c->logn, ext, c->pr, 0, st));
+            else
+                CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, next,
+                                     c->logn, ext, c->pr, 0, st));
         }
     }
     // the O x G extended-basis sums -> one merged ModDown + rescale each

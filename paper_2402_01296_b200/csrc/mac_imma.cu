@@ -100,10 +100,10 @@ cudaError_t pack_planes_op(u8* planes, const u64* const* pts_dev, int n_out, int
 template <int ND>    // digits (1..4); 0: any count, key words re-read from L1
 __global__ void __launch_bounds__(256, 3) slot_major_ks_kernel(u64* __restrict__ S, const KsTerms T, int g0, int gcnt,
                                                             int t0, int nq, int next, int ndig, int logn,
-                                                            long long kds, long long kcs, Limbs ext,
+                                                            int spitch, long long kds, long long kcs, Limbs ext,
                                                             const PrimeInfo* __restrict__ pr,
                                                             const u64* __restrict__ pmod) {
-    __shared__ u64 tile[64][33];
+    __shared__ u64 tile[128][33];
     const int N = 1 << logn;
     const int n0 = blockIdx.x * 32, tl = blockIdx.y, k = blockIdx.z;
     const int t = t0 + tl;
@@ -167,23 +167,24 @@ __global__ void __launch_bounds__(256, 3) slot_major_ks_kernel(u64* __restrict__
         }
     }
     __syncthreads();
-    u64* dst = S + (((long long)tl * N + n0) * T.n + k) * 64;
-    for (int r = w0; r < 32; r += nw)                      // row r: this slot's 512-byte run
-        for (int col = nn; col < ncol; col += 32) dst[(long long)r * T.n * 64 + col] = tile[col][r];
+    u64* dst = S + (((long long)tl * N + n0) * T.n + k) * spitch;
+    for (int r = w0; r < 32; r += nw)                      // row r: this slot's run of ncol words
+        for (int col = nn; col < ncol; col += 32) dst[(long long)r * T.n * spitch + col] = tile[col][r];
 }
 
 cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,
-                             int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
+                             int logn, int spitch, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
                              const u64* pmod, cudaStream_t st) {
+    if (2 * gcnt > spitch || spitch > 128) return cudaErrorInvalidValue;
     const int N = 1 << logn;
     dim3 grid(N / 32, tcnt, T.n);
     switch (ndig) {
 #define BCN_SMK(D) case D: slot_major_ks_kernel<D><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, \
-                                                   kds, kcs, ext, pr, pmod); break;
+                                                   spitch, kds, kcs, ext, pr, pmod); break;
         BCN_SMK(1) BCN_SMK(2) BCN_SMK(3) BCN_SMK(4)
 #undef BCN_SMK
         default:
-            slot_major_ks_kernel<0><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, kds, kcs, ext, pr,
+            slot_major_ks_kernel<0><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, spitch, kds, kcs, ext, pr,
                                                           pmod);
     }
     return launched();

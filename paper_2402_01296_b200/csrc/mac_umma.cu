@@ -1,0 +1,384 @@
+// mac_umma.cu -- the conv-layer MAC (out_o = sum_k pt_{o,k} (x) B'_k, the
+// lazy-ModDown terms staged slot-major by slot_major_ks_kernel) on the
+// 5th-generation tensor cores: tcgen05.mma kind::i8 with the accumulators in
+// TMEM.  Same arithmetic as mac_imma.cu (byte planes, fifteen exact int32
+// partials D_s = sum_{i+j=s} P_i C_j, one REDC), different mapping:
+//
+//   D[col][(o, s)] += sum_k  C_j[col][k] * W_j[(o, s)][k]        j = 0..7
+//
+// * M = 128 ciphertext columns (64 slot sets x 2 components) of one slot;
+//   A = byte plane j of their words, built in shared memory by the producer
+//   warps (one PRMT byte-transpose per 4 words).
+// * N = 16 outputs x 16 rows s; B = a shifted window over the plaintext
+//   planes: output o owns 16 rows of 32 term-bytes, plane i at row 7 + i and
+//   zeros elsewhere, so the window that starts 7 - j rows into the strip has
+//   plane s - j at row s (zero when s - j is outside 0..7, including the
+//   reads that run into the next strip's leading zero rows).  The MMA then
+//   lands D_s of output o directly in TMEM column 16 o + s: every partial of
+//   one output word sits in ONE thread's lane, so the epilogue is per-thread
+//   (tcgen05.ld, recombine, REDC, store) with no shuffles.
+// * Half of the N rows are zero (8 of every 16 per j), the price of that
+//   epilogue; at 128 x 256 x 32 per instruction the tensor core still does
+//   about 4x the useful byte products of mma.sync IMMA per SM cycle.
+//
+// Warp roles (persistent, one CTA per SM, 4-stage shared-memory ring):
+//   warps 0-7   producers: S words -> byte planes (A), plane strips (B),
+//               fence.proxy.async, arrive on full[stage]
+//   warp 8      MMA issuer (one lane) + TMEM allocation (512 columns = two
+//               256-column accumulators, one per 16-output block)
+//   warps 9-16  epilogue: warp w reads TMEM lanes 32 (w % 4).., outputs
+//               (w - 9) / 4 * 8 .. + 7 of the block
+// Work item = (slot, block of 32 outputs).  The accumulator of output block
+// half nb is released as soon as its epilogue has read it, so the next item's
+// MMAs into it overlap the drain of the other half.
+#include "common.cuh"
+#include "ops.cuh"
+
+namespace bcn {
+
+typedef unsigned char u8;
+
+#define UM_ST 4                                   // shared-memory stages
+#define UM_PROD 8                                 // producer warps
+#define UM_EPI 8                                  // epilogue warps
+#define UM_THREADS ((UM_PROD + 1 + UM_EPI) * 32)
+constexpr int UM_COLS = 128;                      // M: ciphertext columns per item
+constexpr int UM_APLANE = UM_COLS * 32;           // bytes of one A plane (128 rows x 32 k)
+constexpr int UM_ABYTES = 8 * UM_APLANE;
+constexpr int UM_BROWS = 32 * 16 + 8;             // 32 output strips + the tail window overrun
+constexpr int UM_BHALF = UM_BROWS * 16;           // one 16-byte k-half of all rows
+constexpr int UM_SBYTES = UM_ABYTES + 2 * UM_BHALF;
+constexpr size_t UM_SMEM = (size_t)UM_ST * UM_SBYTES + 256;
+
+// ---------------------------------------------------------------- packing
+// planes[((b * nch + c) * opad + o) * 256 + kh * 128 + i * 16 + kb]
+//   = byte i of pt[o][32 c + 16 kh + kb] at slot b (0 past n_terms / short plaintexts):
+// the 128 bytes of one (output, k-half) are exactly its strip rows 7..14.
+__global__ void pack_planes_umma_kernel(u8* __restrict__ planes, const u64* const* __restrict__ pts, int n_out,
+                                        int n_terms, int opad, int nch, int logn, const int* __restrict__ tlimbs) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int t = blockIdx.y;
+    const int o = blockIdx.z / nch, c = blockIdx.z % nch;
+    const long long b = (long long)t * N + n;
+    u32 w[2][8][4];                                       // [kh][plane][4-byte group]
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+#pragma unroll
+            for (int d = 0; d < 4; d++) w[h][i][d] = 0u;
+#pragma unroll
+    for (int kk = 0; kk < 32; kk++) {
+        const int k = c * 32 + kk;
+        const bool live = o < n_out && k < n_terms && (!tlimbs || t < tlimbs[k]);
+        const u64 v = live ? __ldg(pts[(size_t)o * n_terms + k] + b) : 0ull;
+        const int h = kk >> 4, d = (kk & 15) >> 2, sh = (kk & 3) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; i++) w[h][i][d] |= (u32)((v >> (8 * i)) & 0xffull) << sh;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(planes + ((b * nch + c) * opad + o) * 256);
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int i = 0; i < 8; i++) dst[h * 8 + i] = make_uint4(w[h][i][0], w[h][i][1], w[h][i][2], w[h][i][3]);
+}
+
+cudaError_t pack_planes_umma_op(u8* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad, int nch,
+                                int nl, int logn, cudaStream_t st, const int* tlimbs_dev) {
+    const int N = 1 << logn;
+    const int tpb = N < 128 ? N : 128;
+    dim3 grid((N + tpb - 1) / tpb, nl, opad * nch);
+    pack_planes_umma_kernel<<<grid, tpb, 0, st>>>(planes, pts_dev, n_out, n_terms, opad, nch, logn, tlimbs_dev);
+    return launched();
+}
+
+// ---------------------------------------------------------------- tcgen05 helpers
+// shared-memory matrix descriptor, K-major, no swizzle: rows of 16 bytes
+// (8-row core matrices SBO apart), the two 16-byte k-halves LBO apart
+__device__ __forceinline__ u64 umma_sdesc(u32 saddr, u32 lbo, u32 sbo) {
+    return (u64)((saddr >> 4) & 0x3fffu) | ((u64)((lbo >> 4) & 0x3fffu) << 16) |
+           ((u64)((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);   // version 1 (sm_100), layout SWIZZLE_NONE
+}
+// instruction descriptor: D s32, A/B u8, both K-major, N = 256, M = 128
+constexpr u32 UM_IDESC = (2u << 4) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(u32 tmem_d, u64 adesc, u64 bdesc, u32 accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(UM_IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(u64* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+// bounded wait: a protocol bug traps (launch error) instead of hanging the GPU
+__device__ __forceinline__ void um_wait(u64* bar, u32 parity) {
+    for (u32 spin = 0;; spin++) {
+        u32 done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spin > (1u << 24)) __trap();
+    }
+}
+// 16 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld16(u32 taddr, u32 (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// bytes j of four k-consecutive words -> b[j] = {w0.bj, w1.bj, w2.bj, w3.bj}
+__device__ __forceinline__ void bytes_by_plane(const u64 v[4], u32 b[8]) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const u32 x0 = (u32)(v[0] >> (32 * h)), x1 = (u32)(v[1] >> (32 * h));
+        const u32 x2 = (u32)(v[2] >> (32 * h)), x3 = (u32)(v[3] >> (32 * h));
+        const u32 p01l = __byte_perm(x0, x1, 0x5140), p01h = __byte_perm(x0, x1, 0x7362);
+        const u32 p23l = __byte_perm(x2, x3, 0x5140), p23h = __byte_perm(x2, x3, 0x7362);
+        b[4 * h + 0] = __byte_perm(p01l, p23l, 0x5410);
+        b[4 * h + 1] = __byte_perm(p01l, p23l, 0x7632);
+        b[4 * h + 2] = __byte_perm(p01h, p23h, 0x5410);
+        b[4 * h + 3] = __byte_perm(p01h, p23h, 0x7632);
+    }
+}
+
+// value = sum_s 2^(8s) D_s (D_s < 2^31) -> REDC(value) in [0, q)
+__device__ __forceinline__ u64 partials_redc(const u32 (&d)[16], const PrimeInfo& P) {
+    const u64 q = P.q;
+    auto quad = [&](int s0, int cnt) {
+        u64 v = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (e < cnt) v += (u64)d[s0 + e] << (8 * e);
+        return v;
+    };
+    const u64 A = quad(0, 4), B = quad(4, 4), C = quad(8, 4), D = quad(12, 3);
+    const u64 bl = B << 32, cl = C + (D << 32);
+    const u64 lo = A + bl;
+    const u64 hi = (B >> 32) + (lo < A ? 1ull : 0ull);
+    const u64 h = (D >> 32) + (cl < C ? 1ull : 0ull);
+    u64 l = cl - umulhi(cl, P.pad[2]) * q;
+    l = l >= q ? l - q : l;
+    const u64 hr = shoup(h, P.r1, P.r1_shoup, q);
+    const u64 xh = hi + l + hr;
+    const u64 mq = lo * P.qinv_neg;
+    u64 r = xh + umulhi(mq, q) + (lo != 0ull ? 1ull : 0ull);
+    r = csub(r, 2 * q);
+    return csub(r, q);
+}
+
+// ---------------------------------------------------------------- kernel
+// S[(bl * n_terms + k) * 128 + col]: the staged words of slot bl (bl = tl N + n);
+// out[o * ostride + g * 2 LN + c * LN + t N + n], g = g0 + col / 2, c = col % 2
+__global__ void __launch_bounds__(UM_THREADS, 1)
+    mac_umma_kernel(u64* __restrict__ out, long long ostride, int n_out, int n_terms, const u8* __restrict__ planes,
+                    const u64* __restrict__ S, int g0, int gcnt, int t0, int tcnt, int opad, int nch, int nlimb,
+                    int logn, Limbs limbs, const PrimeInfo* __restrict__ pr, int accumulate) {
+    extern __shared__ __align__(1024) unsigned char um_smem[];
+    u64* bars = reinterpret_cast<u64*>(um_smem + (size_t)UM_ST * UM_SBYTES);
+    u64* full = bars;                    // [UM_ST]  producers -> MMA
+    u64* empty = bars + UM_ST;           // [UM_ST]  MMA commit -> producers
+    u64* accf = bars + 2 * UM_ST;        // [2]      MMA commit -> epilogue
+    u64* acce = bars + 2 * UM_ST + 2;    // [2]      epilogue -> MMA
+    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * UM_ST + 4);
+
+    const int N = 1 << logn;
+    const long long LN = (long long)nlimb << logn;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nob = (opad + 31) >> 5;
+    const long long items = (long long)tcnt * N * nob;
+
+    // zero the B strips once: only plane rows 7..14 are ever rewritten
+    for (int x = threadIdx.x; x < UM_ST * 2 * UM_BHALF / 16; x += blockDim.x) {
+        const int st = x / (2 * UM_BHALF / 16), r = x % (2 * UM_BHALF / 16);
+        reinterpret_cast<uint4*>(um_smem + (size_t)st * UM_SBYTES + UM_ABYTES)[r] = make_uint4(0, 0, 0, 0);
+    }
+    fence_async_smem();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < UM_ST; s++) {
+            mbar_init(&full[s], UM_PROD * 32);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; s++) {
+            mbar_init(&accf[s], 1);
+            mbar_init(&acce[s], UM_EPI * 32);
+        }
+        fence_barrier_init();
+    }
+    if (warp == UM_PROD) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const u32 tmem = *tmem_slot;
+
+    if (warp < UM_PROD) {
+        // ------------------------------------------------ producers
+        const int tid = threadIdx.x;                     // 0 .. 255
+        const int col_lo = lane >> 2, kq_lo = lane & 3;
+        u32 it = 0;
+        for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+            const long long bl = item / nob;
+            const int ob = (int)(item % nob);
+            const int nbo = min(2, (opad - ob * 32) >> 4);
+            const long long b = bl + (long long)t0 * N;
+            for (int c = 0; c < nch; c++, it++) {
+                const int stage = it % UM_ST;
+                um_wait(&empty[stage], ((it / UM_ST) & 1) ^ 1);
+                u8* As = um_smem + (size_t)stage * UM_SBYTES;
+                u8* Bs = As + UM_ABYTES;
+                const int kmax = min(32, n_terms - c * 32);
+                const u64* src = S + (bl * n_terms + c * 32) * UM_COLS;
+                // A: unit (cg, kq) = 8 columns x 4 terms; lanes (col_lo, kq_lo) write one 128-byte row group
+                u64 v[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int wu = warp * 4 + u;          // 0 .. 31 = (cg, kq_hi)
+                    const int col = (wu >> 1) * 8 + col_lo, k0 = ((wu & 1) * 4 + kq_lo) * 4;
+#pragma unroll
+                    for (int r = 0; r < 4; r++)
+                        v[u][r] = k0 + r < kmax ? __ldg(src + (long long)(k0 + r) * UM_COLS + col) : 0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int wu = warp * 4 + u;
+                    const int col = (wu >> 1) * 8 + col_lo, kh = wu & 1;
+                    u32 bp[8];
+                    bytes_by_plane(v[u], bp);
+                    u8* dst = As + kh * (UM_COLS * 16) + (col >> 3) * 128 + (col & 7) * 16 + kq_lo * 4;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) *reinterpret_cast<u32*>(dst + j * UM_APLANE) = bp[j];
+                }
+                // B: (output, k-half) -> its 128-byte strip run (rows 7..14)
+                const uint4* psrc =
+                    reinterpret_cast<const uint4*>(planes + ((b * nch + c) * opad + ob * 32) * 256);
+                for (int p = tid; p < nbo * 256; p += UM_PROD * 32) {
+                    const int o = p >> 4, kh = (p >> 3) & 1, i = p & 7;
+                    *reinterpret_cast<uint4*>(Bs + kh * UM_BHALF + (o * 16 + 7 + i) * 16) = __ldg(psrc + p);
+                }
+                fence_async_smem();
+                mbar_arrive(&full[stage]);
+            }
+        }
+    } else if (warp == UM_PROD) {
+        // ------------------------------------------------ MMA issuer
+        u32 it = 0, use[2] = {0, 0};
+        for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+            const int ob = (int)(item % nob);
+            const int nbo = min(2, (opad - ob * 32) >> 4);
+            for (int c = 0; c < nch; c++, it++) {
+                const int stage = it % UM_ST;
+                um_wait(&full[stage], (it / UM_ST) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const u32 a0 = smem_addr(um_smem + (size_t)stage * UM_SBYTES);
+                    const u32 b0 = a0 + UM_ABYTES;
+                    for (int nb = 0; nb < nbo; nb++) {
+                        if (c == 0) {
+                            um_wait(&acce[nb], (use[nb] & 1) ^ 1);
+                            tc_fence_after();
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; j++) {
+                            const u64 ad = umma_sdesc(a0 + j * UM_APLANE, UM_COLS * 16, 128);
+                            const u64 bd = umma_sdesc(b0 + (nb * 256 + 7 - j) * 16, UM_BHALF, 128);
+                            umma_i8(tmem + nb * 256, ad, bd, (c > 0 || j > 0) ? 1u : 0u);
+                        }
+                        if (c == nch - 1) umma_commit(&accf[nb]);
+                    }
+                    umma_commit(&empty[stage]);
+                }
+                __syncwarp();
+            }
+            for (int nb = 0; nb < nbo; nb++) use[nb]++;
+        }
+    } else {
+        // ------------------------------------------------ epilogue
+        const int e = warp - UM_PROD - 1;                // 0 .. 7
+        const int quarter = warp & 3;                    // TMEM lanes this warp may read
+        const int ohalf = e >> 2;                        // outputs 8 ohalf .. + 7 of each 16-block
+        const int col = quarter * 32 + lane;
+        const bool live_col = col < 2 * gcnt;
+        u32 use[2] = {0, 0};
+        for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+            const long long bl = item / nob;
+            const int ob = (int)(item % nob);
+            const int nbo = min(2, (opad - ob * 32) >> 4);
+            const long long b = bl + (long long)t0 * N;
+            const int t = (int)(b >> logn);
+            const PrimeInfo& P = pr[limbs.prime[t]];
+            const long long coff = b;                    // t N + n
+            u64* obase = out + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN + coff;
+            for (int nb = 0; nb < nbo; nb++) {
+                um_wait(&accf[nb], use[nb] & 1);
+                tc_fence_after();
+#pragma unroll 2
+                for (int oo = 0; oo < 8; oo++) {
+                    const int ol = ohalf * 8 + oo;
+                    u32 d[16];
+                    tmem_ld16(tmem + ((u32)(quarter * 32) << 16) + nb * 256 + ol * 16, d);
+                    tmem_wait_ld();
+                    const int o = ob * 32 + nb * 16 + ol;
+                    if (live_col && o < n_out) {
+                        u64 r = partials_redc(d, P);
+                        u64* po = obase + (long long)o * ostride;
+                        if (accumulate) r = add_mod(r, *po, P.q);
+                        *po = r;
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&acce[nb]);
+                use[nb]++;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == UM_PROD)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+size_t mac_umma_smem() { return UM_SMEM; }
+
+cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, const u8* planes, const u64* S,
+                        int g0, int gcnt, int t0, int tcnt, int opad, int nlimb, int logn, const Limbs& limbs,
+                        const PrimeInfo* pr, int accumulate, cudaStream_t st) {
+    if (gcnt <= 0 || n_terms <= 0 || n_out <= 0) return cudaSuccess;
+    if (gcnt > UM_COLS / 2) return cudaErrorInvalidValue;
+    const int nch = (n_terms + 31) / 32;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(mac_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UM_SMEM);
+        configured = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long items = (long long)tcnt * (1LL << logn) * ((opad + 31) / 32);
+    const int grid = (int)std::min<long long>(items, sms);
+    mac_umma_kernel<<<grid, UM_THREADS, UM_SMEM, st>>>(out, out_stride, n_out, n_terms, planes, S, g0, gcnt, t0, tcnt,
+                                                       opad, nch, nlimb, logn, limbs, pr, accumulate);
+    return launched();
+}
+
+}  // namespace bcn

@@ -150,8 +150,14 @@ struct KsTerms {
     u32 g[BCN_IMMA_TERMS];            // 1: the source itself
 };
 cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,
-                             int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
+                             int logn, int spitch, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
                              const u64* pmod, cudaStream_t st);
+// tcgen05 conv MAC (mac_umma.cu): planes in the strip layout, S with a 128-word pitch, gcnt <= 64
+cudaError_t pack_planes_umma_op(unsigned char* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad,
+                                int nch, int nl, int logn, cudaStream_t st, const int* tlimbs_dev = nullptr);
+cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, const unsigned char* planes,
+                        const u64* S, int g0, int gcnt, int t0, int tcnt, int opad, int nlimb, int logn,
+                        const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st);
 // slot-major staging of a g-block x limb-block of the ct terms: S[(tl N + n) K + k][64]
 cudaError_t slot_major_op(u64* S, const MacImma& m, int g0, int gcnt, int t0, int tcnt, int nlimb, int logn,
                           cudaStream_t st);

@@ -255,29 +255,34 @@ class Engine:
             _lib.call("bcn_rotsum_keys", self._h, _ptr(out), n, Us, cts, gal, pts, bat, ks, G, level, _stream())
         return out
 
-    def pack_planes_ext(self, pts, level: int) -> torch.Tensor:
+    PLANES_IMMA, PLANES_TCGEN05 = 0, 1
+
+    def pack_planes_ext(self, pts, level: int, layout: int = 0) -> torch.Tensor:
         """Extended-basis byte planes of an O x K plaintext matrix for conv_ks_mac:
-        column k holds level+1+K-limb (rotation) or level+1-limb (identity) plaintexts."""
+        column k holds level+1+K-limb (rotation) or level+1-limb (identity) plaintexts.
+        layout: PLANES_IMMA (mma.sync, any G) or PLANES_TCGEN05 (tcgen05, G >= 64)."""
         O, K = len(pts), len(pts[0])
         nb = ctypes.c_uint64()
         _lib.call("bcn_planes_ext_bytes", self._h, O, K, level, ctypes.byref(nb))
         planes = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
         p_arr = (ctypes.c_uint64 * (O * K))(*[p.data_ptr() for row in pts for p in row])
         limbs = (ctypes.c_int * K)(*[int(p.shape[1]) for p in pts[0]])
-        _lib.call("bcn_pack_planes_ext", self._h, _ptr(planes), O, K, p_arr, limbs, level, _stream())
+        _lib.call("bcn_pack_planes_ext", self._h, _ptr(planes), O, K, p_arr, limbs, level, int(layout), _stream())
         return planes
 
-    def conv_ks_mac(self, srcs, Us, gals, planes: torch.Tensor, n_out: int, level: int) -> torch.Tensor:
+    def conv_ks_mac(self, srcs, Us, gals, planes: torch.Tensor, n_out: int, level: int,
+                    layout: int = 0) -> torch.Tensor:
         """Conv outputs with lazy ModDown: out[o] = Rescale(sum_k pt[o][k] (x) rot_{g_k}(srcs[k]))
-        -> u64[n_out, G, 2, level, N] at level-1 (g_k = 1: srcs[k] itself, Us[k] unused)."""
+        -> u64[n_out, G, 2, level, N] at level-1 (g_k = 1: srcs[k] itself, Us[k] unused).
+        layout: the one planes was packed with."""
         K = len(srcs)
         G = srcs[0].shape[0]
         s_arr = (ctypes.c_uint64 * K)(*[x.data_ptr() for x in srcs])
         u_arr = (ctypes.c_uint64 * K)(*[0 if u is None else u.data_ptr() for u in Us])
         g_arr = (ctypes.c_uint64 * K)(*[int(g) for g in gals])
         out = torch.empty((n_out, G, 2, level, self.N), dtype=torch.int64, device=self.device)
-        _lib.call("bcn_conv_ks_mac", self._h, _ptr(out), n_out, K, s_arr, u_arr, g_arr, _ptr(planes), G, level,
-                  _stream())
+        _lib.call("bcn_conv_ks_mac", self._h, _ptr(out), n_out, K, s_arr, u_arr, g_arr, _ptr(planes), int(layout),
+                  G, level, _stream())
         return out
 
     def rotsum_rescale(self, terms, level: int, keys=None, ct_terms=()) -> torch.Tensor:

@@ -509,16 +509,26 @@ def _premul_key(ctx: HeContext, g: int, pt, level: int):
     return k
 
 
-def _planes_for(ctx: HeContext, pts: list, level: int, ext: bool = False):
+def _conv_layout(G: int) -> int:
+    """Plane layout of the conv MAC: tcgen05.mma (M = 64 slot sets x 2
+    components per pass) once there are enough slot sets to fill it, else
+    mma.sync IMMA.  BCN_TCGEN05=0/1 forces either."""
+    v = os.environ.get("BCN_TCGEN05", "auto")
+    if v in ("0", "1"):
+        return int(v)
+    return 1 if G >= 64 else 0
+
+
+def _planes_for(ctx: HeContext, pts: list, level: int, ext: bool = False, layout: int = 0):
     """Byte planes of an O x K plaintext matrix for the tensor-core MAC, packed
     once and cached next to the plaintexts.  The entry keeps the plaintext
     tensors alive and is only reused for the very same objects."""
-    key = ("planes_ext" if ext else "planes", level, tuple(id(p) for row in pts for p in row))
+    key = ("planes_ext" if ext else "planes", level, layout, tuple(id(p) for row in pts for p in row))
     hit = ctx._pt_cache.get(key)
     if hit is not None and all(a is b for a, b in zip(hit[1], (p for row in pts for p in row))):
         ctx._pt_cache.move_to_end(key)
         return hit[0]
-    planes = ctx.engine.pack_planes_ext(pts, level) if ext else ctx.engine.pack_planes(pts, level)
+    planes = ctx.engine.pack_planes_ext(pts, level, layout) if ext else ctx.engine.pack_planes(pts, level)
     STATS["plane_pack"] += 1
     _cache_put(ctx, key, (planes, [p for row in pts for p in row]))
     return planes
@@ -832,7 +842,9 @@ def materialize_conv(accs: list) -> bool:
             Us.append(None)
             gals.append(1)
     pts = [[t[3] if t[0] == "rot" else t[2] for t in c._terms] for c in lazy]
-    out = eng.conv_ks_mac(srcs, Us, gals, _planes_for(ctx, pts, lvl, ext=True), len(lazy), lvl)
+    layout = _conv_layout(int(srcs[0].shape[0]))
+    out = eng.conv_ks_mac(srcs, Us, gals, _planes_for(ctx, pts, lvl, ext=True, layout=layout), len(lazy), lvl,
+                          layout)
     STATS["mac_launch"] += 1
     STATS["moddown"] += len(lazy)
     STATS["keyswitch_lazy"] += sum(g != 1 for g in gals)

@@ -314,8 +314,9 @@ def test_rotsum_rescale_merged_matches_oracle(N, L):
     assert np.abs(dec - exp).max() < 1e-4
 
 
+@pytest.mark.parametrize("layout", [0, 1], ids=["imma", "tcgen05"])
 @pytest.mark.parametrize("N,L", [(1024, 3), (8192, 3)])
-def test_conv_ks_mac_matches_oracle(N, L):
+def test_conv_ks_mac_matches_oracle(N, L, layout):
     """Conv layer with lazy ModDown (bcn_conv_ks_mac: key-switch inner products
     fused into the slot-major staging, tensor-core MAC over the extended
     basis, one merged ModDown+rescale per output) == Oracle.rotsum_rescale of
@@ -333,9 +334,9 @@ def test_conv_ks_mac_matches_oracle(N, L):
     vals = rng.standard_normal((n_out, len(taps), N // 2))
     pts = [[eng.encode_ext(vals[o, k], L, ql) if r else eng.encode(vals[o, k], L, ql, montgomery=True)
             for k, (_, _, r, _) in enumerate(taps)] for o in range(n_out)]
-    planes = eng.pack_planes_ext(pts, L)
+    planes = eng.pack_planes_ext(pts, L, layout)
     got = eng.conv_ks_mac([t[0] for t in taps], [t[1] if t[2] else None for t in taps],
-                          [ge(t[2], N) if t[2] else 1 for t in taps], planes, n_out, L)
+                          [ge(t[2], N) if t[2] else 1 for t in taps], planes, n_out, L, layout)
     srcs = [oc, oc, oc2, oc2, oc]
     for o in range(n_out):
         want = [orc.rotsum_rescale([(srcs[k][i], r, vals[o, k]) for k, (_, _, r, _) in enumerate(taps) if r],
@@ -378,3 +379,29 @@ def test_conv_ks_mac_blocks_bitexact_vs_eager_path():
     for o in (0, 17, 39):
         want = sum(np.roll(xv[i], -r, axis=1) * vals[o, k] for k, (i, r) in enumerate(taps))
         assert np.abs(dec[o] - want).max() < 1e-3
+
+
+@pytest.mark.parametrize("n_out,rots", [(40, [0, 1, 5, 31]), (16, [0, 1, 2, 3, 4, 5, 6, 7, 9, 11, 13, 17, 19, 23])])
+def test_conv_ks_mac_tcgen05_bitexact_vs_imma(n_out, rots):
+    """The tcgen05.mma kind::i8 conv MAC (TMEM accumulators, strip-window
+    planes, 64 slot sets per pass) is bit-identical to the mma.sync IMMA one:
+    G = 70 (one full 64-set pass + a 6-set remainder), 40 outputs (a 32 block
+    + a 16-row half block) or 16, 12 terms (one 32-term chunk) or 42 terms
+    (two chunks, second partial), 60-bit primes with every byte live."""
+    N, L = 2048, 3
+    hp = make_params(N, L, 60, dnum=2)
+    eng = Engine(hp)
+    rng = np.random.default_rng(43)
+    G, n_src = 70, 3
+    from paper_2402_01296_b200.params import galois_element as ge
+    xs = [eng.encrypt(rng.standard_normal((G, N // 2)) * 0.5, counter=300 + 30 * i) for i in range(n_src)]
+    Us = [eng.modup(x, L) for x in xs]
+    taps = [(i, r) for i in range(n_src) for r in rots]
+    ql = float(hp.q[L])
+    vals = rng.standard_normal((n_out, len(taps), N // 2)) * 0.3
+    pts = [[eng.encode_ext(vals[o, k], L, ql) if r else eng.encode(vals[o, k], L, ql, montgomery=True)
+            for k, (_, r) in enumerate(taps)] for o in range(n_out)]
+    args = ([xs[i] for i, _ in taps], [Us[i] if r else None for i, r in taps], [ge(r, N) if r else 1 for _, r in taps])
+    ref = eng.conv_ks_mac(*args, eng.pack_planes_ext(pts, L, 0), n_out, L, 0)
+    got = eng.conv_ks_mac(*args, eng.pack_planes_ext(pts, L, 1), n_out, L, 1)
+    assert torch.equal(got, ref)
