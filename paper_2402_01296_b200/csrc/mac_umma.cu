@@ -21,16 +21,22 @@
 //   epilogue; at 128 x 256 x 32 per instruction the tensor core still does
 //   about 4x the useful byte products of mma.sync IMMA per SM cycle.
 //
-// Warp roles (persistent, one CTA per SM, 4-stage shared-memory ring):
-//   warps 0-7   producers: S words -> byte planes (A), plane strips (B),
+// Warp roles (persistent, one CTA per SM):
+//   warp 4      bulk-copy issuer (one lane): the chunk's 32 x 128 staged words
+//               (one contiguous 32 KB run of S) and its plane strips, by
+//               cp.async.bulk into a 2-deep raw ring (mbarrier complete_tx)
+//   warps 0-3   transposers, one thread per column: raw words -> byte planes
+//               (A) and plane rows -> strips (B) in a 3-deep stage ring,
 //               fence.proxy.async, arrive on full[stage]
-//   warp 8      MMA issuer (one lane) + TMEM allocation (512 columns = two
+//   warp 5      MMA issuer (one lane) + TMEM allocation (512 columns = two
 //               256-column accumulators, one per 16-output block)
-//   warps 9-16  epilogue: warp w reads TMEM lanes 32 (w % 4).., outputs
-//               (w - 9) / 4 * 8 .. + 7 of the block
+//   warps 6-13  epilogue: warp w reads TMEM lanes 32 (w % 4).. (its 32
+//               columns), outputs 8 ((w - 6) / 4) .. + 7 of the block
 // Work item = (slot, block of 32 outputs).  The accumulator of output block
 // half nb is released as soon as its epilogue has read it, so the next item's
 // MMAs into it overlap the drain of the other half.
+#include <cstdio>
+#include <cstdlib>
 #include "common.cuh"
 #include "ops.cuh"
 
@@ -38,17 +44,22 @@ namespace bcn {
 
 typedef unsigned char u8;
 
-#define UM_ST 4                                   // shared-memory stages
-#define UM_PROD 8                                 // producer warps
-#define UM_EPI 8                                  // epilogue warps
-#define UM_THREADS ((UM_PROD + 1 + UM_EPI) * 32)
+#define UM_ST 3                                   // plane stages (transposers -> MMA)
+#define UM_RS 2                                   // raw stages (bulk copy -> transposers)
+#define UM_TR 4                                   // transposer warps: one thread per column
+#define UM_W_COPY UM_TR                           // bulk-copy issuer warp
+#define UM_W_MMA (UM_TR + 1)                      // MMA issuer warp (also owns TMEM)
+#define UM_W_EPI (UM_TR + 2)                      // first of the epilogue warps
+#define UM_EPI 8                                  // epilogue warps (2 per TMEM lane quarter)
+#define UM_THREADS ((UM_W_EPI + UM_EPI) * 32)     // 14 warps: <= 4 per sub-core, 128 registers
 constexpr int UM_COLS = 128;                      // M: ciphertext columns per item
 constexpr int UM_APLANE = UM_COLS * 32;           // bytes of one A plane (128 rows x 32 k)
 constexpr int UM_ABYTES = 8 * UM_APLANE;
 constexpr int UM_BROWS = 32 * 16 + 8;             // 32 output strips + the tail window overrun
 constexpr int UM_BHALF = UM_BROWS * 16;           // one 16-byte k-half of all rows
 constexpr int UM_SBYTES = UM_ABYTES + 2 * UM_BHALF;
-constexpr size_t UM_SMEM = (size_t)UM_ST * UM_SBYTES + 256;
+constexpr int UM_RBYTES = UM_COLS * 32 * 8 + 32 * 256;   // raw chunk: 32 x 128 words + 32 outputs' planes
+constexpr size_t UM_SMEM = (size_t)UM_ST * UM_SBYTES + (size_t)UM_RS * UM_RBYTES + 128;
 
 // ---------------------------------------------------------------- packing
 // planes[((b * nch + c) * opad + o) * 256 + kh * 128 + i * 16 + kb]
@@ -185,19 +196,27 @@ __device__ __forceinline__ u64 partials_redc(const u32 (&d)[16], const PrimeInfo
 }
 
 // ---------------------------------------------------------------- kernel
+#ifdef BCN_UMMA_PROF      // experiments: per-role wait/busy cycles of CTA 0, printed at exit
+#define UM_TIMED(acc, stmt) do { const long long _t = clock64(); stmt; acc += clock64() - _t; } while (0)
+#else
+#define UM_TIMED(acc, stmt) stmt
+#endif
 // S[(bl * n_terms + k) * 128 + col]: the staged words of slot bl (bl = tl N + n);
 // out[o * ostride + g * 2 LN + c * LN + t N + n], g = g0 + col / 2, c = col % 2
 __global__ void __launch_bounds__(UM_THREADS, 1)
     mac_umma_kernel(u64* __restrict__ out, long long ostride, int n_out, int n_terms, const u8* __restrict__ planes,
                     const u64* __restrict__ S, int g0, int gcnt, int t0, int tcnt, int opad, int nch, int nlimb,
-                    int logn, Limbs limbs, const PrimeInfo* __restrict__ pr, int accumulate) {
+                    int logn, Limbs limbs, const PrimeInfo* __restrict__ pr, int accumulate, int dbg) {
     extern __shared__ __align__(1024) unsigned char um_smem[];
-    u64* bars = reinterpret_cast<u64*>(um_smem + (size_t)UM_ST * UM_SBYTES);
-    u64* full = bars;                    // [UM_ST]  producers -> MMA
-    u64* empty = bars + UM_ST;           // [UM_ST]  MMA commit -> producers
-    u64* accf = bars + 2 * UM_ST;        // [2]      MMA commit -> epilogue
-    u64* acce = bars + 2 * UM_ST + 2;    // [2]      epilogue -> MMA
-    u32* tmem_slot = reinterpret_cast<u32*>(bars + 2 * UM_ST + 4);
+    unsigned char* raw = um_smem + (size_t)UM_ST * UM_SBYTES;                  // [UM_RS] raw chunk images
+    u64* bars = reinterpret_cast<u64*>(raw + (size_t)UM_RS * UM_RBYTES);
+    u64* full = bars;                         // [UM_ST]  transposers -> MMA
+    u64* empty = full + UM_ST;                // [UM_ST]  MMA commit -> transposers
+    u64* rfull = empty + UM_ST;               // [UM_RS]  bulk copies landed -> transposers
+    u64* rempty = rfull + UM_RS;              // [UM_RS]  transposers -> copy issuer
+    u64* accf = rempty + UM_RS;               // [2]      MMA commit -> epilogue
+    u64* acce = accf + 2;                     // [2]      epilogue -> MMA
+    u32* tmem_slot = reinterpret_cast<u32*>(acce + 2);
 
     const int N = 1 << logn;
     const long long LN = (long long)nlimb << logn;
@@ -213,8 +232,12 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
     fence_async_smem();
     if (threadIdx.x == 0) {
         for (int s = 0; s < UM_ST; s++) {
-            mbar_init(&full[s], UM_PROD * 32);
+            mbar_init(&full[s], UM_TR * 32);
             mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < UM_RS; s++) {
+            mbar_init(&rfull[s], 1);
+            mbar_init(&rempty[s], UM_TR * 32);
         }
         for (int s = 0; s < 2; s++) {
             mbar_init(&accf[s], 1);
@@ -222,7 +245,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
         }
         fence_barrier_init();
     }
-    if (warp == UM_PROD) {
+    if (warp == UM_W_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tmem_slot))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -231,56 +254,78 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const u32 tmem = *tmem_slot;
+    long long tw = 0, tw2 = 0;
+    const long long tstart = clock64();
 
-    if (warp < UM_PROD) {
-        // ------------------------------------------------ producers
-        const int tid = threadIdx.x;                     // 0 .. 255
-        const int col_lo = lane >> 2, kq_lo = lane & 3;
+    if (warp == UM_W_COPY) {
+        // ------------------------------------------------ bulk-copy issuer (one lane)
+        if (lane == 0) {
+            u32 it = 0;
+            for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+                const long long bl = item / nob;
+                const int ob = (int)(item - bl * nob);
+                const int nbo = min(2, (opad - ob * 32) >> 4);
+                const long long b = bl + (long long)t0 * N;
+                for (int c = 0; c < nch; c++, it++) {
+                    const int rs = it % UM_RS;
+                    UM_TIMED(tw, um_wait(&rempty[rs], ((it / UM_RS) & 1) ^ 1));
+                    const int kmax = min(32, n_terms - c * 32);
+                    const u32 sb = (u32)kmax * UM_COLS * 8, pb = (u32)nbo * 16 * 256;
+                    unsigned char* dst = raw + (size_t)rs * UM_RBYTES;
+                    mbar_expect_tx(&rfull[rs], sb + pb);
+                    bulk_load(dst, S + (bl * n_terms + c * 32) * UM_COLS, sb, &rfull[rs]);
+                    bulk_load(dst + UM_COLS * 32 * 8, planes + ((b * nch + c) * opad + ob * 32) * 256, pb, &rfull[rs]);
+                }
+            }
+        }
+    } else if (warp < UM_TR) {
+        // ------------------------------------------------ transposers: raw words -> byte planes
+        // thread = one column; per k-half it reads 16 words (lanes: 32 consecutive
+        // columns, conflict-free) and writes one 16-byte core-matrix row per plane
+        // (lanes: 512 contiguous bytes, conflict-free)
+        const int col = threadIdx.x;                     // 0 .. 127
         u32 it = 0;
         for (long long item = blockIdx.x; item < items; item += gridDim.x) {
             const long long bl = item / nob;
-            const int ob = (int)(item % nob);
+            const int ob = (int)(item - bl * nob);
             const int nbo = min(2, (opad - ob * 32) >> 4);
-            const long long b = bl + (long long)t0 * N;
             for (int c = 0; c < nch; c++, it++) {
-                const int stage = it % UM_ST;
-                um_wait(&empty[stage], ((it / UM_ST) & 1) ^ 1);
+                const int rs = it % UM_RS, stage = it % UM_ST;
+                UM_TIMED(tw, um_wait(&rfull[rs], (it / UM_RS) & 1));
+                UM_TIMED(tw2, um_wait(&empty[stage], ((it / UM_ST) & 1) ^ 1));
+                const u64* rw = reinterpret_cast<const u64*>(raw + (size_t)rs * UM_RBYTES);
+                const uint4* rp = reinterpret_cast<const uint4*>(raw + (size_t)rs * UM_RBYTES + UM_COLS * 32 * 8);
                 u8* As = um_smem + (size_t)stage * UM_SBYTES;
                 u8* Bs = As + UM_ABYTES;
-                const int kmax = min(32, n_terms - c * 32);
-                const u64* src = S + (bl * n_terms + c * 32) * UM_COLS;
-                // A: unit (cg, kq) = 8 columns x 4 terms; lanes (col_lo, kq_lo) write one 128-byte row group
-                u64 v[4][4];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int wu = warp * 4 + u;          // 0 .. 31 = (cg, kq_hi)
-                    const int col = (wu >> 1) * 8 + col_lo, k0 = ((wu & 1) * 4 + kq_lo) * 4;
+                for (int kh = 0; kh < 2; kh++) {
+                    u32 pl[8][4];
 #pragma unroll
-                    for (int r = 0; r < 4; r++)
-                        v[u][r] = k0 + r < kmax ? __ldg(src + (long long)(k0 + r) * UM_COLS + col) : 0ull;
+                    for (int q = 0; q < 4; q++) {
+                        u64 v[4];
+#pragma unroll
+                        for (int r = 0; r < 4; r++) v[r] = rw[(kh * 16 + q * 4 + r) * UM_COLS + col];
+                        u32 bp[8];
+                        bytes_by_plane(v, bp);
+#pragma unroll
+                        for (int j = 0; j < 8; j++) pl[j][q] = bp[j];
+                    }
+                    u8* dst = As + kh * (UM_COLS * 16) + (col >> 3) * 128 + (col & 7) * 16;
+#pragma unroll
+                    for (int j = 0; j < 8; j++)
+                        *reinterpret_cast<uint4*>(dst + j * UM_APLANE) = make_uint4(pl[j][0], pl[j][1], pl[j][2], pl[j][3]);
                 }
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int wu = warp * 4 + u;
-                    const int col = (wu >> 1) * 8 + col_lo, kh = wu & 1;
-                    u32 bp[8];
-                    bytes_by_plane(v[u], bp);
-                    u8* dst = As + kh * (UM_COLS * 16) + (col >> 3) * 128 + (col & 7) * 16 + kq_lo * 4;
-#pragma unroll
-                    for (int j = 0; j < 8; j++) *reinterpret_cast<u32*>(dst + j * UM_APLANE) = bp[j];
-                }
-                // B: (output, k-half) -> its 128-byte strip run (rows 7..14)
-                const uint4* psrc =
-                    reinterpret_cast<const uint4*>(planes + ((b * nch + c) * opad + ob * 32) * 256);
-                for (int p = tid; p < nbo * 256; p += UM_PROD * 32) {
+                // B: piece (output, k-half, plane) -> its strip row 7 + plane
+                for (int p = col; p < nbo * 256; p += UM_TR * 32) {
                     const int o = p >> 4, kh = (p >> 3) & 1, i = p & 7;
-                    *reinterpret_cast<uint4*>(Bs + kh * UM_BHALF + (o * 16 + 7 + i) * 16) = __ldg(psrc + p);
+                    *reinterpret_cast<uint4*>(Bs + kh * UM_BHALF + (o * 16 + 7 + i) * 16) = rp[p];
                 }
                 fence_async_smem();
                 mbar_arrive(&full[stage]);
+                mbar_arrive(&rempty[rs]);
             }
         }
-    } else if (warp == UM_PROD) {
+    } else if (warp == UM_W_MMA) {
         // ------------------------------------------------ MMA issuer
         u32 it = 0, use[2] = {0, 0};
         for (long long item = blockIdx.x; item < items; item += gridDim.x) {
@@ -288,21 +333,21 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
             const int nbo = min(2, (opad - ob * 32) >> 4);
             for (int c = 0; c < nch; c++, it++) {
                 const int stage = it % UM_ST;
-                um_wait(&full[stage], (it / UM_ST) & 1);
+                UM_TIMED(tw, um_wait(&full[stage], (it / UM_ST) & 1));
                 tc_fence_after();
                 if (lane == 0) {
                     const u32 a0 = smem_addr(um_smem + (size_t)stage * UM_SBYTES);
                     const u32 b0 = a0 + UM_ABYTES;
                     for (int nb = 0; nb < nbo; nb++) {
                         if (c == 0) {
-                            um_wait(&acce[nb], (use[nb] & 1) ^ 1);
+                            UM_TIMED(tw2, um_wait(&acce[nb], (use[nb] & 1) ^ 1));
                             tc_fence_after();
                         }
 #pragma unroll
                         for (int j = 0; j < 8; j++) {
                             const u64 ad = umma_sdesc(a0 + j * UM_APLANE, UM_COLS * 16, 128);
                             const u64 bd = umma_sdesc(b0 + (nb * 256 + 7 - j) * 16, UM_BHALF, 128);
-                            umma_i8(tmem + nb * 256, ad, bd, (c > 0 || j > 0) ? 1u : 0u);
+                            if (!(dbg & 4)) umma_i8(tmem + nb * 256, ad, bd, (c > 0 || j > 0) ? 1u : 0u);
                         }
                         if (c == nch - 1) umma_commit(&accf[nb]);
                     }
@@ -314,7 +359,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
         }
     } else {
         // ------------------------------------------------ epilogue
-        const int e = warp - UM_PROD - 1;                // 0 .. 7
+        const int e = warp - UM_W_EPI;                   // 0 .. 7
         const int quarter = warp & 3;                    // TMEM lanes this warp may read
         const int ohalf = e >> 2;                        // outputs 8 ohalf .. + 7 of each 16-block
         const int col = quarter * 32 + lane;
@@ -322,39 +367,53 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
         u32 use[2] = {0, 0};
         for (long long item = blockIdx.x; item < items; item += gridDim.x) {
             const long long bl = item / nob;
-            const int ob = (int)(item % nob);
+            const int ob = (int)(item - bl * nob);
             const int nbo = min(2, (opad - ob * 32) >> 4);
-            const long long b = bl + (long long)t0 * N;
-            const int t = (int)(b >> logn);
-            const PrimeInfo& P = pr[limbs.prime[t]];
-            const long long coff = b;                    // t N + n
-            u64* obase = out + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN + coff;
+            const long long b = bl + (long long)t0 * N;  // t N + n
+            const PrimeInfo& P = pr[limbs.prime[(int)(b >> logn)]];
+            u64* obase = out + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN + b;
             for (int nb = 0; nb < nbo; nb++) {
-                um_wait(&accf[nb], use[nb] & 1);
+                UM_TIMED(tw, um_wait(&accf[nb], use[nb] & 1));
                 tc_fence_after();
-#pragma unroll 2
-                for (int oo = 0; oo < 8; oo++) {
-                    const int ol = ohalf * 8 + oo;
-                    u32 d[16];
-                    tmem_ld16(tmem + ((u32)(quarter * 32) << 16) + nb * 256 + ol * 16, d);
+                // two groups of four outputs: four TMEM loads in flight per wait, four
+                // independent recombine+REDC chains; the accumulator is released as
+                // soon as the last group is in registers
+#pragma unroll 1
+                for (int og = 0; og < 2; og++) {
+                    u32 d[4][16];
+#pragma unroll
+                    for (int x = 0; x < 4; x++)
+                        tmem_ld16(tmem + ((u32)(quarter * 32) << 16) + nb * 256 + (ohalf * 8 + og * 4 + x) * 16, d[x]);
                     tmem_wait_ld();
-                    const int o = ob * 32 + nb * 16 + ol;
-                    if (live_col && o < n_out) {
-                        u64 r = partials_redc(d, P);
-                        u64* po = obase + (long long)o * ostride;
-                        if (accumulate) r = add_mod(r, *po, P.q);
-                        *po = r;
+                    if (og == 1) {
+                        tc_fence_before();
+                        mbar_arrive(&acce[nb]);
+                    }
+#pragma unroll
+                    for (int x = 0; x < 4; x++) {
+                        const int o = ob * 32 + nb * 16 + ohalf * 8 + og * 4 + x;
+                        if (live_col && o < n_out && !(dbg & 1)) {
+                            u64 r = partials_redc(d[x], P);
+                            u64* po = obase + (long long)o * ostride;
+                            if (accumulate) r = add_mod(r, *po, P.q);
+                            *po = r;
+                        }
                     }
                 }
-                tc_fence_before();
-                mbar_arrive(&acce[nb]);
                 use[nb]++;
             }
         }
     }
+#ifdef BCN_UMMA_PROF
+    if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == UM_W_COPY || warp == UM_W_MMA || warp == UM_W_EPI))
+        printf("umma role %d: total %lld wait %lld wait2 %lld\n", warp, clock64() - tstart, tw, tw2);
+#endif
+    (void)tw;
+    (void)tw2;
+    (void)tstart;
     tc_fence_before();
     __syncthreads();
-    if (warp == UM_PROD)
+    if (warp == UM_W_MMA)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
@@ -376,8 +435,9 @@ cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long items = (long long)tcnt * (1LL << logn) * ((opad + 31) / 32);
     const int grid = (int)std::min<long long>(items, sms);
+    static const int dbg = getenv("BCN_UMMA_DBG") ? atoi(getenv("BCN_UMMA_DBG")) : 0;   // experiments only
     mac_umma_kernel<<<grid, UM_THREADS, UM_SMEM, st>>>(out, out_stride, n_out, n_terms, planes, S, g0, gcnt, t0, tcnt,
-                                                       opad, nch, nlimb, logn, limbs, pr, accumulate);
+                                                       opad, nch, nlimb, logn, limbs, pr, accumulate, dbg);
     return launched();
 }
 

@@ -42,9 +42,10 @@ elif what == "convks":
     nb = ctypes.c_uint64()
     _lib.call("bcn_planes_ext_bytes", eng._h, O, len(terms), lvl, ctypes.byref(nb))
     planes = torch.randint(0, 256, (int(nb.value),), dtype=torch.uint8, device="cuda")
+    layout = int(os.environ.get("PROF_LAYOUT", "0"))     # 1: tcgen05 (use PROF_G=64)
     for _ in range(2):
         eng.conv_ks_mac([t[0] for t in terms], [t[1] if t[2] != 1 else None for t in terms], [t[2] for t in terms],
-                        planes, O, lvl)
+                        planes, O, lvl, layout)
     torch.cuda.synchronize()
 elif what == "rotsum3":
     # pooling / compaction shape of cifar3: 3 rotations of one source at level 7, G = 32
