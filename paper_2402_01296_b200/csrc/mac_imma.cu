@@ -98,7 +98,10 @@ cudaError_t pack_planes_op(u8* planes, const u64* const* pts_dev, int n_out, int
 // aligned 32-block is the image of one aligned 32-block, so the gathers stay
 // inside one 256-byte segment.
 template <int ND>    // digits (1..4); 0: any count, key words re-read from L1
-__global__ void __launch_bounds__(256, 3) slot_major_ks_kernel(u64* __restrict__ S, const KsTerms T, int g0, int gcnt,
+#ifndef BCN_SMKS_MINB
+#define BCN_SMKS_MINB 4
+#endif
+__global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* __restrict__ S, const KsTerms T, int g0, int gcnt,
                                                             int t0, int nq, int next, int ndig, int logn,
                                                             int spitch, long long kds, long long kcs, Limbs ext,
                                                             const PrimeInfo* __restrict__ pr,
