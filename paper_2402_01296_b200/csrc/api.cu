@@ -87,6 +87,8 @@ struct bcn_ctx {
     std::vector<u64> pmod_host;   // [2 nq] Shoup pairs of P mod q_i
     PrimeInfo* pr = nullptr;
     ulonglong2* tw = nullptr;
+    double2* twf = nullptr;       // FP64 twiddles {w, w/q} (same layout as tw)
+    bool fp_ntt = true;           // BCN_NTT_FP64=0: integer butterflies for every prime
     double* ksi_re = nullptr;
     double* ksi_im = nullptr;
     int* rot = nullptr;
@@ -171,6 +173,7 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.digit_stride = 0;
     a.limbs = l;
     a.tw = c->tw;
+    a.twf = c->fp_ntt ? c->twf : nullptr;
     a.pr = c->pr;
     a.skip_alpha = 0;
     a.skip_dnum = 1;
@@ -479,6 +482,19 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
     CUDA_TRY(cudaMemcpy(c->pr, c->hpr.data(), sizeof(PrimeInfo) * nb, cudaMemcpyHostToDevice));
     CUDA_TRY(dmalloc((void**)&c->tw, sizeof(ulonglong2) * tw.size(), &c->table_bytes));
     CUDA_TRY(cudaMemcpy(c->tw, tw.data(), sizeof(ulonglong2) * tw.size(), cudaMemcpyHostToDevice));
+    {   // FP64 companions: {w, w/q} (correctly rounded division of exact doubles; only primes < 2^50 use them)
+        std::vector<double2> twf(tw.size());
+        for (int i = 0; i < nb; i++) {
+            const double qd = (double)c->primes[i];
+            for (size_t k = 0; k < (size_t)2 * N; k++) {
+                const double w = (double)tw[(size_t)i * 2 * N + k].x;
+                twf[(size_t)i * 2 * N + k] = make_double2(w, w / qd);
+            }
+        }
+        CUDA_TRY(dmalloc((void**)&c->twf, sizeof(double2) * twf.size(), &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(c->twf, twf.data(), sizeof(double2) * twf.size(), cudaMemcpyHostToDevice));
+        c->fp_ntt = !getenv_flag_off("BCN_NTT_FP64");
+    }
     // canonical-embedding tables: ksi[k] = exp(2 pi i k / M) as computed by numpy on the host
     // are uploaded by the Python layer through bcn_ctx_set_fft (see below); rot[j] = 5^j mod M here.
     const u64 M = 2 * N, S = N / 2;
@@ -552,7 +568,7 @@ int bcn_ctx_destroy(bcn_ctx* c) {
         cudaFree(kv.second.mdr); cudaFree(kv.second.mdr_scale); cudaFree(kv.second.pqinv);
     }
     for (auto& kv : c->keys) cudaFree(kv.second);
-    cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
+    cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->twf); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
     cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod); cudaFree(c->md_scale);
     if (c->scratch) cudaFree(c->scratch);
     if (c->ptr_dev) cudaFree(c->ptr_dev);

@@ -221,6 +221,223 @@ __device__ __forceinline__ void cfwd_rest(u64* x, const EPI& epi, u64* sm, int r
     }
 }
 
+// ------------------------------------------------- FP64 butterflies (q < 2^50)
+// For primes below 2^50 the butterflies run on the FP64 pipe instead of the
+// 64-bit integer multiplies on the IMAD pipe (tools/micro/bfly_bench.cu:
+// 6.3 vs 3.1 butterflies/clk/SM on this B200).  Residues are exact integers
+// held in doubles, signed, |x| < 2^51; SMEM holds the double bits.
+//   fmm(a, w, wq):  a*w mod q for |a| < 2^51 (so |a wq| < 2^51 and the
+//                   add-1.5*2^52 rounding lands on an integer), w < q,
+//                   wq = fl(w/q).  hi + lo = a*w exactly (FMA two-product);
+//                   qt = rint(a*wq) is within 0.5 + |a| 2^-54 / q*q of a*w/q,
+//                   so the result a*w - qt*q (exact: an integer < 2^53) has
+//                   |r| <= 0.61 q.
+//   fred(x):        x - q rint(x/q), |x| < 2^51  ->  |r| <= 0.5 q (+2^-50 q).
+// Forward (CT): u is reduced on odd stages only; with v = fmm(...) <= 0.61 q
+// every value stays <= 1.75 q < 2q (the fmm input bound).  Inverse (GS): the
+// sum is reduced every stage, every value stays <= 0.61 q.  Outputs are
+// canonicalised (fred, +q if negative) -- the same canonical residues as the
+// integer path, so the two are interchangeable bit for bit.
+static constexpr double FMAGIC = 6755399441055744.0;   // 1.5 * 2^52
+
+__device__ __forceinline__ double fmm(double a, double w, double wq, double q) {
+    const double hi = __dmul_rn(a, w);
+    const double lo = __fma_rn(a, w, -hi);
+    const double qt = __dadd_rn(__fma_rn(a, wq, FMAGIC), -FMAGIC);
+    return __dadd_rn(__fma_rn(-qt, q, hi), lo);
+}
+__device__ __forceinline__ double fred(double x, double qinv, double q) {
+    const double qt = __dadd_rn(__fma_rn(x, qinv, FMAGIC), -FMAGIC);
+    return __fma_rn(-qt, q, x);
+}
+// |x| < q  ->  [0, q) as u64 (bits of x + 2^52 carry x in the low mantissa)
+__device__ __forceinline__ u64 fcanon_small(double x, double q) {
+    const double y = x < 0.0 ? __dadd_rn(x, q) : x;
+    return (u64)__double_as_longlong(__dadd_rn(y, 4503599627370496.0)) & ((1ull << 52) - 1);
+}
+__device__ __forceinline__ u64 fcanon(double x, double qinv, double q) { return fcanon_small(fred(x, qinv, q), q); }
+// canonical u64 < 2^52 -> exact double
+__device__ __forceinline__ double fload(u64 v) {
+    return __dadd_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), -4503599627370496.0);
+}
+
+struct FQ {                     // per-prime FP64 constants
+    double q, qinv;
+};
+
+template <int LOGN, class PRO>
+__device__ __forceinline__ void dfwd_passA(double* x, const PRO& pro, double* const* peers, int rank,
+                                           const double2* __restrict__ W, FQ f, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = rank * (TL / C::CS) + tid + i * C::T;
+#pragma unroll
+        for (int k = 0; k < BS; k++) x[i * BS + k] = fload(pro(b + k * TL));
+#pragma unroll
+        for (int ls = 0; ls < R; ls++) {
+            const int h = BS >> (ls + 1);
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                if (k & h) continue;
+                const double2 w = W[(1 << ls) + (k >> (R - ls))];
+                double u = x[i * BS + k];
+                if (ls & 1) u = fred(u, f.qinv, f.q);
+                const double v = fmm(x[i * BS + k + h], w.x, w.y, f.q);
+                x[i * BS + k] = __dadd_rn(u, v);
+                x[i * BS + k + h] = __dadd_rn(u, -v);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = b + k * TL;
+            peers[k >> (R - C::LOGCS)][cswz(local_idx<LOGN>(j))] = x[i * BS + k];
+        }
+    }
+}
+
+template <int LOGN, int S0, bool LAST, class EPI>
+__device__ __forceinline__ void dfwd_pass(double* x, const EPI& epi, double* sm, int rank,
+                                          const double2* __restrict__ W, FQ f, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
+    const int b = rank * ((C::N >> R) / C::CS) + tid;
+    const int gi = b / TL;
+    const int base = gi * (C::N >> S0) + (b % TL);
+    const int lbase = base - rank * C::PART;
+#pragma unroll
+    for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+#pragma unroll
+    for (int ls = 0; ls < R; ls++) {
+        const int h = BS >> (ls + 1);
+        const int s = S0 + ls;
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            if (k & h) continue;
+            const double2 w = W[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const double u = (s & 1) ? fred(x[k], f.qinv, f.q) : x[k];
+            const double v = fmm(x[k + h], w.x, w.y, f.q);
+            x[k] = __dadd_rn(u, v);
+            x[k + h] = __dadd_rn(u, -v);
+        }
+    }
+    if constexpr (LAST) {
+        static_assert(TL == 1, "last pass is contiguous");
+#pragma unroll
+        for (int k = 0; k < BS; k += 2) {
+            ulonglong2 v;
+            v.x = epi(base + k, fcanon(x[k], f.qinv, f.q));
+            v.y = epi(base + k + 1, fcanon(x[k + 1], f.qinv, f.q));
+            *reinterpret_cast<ulonglong2*>(epi.out + base + k) = v;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < BS; k++) sm[cswz(lbase + k * TL)] = x[k];
+    }
+}
+
+template <int LOGN, int S0, class EPI>
+__device__ __forceinline__ void dfwd_rest(double* x, const EPI& epi, double* sm, int rank,
+                                          const double2* __restrict__ W, FQ f, int tid) {
+    using C = CCfg<LOGN>;
+    if constexpr (S0 < LOGN) {
+        if constexpr (S0 > C::R0) __syncthreads();
+        dfwd_pass<LOGN, S0, (S0 + C::LOGE >= LOGN), EPI>(x, epi, sm, rank, W, f, tid);
+        dfwd_rest<LOGN, S0 + C::LOGE, EPI>(x, epi, sm, rank, W, f, tid);
+    }
+}
+
+template <int LOGN, int S0, bool FIRST>
+__device__ __forceinline__ void dinv_pass(double* x, const u64* __restrict__ gin, double* sm, int rank,
+                                          const double2* __restrict__ Wi, FQ f, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::LOGE, BS = 1 << R, TL = C::N >> (S0 + R);
+    const int b = rank * ((C::N >> R) / C::CS) + tid;
+    const int gi = b / TL;
+    const int base = gi * (C::N >> S0) + (b % TL);
+    const int lbase = base - rank * C::PART;
+    if constexpr (FIRST) {
+        static_assert(TL == 1, "first inverse pass is contiguous");
+#pragma unroll
+        for (int k = 0; k < BS; k += 2) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + base + k);
+            x[k] = fload(v.x);
+            x[k + 1] = fload(v.y);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+    }
+#pragma unroll
+    for (int ls = R - 1; ls >= 0; ls--) {
+        const int h = BS >> (ls + 1);
+        const int s = S0 + ls;
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            if (k & h) continue;
+            const double2 w = Wi[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const double u = x[k], v = x[k + h];
+            x[k] = fred(__dadd_rn(u, v), f.qinv, f.q);
+            x[k + h] = fmm(__dadd_rn(u, -v), w.x, w.y, f.q);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < BS; k++) sm[cswz(lbase + k * TL)] = x[k];
+}
+
+template <int LOGN, int S0>
+__device__ __forceinline__ void dinv_rest(double* x, const u64* gin, double* sm, int rank,
+                                          const double2* __restrict__ Wi, FQ f, int tid) {
+    using C = CCfg<LOGN>;
+    if constexpr (S0 >= C::R0) {
+        dinv_pass<LOGN, S0, (S0 == LOGN - C::LOGE)>(x, gin, sm, rank, Wi, f, tid);
+        if constexpr (S0 - C::LOGE >= C::R0) __syncthreads();
+        dinv_rest<LOGN, S0 - C::LOGE>(x, gin, sm, rank, Wi, f, tid);
+    }
+}
+
+// last inverse stages; the final stage folds n^-1 (x scale) into its two multipliers
+template <int LOGN>
+__device__ __forceinline__ void dinv_passA(double* x, u64* __restrict__ g, double* const* peers, int rank,
+                                           const double2* __restrict__ Wi, FQ f, double2 nw, double2 ww, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = rank * (TL / C::CS) + tid + i * C::T;
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = b + k * TL;
+            x[i * BS + k] = peers[k >> (R - C::LOGCS)][cswz(local_idx<LOGN>(j))];
+        }
+#pragma unroll
+        for (int ls = R - 1; ls >= 0; ls--) {
+            const int h = BS >> (ls + 1);
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                if (k & h) continue;
+                const double u = x[i * BS + k], v = x[i * BS + k + h];
+                if (ls == 0) {
+                    x[i * BS + k] = fmm(__dadd_rn(u, v), nw.x, nw.y, f.q);
+                    x[i * BS + k + h] = fmm(__dadd_rn(u, -v), ww.x, ww.y, f.q);
+                } else {
+                    const double2 w = Wi[(1 << ls) + (k >> (R - ls))];
+                    x[i * BS + k] = fred(__dadd_rn(u, v), f.qinv, f.q);
+                    x[i * BS + k + h] = fmm(__dadd_rn(u, -v), w.x, w.y, f.q);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BS; k++) g[b + k * TL] = fcanon_small(x[i * BS + k], f.q);
+    }
+}
+
+__device__ __forceinline__ double2 fpair(u64 w, double q) {
+    const double wd = (double)w;
+    return make_double2(wd, __ddiv_rn(wd, q));
+}
+
 __device__ __forceinline__ bool cskip(const NttArgs& a, int t, int poly) {
     if (a.skip_alpha <= 0) return false;
     return t <= a.skip_level && t / a.skip_alpha == poly % a.skip_dnum;
@@ -303,8 +520,23 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
         epi.c = nullptr;
         epi.w = epi.wp = 0;
     }
-    u64 x[C::E];
     const int tid = threadIdx.x;
+    if (a.twf && q < (1ull << 50)) {         // FP64 butterflies (uniform per cluster: one limb)
+        double* dpeers[C::CS];
+#pragma unroll
+        for (int r = 0; r < C::CS; r++) dpeers[r] = reinterpret_cast<double*>(peers[r]);
+        const double2* Wf = a.twf + (size_t)pidx * 2 * C::N;
+        FQ f;
+        f.q = (double)q;
+        f.qinv = 1.0 / f.q;
+        double xf[C::E];
+        cluster.sync();
+        dfwd_passA<LOGN, Prologue<PM>>(xf, pro, dpeers, rank, Wf, f, tid);
+        cluster.sync();
+        dfwd_rest<LOGN, C::R0, Epilogue<EM>>(xf, epi, reinterpret_cast<double*>(sm), rank, Wf, f, tid);
+        return;
+    }
+    u64 x[C::E];
     cluster.sync();                          // peer SMEM is live before remote stores
     cfwd_passA<LOGN, Prologue<PM>>(x, pro, peers, rank, W, q, tid);
     cluster.sync();                          // all chunks delivered
@@ -416,8 +648,32 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     const ulonglong2* Wi = a.tw + (size_t)pidx * 2 * C::N + C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
     const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
-    u64 x[C::E];
     const int tid = threadIdx.x;
+    if (a.twf && q < (1ull << 50)) {         // FP64 butterflies
+        double* dpeers[C::CS];
+#pragma unroll
+        for (int r = 0; r < C::CS; r++) dpeers[r] = reinterpret_cast<double*>(peers[r]);
+        const double2* Wif = a.twf + (size_t)pidx * 2 * C::N + C::N;
+        FQ f;
+        f.q = (double)q;
+        f.qinv = 1.0 / f.q;
+        double xf[C::E];
+        dinv_rest<LOGN, LOGN - C::LOGE>(xf, gin, reinterpret_cast<double*>(sm), rank, Wif, f, tid);
+        cluster.sync();
+        double2 nw, ww;
+        if (a.inv_scale) {
+            const u64* sc = a.inv_scale + 4 * t;
+            nw = fpair(sc[0], f.q);
+            ww = fpair(sc[2], f.q);
+        } else {
+            nw = fpair(P.pad[0], f.q);
+            ww = Wif[0];
+        }
+        dinv_passA<LOGN>(xf, g, dpeers, rank, Wif, f, nw, ww, tid);
+        cluster.sync();
+        return;
+    }
+    u64 x[C::E];
     cinv_rest<LOGN, LOGN - C::LOGE>(x, gin, sm, rank, Wi, q, tid);
     cluster.sync();                          // both halves complete
     const ulonglong2 wn = Wi[0];

@@ -49,6 +49,40 @@ def test_ntt_matches_oracle(logn):
     np.testing.assert_array_equal(to_numpy_u64(t), x)
 
 
+@pytest.mark.parametrize("logn,bits", [(13, 50), (14, 50), (14, 49), (14, 45)])
+def test_ntt_fp64_path_edges(logn, bits, monkeypatch):
+    """Primes < 2^50 take the FP64 butterflies of the cluster NTT (q0 and the
+    60-bit special primes stay on the integer path): worst-case residues
+    (all q-1, alternating 0 / q-1, a single spike) and uniform ones, forward
+    and inverse, against the oracle; then the same data with BCN_NTT_FP64=0."""
+    N = 1 << logn
+    outs = []
+    for fp in ("1", "0"):
+        monkeypatch.setenv("BCN_NTT_FP64", fp)
+        eng, orc, hp = _pair(N, 4, bits, dnum=2, seed=3)
+        basis = list(hp.q) + list(hp.p)
+        assert any(q < (1 << 50) for q in basis)
+        rng = np.random.default_rng(bits)
+        qs = np.array(basis, dtype=np.uint64)[:, None]
+        alt = np.where(np.arange(N) % 2 == 0, 0, 1).astype(np.uint64)[None] * (qs - np.uint64(1))
+        spike = np.zeros((len(basis), N), np.uint64)
+        spike[:, N // 3] = (qs[:, 0] - np.uint64(1))
+        x = np.stack([np.broadcast_to(qs - np.uint64(1), (len(basis), N)), alt, spike,
+                      np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in basis])])
+        t = torch.from_numpy(x.view(np.int64).copy()).cuda()
+        eng.ntt(t, 0)
+        got = to_numpy_u64(t)
+        exp = np.stack([O.ntt(x[i], basis) for i in range(len(x))])
+        np.testing.assert_array_equal(got, exp)
+        eng.ntt(t, 0, inverse=True)
+        np.testing.assert_array_equal(to_numpy_u64(t), x)
+        y = torch.from_numpy(exp.view(np.int64).copy()).cuda()
+        eng.ntt(y, 0, inverse=True)
+        np.testing.assert_array_equal(to_numpy_u64(y), x)
+        outs.append(got)
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
 def test_secret_key_matches():
     eng, orc, hp = _pair(64, 4)
     np.testing.assert_array_equal(to_numpy_u64(eng.export_secret()), orc.keys.s_ntt)
