@@ -449,8 +449,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded cfg4 images, N(0,0.05) weights)",
-            "config": {"workload": "cifar3 bi-CryptoNet, BASELINE config 4: N=2^14, 15 limbs (q0 60b, 14x50b), "
-                                   "K=5 special 60b, dnum=3, Delta=2^50, BHW 32 images/slot set",
+            "config": {"workload": "cifar3 bi-CryptoNet, BASELINE config 4: N=2^14, 15 limbs (q0 + 14 rescale primes, "
+                                   "all 50b), K=5 special 50b, dnum=3, Delta=2^50, BHW 32 images/slot set",
                        "images_per_rank_per_step": args.images, "slot_sets_per_device_batch": args.chunk,
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "e2e": res["e2e"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],

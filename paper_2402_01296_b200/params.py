@@ -3,10 +3,15 @@
 The reference sizes the chain as max_level = required_levels(net) + 1
 (pkg/src/bibranch/catalog.py:286-346) and carries a single float `scale`
 (sim.py:111-121).  Here a level-l ciphertext has limbs q_0..q_l: q_0 is a
-`q0_bits` prime (decryption headroom), q_1..q_L are `scale_bits` primes (the
-rescale primes, so Mul_PC keeps the scale exactly and Mul_CC keeps it to
-~2^-30), and K = ceil((L+1)/dnum) `special_bits` primes extend the basis for
-hybrid key switching.  All primes are 1 mod 2N and < 2^61.
+`q0_bits` prime, q_1..q_L are `scale_bits` primes (the rescale primes, so
+Mul_PC keeps the scale exactly and Mul_CC keeps it to ~2^-30), and
+K = ceil((L+1)/dnum) `special_bits` primes extend the basis for hybrid key
+switching.  All primes are 1 mod 2N and < 2^61.  q_0 and the specials default
+to max(50, scale_bits) bits: a ciphertext never drops below level 1, so
+decryption always has q_0 q_1 (>= 2^99) of headroom, and P ~ each digit's
+modulus keeps the key-switch noise near 2^18 against Delta = 2^50.  At
+scale_bits <= 50 every prime is then below 2^50, which is what lets the
+cluster NTT run all limbs on the FP64 pipe (csrc/ntt_cluster.cu).
 """
 
 from __future__ import annotations
@@ -63,8 +68,8 @@ class HeParams:
     N: int
     max_level: int
     scale_bits: int
-    q0_bits: int = 60
-    special_bits: int = 60
+    q0_bits: int = 50
+    special_bits: int = 50
     dnum: int = 3
     n_special: int | None = None
     seed: int = 0
@@ -88,8 +93,11 @@ class HeParams:
         return float(2.0 ** self.scale_bits)
 
 
-def make_params(N: int, max_level: int, scale_bits: int = 50, *, q0_bits: int = 60, special_bits: int = 60,
-                dnum: int = 3, n_special: int | None = None, seed: int = 0) -> HeParams:
+def make_params(N: int, max_level: int, scale_bits: int = 50, *, q0_bits: int | None = None,
+                special_bits: int | None = None, dnum: int = 3, n_special: int | None = None,
+                seed: int = 0) -> HeParams:
+    q0_bits = max(50, scale_bits) if q0_bits is None else q0_bits
+    special_bits = max(50, scale_bits) if special_bits is None else special_bits
     alpha = -(-(max_level + 1) // dnum)
     K = alpha if n_special is None else n_special
     q0 = ntt_primes(q0_bits, 1, N)

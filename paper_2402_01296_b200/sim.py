@@ -306,7 +306,7 @@ class Ciphertext:
 
 def make_context(poly_degree: int, max_level: int, scale: float, scheme: str = "CKKS",
                  noise_model: bool = False, *, dnum: int | None = None, seed: int = 0,
-                 q0_bits: int = 60, special_bits: int = 60, device=None) -> HeContext:
+                 q0_bits: int | None = None, special_bits: int | None = None, device=None) -> HeContext:
     """Reference checks (sim.py:142-169) plus the RNS chain (params.py).
 
     Real CKKS noise replaces the optional fixed-point rounding model, so
