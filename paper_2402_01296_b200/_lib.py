@@ -18,7 +18,7 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbcn.so")
+LIB_PATH = os.environ.get("BCN_LIB") or os.path.join(HERE, "libbcn.so")   # BCN_LIB: experiments only
 
 BCN_OK, BCN_ERR_PARAM, BCN_ERR_DEPTH, BCN_ERR_USAGE, BCN_ERR_CUDA, BCN_ERR_CAPACITY = range(6)
 _ERRORS = {

@@ -483,13 +483,24 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
     CUDA_TRY(dmalloc((void**)&c->tw, sizeof(ulonglong2) * tw.size(), &c->table_bytes));
     CUDA_TRY(cudaMemcpy(c->tw, tw.data(), sizeof(ulonglong2) * tw.size(), cudaMemcpyHostToDevice));
     {   // FP64 companions: {w, w/q} (correctly rounded division of exact doubles; only primes < 2^50 use them)
+        // layout: pass-transposed for the cluster NTT's radix-16 passes (ntt_cluster.cu):
+        // entry 2^s + (gi << ls) + j of stage s = S0 + ls lives at 2^s + j 2^S0 + gi
         std::vector<double2> twf(tw.size());
+        const int R0 = (logn % 4) ? (logn % 4) : 4;
+        auto pos = [&](u64 k) -> u64 {
+            if (k == 0 || (logn != 13 && logn != 14)) return k;
+            int s = 63 - __builtin_clzll(k);
+            const int S0 = s < R0 ? 0 : R0 + 4 * ((s - R0) / 4), ls = s - S0;
+            const u64 r = k - (1ull << s), gi = r >> ls, j = r & ((1ull << ls) - 1);
+            return (1ull << s) + (j << S0) + gi;
+        };
         for (int i = 0; i < nb; i++) {
             const double qd = (double)c->primes[i];
-            for (size_t k = 0; k < (size_t)2 * N; k++) {
-                const double w = (double)tw[(size_t)i * 2 * N + k].x;
-                twf[(size_t)i * 2 * N + k] = make_double2(w, w / qd);
-            }
+            for (int half = 0; half < 2; half++)
+                for (u64 k = 0; k < (u64)N; k++) {
+                    const double w = (double)tw[(size_t)i * 2 * N + (size_t)half * N + k].x;
+                    twf[(size_t)i * 2 * N + (size_t)half * N + pos(k)] = make_double2(w, w / qd);
+                }
         }
         CUDA_TRY(dmalloc((void**)&c->twf, sizeof(double2) * twf.size(), &c->table_bytes));
         CUDA_TRY(cudaMemcpy(c->twf, twf.data(), sizeof(double2) * twf.size(), cudaMemcpyHostToDevice));

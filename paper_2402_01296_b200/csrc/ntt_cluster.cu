@@ -222,6 +222,11 @@ __device__ __forceinline__ void cfwd_rest(u64* x, const EPI& epi, u64* sm, int r
 }
 
 // ------------------------------------------------- FP64 butterflies (q < 2^50)
+// Twiddle table twf: {w, w/q} per entry, and within each stage s of a
+// radix-16 pass starting at stage S0 the entries are transposed so that the
+// threads of a warp (consecutive block index gi) read consecutive entries:
+// twf[2^s + j 2^S0 + gi] = W[2^s + (gi << (s - S0)) + j]  (api.cu builds it;
+// one 512-B run per warp-wide load instead of 2^(s-S0) strided lines).
 // For primes below 2^50 the butterflies run on the FP64 pipe instead of the
 // 64-bit integer multiplies on the IMAD pipe (tools/micro/bfly_bench.cu:
 // 6.3 vs 3.1 butterflies/clk/SM on this B200).  Residues are exact integers
@@ -315,7 +320,7 @@ __device__ __forceinline__ void dfwd_pass(double* x, const EPI& epi, double* sm,
 #pragma unroll
         for (int k = 0; k < BS; k++) {
             if (k & h) continue;
-            const double2 w = W[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const double2 w = W[(1 << s) + ((k >> (R - ls)) << S0) + gi];   // pass-transposed table
             const double u = (s & 1) ? fred(x[k], f.qinv, f.q) : x[k];
             const double v = fmm(x[k + h], w.x, w.y, f.q);
             x[k] = __dadd_rn(u, v);
@@ -323,13 +328,22 @@ __device__ __forceinline__ void dfwd_pass(double* x, const EPI& epi, double* sm,
         }
     }
     if constexpr (LAST) {
+        // each thread holds 16 consecutive words: exchange through SMEM so that
+        // the epilogue's reads and the HBM stores are warp-coalesced (a direct
+        // store would touch 32 lines per instruction)
         static_assert(TL == 1, "last pass is contiguous");
+        u64* su = reinterpret_cast<u64*>(sm);
 #pragma unroll
-        for (int k = 0; k < BS; k += 2) {
+        for (int k = 0; k < BS; k++) su[cswz(lbase + k)] = fcanon(x[k], f.qinv, f.q);
+        __syncthreads();
+        const int j0 = rank * C::PART;
+#pragma unroll
+        for (int m = 0; m < C::PART / (2 * C::T); m++) {
+            const int e = 2 * tid + m * 2 * C::T;
             ulonglong2 v;
-            v.x = epi(base + k, fcanon(x[k], f.qinv, f.q));
-            v.y = epi(base + k + 1, fcanon(x[k + 1], f.qinv, f.q));
-            *reinterpret_cast<ulonglong2*>(epi.out + base + k) = v;
+            v.x = epi(j0 + e, su[cswz(e)]);
+            v.y = epi(j0 + e + 1, su[cswz(e + 1)]);
+            *reinterpret_cast<ulonglong2*>(epi.out + j0 + e) = v;
         }
     } else {
 #pragma unroll
@@ -358,17 +372,20 @@ __device__ __forceinline__ void dinv_pass(double* x, const u64* __restrict__ gin
     const int base = gi * (C::N >> S0) + (b % TL);
     const int lbase = base - rank * C::PART;
     if constexpr (FIRST) {
+        // coalesced HBM reads into SMEM, then the per-thread contiguous runs from SMEM
         static_assert(TL == 1, "first inverse pass is contiguous");
+        const int j0 = rank * C::PART;
 #pragma unroll
-        for (int k = 0; k < BS; k += 2) {
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + base + k);
-            x[k] = fload(v.x);
-            x[k + 1] = fload(v.y);
+        for (int m = 0; m < C::PART / (2 * C::T); m++) {
+            const int e = 2 * tid + m * 2 * C::T;
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + j0 + e);
+            sm[cswz(e)] = fload(v.x);
+            sm[cswz(e + 1)] = fload(v.y);
         }
-    } else {
-#pragma unroll
-        for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+        __syncthreads();
     }
+#pragma unroll
+    for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
 #pragma unroll
     for (int ls = R - 1; ls >= 0; ls--) {
         const int h = BS >> (ls + 1);
@@ -376,7 +393,7 @@ __device__ __forceinline__ void dinv_pass(double* x, const u64* __restrict__ gin
 #pragma unroll
         for (int k = 0; k < BS; k++) {
             if (k & h) continue;
-            const double2 w = Wi[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const double2 w = Wi[(1 << s) + ((k >> (R - ls)) << S0) + gi];  // pass-transposed table
             const double u = x[k], v = x[k + h];
             x[k] = fred(__dadd_rn(u, v), f.qinv, f.q);
             x[k + h] = fmm(__dadd_rn(u, -v), w.x, w.y, f.q);
