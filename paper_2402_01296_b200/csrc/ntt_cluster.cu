@@ -196,13 +196,18 @@ __device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int r
         }
     }
     if constexpr (LAST) {
-        static_assert(TL == 1, "last pass is contiguous");
+        static_assert(TL == 1, "last pass is contiguous");   // coalesced stores via SMEM (see dfwd_pass)
 #pragma unroll
-        for (int k = 0; k < BS; k += 2) {
+        for (int k = 0; k < BS; k++) sm[cswz(lbase + k)] = fwd_final(x[k], q);
+        __syncthreads();
+        const int j0 = rank * C::PART;
+#pragma unroll
+        for (int m = 0; m < C::PART / (2 * C::T); m++) {
+            const int e = 2 * tid + m * 2 * C::T;
             ulonglong2 v;
-            v.x = epi(base + k, fwd_final(x[k], q));
-            v.y = epi(base + k + 1, fwd_final(x[k + 1], q));
-            *reinterpret_cast<ulonglong2*>(epi.out + base + k) = v;
+            v.x = epi(j0 + e, sm[cswz(e)]);
+            v.y = epi(j0 + e + 1, sm[cswz(e + 1)]);
+            *reinterpret_cast<ulonglong2*>(epi.out + j0 + e) = v;
         }
     } else {
 #pragma unroll
@@ -572,17 +577,19 @@ __device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ gin, u
     const int base = gi * (C::N >> S0) + (b % TL);
     const int lbase = base - rank * C::PART;
     if constexpr (FIRST) {
-        static_assert(TL == 1, "first inverse pass is contiguous");
+        static_assert(TL == 1, "first inverse pass is contiguous");   // coalesced loads via SMEM
+        const int j0 = rank * C::PART;
 #pragma unroll
-        for (int k = 0; k < BS; k += 2) {
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + base + k);
-            x[k] = v.x;
-            x[k + 1] = v.y;
+        for (int m = 0; m < C::PART / (2 * C::T); m++) {
+            const int e = 2 * tid + m * 2 * C::T;
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + j0 + e);
+            sm[cswz(e)] = v.x;
+            sm[cswz(e + 1)] = v.y;
         }
-    } else {
-#pragma unroll
-        for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+        __syncthreads();
     }
+#pragma unroll
+    for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
 #pragma unroll
     for (int ls = R - 1; ls >= 0; ls--) {
         const int h = BS >> (ls + 1);
