@@ -275,9 +275,11 @@ struct FQ {                     // per-prime FP64 constants
     double q, qinv;
 };
 
+// pass A: the loads (issued before the cluster barrier that guards the
+// scatter, so their HBM latency overlaps the barrier wait), then the
+// butterflies on registers and the scatter to the owners' SMEM
 template <int LOGN, class PRO>
-__device__ __forceinline__ void dfwd_passA(double* x, const PRO& pro, double* const* peers, int rank,
-                                           const double2* __restrict__ W, FQ f, int tid) {
+__device__ __forceinline__ void dfwd_passA_load(double* x, const PRO& pro, int rank, int tid) {
     using C = CCfg<LOGN>;
     constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
 #pragma unroll
@@ -285,6 +287,17 @@ __device__ __forceinline__ void dfwd_passA(double* x, const PRO& pro, double* co
         const int b = rank * (TL / C::CS) + tid + i * C::T;
 #pragma unroll
         for (int k = 0; k < BS; k++) x[i * BS + k] = fload(pro(b + k * TL));
+    }
+}
+
+template <int LOGN>
+__device__ __forceinline__ void dfwd_passA_core(double* x, double* const* peers, int rank,
+                                                const double2* __restrict__ W, FQ f, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = rank * (TL / C::CS) + tid + i * C::T;
 #pragma unroll
         for (int ls = 0; ls < R; ls++) {
             const int h = BS >> (ls + 1);
@@ -552,9 +565,10 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
         f.q = (double)q;
         f.qinv = 1.0 / f.q;
         double xf[C::E];
-        cluster.sync();
-        dfwd_passA<LOGN, Prologue<PM>>(xf, pro, dpeers, rank, Wf, f, tid);
-        cluster.sync();
+        dfwd_passA_load<LOGN, Prologue<PM>>(xf, pro, rank, tid);
+        cluster.sync();                      // peer SMEM is live before remote stores
+        dfwd_passA_core<LOGN>(xf, dpeers, rank, Wf, f, tid);
+        cluster.sync();                      // all chunks delivered
         dfwd_rest<LOGN, C::R0, Epilogue<EM>>(xf, epi, reinterpret_cast<double*>(sm), rank, Wf, f, tid);
         return;
     }
