@@ -88,6 +88,8 @@ struct bcn_ctx {
     PrimeInfo* pr = nullptr;
     ulonglong2* tw = nullptr;
     double2* twf = nullptr;       // FP64 twiddles {w, w/q} (same layout as tw)
+    double2* fq = nullptr;        // per prime {q, 1/q} (FP64 base conversions)
+    bool fp_conv = false;         // every basis prime in (2^49, 2^50): base conversions on the FP64 pipe
     bool fp_ntt = true;           // BCN_NTT_FP64=0: integer butterflies for every prime
     double* ksi_re = nullptr;
     double* ksi_im = nullptr;
@@ -257,6 +259,7 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
                 u64 pm = 1;
                 for (int k = i0; k < i1; k++) if (k != i) pm = mulmod_h(pm, c->primes[k] % qt, qt);
                 t.hat_m[(i - i0) * BCN_MAX_LIMBS + e] = mont_h(pm, qt);
+                t.hat_d[(i - i0) * BCN_MAX_LIMBS + e] = make_double2((double)pm, (double)pm / (double)qt);
             }
         }
     }
@@ -275,6 +278,7 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
             u64 pm = 1;
             for (int k2 = 0; k2 < c->K; k2++) if (k2 != k) pm = mulmod_h(pm, c->primes[c->nq + k2] % qi, qi);
             down.hat_m[k * BCN_MAX_LIMBS + i] = mont_h(pm, qi);
+            down.hat_d[k * BCN_MAX_LIMBS + i] = make_double2((double)pm, (double)pm / (double)qi);
         }
     }
     std::vector<u64> pinv(2 * (level + 1)), qlinv(2 * std::max(level, 1));
@@ -323,6 +327,7 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
                 u64 pm = 1;
                 for (int b = 0; b < ns; b++) if (b != a) pm = mulmod_h(pm, c->primes[sp[b]] % qi, qi);
                 m.hat_m[a * BCN_MAX_LIMBS + i] = mont_h(pm, qi);
+                m.hat_d[a * BCN_MAX_LIMBS + i] = make_double2((double)pm, (double)pm / (double)qi);
             }
             const u64 x = mulmod_h(c->hpr[sp[a]].pad[0], hinv, sa), y = mulmod_h(c->wn_host[sp[a]], hinv, sa);
             msc[4 * a] = x; msc[4 * a + 1] = shoup_h(x, sa);
@@ -505,6 +510,15 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
         CUDA_TRY(dmalloc((void**)&c->twf, sizeof(double2) * twf.size(), &c->table_bytes));
         CUDA_TRY(cudaMemcpy(c->twf, twf.data(), sizeof(double2) * twf.size(), cudaMemcpyHostToDevice));
         c->fp_ntt = !getenv_flag_off("BCN_NTT_FP64");
+        std::vector<double2> fq(nb);
+        bool band = true;
+        for (int i = 0; i < nb; i++) {
+            fq[i] = make_double2((double)c->primes[i], 1.0 / (double)c->primes[i]);
+            band &= c->primes[i] > (1ull << 49) && c->primes[i] < (1ull << 50);
+        }
+        CUDA_TRY(dmalloc((void**)&c->fq, sizeof(double2) * nb, &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(c->fq, fq.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice));
+        c->fp_conv = band && !getenv_flag_off("BCN_CONV_FP64");
     }
     // canonical-embedding tables: ksi[k] = exp(2 pi i k / M) as computed by numpy on the host
     // are uploaded by the Python layer through bcn_ctx_set_fft (see below); rot[j] = 5^j mod M here.
@@ -579,7 +593,7 @@ int bcn_ctx_destroy(bcn_ctx* c) {
         cudaFree(kv.second.mdr); cudaFree(kv.second.mdr_scale); cudaFree(kv.second.pqinv);
     }
     for (auto& kv : c->keys) cudaFree(kv.second);
-    cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->twf); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
+    cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->twf); cudaFree(c->fq); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
     cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod); cudaFree(c->md_scale);
     if (c->scratch) cudaFree(c->scratch);
     if (c->ptr_dev) cudaFree(c->ptr_dev);
@@ -1247,7 +1261,8 @@ static int modup_impl(bcn_ctx* c, u64* U, const u64* x, long long x_stride, int 
     }
     // coefficient-domain copy of x
     CUDA_TRY(ntt_run_src(c, true, tmp, nl * N, x, x_stride, N, ql, G, st));     // coefficient form of x
-    CUDA_TRY(modup_op(U, tmp, nl * N, x, x_stride, G, nl, next, c->alpha, ndig, c->logn, ext, c->pr, T->modup, st));
+    CUDA_TRY(modup_op(U, tmp, nl * N, x, x_stride, G, nl, next, c->alpha, ndig, c->logn, ext, c->pr, T->modup, st,
+                      c->fp_conv ? c->fq : nullptr));
     NttArgs a = ntt_args(c, U, (long long)next * N, ext);
     a.skip_alpha = c->alpha;
     a.skip_dnum = ndig;
@@ -1294,7 +1309,7 @@ static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int l
             // a plain-prologue NTT with the fused combine: the prologue form re-reads the
             // sources for every output limb and stalls on their latency
             CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown,
-                                     st));
+                                     st, c->fp_conv ? c->fq : nullptr));
             a.src = Z;
             a.src_poly_stride = (long long)nl * N;
             a.src_limb_stride = N;
@@ -1318,7 +1333,7 @@ static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int l
         return BCN_OK;
     }
     CUDA_TRY(ntt_run(c, true, A + (size_t)nl * N, (long long)next * N, pl, 2 * G, st));
-    CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st));
+    CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st, c->fp_conv ? c->fq : nullptr));
     CUDA_TRY(ntt_run(c, false, Z, (long long)nl * N, ql, 2 * G, st));
     CUDA_TRY(moddown_combine_op(out, os, A, next, Z, addend, as, add_c1, g, G, nl, c->logn, ql, c->pr, T->pinv, st));
     return BCN_OK;
@@ -1447,7 +1462,7 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
         NttArgs a = ntt_args(c, out, (long long)level * N, ql);
         if (split) {   // conversion once per coefficient, then plain-prologue NTT + fused combine
             Limbs ext = limbs_ext(c, level);
-            CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st));
+            CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st, c->fp_conv ? c->fq : nullptr));
             a.src = Z;
             a.src_poly_stride = (long long)level * N;
             a.src_limb_stride = N;
@@ -1473,7 +1488,7 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
     }
     CUDA_TRY(ntt_run(c, true, B + (size_t)level * N, (long long)next * N, sl, 2 * G, st));
     Limbs ext = limbs_ext(c, level);
-    CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st));
+    CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st, c->fp_conv ? c->fq : nullptr));
     CUDA_TRY(ntt_run(c, false, Z, (long long)level * N, ql, 2 * G, st));
     CUDA_TRY(mdr_combine_op(out, B, (long long)next * N, Z, C, c_gstride, add_c1, 2 * G, level, c->logn, ql, c->pr,
                             T->pqinv, T->qlinv, st));

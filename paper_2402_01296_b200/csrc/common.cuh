@@ -190,6 +190,50 @@ struct Acc4 {
     }
 };
 
+// ---- FP64 modular arithmetic for primes q < 2^50 ----
+// Residues are exact integers held in doubles.  fmm(a, w, w/q): a*w mod q
+// with |result| <= 0.61 q for |a| < 2q (the quotient a*w/q must stay below
+// 2^51 for the add-1.5*2^52 rounding); fred(x): x mod q into [-q/2, q/2]
+// (+2^-50 q) for any exact |x| < 2^53.
+static constexpr double FMAGIC = 6755399441055744.0;   // 1.5 * 2^52
+
+__device__ __forceinline__ double fmm(double a, double w, double wq, double q) {
+    const double hi = __dmul_rn(a, w);
+    const double lo = __fma_rn(a, w, -hi);
+    const double qt = __dadd_rn(__fma_rn(a, wq, FMAGIC), -FMAGIC);
+    return __dadd_rn(__fma_rn(-qt, q, hi), lo);
+}
+__device__ __forceinline__ double fred(double x, double qinv, double q) {
+    const double qt = __dadd_rn(__fma_rn(x, qinv, FMAGIC), -FMAGIC);
+    return __fma_rn(-qt, q, x);
+}
+// |x| < q  ->  [0, q) as u64 (bits of x + 2^52 carry x in the low mantissa)
+__device__ __forceinline__ u64 fcanon_small(double x, double q) {
+    const double y = x < 0.0 ? __dadd_rn(x, q) : x;
+    return (u64)__double_as_longlong(__dadd_rn(y, 4503599627370496.0)) & ((1ull << 52) - 1);
+}
+__device__ __forceinline__ u64 fcanon(double x, double qinv, double q) { return fcanon_small(fred(x, qinv, q), q); }
+// canonical u64 < 2^52 -> exact double
+__device__ __forceinline__ double fload(u64 v) {
+    return __dadd_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), -4503599627370496.0);
+}
+
+// sum_k y[k] * h[k] mod t, canonical, for canonical y[k] < 2t held as exact
+// doubles and constant pairs h[k] = {h, h/t} (h < t < 2^50); nk <= 12 keeps
+// the unreduced sum below 8t <= 2^53
+template <int YK>
+__device__ __forceinline__ u64 fdot_canon(const double* y, const double2* __restrict__ h, int hstride, int nk,
+                                          double t, double tinv) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < YK; k++)
+        if (k < nk) {
+            const double2 hk = h[k * hstride];
+            acc = __dadd_rn(acc, fmm(y[k], hk.x, hk.y, t));
+        }
+    return fcanon(acc, tinv, t);
+}
+
 // ---- bulk async copies (TMA engine, 1-D) completing on an mbarrier ----
 __device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* bar, u32 count) {

@@ -248,29 +248,6 @@ __device__ __forceinline__ void cfwd_rest(u64* x, const EPI& epi, u64* sm, int r
 // sum is reduced every stage, every value stays <= 0.61 q.  Outputs are
 // canonicalised (fred, +q if negative) -- the same canonical residues as the
 // integer path, so the two are interchangeable bit for bit.
-static constexpr double FMAGIC = 6755399441055744.0;   // 1.5 * 2^52
-
-__device__ __forceinline__ double fmm(double a, double w, double wq, double q) {
-    const double hi = __dmul_rn(a, w);
-    const double lo = __fma_rn(a, w, -hi);
-    const double qt = __dadd_rn(__fma_rn(a, wq, FMAGIC), -FMAGIC);
-    return __dadd_rn(__fma_rn(-qt, q, hi), lo);
-}
-__device__ __forceinline__ double fred(double x, double qinv, double q) {
-    const double qt = __dadd_rn(__fma_rn(x, qinv, FMAGIC), -FMAGIC);
-    return __fma_rn(-qt, q, x);
-}
-// |x| < q  ->  [0, q) as u64 (bits of x + 2^52 carry x in the low mantissa)
-__device__ __forceinline__ u64 fcanon_small(double x, double q) {
-    const double y = x < 0.0 ? __dadd_rn(x, q) : x;
-    return (u64)__double_as_longlong(__dadd_rn(y, 4503599627370496.0)) & ((1ull << 52) - 1);
-}
-__device__ __forceinline__ u64 fcanon(double x, double qinv, double q) { return fcanon_small(fred(x, qinv, q), q); }
-// canonical u64 < 2^52 -> exact double
-__device__ __forceinline__ double fload(u64 v) {
-    return __dadd_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), -4503599627370496.0);
-}
-
 struct FQ {                     // per-prime FP64 constants
     double q, qinv;
 };

@@ -13,6 +13,7 @@ struct ConvTable {
     u64 hatinv[BCN_MAX_ALPHA];
     u64 hatinv_p[BCN_MAX_ALPHA];
     u64 hat_m[BCN_MAX_ALPHA * BCN_MAX_LIMBS];
+    double2 hat_d[BCN_MAX_ALPHA * BCN_MAX_LIMBS];   // {hat, hat / target prime} for the FP64 conversions
 };
 
 namespace bcn {
@@ -173,12 +174,13 @@ cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, in
                          u32 g, cudaStream_t st);
 cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, long long x_stride, int npoly, int nq,
                      int next, int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr,
-                     const ConvTable* tab, cudaStream_t st);
+                     const ConvTable* tab, cudaStream_t st, const double2* fq = nullptr);
 cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
                      long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
                      const PrimeInfo* pr, cudaStream_t st);
 cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
-                            const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st);
+                            const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st,
+                            const double2* fq = nullptr);
 cudaError_t moddown_combine_op(u64* out, long long os, const u64* A, int next, const u64* Z, const u64* addend,
                                long long as, int add_c1, u32 g, int npoly, int nq, int logn, const Limbs& ql,
                                const PrimeInfo* pr, const u64* pinv, cudaStream_t st);

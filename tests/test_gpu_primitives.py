@@ -51,8 +51,8 @@ def test_ntt_matches_oracle(logn):
 
 @pytest.mark.parametrize("logn,bits", [(13, 50), (14, 50), (14, 49), (14, 45)])
 def test_ntt_fp64_path_edges(logn, bits, monkeypatch):
-    """Primes < 2^50 take the FP64 butterflies of the cluster NTT (q0 and the
-    60-bit special primes stay on the integer path): worst-case residues
+    """Primes < 2^50 take the FP64 butterflies of the cluster NTT (primes of
+    2^50 and above stay on the integer path): worst-case residues
     (all q-1, alternating 0 / q-1, a single spike) and uniform ones, forward
     and inverse, against the oracle; then the same data with BCN_NTT_FP64=0."""
     N = 1 << logn
@@ -439,3 +439,32 @@ def test_conv_ks_mac_tcgen05_bitexact_vs_imma(n_out, rots):
     ref = eng.conv_ks_mac(*args, eng.pack_planes_ext(pts, L, 0), n_out, L, 0)
     got = eng.conv_ks_mac(*args, eng.pack_planes_ext(pts, L, 1), n_out, L, 1)
     assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("N,L,dnum", [(2048, 5, 3), (8192, 6, 2), (16384, 8, 3)])
+def test_fp64_base_conversions_match_oracle(N, L, dnum, monkeypatch):
+    """All primes in (2^49, 2^50) (the default 50-bit chains): ModUp, ModDown
+    and the merged ModDown+rescale base conversions run on the FP64 pipe.
+    Rotation, square+relinearise and the merged rotation sum against the
+    oracle, and against the integer conversions (BCN_CONV_FP64=0)."""
+    from paper_2402_01296_b200.params import galois_element as ge
+    outs = []
+    for fp in ("1", "0"):
+        monkeypatch.setenv("BCN_CONV_FP64", fp)
+        eng, orc, hp = _pair(N, L, 50, dnum=dnum, seed=5)
+        assert all((1 << 49) < q < (1 << 50) for q in list(hp.q) + list(hp.p))
+        rng = np.random.default_rng(17)
+        v, ct, oc = _enc2(eng, orc, N, rng)
+        rot = eng.rotate(ct, 3, L)
+        _assert_ct(rot, [orc.rotate(oc[i], 3) for i in range(2)])
+        eng.keygen_relin()
+        sq = eng.mul_cc(ct, ct, L)
+        _assert_ct(sq, [orc.mul_cc(oc[i], oc[i]) for i in range(2)])
+        p1 = rng.standard_normal(N // 2)
+        ql = float(hp.q[L])
+        U = eng.modup(ct, L)
+        rs = eng.rotsum_rescale([(ct, U, ge(1, N), eng.encode_ext(p1, L, ql)), (ct, U, ge(7, N), None)], L)
+        _assert_ct(rs, [orc.rotsum_rescale([(oc[i], 1, p1), (oc[i], 7, None)], [], L) for i in range(2)])
+        outs.append([to_numpy_u64(x) for x in (rot, sq, rs)])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
