@@ -1028,7 +1028,8 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
         for (int t0 = 0; t0 < next; t0 += tcnt) {
             const int tc = std::min(tcnt, next - t0);
             CUDA_TRY(slot_major_ks_op(S, KT, g0, gcnt, t0, tc, nl, next, T->ndig, c->logn, spitch,
-                                      2LL * c->nbasis * N, (long long)c->nbasis * N, ext, c->pr, c->pmod, st));
+                                      2LL * c->nbasis * N, (long long)c->nbasis * N, ext, c->pr, c->pmod, st,
+                                      c->fp_conv ? c->fq : nullptr));
             if (tc05)
                 CUDA_TRY(mac_umma_op(acc, cw, n_out, n_terms, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad,
                                      next, c->logn, ext, c->pr, 0, st));

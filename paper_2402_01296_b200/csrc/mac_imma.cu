@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                                                             int t0, int nq, int next, int ndig, int logn,
                                                             int spitch, long long kds, long long kcs, Limbs ext,
                                                             const PrimeInfo* __restrict__ pr,
-                                                            const u64* __restrict__ pmod) {
+                                                            const u64* __restrict__ pmod,
+                                                            const double2* __restrict__ fq) {
     __shared__ u64 tile[128][33];
     const int N = 1 << logn;
     const int n0 = blockIdx.x * 32, tl = blockIdx.y, k = blockIdx.z;
@@ -142,6 +143,40 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
         const int nd = ND > 0 ? ND : ndig;
         const long long dstr = (long long)next * N;
         const u64* Ub = T.U[k] + (long long)t * N + sn;
+        if constexpr (ND > 0) {
+            if (fq) {
+                // component 0 on the FP64 pipe, component 1 on the IMAD pipe: the two
+                // inner products of one set of U words run on different units.  The
+                // key words are Montgomery (k 2^64): REDC once per thread to k, then
+                // {k, k/q} as doubles (companion from fl(1/q): |a w/q - qt| <= 0.75).
+                const double2 f = fq[kt];
+                double kd[ND], kq[ND];
+#pragma unroll
+                for (int j = 0; j < ND; j++) {
+                    kd[j] = fload(redc(0ull, k0[j], q, P.qinv_neg));
+                    kq[j] = __dmul_rn(kd[j], f.y);
+                }
+#pragma unroll 2
+                for (int gi = w0; gi < gcnt; gi += nw) {
+                    const int gs = g0 + gi;
+                    const u64* Up = Ub + (long long)gs * nd * dstr;
+                    Acc4 a1;
+                    a1.zero();
+                    double acc = 0.0;
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const u64 u = __ldg(Up + j * dstr);
+                        acc = __dadd_rn(acc, fmm(fload(u), kd[j], kq[j], f.x));
+                        a1.mac(u, k1[j]);
+                    }
+                    u64 v0 = fcanon(acc, f.y, f.x);
+                    if (qlimb) v0 = add_mod(v0, shoup(__ldg(src + (long long)gs * 2 * LNs + sn), pw, pwp, q), q);
+                    tile[2 * gi][nn] = v0;
+                    tile[2 * gi + 1][nn] = a1.reduce(q, P.qinv_neg, P.pad[2]);
+                }
+                goto staged;
+            }
+        }
 #pragma unroll 2
         for (int gi = w0; gi < gcnt; gi += nw) {
             const int gs = g0 + gi;
@@ -169,6 +204,7 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
             tile[2 * gi + 1][nn] = a1.reduce(q, P.qinv_neg, P.pad[2]);
         }
     }
+staged:
     __syncthreads();
     u64* dst = S + (((long long)tl * N + n0) * T.n + k) * spitch;
     for (int r = w0; r < 32; r += nw)                      // row r: this slot's run of ncol words
@@ -177,18 +213,19 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
 
 cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,
                              int logn, int spitch, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
-                             const u64* pmod, cudaStream_t st) {
+                             const u64* pmod, cudaStream_t st, const double2* fq) {
     if (2 * gcnt > spitch || spitch > 128) return cudaErrorInvalidValue;
+    if (ndig > 12) fq = nullptr;
     const int N = 1 << logn;
     dim3 grid(N / 32, tcnt, T.n);
     switch (ndig) {
 #define BCN_SMK(D) case D: slot_major_ks_kernel<D><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, \
-                                                   spitch, kds, kcs, ext, pr, pmod); break;
+                                                   spitch, kds, kcs, ext, pr, pmod, fq); break;
         BCN_SMK(1) BCN_SMK(2) BCN_SMK(3) BCN_SMK(4)
 #undef BCN_SMK
         default:
             slot_major_ks_kernel<0><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, spitch, kds, kcs, ext, pr,
-                                                          pmod);
+                                                          pmod, fq);
     }
     return launched();
 }

@@ -348,15 +348,17 @@ def test_rotsum_rescale_merged_matches_oracle(N, L):
     assert np.abs(dec - exp).max() < 1e-4
 
 
+@pytest.mark.parametrize("bits", [40, 50], ids=["int-staging", "fp64-staging"])
 @pytest.mark.parametrize("layout", [0, 1], ids=["imma", "tcgen05"])
 @pytest.mark.parametrize("N,L", [(1024, 3), (8192, 3)])
-def test_conv_ks_mac_matches_oracle(N, L, layout):
+def test_conv_ks_mac_matches_oracle(N, L, layout, bits):
     """Conv layer with lazy ModDown (bcn_conv_ks_mac: key-switch inner products
     fused into the slot-major staging, tensor-core MAC over the extended
     basis, one merged ModDown+rescale per output) == Oracle.rotsum_rescale of
     each output bit for bit (identity taps enter as P*x, rotations as
-    inner product + P*sigma(c0))."""
-    eng, orc, hp = _pair(N, L, dnum=2)
+    inner product + P*sigma(c0)).  At 50 bits every prime is in (2^49, 2^50)
+    and the staging's component-0 inner products run on the FP64 pipe."""
+    eng, orc, hp = _pair(N, L, bits, dnum=2)
     rng = np.random.default_rng(37)
     v, ct, oc = _enc2(eng, orc, N, rng)
     w, ct2, oc2 = _enc2(eng, orc, N, rng, counter=51)
