@@ -174,11 +174,10 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                     tile[2 * gi][nn] = v0;
                     tile[2 * gi + 1][nn] = a1.reduce(q, P.qinv_neg, P.pad[2]);
                 }
-                goto staged;
             }
         }
 #pragma unroll 2
-        for (int gi = w0; gi < gcnt; gi += nw) {
+        for (int gi = w0; gi < gcnt && !(ND > 0 && fq); gi += nw) {
             const int gs = g0 + gi;
             const u64* Up = Ub + (long long)gs * nd * dstr;
             Acc4 a0, a1;
@@ -204,7 +203,6 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
             tile[2 * gi + 1][nn] = a1.reduce(q, P.qinv_neg, P.pad[2]);
         }
     }
-staged:
     __syncthreads();
     u64* dst = S + (((long long)tl * N + n0) * T.n + k) * spitch;
     for (int r = w0; r < 32; r += nw)                      // row r: this slot's run of ncol words

@@ -20,13 +20,11 @@ template <int OP>
 __global__ void binary_kernel(u64* __restrict__ out, long long os, const u64* __restrict__ a, long long as,
                               const u64* __restrict__ b, long long bs, int nlimb, int logn, Limbs limbs,
                               const PrimeInfo* __restrict__ pr, long long total) {
+    // grid (N / blockDim, limb, poly): no per-element division
     const int N = 1 << logn;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int n = (int)(idx & (N - 1));
-        const long long rest = idx >> logn;
-        const int t = (int)(rest % nlimb);
-        const long long p = rest / nlimb;
+    const int n = blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
+    const long long p = blockIdx.z;
+    if (n < N) {
         const PrimeInfo& P = pr[limbs.prime[t]];
         const u64 x = a[p * as + (long long)t * N + n];
         const u64 y = b[p * bs + (long long)t * N + n];
@@ -36,13 +34,17 @@ __global__ void binary_kernel(u64* __restrict__ out, long long os, const u64* __
         else r = mont_mul(x, y, P.q, P.qinv_neg);   // y in Montgomery form
         out[p * os + (long long)t * N + n] = r;
     }
+    (void)nlimb;
+    (void)total;
 }
 
 cudaError_t binary_op(int op, u64* out, long long os, const u64* a, long long as, const u64* b, long long bs,
                       int npoly, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st) {
     long long total = (long long)npoly * nlimb << logn;
     if (total == 0) return cudaSuccess;
-    int tpb = 256, nb = blocks_for(total, tpb);
+    if (npoly > 65535) return cudaErrorInvalidValue;
+    const int N = 1 << logn, tpb = N < 256 ? N : 256;
+    const dim3 nb(N / tpb, nlimb, npoly);
     if (op == 0) binary_kernel<0><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
     else if (op == 1) binary_kernel<1><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
     else binary_kernel<2><<<nb, tpb, 0, st>>>(out, os, a, as, b, bs, nlimb, logn, limbs, pr, total);
@@ -117,13 +119,13 @@ cudaError_t mac_op(u64* out, const u64* ct, long long ct_stride, const u64* pt, 
 __global__ void __launch_bounds__(256) mac_terms_kernel(u64* __restrict__ out, const MacTerms terms, int nlimb,
                                                         int logn, Limbs limbs, const PrimeInfo* __restrict__ pr,
                                                         int accumulate, long long total) {
+    // grid (N / blockDim, limb, slot set)
     const int N = 1 << logn;
     const long long LN = (long long)nlimb << logn;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long g = idx / LN;
-        const long long off = idx - g * LN;
-        const int t = (int)(off >> logn);
+    const int n = blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
+    const long long g = blockIdx.z;
+    if (n < N) {
+        const long long off = (long long)t * N + n;
         const PrimeInfo& P = pr[limbs.prime[t]];
         const u64 q = P.q;
         Acc4 a0, a1;
@@ -145,15 +147,17 @@ __global__ void __launch_bounds__(256) mac_terms_kernel(u64* __restrict__ out, c
         }
         o[0] = r0;
         o[LN] = r1;
-        (void)N;
     }
+    (void)total;
 }
 
 cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
                          const PrimeInfo* pr, int accumulate, cudaStream_t st) {
     long long total = (long long)G * nlimb << logn;
     if (!total || terms.n <= 0) return cudaSuccess;
-    mac_terms_kernel<<<blocks_for(total, 256), 256, 0, st>>>(out, terms, nlimb, logn, limbs, pr, accumulate, total);
+    if (G > 65535) return cudaErrorInvalidValue;
+    const int N = 1 << logn, tpb = N < 256 ? N : 256;
+    mac_terms_kernel<<<dim3(N / tpb, nlimb, G), tpb, 0, st>>>(out, terms, nlimb, logn, limbs, pr, accumulate, total);
     return launched();
 }
 
@@ -341,13 +345,13 @@ cudaError_t mac_multi_op(u64* out, long long out_stride, const MacMulti& m, int 
 __global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, long long as,
                               const u64* __restrict__ b, long long bs, int nlimb, int logn, Limbs limbs,
                               const PrimeInfo* __restrict__ pr, long long total) {
+    // grid (N / blockDim, limb, slot set)
     const int N = 1 << logn;
     const long long LN = (long long)nlimb * N;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long g = idx / LN;
-        const long long off = idx - g * LN;
-        const int t = (int)(off >> logn);
+    const int n = blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
+    const long long g = blockIdx.z;
+    if (n < N) {
+        const long long off = (long long)t * N + n;
         const PrimeInfo& P = pr[limbs.prime[t]];
         const u64 q = P.q;
         const u64 a0 = a[g * as + off], a1 = a[g * as + LN + off];
@@ -360,13 +364,16 @@ __global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, lo
         o[LN] = acc.reduce(q, P.qinv_neg);
         o[2 * LN] = mont_mul(a1, b1, q, P.qinv_neg);
     }
+    (void)total;
 }
 
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,
                       int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st) {
     long long total = (long long)G * nlimb << logn;
     if (!total) return cudaSuccess;
-    tensor_kernel<<<blocks_for(total, 256), 256, 0, st>>>(d, a, as, b, bs, nlimb, logn, limbs, pr, total);
+    if (G > 65535) return cudaErrorInvalidValue;
+    const int N = 1 << logn, tpb = N < 256 ? N : 256;
+    tensor_kernel<<<dim3(N / tpb, nlimb, G), tpb, 0, st>>>(d, a, as, b, bs, nlimb, logn, limbs, pr, total);
     return launched();
 }
 
@@ -1058,20 +1065,37 @@ cudaError_t gather_limb_op(u64* dst, const u64* src, long long stride, long long
 }
 
 // copy limbs [0, nlimb) of each poly between differently-strided buffers
+// grid (words / (2 blockDim), poly): 16-byte moves, no per-element division
 __global__ void copy_limbs_kernel(u64* __restrict__ dst, long long ds, const u64* __restrict__ src, long long ss,
                                   long long per_poly, long long total) {
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long p = idx / per_poly, o = idx - p * per_poly;
-        dst[p * ds + o] = src[p * ss + o];
+    const long long p = blockIdx.y;
+    const long long o = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+    if (o < per_poly) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(src + p * ss + o);
+        *reinterpret_cast<ulonglong2*>(dst + p * ds + o) = v;
     }
+    (void)total;
+}
+__global__ void copy_limbs_scalar_kernel(u64* __restrict__ dst, long long ds, const u64* __restrict__ src,
+                                         long long ss, long long per_poly) {
+    const long long p = blockIdx.y;
+    const long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < per_poly) dst[p * ds + o] = src[p * ss + o];
 }
 
 cudaError_t copy_limbs_op(u64* dst, long long ds, const u64* src, long long ss, int npoly, long long per_poly,
                           cudaStream_t st) {
     long long total = (long long)npoly * per_poly;
     if (!total) return cudaSuccess;
-    copy_limbs_kernel<<<blocks_for(total, 256), 256, 0, st>>>(dst, ds, src, ss, per_poly, total);
+    if (npoly > 65535) return cudaErrorInvalidValue;
+    const bool vec = per_poly % 2 == 0 && ds % 2 == 0 && ss % 2 == 0 && ((uintptr_t)dst & 15) == 0 &&
+                     ((uintptr_t)src & 15) == 0;
+    if (vec)
+        copy_limbs_kernel<<<dim3((unsigned)((per_poly / 2 + 255) / 256), npoly), 256, 0, st>>>(dst, ds, src, ss, per_poly,
+                                                                                           total);
+    else
+        copy_limbs_scalar_kernel<<<dim3((unsigned)((per_poly + 255) / 256), npoly), 256, 0, st>>>(dst, ds, src, ss,
+                                                                                               per_poly);
     return launched();
 }
 
