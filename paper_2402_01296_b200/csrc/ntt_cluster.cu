@@ -59,6 +59,13 @@ template <int LOGCS> __device__ __forceinline__ int ntt_limb() { return blockIdx
 template <int LOGCS> __device__ __forceinline__ int ntt_poly() { return blockIdx.x >> LOGCS; }
 #endif
 
+// cluster barrier without the release fence of cluster.sync(): for the
+// barriers that only need the peers to have started / to be done reading,
+// so the arrive does not wait for this thread's outstanding HBM loads/stores
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ int cswz(int j) { return j ^ ((j >> 4) & 15); }
 
 // local index of global word j in its owner CTA (owner = j / PART)
@@ -543,14 +550,14 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
         f.qinv = 1.0 / f.q;
         double xf[C::E];
         dfwd_passA_load<LOGN, Prologue<PM>>(xf, pro, rank, tid);
-        cluster.sync();                      // peer SMEM is live before remote stores
+        cluster_sync_relaxed();   // peers are running (no ordering: the pending HBM loads need not drain)
         dfwd_passA_core<LOGN>(xf, dpeers, rank, Wf, f, tid);
         cluster.sync();                      // all chunks delivered
         dfwd_rest<LOGN, C::R0, Epilogue<EM>>(xf, epi, reinterpret_cast<double*>(sm), rank, Wf, f, tid);
         return;
     }
     u64 x[C::E];
-    cluster.sync();                          // peer SMEM is live before remote stores
+    cluster_sync_relaxed();   // peers are running (no ordering needed)
     cfwd_passA<LOGN, Prologue<PM>>(x, pro, peers, rank, W, q, tid);
     cluster.sync();                          // all chunks delivered
     cfwd_rest<LOGN, C::R0, Epilogue<EM>>(x, epi, sm, rank, W, q, tid);
@@ -685,7 +692,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
             ww = Wif[0];
         }
         dinv_passA<LOGN>(xf, g, dpeers, rank, Wif, f, nw, ww, tid);
-        cluster.sync();
+        cluster_sync_relaxed();   // peers' reads of our SMEM have returned (their values were stored)
         return;
     }
     u64 x[C::E];
@@ -698,7 +705,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     } else {
         cinv_passA<LOGN>(x, g, peers, rank, Wi, q, P.pad[0], P.pad[1], wn.x, wn.y, tid);
     }
-    cluster.sync();                          // peer finished reading our SMEM
+    cluster_sync_relaxed();   // peers' reads of our SMEM have returned (their values were stored)
 }
 
 template <int LOGN>
