@@ -304,6 +304,65 @@ __device__ __forceinline__ void dfwd_passA_core(double* x, double* const* peers,
     }
 }
 
+// DSMEM scatter with st.async: each remote store decrements the owner CTA's
+// mbarrier transaction count, so the owner waits for exactly its own 32 KiB
+// instead of a release-fenced cluster barrier (which drains every thread's
+// remote stores and waits for the slowest CTA of the cluster)
+__device__ __forceinline__ u32 mapa_rank(u32 saddr, u32 rank) {
+    u32 r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_f64(u32 raddr, double v, u32 rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+
+// bounded wait: a protocol bug traps (launch error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait_bounded(u64* bar, u32 parity) {
+    for (u32 spin = 0;; spin++) {
+        u32 done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spin > (1u << 26)) __trap();
+    }
+}
+
+template <int LOGN>
+__device__ __forceinline__ void dfwd_passA_core_async(double* x, const u32* rsm, const u32* rbar, int rank,
+                                                      const double2* __restrict__ W, FQ f, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int R = C::R0, BS = 1 << R, NB = C::E / BS, TL = C::N >> R;
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = rank * (TL / C::CS) + tid + i * C::T;
+#pragma unroll
+        for (int ls = 0; ls < R; ls++) {
+            const int h = BS >> (ls + 1);
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                if (k & h) continue;
+                const double2 w = W[(1 << ls) + (k >> (R - ls))];
+                double u = x[i * BS + k];
+                if (ls & 1) u = fred(u, f.qinv, f.q);
+                const double v = fmm(x[i * BS + k + h], w.x, w.y, f.q);
+                x[i * BS + k] = __dadd_rn(u, v);
+                x[i * BS + k + h] = __dadd_rn(u, -v);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < BS; k++) {
+            const int j = b + k * TL, r = k >> (R - C::LOGCS);
+            st_async_f64(rsm[r] + 8u * (u32)cswz(local_idx<LOGN>(j)), x[i * BS + k], rbar[r]);
+        }
+    }
+}
+
 template <int LOGN, int S0, bool LAST, class EPI>
 __device__ __forceinline__ void dfwd_pass(double* x, const EPI& epi, double* sm, int rank,
                                           const double2* __restrict__ W, FQ f, int tid) {
@@ -549,11 +608,24 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
         f.q = (double)q;
         f.qinv = 1.0 / f.q;
         double xf[C::E];
+        __shared__ __align__(8) u64 xbar;
+        if (tid == 0) {
+            mbar_init(&xbar, 1);
+            fence_barrier_init();
+        }
         dfwd_passA_load<LOGN, Prologue<PM>>(xf, pro, rank, tid);
-        cluster_sync_relaxed();   // peers are running (no ordering: the pending HBM loads need not drain)
-        dfwd_passA_core<LOGN>(xf, dpeers, rank, Wf, f, tid);
-        cluster.sync();                      // all chunks delivered
+        cluster_sync_relaxed();   // peers are running and their barriers initialised
+        if (tid == 0) mbar_expect_tx(&xbar, (u32)(C::PART * sizeof(double)));
+        u32 rsm[C::CS], rbar[C::CS];
+#pragma unroll
+        for (int r = 0; r < C::CS; r++) {
+            rsm[r] = mapa_rank(smem_addr(sm), (u32)r);
+            rbar[r] = mapa_rank(smem_addr(&xbar), (u32)r);
+        }
+        dfwd_passA_core_async<LOGN>(xf, rsm, rbar, rank, Wf, f, tid);
+        mbar_wait_bounded(&xbar, 0);         // this CTA's PART words have all landed
         dfwd_rest<LOGN, C::R0, Epilogue<EM>>(xf, epi, reinterpret_cast<double*>(sm), rank, Wf, f, tid);
+        (void)dpeers;
         return;
     }
     u64 x[C::E];
