@@ -465,8 +465,18 @@ def test_fp64_base_conversions_match_oracle(N, L, dnum, monkeypatch):
         p1 = rng.standard_normal(N // 2)
         ql = float(hp.q[L])
         U = eng.modup(ct, L)
-        rs = eng.rotsum_rescale([(ct, U, ge(1, N), eng.encode_ext(p1, L, ql)), (ct, U, ge(7, N), None)], L)
-        _assert_ct(rs, [orc.rotsum_rescale([(oc[i], 1, p1), (oc[i], 7, None)], [], L) for i in range(2)])
-        outs.append([to_numpy_u64(x) for x in (rot, sq, rs)])
+        terms = [(ct, U, ge(1, N), eng.encode_ext(p1, L, ql)), (ct, U, ge(7, N), None)]
+        rs = eng.rotsum_rescale(terms, L)
+        want = [orc.rotsum_rescale([(oc[i], 1, p1), (oc[i], 7, None)], [], L) for i in range(2)]
+        _assert_ct(rs, want)
+        # premultiplied keys: every term fused
+        rs2 = eng.rotsum_rescale(terms, L, keys=[eng.premul_key(terms[0][2], terms[0][3], L), None])
+        _assert_ct(rs2, want)
+        vals = rng.standard_normal((13, N // 2))
+        many = [(ct, U, ge(r, N), eng.encode_ext(vals[r - 1], L, ql)) for r in range(1, 14)]
+        rs3 = eng.rotsum(many, L, keys=[eng.premul_key(t[2], t[3], L) for t in many])
+        if N <= 8192:        # 13 fused terms
+            _assert_ct(rs3, [orc.rotsum([(oc[i], r, vals[r - 1]) for r in range(1, 14)], L) for i in range(2)])
+        outs.append([to_numpy_u64(x) for x in (rot, sq, rs, rs2, rs3)])
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
