@@ -87,7 +87,8 @@ struct bcn_ctx {
     std::vector<u64> pmod_host;   // [2 nq] Shoup pairs of P mod q_i
     PrimeInfo* pr = nullptr;
     ulonglong2* tw = nullptr;
-    double2* twf = nullptr;       // FP64 twiddles {w, w/q} (same layout as tw)
+    ulonglong2* twt = nullptr;    // tw in the cluster NTT's pass-transposed layout
+    double2* twf = nullptr;       // FP64 twiddles {w, w/q} (pass-transposed layout)
     double2* fq = nullptr;        // per prime {q, 1/q} (FP64 base conversions)
     bool fp_conv = false;         // every basis prime in (2^49, 2^50): base conversions on the FP64 pipe
     bool fp_ntt = true;           // BCN_NTT_FP64=0: integer butterflies for every prime
@@ -175,6 +176,7 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.digit_stride = 0;
     a.limbs = l;
     a.tw = c->tw;
+    a.twt = c->twt;
     a.twf = c->fp_ntt ? c->twf : nullptr;
     a.pr = c->pr;
     a.skip_alpha = 0;
@@ -491,6 +493,7 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
         // layout: pass-transposed for the cluster NTT's radix-16 passes (ntt_cluster.cu):
         // entry 2^s + (gi << ls) + j of stage s = S0 + ls lives at 2^s + j 2^S0 + gi
         std::vector<double2> twf(tw.size());
+        std::vector<ulonglong2> twt(tw.size());
         const int R0 = (logn % 4) ? (logn % 4) : 4;
         auto pos = [&](u64 k) -> u64 {
             if (k == 0 || (logn != 13 && logn != 14)) return k;
@@ -503,10 +506,14 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
             const double qd = (double)c->primes[i];
             for (int half = 0; half < 2; half++)
                 for (u64 k = 0; k < (u64)N; k++) {
-                    const double w = (double)tw[(size_t)i * 2 * N + (size_t)half * N + k].x;
+                    const ulonglong2 e = tw[(size_t)i * 2 * N + (size_t)half * N + k];
+                    const double w = (double)e.x;
                     twf[(size_t)i * 2 * N + (size_t)half * N + pos(k)] = make_double2(w, w / qd);
+                    twt[(size_t)i * 2 * N + (size_t)half * N + pos(k)] = e;
                 }
         }
+        CUDA_TRY(dmalloc((void**)&c->twt, sizeof(ulonglong2) * twt.size(), &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(c->twt, twt.data(), sizeof(ulonglong2) * twt.size(), cudaMemcpyHostToDevice));
         CUDA_TRY(dmalloc((void**)&c->twf, sizeof(double2) * twf.size(), &c->table_bytes));
         CUDA_TRY(cudaMemcpy(c->twf, twf.data(), sizeof(double2) * twf.size(), cudaMemcpyHostToDevice));
         c->fp_ntt = !getenv_flag_off("BCN_NTT_FP64");
@@ -593,7 +600,7 @@ int bcn_ctx_destroy(bcn_ctx* c) {
         cudaFree(kv.second.mdr); cudaFree(kv.second.mdr_scale); cudaFree(kv.second.pqinv);
     }
     for (auto& kv : c->keys) cudaFree(kv.second);
-    cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->twf); cudaFree(c->fq); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
+    cudaFree(c->pr); cudaFree(c->tw); cudaFree(c->twt); cudaFree(c->twf); cudaFree(c->fq); cudaFree(c->ksi_re); cudaFree(c->ksi_im); cudaFree(c->rot);
     cudaFree(c->s_ntt); cudaFree(c->s_mont); cudaFree(c->pmod); cudaFree(c->md_scale);
     if (c->scratch) cudaFree(c->scratch);
     if (c->ptr_dev) cudaFree(c->ptr_dev);

@@ -195,7 +195,7 @@ __device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int r
 #pragma unroll
         for (int k = 0; k < BS; k++) {
             if (k & h) continue;
-            const ulonglong2 w = W[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const ulonglong2 w = W[(1 << s) + ((k >> (R - ls)) << S0) + gi];   // pass-transposed table
             const u64 u = fwd_reduce(s) ? csub(x[k], fwd_rbound(q)) : x[k];
             const u64 v = shoup_lazy(x[k + h], w.x, w.y, q);
             x[k] = u + v;
@@ -544,7 +544,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     for (int r = 0; r < C::CS; r++) peers[r] = cluster.map_shared_rank(sm, r);
     const int pidx = a.limbs.prime[t];
     const u64 q = a.pr[pidx].q;
-    const ulonglong2* W = a.tw + (size_t)pidx * 2 * C::N;
+    const ulonglong2* W = a.twt + (size_t)pidx * 2 * C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
     const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
     Prologue<PM> pro;
@@ -667,7 +667,7 @@ __device__ __forceinline__ void cinv_pass(u64* x, const u64* __restrict__ gin, u
 #pragma unroll
         for (int k = 0; k < BS; k++) {
             if (k & h) continue;
-            const ulonglong2 w = Wi[(1 << s) + (gi << ls) + (k >> (R - ls))];
+            const ulonglong2 w = Wi[(1 << s) + ((k >> (R - ls)) << S0) + gi];  // pass-transposed table
             const u64 u = x[k], v = x[k + h];
             x[k] = csub(u + v, q2);
             x[k + h] = shoup_lazy(u - v + q2, w.x, w.y, q);
@@ -739,7 +739,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     const int pidx = a.limbs.prime[t];
     const PrimeInfo& P = a.pr[pidx];
     const u64 q = P.q;
-    const ulonglong2* Wi = a.tw + (size_t)pidx * 2 * C::N + C::N;
+    const ulonglong2* Wi = a.twt + (size_t)pidx * 2 * C::N + C::N;
     u64* g = a.data + (size_t)poly * a.poly_stride + (size_t)t * C::N;
     const u64* gin = a.src ? a.src + (size_t)poly * a.src_poly_stride + (size_t)t * a.src_limb_stride : g;
     const int tid = threadIdx.x;
