@@ -507,7 +507,7 @@ int bcn_ctx_create(bcn_ctx** out, int logn, int max_level, const uint64_t* q, in
             for (int half = 0; half < 2; half++)
                 for (u64 k = 0; k < (u64)N; k++) {
                     const ulonglong2 e = tw[(size_t)i * 2 * N + (size_t)half * N + k];
-                    const double w = (double)e.x;
+                    const double w = e.x > c->primes[i] / 2 ? (double)e.x - qd : (double)e.x;   // signed, |w| <= q/2
                     twf[(size_t)i * 2 * N + (size_t)half * N + pos(k)] = make_double2(w, w / qd);
                     twt[(size_t)i * 2 * N + (size_t)half * N + pos(k)] = e;
                 }

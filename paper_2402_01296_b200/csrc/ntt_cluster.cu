@@ -242,22 +242,25 @@ __device__ __forceinline__ void cfwd_rest(u64* x, const EPI& epi, u64* sm, int r
 // For primes below 2^50 the butterflies run on the FP64 pipe instead of the
 // 64-bit integer multiplies on the IMAD pipe (tools/micro/bfly_bench.cu:
 // 6.3 vs 3.1 butterflies/clk/SM on this B200).  Residues are exact integers
-// held in doubles, signed, |x| < 2^51; SMEM holds the double bits.
-//   fmm(a, w, wq):  a*w mod q for |a| < 2^51 (so |a wq| < 2^51 and the
-//                   add-1.5*2^52 rounding lands on an integer), w < q,
-//                   wq = fl(w/q).  hi + lo = a*w exactly (FMA two-product);
-//                   qt = rint(a*wq) is within 0.5 + |a| 2^-54 / q*q of a*w/q,
-//                   so the result a*w - qt*q (exact: an integer < 2^53) has
-//                   |r| <= 0.61 q.
-//   fred(x):        x - q rint(x/q), |x| < 2^51  ->  |r| <= 0.5 q (+2^-50 q).
-// Forward (CT): u is reduced on odd stages only; with v = fmm(...) <= 0.61 q
-// every value stays <= 1.75 q < 2q (the fmm input bound).  Inverse (GS): the
-// sum is reduced every stage, every value stays <= 0.61 q.  Outputs are
-// canonicalised (fred, +q if negative) -- the same canonical residues as the
-// integer path, so the two are interchangeable bit for bit.
+// held in doubles, signed, |x| < 2^53; SMEM holds the double bits.  fmm /
+// fred are in common.cuh; the twiddles are signed (|w| <= q/2), which widens
+// fmm's input range to |a| < 4q, and the reduction schedule is fwd_fred /
+// inv_fred below.  Outputs are canonicalised (fred, +q if negative) -- the
+// same canonical residues as the integer path, interchangeable bit for bit.
 struct FQ {                     // per-prime FP64 constants
     double q, qinv;
 };
+
+// FP64 lazy-reduction schedule.  Twiddles are stored signed, |w| <= q/2, so
+// fmm(a, w) only needs |a| < 4q (quotient |a w / q| < 2^51) and returns
+// |v| <= 0.5q + |a| 2^-55 <= 0.63q.
+//   forward (CT): u is reduced on stages s = 3 mod 4; starting from
+//     canonical input every value stays <= 1.13q + 3 * 0.63q < 3.1q (< 4q);
+//   inverse (GS): the sum is reduced on every other stage counted from the
+//     first (t = LOGN-1-s odd); every value stays <= 2q before a reduced
+//     stage and <= 1.25q after it, so u - v stays < 4q.
+__device__ __forceinline__ constexpr bool fwd_fred(int s) { return (s & 3) == 3; }
+template <int LOGN> __device__ __forceinline__ constexpr bool inv_fred(int s) { return ((LOGN - 1 - s) & 1) == 1; }
 
 // pass A: the loads (issued before the cluster barrier that guards the
 // scatter, so their HBM latency overlaps the barrier wait), then the
@@ -290,7 +293,7 @@ __device__ __forceinline__ void dfwd_passA_core(double* x, double* const* peers,
                 if (k & h) continue;
                 const double2 w = W[(1 << ls) + (k >> (R - ls))];
                 double u = x[i * BS + k];
-                if (ls & 1) u = fred(u, f.qinv, f.q);
+                if (fwd_fred(ls)) u = fred(u, f.qinv, f.q);
                 const double v = fmm(x[i * BS + k + h], w.x, w.y, f.q);
                 x[i * BS + k] = __dadd_rn(u, v);
                 x[i * BS + k + h] = __dadd_rn(u, -v);
@@ -349,7 +352,7 @@ __device__ __forceinline__ void dfwd_passA_core_async(double* x, const u32* rsm,
                 if (k & h) continue;
                 const double2 w = W[(1 << ls) + (k >> (R - ls))];
                 double u = x[i * BS + k];
-                if (ls & 1) u = fred(u, f.qinv, f.q);
+                if (fwd_fred(ls)) u = fred(u, f.qinv, f.q);
                 const double v = fmm(x[i * BS + k + h], w.x, w.y, f.q);
                 x[i * BS + k] = __dadd_rn(u, v);
                 x[i * BS + k + h] = __dadd_rn(u, -v);
@@ -382,7 +385,7 @@ __device__ __forceinline__ void dfwd_pass(double* x, const EPI& epi, double* sm,
         for (int k = 0; k < BS; k++) {
             if (k & h) continue;
             const double2 w = W[(1 << s) + ((k >> (R - ls)) << S0) + gi];   // pass-transposed table
-            const double u = (s & 1) ? fred(x[k], f.qinv, f.q) : x[k];
+            const double u = fwd_fred(s) ? fred(x[k], f.qinv, f.q) : x[k];
             const double v = fmm(x[k + h], w.x, w.y, f.q);
             x[k] = __dadd_rn(u, v);
             x[k + h] = __dadd_rn(u, -v);
@@ -456,7 +459,8 @@ __device__ __forceinline__ void dinv_pass(double* x, const u64* __restrict__ gin
             if (k & h) continue;
             const double2 w = Wi[(1 << s) + ((k >> (R - ls)) << S0) + gi];  // pass-transposed table
             const double u = x[k], v = x[k + h];
-            x[k] = fred(__dadd_rn(u, v), f.qinv, f.q);
+            const double sum = __dadd_rn(u, v);
+            x[k] = inv_fred<LOGN>(s) ? fred(sum, f.qinv, f.q) : sum;
             x[k + h] = fmm(__dadd_rn(u, -v), w.x, w.y, f.q);
         }
     }
@@ -501,7 +505,8 @@ __device__ __forceinline__ void dinv_passA(double* x, u64* __restrict__ g, doubl
                     x[i * BS + k + h] = fmm(__dadd_rn(u, -v), ww.x, ww.y, f.q);
                 } else {
                     const double2 w = Wi[(1 << ls) + (k >> (R - ls))];
-                    x[i * BS + k] = fred(__dadd_rn(u, v), f.qinv, f.q);
+                    const double sum = __dadd_rn(u, v);
+                    x[i * BS + k] = inv_fred<LOGN>(ls) ? fred(sum, f.qinv, f.q) : sum;
                     x[i * BS + k + h] = fmm(__dadd_rn(u, -v), w.x, w.y, f.q);
                 }
             }
@@ -511,8 +516,9 @@ __device__ __forceinline__ void dinv_passA(double* x, u64* __restrict__ g, doubl
     }
 }
 
-__device__ __forceinline__ double2 fpair(u64 w, double q) {
-    const double wd = (double)w;
+__device__ __forceinline__ double2 fpair(u64 w, double q) {      // signed twiddle pair (see fwd_fred)
+    double wd = (double)w;
+    if (wd > 0.5 * q) wd = __dadd_rn(wd, -q);
     return make_double2(wd, __ddiv_rn(wd, q));
 }
 
