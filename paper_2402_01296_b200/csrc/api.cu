@@ -1643,7 +1643,7 @@ int bcn_mul_cc(bcn_ctx* c, uint64_t* out, const uint64_t* a, int a_nlimb, const 
     u64* R = U + uw;
     u64* tmp = R + rw;
     CUDA_TRY(tensor_op(d, (const u64*)a, 2LL * a_nlimb * N, (const u64*)b, 2LL * b_nlimb * N, G, nl, c->logn,
-                       limbs_range(0, nl), c->pr, st));
+                       limbs_range(0, nl), c->pr, st, c->fp_conv ? c->fq : nullptr));
     e = modup_impl(c, U, d + 2 * nl * N, 3LL * nl * N, G, level, tmp, st);
     if (e) return e;
     if (rescale && !getenv_flag_off("BCN_MERGED_RESCALE")) {

@@ -344,7 +344,7 @@ cudaError_t mac_multi_op(u64* out, long long out_stride, const MacMulti& m, int 
 // a, b: [G][2][L][N] with strides; d: [G][3][L][N]
 __global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, long long as,
                               const u64* __restrict__ b, long long bs, int nlimb, int logn, Limbs limbs,
-                              const PrimeInfo* __restrict__ pr, long long total) {
+                              const PrimeInfo* __restrict__ pr, long long total, const double2* __restrict__ fq) {
     // grid (N / blockDim, limb, slot set)
     const int N = 1 << logn;
     const long long LN = (long long)nlimb * N;
@@ -354,9 +354,19 @@ __global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, lo
         const long long off = (long long)t * N + n;
         const PrimeInfo& P = pr[limbs.prime[t]];
         const u64 q = P.q;
+        u64* o = d + g * 3 * LN + off;
+        if (fq) {                                    // FP64 pipe: plain products, exact two-product fmm
+            const double2 f = fq[limbs.prime[t]];
+            const double a0 = fload(a[g * as + off]), a1 = fload(a[g * as + LN + off]);
+            const double b0 = fload(b[g * bs + off]), b1 = fload(b[g * bs + LN + off]);
+            const double b0q = __dmul_rn(b0, f.y), b1q = __dmul_rn(b1, f.y);   // |a (b/q - bq)| <= 0.25
+            o[0] = fcanon_small(fmm(a0, b0, b0q, f.x), f.x);
+            o[LN] = fcanon(__dadd_rn(fmm(a0, b1, b1q, f.x), fmm(a1, b0, b0q, f.x)), f.y, f.x);
+            o[2 * LN] = fcanon_small(fmm(a1, b1, b1q, f.x), f.x);
+            return;
+        }
         const u64 a0 = a[g * as + off], a1 = a[g * as + LN + off];
         const u64 b0 = to_mont(b[g * bs + off], P), b1 = to_mont(b[g * bs + LN + off], P);
-        u64* o = d + g * 3 * LN + off;
         o[0] = mont_mul(a0, b0, q, P.qinv_neg);
         Acc128 acc; acc.zero();
         acc.mac(a0, b1, q);
@@ -368,12 +378,12 @@ __global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, lo
 }
 
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,
-                      int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st) {
+                      int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st, const double2* fq) {
     long long total = (long long)G * nlimb << logn;
     if (!total) return cudaSuccess;
     if (G > 65535) return cudaErrorInvalidValue;
     const int N = 1 << logn, tpb = N < 256 ? N : 256;
-    tensor_kernel<<<dim3(N / tpb, nlimb, G), tpb, 0, st>>>(d, a, as, b, bs, nlimb, logn, limbs, pr, total);
+    tensor_kernel<<<dim3(N / tpb, nlimb, G), tpb, 0, st>>>(d, a, as, b, bs, nlimb, logn, limbs, pr, total, fq);
     return launched();
 }
 

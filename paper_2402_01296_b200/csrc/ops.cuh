@@ -170,7 +170,7 @@ cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const 
 cudaError_t mac_terms_op(u64* out, const MacTerms& terms, int G, int nlimb, int logn, const Limbs& limbs,
                          const PrimeInfo* pr, int accumulate, cudaStream_t st);
 cudaError_t tensor_op(u64* d, const u64* a, long long as, const u64* b, long long bs, int G, int nlimb,
-                      int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st);
+                      int logn, const Limbs& limbs, const PrimeInfo* pr, cudaStream_t st, const double2* fq = nullptr);
 cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, int npoly, int nlimb, int logn,
                          u32 g, cudaStream_t st);
 cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, long long x_stride, int npoly, int nq,
