@@ -72,6 +72,8 @@ struct LevelTables {
     u64* upscale = nullptr;         // [4 (level+1)] ModUp INTT constants {n^-1 h_i, sh, w1 n^-1 h_i, sh}
     // merged ModDown + rescale (P' = q_level * P, sources {q_level, p_0..p_{K-1}}, targets q_0..q_{level-1})
     ConvTable* mdr = nullptr;       // [1]
+    FConvSet fc_up;                 // FP64 conversion constants (kernel parameters), see ops.cuh
+    FConv fc_down, fc_mdr;
     u64* mdr_scale = nullptr;       // [4 (K+1)] INTT constants with (P'/s)^-1 folded in
     u64* pqinv = nullptr;           // [2 level] Shoup pairs of (P q_level)^-1 mod q_i
     int ndig = 0;
@@ -261,7 +263,10 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
                 u64 pm = 1;
                 for (int k = i0; k < i1; k++) if (k != i) pm = mulmod_h(pm, c->primes[k] % qt, qt);
                 t.hat_m[(i - i0) * BCN_MAX_LIMBS + e] = mont_h(pm, qt);
-                t.hat_d[(i - i0) * BCN_MAX_LIMBS + e] = make_double2((double)pm, (double)pm / (double)qt);
+                if (j < 3 && i - i0 < BCN_FC_SRC && e < BCN_FC_TGT) {
+                    T.fc_up.d[j].h[i - i0][e] = make_double2((double)pm, (double)pm / (double)qt);
+                    T.fc_up.d[j].fq[e] = make_double2((double)qt, 1.0 / (double)qt);
+                }
             }
         }
     }
@@ -280,7 +285,10 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
             u64 pm = 1;
             for (int k2 = 0; k2 < c->K; k2++) if (k2 != k) pm = mulmod_h(pm, c->primes[c->nq + k2] % qi, qi);
             down.hat_m[k * BCN_MAX_LIMBS + i] = mont_h(pm, qi);
-            down.hat_d[k * BCN_MAX_LIMBS + i] = make_double2((double)pm, (double)pm / (double)qi);
+            if (k < BCN_FC_SRC && i < BCN_FC_TGT) {
+                T.fc_down.h[k][i] = make_double2((double)pm, (double)pm / (double)qi);
+                T.fc_down.fq[i] = make_double2((double)qi, 1.0 / (double)qi);
+            }
         }
     }
     std::vector<u64> pinv(2 * (level + 1)), qlinv(2 * std::max(level, 1));
@@ -329,7 +337,10 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
                 u64 pm = 1;
                 for (int b = 0; b < ns; b++) if (b != a) pm = mulmod_h(pm, c->primes[sp[b]] % qi, qi);
                 m.hat_m[a * BCN_MAX_LIMBS + i] = mont_h(pm, qi);
-                m.hat_d[a * BCN_MAX_LIMBS + i] = make_double2((double)pm, (double)pm / (double)qi);
+                if (a < BCN_FC_SRC && i < BCN_FC_TGT) {
+                    T.fc_mdr.h[a][i] = make_double2((double)pm, (double)pm / (double)qi);
+                    T.fc_mdr.fq[i] = make_double2((double)qi, 1.0 / (double)qi);
+                }
             }
             const u64 x = mulmod_h(c->hpr[sp[a]].pad[0], hinv, sa), y = mulmod_h(c->wn_host[sp[a]], hinv, sa);
             msc[4 * a] = x; msc[4 * a + 1] = shoup_h(x, sa);
@@ -1270,7 +1281,7 @@ static int modup_impl(bcn_ctx* c, u64* U, const u64* x, long long x_stride, int 
     // coefficient-domain copy of x
     CUDA_TRY(ntt_run_src(c, true, tmp, nl * N, x, x_stride, N, ql, G, st));     // coefficient form of x
     CUDA_TRY(modup_op(U, tmp, nl * N, x, x_stride, G, nl, next, c->alpha, ndig, c->logn, ext, c->pr, T->modup, st,
-                      c->fp_conv ? c->fq : nullptr));
+                      c->fp_conv ? &T->fc_up : nullptr));
     NttArgs a = ntt_args(c, U, (long long)next * N, ext);
     a.skip_alpha = c->alpha;
     a.skip_dnum = ndig;
@@ -1317,7 +1328,7 @@ static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int l
             // a plain-prologue NTT with the fused combine: the prologue form re-reads the
             // sources for every output limb and stalls on their latency
             CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown,
-                                     st, c->fp_conv ? c->fq : nullptr));
+                                     st, c->fp_conv ? &T->fc_down : nullptr));
             a.src = Z;
             a.src_poly_stride = (long long)nl * N;
             a.src_limb_stride = N;
@@ -1341,7 +1352,7 @@ static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int l
         return BCN_OK;
     }
     CUDA_TRY(ntt_run(c, true, A + (size_t)nl * N, (long long)next * N, pl, 2 * G, st));
-    CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st, c->fp_conv ? c->fq : nullptr));
+    CUDA_TRY(moddown_conv_op(Z, A, (long long)next * N, 2 * G, nl, c->K, c->logn, ext, c->pr, T->moddown, st, c->fp_conv ? &T->fc_down : nullptr));
     CUDA_TRY(ntt_run(c, false, Z, (long long)nl * N, ql, 2 * G, st));
     CUDA_TRY(moddown_combine_op(out, os, A, next, Z, addend, as, add_c1, g, G, nl, c->logn, ql, c->pr, T->pinv, st));
     return BCN_OK;
@@ -1470,7 +1481,7 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
         NttArgs a = ntt_args(c, out, (long long)level * N, ql);
         if (split) {   // conversion once per coefficient, then plain-prologue NTT + fused combine
             Limbs ext = limbs_ext(c, level);
-            CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st, c->fp_conv ? c->fq : nullptr));
+            CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st, c->fp_conv ? &T->fc_mdr : nullptr));
             a.src = Z;
             a.src_poly_stride = (long long)level * N;
             a.src_limb_stride = N;
@@ -1496,7 +1507,7 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
     }
     CUDA_TRY(ntt_run(c, true, B + (size_t)level * N, (long long)next * N, sl, 2 * G, st));
     Limbs ext = limbs_ext(c, level);
-    CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st, c->fp_conv ? c->fq : nullptr));
+    CUDA_TRY(moddown_conv_op(Z, B, (long long)next * N, 2 * G, level, sl.n, c->logn, ext, c->pr, T->mdr, st, c->fp_conv ? &T->fc_mdr : nullptr));
     CUDA_TRY(ntt_run(c, false, Z, (long long)level * N, ql, 2 * G, st));
     CUDA_TRY(mdr_combine_op(out, B, (long long)next * N, Z, C, c_gstride, add_c1, 2 * G, level, c->logn, ql, c->pr,
                             T->pqinv, T->qlinv, st));

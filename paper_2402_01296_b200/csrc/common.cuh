@@ -218,22 +218,6 @@ __device__ __forceinline__ double fload(u64 v) {
     return __dadd_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), -4503599627370496.0);
 }
 
-// sum_k y[k] * h[k] mod t, canonical, for canonical y[k] < 2t held as exact
-// doubles and constant pairs h[k] = {h, h/t} (h < t < 2^50); nk <= 12 keeps
-// the unreduced sum below 8t <= 2^53
-template <int YK>
-__device__ __forceinline__ u64 fdot_canon(const double* y, const double2* __restrict__ h, int hstride, int nk,
-                                          double t, double tinv) {
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < YK; k++)
-        if (k < nk) {
-            const double2 hk = h[k * hstride];
-            acc = __dadd_rn(acc, fmm(y[k], hk.x, hk.y, t));
-        }
-    return fcanon(acc, tinv, t);
-}
-
 // ---- bulk async copies (TMA engine, 1-D) completing on an mbarrier ----
 __device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* bar, u32 count) {

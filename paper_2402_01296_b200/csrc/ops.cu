@@ -419,7 +419,7 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, lo
                              const u64* __restrict__ xn, long long x_stride, int nq, int next, int alpha, int ndig,
                              int logn,
                              Limbs ext, const PrimeInfo* __restrict__ pr, const ConvTable* __restrict__ tab,
-                             const double2* __restrict__ fq) {
+                             const __grid_constant__ FConvSet fc, int use_fp) {
     constexpr int YA = A > 0 ? A : BCN_MAX_ALPHA;
     const int N = 1 << logn;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -443,14 +443,19 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, lo
             y[i] = 0ull;
         }
     }
-    if (fq) {                                          // FP64 pipe (every basis prime in (2^49, 2^50))
+    if (use_fp) {                                      // FP64 pipe (every basis prime in (2^49, 2^50))
         double yd[YA];
 #pragma unroll
         for (int i = 0; i < YA; i++) yd[i] = fload(y[i]);
+        const FConv& F = fc.d[j];
         for (int t = 0; t < next; t++) {
             if (t >= i0 && t < i0 + na) continue;
-            const double2 f = fq[ext.prime[t]];
-            Up[(long long)t * N] = fdot_canon<YA>(yd, T.hat_d + t, BCN_MAX_LIMBS, na, f.x, f.y);
+            const double2 f = F.fq[t];
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < YA; i++)
+                if (i < na) acc = __dadd_rn(acc, fmm(yd[i], F.h[i][t].x, F.h[i][t].y, f.x));
+            Up[(long long)t * N] = fcanon(acc, f.y, f.x);
         }
         return;
     }
@@ -468,19 +473,21 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, lo
 
 cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, long long x_stride, int npoly, int nq,
                      int next, int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr,
-                     const ConvTable* tab, cudaStream_t st, const double2* fq) {
+                     const ConvTable* tab, cudaStream_t st, const FConvSet* fcp) {
     const int N = 1 << logn;
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, npoly, ndig);
-    if (alpha > 12) fq = nullptr;                      // fdot_canon's unreduced-sum bound
+    static FConvSet none;
+    const int use_fp = fcp && alpha <= BCN_FC_SRC && next <= BCN_FC_TGT && ndig <= 3;
+    const FConvSet& fc = use_fp ? *fcp : none;
     switch (alpha) {
 #define BCN_MU(AA) case AA: modup_kernel<AA><<<grid, tpb, 0, st>>>(U, xc, xc_stride, xn, x_stride, nq, next, alpha, \
-                                                                  ndig, logn, ext, pr, tab, fq); break;
+                                                                  ndig, logn, ext, pr, tab, fc, use_fp); break;
         BCN_MU(1) BCN_MU(2) BCN_MU(3) BCN_MU(4) BCN_MU(5) BCN_MU(6) BCN_MU(7) BCN_MU(8)
 #undef BCN_MU
         default:
             modup_kernel<0><<<grid, tpb, 0, st>>>(U, xc, xc_stride, xn, x_stride, nq, next, alpha, ndig, logn, ext, pr,
-                                                  tab, fq);
+                                                  tab, fc, 0);
     }
     return launched();
 }
@@ -908,7 +915,7 @@ cudaError_t mdr_combine_op(u64* out, const u64* B, long long bps, const u64* Z, 
 template <int KK>    // source count at compile time: y[] in registers (0: runtime count, local array)
 __global__ void moddown_conv_kernel(u64* __restrict__ Z, const u64* __restrict__ A, long long a_stride,
                                     int nq, int K, int logn, Limbs ext, const PrimeInfo* __restrict__ pr,
-                                    const ConvTable* __restrict__ tab, const double2* __restrict__ fq) {
+                                    const ConvTable* __restrict__ tab, const __grid_constant__ FConv fc, int use_fp) {
     constexpr int YK = KK > 0 ? KK : BCN_MAX_ALPHA;
     const int N = 1 << logn;
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -926,13 +933,17 @@ __global__ void moddown_conv_kernel(u64* __restrict__ Z, const u64* __restrict__
         }
     }
     u64* zp = Z + p * (long long)nq * N + n;
-    if (fq) {                                          // FP64 pipe (every basis prime in (2^49, 2^50))
+    if (use_fp) {                                      // FP64 pipe (every basis prime in (2^49, 2^50))
         double yd[YK];
 #pragma unroll
         for (int k = 0; k < YK; k++) yd[k] = k < nk ? fload(y[k]) : 0.0;
         for (int i = 0; i < nq; i++) {
-            const double2 f = fq[ext.prime[i]];
-            zp[(long long)i * N] = fdot_canon<YK>(yd, T.hat_d + i, BCN_MAX_LIMBS, nk, f.x, f.y);
+            const double2 f = fc.fq[i];
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < YK; k++)
+                if (k < nk) acc = __dadd_rn(acc, fmm(yd[k], fc.h[k][i].x, fc.h[k][i].y, f.x));
+            zp[(long long)i * N] = fcanon(acc, f.y, f.x);
         }
         return;
     }
@@ -948,16 +959,18 @@ __global__ void moddown_conv_kernel(u64* __restrict__ Z, const u64* __restrict__
 
 cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
                             const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st,
-                            const double2* fq) {
+                            const FConv* fcp) {
     const int N = 1 << logn;
     int tpb = N < 256 ? N : 256;
     dim3 grid((N + tpb - 1) / tpb, npoly);
-    if (K > 12) fq = nullptr;                          // fdot_canon's unreduced-sum bound
+    static FConv none;
+    const int use_fp = fcp && K <= BCN_FC_SRC && nq <= BCN_FC_TGT;
+    const FConv& fc = use_fp ? *fcp : none;
     switch (K) {
-#define BCN_MC(KV) case KV: moddown_conv_kernel<KV><<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab, fq); break;
+#define BCN_MC(KV) case KV: moddown_conv_kernel<KV><<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab, fc, use_fp); break;
         BCN_MC(1) BCN_MC(2) BCN_MC(3) BCN_MC(4) BCN_MC(5) BCN_MC(6) BCN_MC(7) BCN_MC(8) BCN_MC(9)
 #undef BCN_MC
-        default: moddown_conv_kernel<0><<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab, fq);
+        default: moddown_conv_kernel<0><<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab, fc, 0);
     }
     return launched();
 }

@@ -13,7 +13,20 @@ struct ConvTable {
     u64 hatinv[BCN_MAX_ALPHA];
     u64 hatinv_p[BCN_MAX_ALPHA];
     u64 hat_m[BCN_MAX_ALPHA * BCN_MAX_LIMBS];
-    double2 hat_d[BCN_MAX_ALPHA * BCN_MAX_LIMBS];   // {hat, hat / target prime} for the FP64 conversions
+};
+
+// FP64 base-conversion constants passed BY VALUE as a kernel parameter: the
+// kernel reads them from the constant bank (uniform LDC), not through the
+// L1/LSU pipe that the per-thread data loads need (a global table read by
+// every warp kept that pipe 77-87% busy).
+#define BCN_FC_SRC 8
+#define BCN_FC_TGT 24
+struct FConv {
+    double2 h[BCN_FC_SRC][BCN_FC_TGT];   // {hat_k mod t, that / t} per source k, target limb t
+    double2 fq[BCN_FC_TGT];              // target {t, 1/t}
+};
+struct FConvSet {                        // one FConv per ModUp digit
+    FConv d[3];
 };
 
 namespace bcn {
@@ -175,13 +188,13 @@ cudaError_t automorph_op(u64* out, long long os, const u64* in, long long is, in
                          u32 g, cudaStream_t st);
 cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, long long x_stride, int npoly, int nq,
                      int next, int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr,
-                     const ConvTable* tab, cudaStream_t st, const double2* fq = nullptr);
+                     const ConvTable* tab, cudaStream_t st, const FConvSet* fc = nullptr);
 cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
                      long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
                      const PrimeInfo* pr, cudaStream_t st);
 cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
                             const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st,
-                            const double2* fq = nullptr);
+                            const FConv* fc = nullptr);
 cudaError_t moddown_combine_op(u64* out, long long os, const u64* A, int next, const u64* Z, const u64* addend,
                                long long as, int add_c1, u32 g, int npoly, int nq, int logn, const Limbs& ql,
                                const PrimeInfo* pr, const u64* pinv, cudaStream_t st);
