@@ -69,6 +69,7 @@ struct LevelTables {
     u64* pinv = nullptr;            // [2 * (level+1)] Shoup pairs of P^-1 mod q_i
     u64* qlinv = nullptr;           // [2 * level] Shoup pairs of q_level^-1 mod q_i
     u64* qtopmod = nullptr;         // [level] q_level mod q_i (fused rescale lift)
+    u64* lift1 = nullptr;           // [2 (level+1)] {0, floor(2^64 / q_i)}: plain lift prologue (K = 1 ModDown)
     u64* upscale = nullptr;         // [4 (level+1)] ModUp INTT constants {n^-1 h_i, sh, w1 n^-1 h_i, sh}
     // merged ModDown + rescale (P' = q_level * P, sources {q_level, p_0..p_{K-1}}, targets q_0..q_{level-1})
     ConvTable* mdr = nullptr;       // [1]
@@ -377,6 +378,15 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
     CUDA_TRY(cudaMemcpy(T.upscale, ups.data(), sizeof(u64) * ups.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(dmalloc((void**)&T.qtopmod, sizeof(u64) * qtm.size(), &c->table_bytes));
     CUDA_TRY(cudaMemcpy(T.qtopmod, qtm.data(), sizeof(u64) * qtm.size(), cudaMemcpyHostToDevice));
+    {
+        std::vector<u64> l1(2 * (level + 1));
+        for (int i = 0; i <= level; i++) {
+            l1[2 * i] = 0;
+            l1[2 * i + 1] = (u64)(((u128)1 << 64) / c->primes[i]);
+        }
+        CUDA_TRY(dmalloc((void**)&T.lift1, sizeof(u64) * l1.size(), &c->table_bytes));
+        CUDA_TRY(cudaMemcpy(T.lift1, l1.data(), sizeof(u64) * l1.size(), cudaMemcpyHostToDevice));
+    }
     CUDA_TRY(cudaMemcpy(T.modup, up.data(), sizeof(ConvTable) * ndig, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(T.moddown, &down, sizeof(ConvTable), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(T.pinv, pinv.data(), sizeof(u64) * pinv.size(), cudaMemcpyHostToDevice));
@@ -607,7 +617,7 @@ int bcn_ctx_destroy(bcn_ctx* c) {
     for (auto& kv : c->lt) {
         cudaFree(kv.second.modup); cudaFree(kv.second.moddown);
         cudaFree(kv.second.pinv); cudaFree(kv.second.qlinv);
-        cudaFree(kv.second.qtopmod); cudaFree(kv.second.upscale);
+        cudaFree(kv.second.qtopmod); cudaFree(kv.second.lift1); cudaFree(kv.second.upscale);
         cudaFree(kv.second.mdr); cudaFree(kv.second.mdr_scale); cudaFree(kv.second.pqinv);
     }
     for (auto& kv : c->keys) cudaFree(kv.second);
@@ -1323,7 +1333,16 @@ static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int l
         if (!split) ia.inv_scale = c->md_scale;
         CUDA_TRY(ntt_launch(true, c->logn, ia, c->K, 2 * G, st));
         NttArgs a = ntt_args(c, out, (long long)nl * N, ql);
-        if (split) {
+        if (c->K == 1 && !getenv_flag_off("BCN_K1_LIFT")) {
+            // one special prime: the conversion is y mod q_t (the hat factors are 1), so the
+            // NTT's lift prologue reads the INTT'd special limb directly (no Z round trip);
+            // qtop = ~0 disables the centring (the oracle's fast base conversion is not centred)
+            a.pro = 1;
+            a.pro_src = A + (size_t)nl * N;
+            a.pro_stride = (long long)next * N;
+            a.pro_qtop = ~0ull;
+            a.pro_tab = T->lift1;
+        } else if (split) {
             // base conversion once per coefficient (sources read once, in registers), then
             // a plain-prologue NTT with the fused combine: the prologue form re-reads the
             // sources for every output limb and stalls on their latency

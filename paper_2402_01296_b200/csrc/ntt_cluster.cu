@@ -798,6 +798,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
@@ -813,6 +814,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     else if (a.pro == 2 && a.epi == 0) ntt_fwd_cluster<LOGN, 2, 0><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 2 && a.epi == 3) ntt_fwd_cluster<LOGN, 2, 3><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 0 && a.epi == 2) ntt_fwd_cluster<LOGN, 0, 2><<<grid, C::T, smem, st>>>(a);
+    else if (a.pro == 1 && a.epi == 2) ntt_fwd_cluster<LOGN, 1, 2><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 0 && a.epi == 3) ntt_fwd_cluster<LOGN, 0, 3><<<grid, C::T, smem, st>>>(a);
     else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(a);
     return launched();

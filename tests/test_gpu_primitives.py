@@ -480,3 +480,28 @@ def test_fp64_base_conversions_match_oracle(N, L, dnum, monkeypatch):
         outs.append([to_numpy_u64(x) for x in (rot, sq, rs, rs2, rs3)])
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("N,L,dnum", [(8192, 7, 2), (16384, 7, 2)])
+def test_single_special_prime_moddown_matches_oracle(N, L, dnum, monkeypatch):
+    """K = 1 special prime (BASELINE config 3): the ModDown conversion is
+    y mod q_t, read straight from the INTT'd special limb by the NTT's lift
+    prologue.  Rotation and square+relinearise against the oracle, and
+    against the base-conversion kernel path (BCN_K1_LIFT=0)."""
+    outs = []
+    for lift in ("1", "0"):
+        monkeypatch.setenv("BCN_K1_LIFT", lift)
+        hp = make_params(N, L, 50, dnum=dnum, n_special=1, seed=13)
+        op = O.make_params(N, L, 50, dnum=dnum, n_special=1, seed=13)
+        assert list(hp.q) == op.q and list(hp.p) == op.p and len(hp.p) == 1
+        eng, orc = Engine(hp), O.Oracle(op)
+        rng = np.random.default_rng(23)
+        v, ct, oc = _enc2(eng, orc, N, rng)
+        rot = eng.rotate(ct, 9, L)
+        _assert_ct(rot, [orc.rotate(oc[i], 9) for i in range(2)])
+        eng.keygen_relin()
+        sq = eng.mul_cc(ct, ct, L)
+        _assert_ct(sq, [orc.mul_cc(oc[i], oc[i]) for i in range(2)])
+        outs.append([to_numpy_u64(rot), to_numpy_u64(sq)])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
