@@ -1318,8 +1318,11 @@ int bcn_modup(bcn_ctx* c, uint64_t* U, const uint64_t* ct, int ct_nlimb, int G, 
 // N = 2^13 / 2^14: the INTT of the special limbs folds (P/p_k)^-1 into its last
 // stage (outputs y_k), then ONE fused cluster NTT converts y -> q_t in its
 // prologue and applies the combine + addend in its epilogue; other N: staged.
+// fU / fkey (optional, fused form): A's q-limbs were not materialised; the NTT's
+// epilogue computes them as the key-switch inner product sum_d sigma(U_d) key_d.
 static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int level, const u64* addend,
-                        long long as, int add_c1, u32 g, const LevelTables* T, u64* Z, cudaStream_t st) {
+                        long long as, int add_c1, u32 g, const LevelTables* T, u64* Z, cudaStream_t st,
+                        const u64* fU = nullptr, const u64* fkey = nullptr) {
     const long long N = c->N;
     const int nl = level + 1, next = nl + c->K;
     Limbs ext = limbs_ext(c, level);
@@ -1362,6 +1365,16 @@ static int moddown_tail(bcn_ctx* c, u64* out, long long os, u64* A, int G, int l
         a.epi_c = A;
         a.epi_cps = (long long)next * N;
         a.epi_cls = N;
+        if (fU) {
+            a.epi = 4;
+            a.epi_U = fU;
+            a.epi_Ups = (long long)T->ndig * next * N;
+            a.epi_Uds = (long long)next * N;
+            a.epi_key = fkey;
+            a.epi_kds = 2LL * c->nbasis * N;
+            a.epi_kcs = (long long)c->nbasis * N;
+            a.epi_ndig = T->ndig;
+        }
         a.epi_tab = T->pinv;
         a.epi_add = addend;
         a.epi_aps = as;
@@ -1388,6 +1401,14 @@ static int keyswitch_tail(bcn_ctx* c, u64* out, long long os, const u64* U, int 
     Limbs ext = limbs_ext(c, level);
     u64* A = tmp;                                   // [G][2][next][N]
     u64* Z = A + (size_t)G * 2 * next * N;          // [G][2][nl][N]
+    if ((c->logn == 13 || c->logn == 14) && os == 2LL * nl * N && !getenv_flag_off("BCN_FUSED_MODDOWN") &&
+        !getenv_flag_off("BCN_FUSED_INNER")) {
+        // inner product of the special limbs only (the INTT needs them); the q-limbs'
+        // inner products are computed by the ModDown NTT's epilogue (epilogue 4)
+        CUDA_TRY(inner_op(A, U, G, next, ndig, c->logn, (u32)g, key, 2LL * c->nbasis * N, (long long)c->nbasis * N,
+                          ext, ext, c->pr, st, nl, c->K));
+        return moddown_tail(c, out, os, A, G, level, addend, as, add_c1, (u32)g, T, Z, st, U, key);
+    }
     CUDA_TRY(inner_op(A, U, G, next, ndig, c->logn, (u32)g, key, 2LL * c->nbasis * N, (long long)c->nbasis * N, ext,
                       ext, c->pr, st));
     // INTT of the special limbs of both components

@@ -101,7 +101,8 @@ struct Prologue {             // MODE 0 plain, 1 rescale lift, 2 ModDown base co
 // fused epilogue: what the forward transform writes for canonical result v at j
 template <int MODE>
 struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top^-1, 2 ModDown combine,
-                              // 3 merged ModDown + rescale: (c - v) (P q_l)^-1 + addend q_l^-1
+                              // 3 merged ModDown + rescale: (c - v) (P q_l)^-1 + addend q_l^-1,
+                              // 4 ModDown combine with c = the key-switch inner product computed here
     u64* out;
     const u64* c;
     u64 q, w, wp;
@@ -109,9 +110,24 @@ struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top
     u32 g = 1;
     int logn = 0;
     u64 w2 = 0, wp2 = 0;
+    const u64* U = nullptr;     // mode 4: U[d * uds + sigma(j)] (this ct, this limb)
+    const u64* kp = nullptr;    //         key[d * kds + j] (this component, this limb)
+    long long uds = 0, kds = 0;
+    int ndig = 0;
+    u64 qinv_neg = 0, inv1 = 0;
     __device__ __forceinline__ u64 operator()(int j, u64 v) const {
         if constexpr (MODE == 0) {
             return v;
+        } else if constexpr (MODE == 4) {
+            // the IMAD-pipe inner product runs inside the FP64-pipe NTT: no A round trip
+            const int sj = g == 1u ? j : (int)automorph_src((u32)j, g, logn);
+            Acc4 acc;
+            acc.zero();
+            for (int d = 0; d < ndig; d++) acc.mac(__ldg(U + d * uds + sj), __ldg(kp + d * kds + j));
+            const u64 a = acc.reduce(q, qinv_neg, inv1);
+            u64 r = shoup(a + q - v, w, wp, q);
+            if (add) r = add_mod(r, add[sj], q);
+            return r;
         } else {
             u64 r = shoup(c[j] + q - v, w, wp, q);
             if constexpr (MODE == 2) {
@@ -583,11 +599,21 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     Epilogue<EM> epi;
     epi.out = g;
     epi.q = q;
-    if constexpr (EM == 1 || EM == 2 || EM == 3) {
-        epi.c = a.epi_c + (size_t)poly * a.epi_cps + (size_t)t * a.epi_cls;
+    if constexpr (EM == 1 || EM == 2 || EM == 3 || EM == 4) {
+        epi.c = EM == 4 ? nullptr : a.epi_c + (size_t)poly * a.epi_cps + (size_t)t * a.epi_cls;
         epi.w = a.epi_tab[2 * t];
         epi.wp = a.epi_tab[2 * t + 1];
-        if constexpr (EM == 2 || EM == 3) {
+        if constexpr (EM == 4) {
+            const int kt = a.limbs.prime[t];
+            epi.U = a.epi_U + (size_t)(poly >> 1) * a.epi_Ups + (size_t)t * C::N;
+            epi.uds = a.epi_Uds;
+            epi.kp = a.epi_key + (size_t)(poly & 1) * a.epi_kcs + (size_t)kt * C::N;
+            epi.kds = a.epi_kds;
+            epi.ndig = a.epi_ndig;
+            epi.qinv_neg = a.pr[pidx].qinv_neg;
+            epi.inv1 = a.pr[pidx].pad[2];
+        }
+        if constexpr (EM == 2 || EM == 3 || EM == 4) {
             const int comp = poly & 1;
             const long long acs = a.epi_acs ? a.epi_acs : (long long)a.limbs.n * C::N;
             epi.add = (a.epi_add && (comp == 0 || a.epi_add_c1))
@@ -799,6 +825,8 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
@@ -815,6 +843,8 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     else if (a.pro == 2 && a.epi == 3) ntt_fwd_cluster<LOGN, 2, 3><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 0 && a.epi == 2) ntt_fwd_cluster<LOGN, 0, 2><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 1 && a.epi == 2) ntt_fwd_cluster<LOGN, 1, 2><<<grid, C::T, smem, st>>>(a);
+    else if (a.pro == 0 && a.epi == 4) ntt_fwd_cluster<LOGN, 0, 4><<<grid, C::T, smem, st>>>(a);
+    else if (a.pro == 1 && a.epi == 4) ntt_fwd_cluster<LOGN, 1, 4><<<grid, C::T, smem, st>>>(a);
     else if (a.pro == 0 && a.epi == 3) ntt_fwd_cluster<LOGN, 0, 3><<<grid, C::T, smem, st>>>(a);
     else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(a);
     return launched();

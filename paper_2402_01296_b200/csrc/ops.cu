@@ -502,12 +502,12 @@ template <int BLK>
 __global__ void __launch_bounds__(256) inner_kernel(u64* __restrict__ A, const u64* __restrict__ U, int next,
                                                     int ndig, int logn, u32 g, const u64* __restrict__ key,
                                                     long long key_digit_stride, long long key_comp_stride,
-                                                    Limbs ext, Limbs keyl, const PrimeInfo* __restrict__ pr) {
+                                                    Limbs ext, Limbs keyl, const PrimeInfo* __restrict__ pr, int t0) {
     extern __shared__ u64 sm[];
     const int N = 1 << logn;
     const int logb = __ffs(BLK) - 1;
     const int blk = blockIdx.x;
-    const int t = blockIdx.y;
+    const int t = t0 + blockIdx.y;
     const long long p = blockIdx.z;
     const PrimeInfo& P = pr[ext.prime[t]];
     const u64 q = P.q;
@@ -538,23 +538,25 @@ __global__ void __launch_bounds__(256) inner_kernel(u64* __restrict__ A, const u
 
 cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
                      long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
-                     const PrimeInfo* pr, cudaStream_t st) {
+                     const PrimeInfo* pr, cudaStream_t st, int t0, int tcnt) {
     const int N = 1 << logn;
+    if (tcnt < 0) tcnt = next - t0;
+    if (tcnt <= 0) return cudaSuccess;
     if (N >= 1024) {
         constexpr int BLK = 1024;
         size_t smem = (size_t)ndig * BLK * sizeof(u64);
         static bool cfg = false;
         if (!cfg) { cudaFuncSetAttribute(inner_kernel<BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
-        dim3 grid(N / BLK, next, npoly);
+        dim3 grid(N / BLK, tcnt, npoly);
         inner_kernel<BLK><<<grid, 256, smem, st>>>(A, U, next, ndig, logn, g, key, key_digit_stride,
-                                                   key_comp_stride, ext, keyl, pr);
+                                                   key_comp_stride, ext, keyl, pr, t0);
     } else {
         // small rings: one block covers the whole polynomial
         size_t smem = (size_t)ndig * N * sizeof(u64);
-        dim3 grid(1, next, npoly);
+        dim3 grid(1, tcnt, npoly);
         switch (N) {
 #define BCN_SMALL(NN) case NN: inner_kernel<NN><<<grid, 256, smem, st>>>(A, U, next, ndig, logn, g, key, \
-                        key_digit_stride, key_comp_stride, ext, keyl, pr); break;
+                        key_digit_stride, key_comp_stride, ext, keyl, pr, t0); break;
             BCN_SMALL(8) BCN_SMALL(16) BCN_SMALL(32) BCN_SMALL(64) BCN_SMALL(128) BCN_SMALL(256) BCN_SMALL(512)
 #undef BCN_SMALL
             default: return cudaErrorInvalidValue;

@@ -79,6 +79,13 @@ struct NttArgs {
     // addend component stride epi_acs (0: limbs.n * N)
     const u64* epi_tab2;
     long long epi_acs;
+    // epilogue 4 (fused key-switch inner product): c[j] of epilogue 2 is computed on the fly as
+    // REDC(sum_d U[ct][d][t][sigma(j)] * key[d][comp][t][j]) (U: [G][ndig][next][N], key Montgomery)
+    const u64* epi_U;
+    long long epi_Ups, epi_Uds;
+    const u64* epi_key;
+    long long epi_kds, epi_kcs;
+    int epi_ndig;
     // skipped limbs (skip_alpha) copy copy_src[(poly / skip_dnum) * copy_stride + t * N + n]
     // instead of being left untouched (ModUp: the digit's own NTT-domain limbs)
     const u64* copy_src;
@@ -191,7 +198,7 @@ cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, 
                      const ConvTable* tab, cudaStream_t st, const FConvSet* fc = nullptr);
 cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
                      long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
-                     const PrimeInfo* pr, cudaStream_t st);
+                     const PrimeInfo* pr, cudaStream_t st, int t0 = 0, int tcnt = -1);
 cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
                             const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st,
                             const FConv* fc = nullptr);
