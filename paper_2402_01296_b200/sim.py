@@ -841,6 +841,10 @@ def materialize_conv(accs: list) -> bool:
             srcs.append(t[1])
             Us.append(None)
             gals.append(1)
+    if int(srcs[0].shape[0]) < int(os.environ.get("BCN_CONV_TC_MIN_G", "4")):
+        # a handful of slot sets (single-image latency) fills a tiny fraction of the
+        # tensor-core tiles (M = 2G columns): one CUDA-core rotation sum per output is faster
+        return False
     pts = [[t[3] if t[0] == "rot" else t[2] for t in c._terms] for c in lazy]
     layout = _conv_layout(int(srcs[0].shape[0]))
     out = eng.conv_ks_mac(srcs, Us, gals, _planes_for(ctx, pts, lvl, ext=True, layout=layout), len(lazy), lvl,
