@@ -149,6 +149,13 @@ __device__ __forceinline__ u64 signed_to_residue(i64 v, u64 q) {
     i64 r = v % (i64)q;
     return r < 0 ? (u64)(r + (i64)q) : (u64)r;
 }
+// the same without a 64-bit division: |v| mod q by a Shoup multiply by 1
+// (inv1 = floor(2^64 / q)), then the sign
+__device__ __forceinline__ u64 signed_to_residue_fast(i64 v, u64 q, u64 inv1) {
+    const u64 a = v < 0 ? (u64)0 - (u64)v : (u64)v;
+    const u64 r = shoup(a, 1ull, inv1, q);
+    return v < 0 ? neg_mod(r, q) : r;
+}
 
 // ---- exact u128 multiply-accumulate (4 x 32-bit words, no reduction) ----
 // acc += a*b for a, b < 2^61: four IMAD.WIDE.U32 (a0b0 and a1b1 straight into

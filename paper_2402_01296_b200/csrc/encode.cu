@@ -29,11 +29,11 @@ __global__ void encode_kernel(u64* __restrict__ out, long long os, const double*
     }
     __syncthreads();
     for (int len = S; len >= 2; len >>= 1) {
-        const int h = len >> 1, lenq = len << 2;
+        const int h = len >> 1, lenq = len << 2, lgh = __ffs(h) - 1;
         for (int pr_ = threadIdx.x; pr_ < (S >> 1); pr_ += blockDim.x) {
-            const int blk = pr_ / h, jj = pr_ - blk * h;
+            const int blk = pr_ >> lgh, jj = pr_ & (h - 1);      // h, lenq: powers of two
             const int i1 = blk * len + jj, i2 = i1 + h;
-            const int idx = (lenq - (ft.rot[jj] % lenq)) * (M / lenq);
+            const int idx = (lenq - (ft.rot[jj] & (lenq - 1))) << (logn + 1 - lgh - 3);   // M / lenq, M = 2N = 2^(logn+1), lenq = 8h
             const double tr = ft.re[idx], ti = ft.im[idx];
             const double ar = xr[i1], ai = xi[i1], cr = xr[i2], ci = xi[i2];
             const double ur = __dadd_rn(ar, cr), ui = __dadd_rn(ai, ci);
@@ -57,9 +57,9 @@ __global__ void encode_kernel(u64* __restrict__ out, long long os, const double*
             ci += cbd21(draw(seed, 2u, 0u, id_base + p, (u32)(i + S)));
         }
         for (int t = 0; t < limbs.n; t++) {
-            const u64 q = pr[limbs.prime[t]].q;
-            o[(long long)t * N + i] = signed_to_residue(cr, q);
-            o[(long long)t * N + i + S] = signed_to_residue(ci, q);
+            const PrimeInfo& P = pr[limbs.prime[t]];
+            o[(long long)t * N + i] = signed_to_residue_fast(cr, P.q, P.pad[2]);
+            o[(long long)t * N + i + S] = signed_to_residue_fast(ci, P.q, P.pad[2]);
         }
     }
 }
@@ -128,11 +128,11 @@ __global__ void decode_kernel(double* __restrict__ out, int nout, const u64* __r
     }
     __syncthreads();
     for (int len = 2; len <= S; len <<= 1) {
-        const int h = len >> 1, lenq = len << 2;
+        const int h = len >> 1, lenq = len << 2, lgh = __ffs(h) - 1;
         for (int pr_ = threadIdx.x; pr_ < (S >> 1); pr_ += blockDim.x) {
-            const int blk = pr_ / h, jj = pr_ - blk * h;
+            const int blk = pr_ >> lgh, jj = pr_ & (h - 1);      // h, lenq: powers of two
             const int i1 = blk * len + jj, i2 = i1 + h;
-            const int idx = (ft.rot[jj] % lenq) * (M / lenq);
+            const int idx = (ft.rot[jj] & (lenq - 1)) << (logn + 1 - lgh - 3);   // M / lenq, M = 2N = 2^(logn+1), lenq = 8h
             const double tr = ft.re[idx], ti = ft.im[idx];
             const double ur = xr[i1], ui = xi[i1], cr = xr[i2], ci = xi[i2];
             const double vr = __dsub_rn(__dmul_rn(cr, tr), __dmul_rn(ci, ti));
@@ -195,7 +195,8 @@ __global__ void sample_small_kernel(u64* __restrict__ out, long long os, int nli
         const uint4 o = draw(seed, domain, 0u, id_base + (u64)p * id_step, (u32)n);
         const i64 v = ternary ? (i64)(o.x % 3u) - 1 : cbd21(o);
         for (int t = 0; t < nlimb; t++)
-            out[p * os + ((long long)t << logn) + n] = signed_to_residue(v, pr[limbs.prime[t]].q);
+            out[p * os + ((long long)t << logn) + n] = signed_to_residue_fast(v, pr[limbs.prime[t]].q,
+                                                                                pr[limbs.prime[t]].pad[2]);
     }
 }
 
