@@ -172,3 +172,21 @@ def test_depth_exhaustion_is_exact():
     assert ct.level == 0
     with pytest.raises(AssertionError):
         o.rescale(ct)
+
+
+@pytest.mark.parametrize("N,L,dnum,K", [(16384, 14, 3, None), (8192, 10, 3, None), (16384, 7, 2, 1)])
+def test_default_chains_are_fp64_eligible(N, L, dnum, K):
+    """The default chains (q0 and the specials at max(50, scale_bits) bits) put
+    every prime in (2^49, 2^50): the condition under which the engine runs
+    the NTT, the base conversions and the Mul_CC tensor product on the FP64
+    pipe (csrc/api.cu fp_conv).  Primes stay distinct and 1 mod 2N."""
+    from paper_2402_01296_b200.params import make_params
+    hp = make_params(N, L, 50, dnum=dnum, n_special=K)
+    op = O.make_params(N, L, 50, dnum=dnum, n_special=K)
+    basis = list(hp.q) + list(hp.p)
+    assert basis == op.q + op.p
+    assert len(set(basis)) == len(basis)
+    assert all((1 << 49) < q < (1 << 50) and q % (2 * N) == 1 for q in basis)
+    # a scale above 2^50 keeps q0 / specials at least as wide as the rescale primes
+    wide = make_params(N, 4, 55, dnum=dnum)
+    assert all(q.bit_length() == 55 for q in list(wide.q) + list(wide.p))
