@@ -6,9 +6,13 @@
 //                (NTT twiddles, q_l^-1, P^-1, base-conversion scalars);
 //   * Montgomery REDC -- stored operands kept as x*2^64 mod q (switching
 //                keys, plaintext multipliers, the secret key);
-//   * u128 lazy accumulation of several products followed by ONE REDC.
+//   * u128 lazy accumulation of several products followed by ONE REDC;
+//   * FP64 (primes q < 2^50): exact integers in doubles, a*w mod q by the
+//     FMA two-product and a rounded quotient (fmm / fred below) -- on the
+//     FP64 pipe, which the integer kernels leave idle (NTT butterflies,
+//     base conversions, the Mul_CC tensor product).
 // Every value written back to HBM is canonical ([0, q)) so ciphertexts are
-// comparable bit for bit with oracle/ckks.py.
+// comparable bit for bit with oracle/ckks.py, whichever flavour produced them.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

@@ -15,8 +15,10 @@
 //            last pass writes HBM.
 //   inverse: the mirror image -- local passes first, one cluster barrier,
 //            pass A reads its inputs from the owners' SMEM.
-// Butterflies, twiddle indexing, lazy bounds and output order are exactly
-// those of ntt.cu (same contract with the oracle).
+// Output order and values are exactly those of ntt.cu (same contract with
+// the oracle).  The integer butterflies follow ntt.cu's lazy bounds; the
+// FP64 butterflies (primes < 2^50) have their own bounds and a
+// pass-transposed twiddle table (see "FP64 butterflies" below).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
