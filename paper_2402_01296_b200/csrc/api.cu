@@ -181,6 +181,8 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.tw = c->tw;
     a.twt = c->twt;
     a.twf = c->fp_ntt ? c->twf : nullptr;
+    a.fp_all = 1;
+    for (int i = 0; i < l.n; i++) a.fp_all &= c->primes[l.prime[i]] < (1ull << 50) ? 1 : 0;
     a.pr = c->pr;
     a.skip_alpha = 0;
     a.skip_dnum = 1;
