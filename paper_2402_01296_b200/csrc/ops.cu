@@ -471,6 +471,56 @@ __global__ void modup_kernel(u64* __restrict__ U, const u64* __restrict__ xc, lo
     (void)nq;
 }
 
+// FP64 form: two coefficients per thread (n, n + blockDim) share every
+// constant-bank load of the conversion table (the kernel is issue-bound)
+template <int A>
+__global__ void modup_fp_kernel(u64* __restrict__ U, const u64* __restrict__ xc, long long xc_stride,
+                                const u64* __restrict__ xn, long long x_stride, int next, int alpha, int ndig, int logn,
+                                Limbs ext, const PrimeInfo* __restrict__ pr, const ConvTable* __restrict__ tab,
+                                const __grid_constant__ FConvSet fc) {
+    constexpr int YA = A;
+    const int N = 1 << logn;
+    const int n = blockIdx.x * 2 * blockDim.x + threadIdx.x;   // and n + blockDim.x (N >= 2 blockDim)
+    const long long p = blockIdx.y;
+    const int j = blockIdx.z;
+    const ConvTable& T = tab[j];
+    const int i0 = j * alpha;
+    const int na = T.n_src;
+    const u64* xcp = xc + p * xc_stride + n;
+    const u64* xnp = xn + p * x_stride + n;
+    u64* Up = U + (p * ndig + j) * (long long)next * N + n;
+    const int h = blockDim.x;
+    double y0[YA], y1[YA];
+#pragma unroll
+    for (int i = 0; i < YA; i++) {
+        if (i < na) {
+            const PrimeInfo& P = pr[ext.prime[i0 + i]];
+            const long long o = (long long)(i0 + i) * N;
+            y0[i] = fload(shoup(__ldg(xcp + o), T.hatinv[i], T.hatinv_p[i], P.q));
+            y1[i] = fload(shoup(__ldg(xcp + o + h), T.hatinv[i], T.hatinv_p[i], P.q));
+            Up[o] = __ldg(xnp + o);
+            Up[o + h] = __ldg(xnp + o + h);
+        } else {
+            y0[i] = y1[i] = 0.0;
+        }
+    }
+    const FConv& F = fc.d[j];
+    for (int t = 0; t < next; t++) {
+        if (t >= i0 && t < i0 + na) continue;
+        const double2 f = F.fq[t];
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < YA; i++)
+            if (i < na) {
+                const double2 hh = F.h[i][t];
+                a0 = __dadd_rn(a0, fmm(y0[i], hh.x, hh.y, f.x));
+                a1 = __dadd_rn(a1, fmm(y1[i], hh.x, hh.y, f.x));
+            }
+        Up[(long long)t * N] = fcanon(a0, f.y, f.x);
+        Up[(long long)t * N + h] = fcanon(a1, f.y, f.x);
+    }
+}
+
 cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, long long x_stride, int npoly, int nq,
                      int next, int alpha, int ndig, int logn, const Limbs& ext, const PrimeInfo* pr,
                      const ConvTable* tab, cudaStream_t st, const FConvSet* fcp) {
@@ -480,6 +530,16 @@ cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, 
     static FConvSet none;
     const int use_fp = fcp && alpha <= BCN_FC_SRC && next <= BCN_FC_TGT && ndig <= 3;
     const FConvSet& fc = use_fp ? *fcp : none;
+    if (use_fp && N >= 512 && alpha >= 1) {
+        const dim3 g2(N / 512, npoly, ndig);
+        switch (alpha) {
+#define BCN_MF(AA) case AA: modup_fp_kernel<AA><<<g2, 256, 0, st>>>(U, xc, xc_stride, xn, x_stride, next, alpha, ndig, \
+                                                                    logn, ext, pr, tab, *fcp); return launched();
+            BCN_MF(1) BCN_MF(2) BCN_MF(3) BCN_MF(4) BCN_MF(5) BCN_MF(6) BCN_MF(7) BCN_MF(8)
+#undef BCN_MF
+            default: break;
+        }
+    }
     switch (alpha) {
 #define BCN_MU(AA) case AA: modup_kernel<AA><<<grid, tpb, 0, st>>>(U, xc, xc_stride, xn, x_stride, nq, next, alpha, \
                                                                   ndig, logn, ext, pr, tab, fc, use_fp); break;
