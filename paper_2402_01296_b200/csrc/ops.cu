@@ -1019,6 +1019,39 @@ __global__ void moddown_conv_kernel(u64* __restrict__ Z, const u64* __restrict__
     }
 }
 
+// FP64 form, two coefficients per thread (see modup_fp_kernel)
+template <int KK>
+__global__ void moddown_conv_fp_kernel(u64* __restrict__ Z, const u64* __restrict__ A, long long a_stride, int nq,
+                                       int logn, Limbs ext, const PrimeInfo* __restrict__ pr,
+                                       const ConvTable* __restrict__ tab, const __grid_constant__ FConv fc) {
+    const int N = 1 << logn;
+    const int n = blockIdx.x * 2 * blockDim.x + threadIdx.x;   // and n + blockDim.x
+    const int h = blockDim.x;
+    const long long p = blockIdx.y;
+    const ConvTable& T = *tab;
+    double y0[KK], y1[KK];
+    const u64* ap = A + p * a_stride + (long long)nq * N + n;
+#pragma unroll
+    for (int k = 0; k < KK; k++) {
+        const PrimeInfo& P = pr[ext.prime[nq + k]];
+        y0[k] = fload(shoup(__ldg(ap + (long long)k * N), T.hatinv[k], T.hatinv_p[k], P.q));
+        y1[k] = fload(shoup(__ldg(ap + (long long)k * N + h), T.hatinv[k], T.hatinv_p[k], P.q));
+    }
+    u64* zp = Z + p * (long long)nq * N + n;
+    for (int i = 0; i < nq; i++) {
+        const double2 f = fc.fq[i];
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < KK; k++) {
+            const double2 hh = fc.h[k][i];
+            a0 = __dadd_rn(a0, fmm(y0[k], hh.x, hh.y, f.x));
+            a1 = __dadd_rn(a1, fmm(y1[k], hh.x, hh.y, f.x));
+        }
+        zp[(long long)i * N] = fcanon(a0, f.y, f.x);
+        zp[(long long)i * N + h] = fcanon(a1, f.y, f.x);
+    }
+}
+
 cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
                             const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st,
                             const FConv* fcp) {
@@ -1028,6 +1061,16 @@ cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly,
     static FConv none;
     const int use_fp = fcp && K <= BCN_FC_SRC && nq <= BCN_FC_TGT;
     const FConv& fc = use_fp ? *fcp : none;
+    if (use_fp && N >= 512) {
+        const dim3 g2(N / 512, npoly);
+        switch (K) {
+#define BCN_MF(KV) case KV: moddown_conv_fp_kernel<KV><<<g2, 256, 0, st>>>(Z, A, a_stride, nq, logn, ext, pr, tab, \
+                                                                           *fcp); return launched();
+            BCN_MF(1) BCN_MF(2) BCN_MF(3) BCN_MF(4) BCN_MF(5) BCN_MF(6) BCN_MF(7) BCN_MF(8)
+#undef BCN_MF
+            default: break;
+        }
+    }
     switch (K) {
 #define BCN_MC(KV) case KV: moddown_conv_kernel<KV><<<grid, tpb, 0, st>>>(Z, A, a_stride, nq, K, logn, ext, pr, tab, fc, use_fp); break;
         BCN_MC(1) BCN_MC(2) BCN_MC(3) BCN_MC(4) BCN_MC(5) BCN_MC(6) BCN_MC(7) BCN_MC(8) BCN_MC(9)
