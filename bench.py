@@ -429,7 +429,7 @@ def main():
             "peak_kind": peak_kind, "traffic": tr, "algorithmic_bytes_per_launch": ntt["bytes"],
             "algorithmic_bytes_per_unit": "16 B per coefficient (one u64 read + one u64 write)",
             "launch_ms": ntt["ms"], "note": "butterflies on the FP64 pipe (all primes < 2^50); no single "
-                                            "unit saturated (ncu: FP64 pipe ~53%, L1 wavefronts ~47%, DRAM ~25%): "
+                                            "unit saturated (ncu: FP64 pipe ~56%, L1 wavefronts ~54%, DRAM ~28%): "
                                             "latency-bound; frac is the HBM-roofline fraction"}
         extras["roofline_intt14"] = {"achieved": n14["inv"]["GBps"], "frac": n14["inv"]["GBps"] / peak}
         for name in ("ntt", "intt", "mac"):
