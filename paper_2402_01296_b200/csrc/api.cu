@@ -187,6 +187,7 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.skip_alpha = 0;
     a.skip_dnum = 1;
     a.skip_level = 0;
+    a.grid_pm = 0;
     a.src = nullptr;
     a.src_poly_stride = 0;
     a.src_limb_stride = 0;

@@ -50,16 +50,19 @@ template <int LOGN> struct CCfg {
 #endif
 };
 
-// grid order: consecutive clusters transform the same limb (same prime, same
-// twiddle table) of consecutive polys, so the twiddles stay hot in L1/L2
-// (BCN_NTT_LIMB_MAJOR restores limb-fastest order for comparison)
-#ifdef BCN_NTT_LIMB_MAJOR
-template <int LOGCS> __device__ __forceinline__ int ntt_limb() { return blockIdx.x >> LOGCS; }
-template <int LOGCS> __device__ __forceinline__ int ntt_poly() { return blockIdx.y; }
-#else
-template <int LOGCS> __device__ __forceinline__ int ntt_limb() { return blockIdx.y; }
-template <int LOGCS> __device__ __forceinline__ int ntt_poly() { return blockIdx.x >> LOGCS; }
-#endif
+// grid order: limb fastest -- consecutive clusters transform consecutive limbs
+// of one poly, i.e. one contiguous run of HBM.  With the FP64 butterflies this
+// measured faster than poly-fastest order (same prime, same twiddle table for
+// consecutive clusters), which the integer kernels had preferred: N = 2^14
+// forward 0.115 vs 0.120, inverse 0.105 vs 0.109 us per limb-poly; the cifar3
+// forward is unchanged.  Poly-fastest order is kept for launches with more
+// than 65535 polys (grid.y limit) and under BCN_NTT_POLY_MAJOR=1.
+template <int LOGCS> __device__ __forceinline__ int ntt_limb(const NttArgs& a) {
+    return a.grid_pm ? blockIdx.y : blockIdx.x >> LOGCS;
+}
+template <int LOGCS> __device__ __forceinline__ int ntt_poly(const NttArgs& a) {
+    return a.grid_pm ? blockIdx.x >> LOGCS : blockIdx.y;
+}
 
 // cluster barrier without the release fence of cluster.sync(): for the
 // barriers that only need the peers to have started / to be done reading,
@@ -552,7 +555,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ u64 sm[];
     const int rank = (int)cluster.block_rank();
-    const int t = ntt_limb<C::LOGCS>(), poly = ntt_poly<C::LOGCS>();
+    const int t = ntt_limb<C::LOGCS>(a), poly = ntt_poly<C::LOGCS>(a);
     if (cskip(a, t, poly)) {                // all CTAs of the cluster skip together
         if (a.copy_src) {                    // ModUp: the digit's own limb, already in NTT form
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
@@ -773,7 +776,7 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ u64 sm[];
     const int rank = (int)cluster.block_rank();
-    const int t = ntt_limb<C::LOGCS>(), poly = ntt_poly<C::LOGCS>();
+    const int t = ntt_limb<C::LOGCS>(a), poly = ntt_poly<C::LOGCS>(a);
     u64* peers[C::CS];
 #pragma unroll
     for (int r = 0; r < C::CS; r++) peers[r] = cluster.map_shared_rank(sm, r);
@@ -846,27 +849,26 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         cudaFuncSetAttribute(ntt_inv_cluster<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-#ifdef BCN_NTT_LIMB_MAJOR
-    dim3 grid(C::CS * nlimbs, npolys);
-#else
-    dim3 grid(C::CS * npolys, nlimbs);
-#endif
+    static const bool pm_env = getenv("BCN_NTT_POLY_MAJOR") && getenv("BCN_NTT_POLY_MAJOR")[0] == '1';
+    NttArgs b = a;
+    b.grid_pm = (pm_env || npolys > 65535) ? 1 : 0;
+    const dim3 grid = b.grid_pm ? dim3(C::CS * npolys, nlimbs) : dim3(C::CS * nlimbs, npolys);
     // FP64-only instantiations where they measured faster (the inverse, the merged tails
     // <0,3>: 74.8 -> 70.9 ms per cifar3 forward); the plain forward <0,0> measured slower
     const bool fpo = a.twf && a.fp_all;
-    if (inverse && a.twf && a.fp_all) ntt_inv_cluster<LOGN, true><<<grid, C::T, smem, st>>>(a);
-    else if (inverse) ntt_inv_cluster<LOGN, false><<<grid, C::T, smem, st>>>(a);
-    else if (fpo && a.pro == 0 && a.epi == 3) ntt_fwd_cluster<LOGN, 0, 3, true><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 2 && a.epi == 2) ntt_fwd_cluster<LOGN, 2, 2><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 2 && a.epi == 0) ntt_fwd_cluster<LOGN, 2, 0><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 2 && a.epi == 3) ntt_fwd_cluster<LOGN, 2, 3><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 0 && a.epi == 2) ntt_fwd_cluster<LOGN, 0, 2><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 1 && a.epi == 2) ntt_fwd_cluster<LOGN, 1, 2><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 0 && a.epi == 4) ntt_fwd_cluster<LOGN, 0, 4><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 1 && a.epi == 4) ntt_fwd_cluster<LOGN, 1, 4><<<grid, C::T, smem, st>>>(a);
-    else if (a.pro == 0 && a.epi == 3) ntt_fwd_cluster<LOGN, 0, 3><<<grid, C::T, smem, st>>>(a);
-    else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(a);
+    if (inverse && a.twf && a.fp_all) ntt_inv_cluster<LOGN, true><<<grid, C::T, smem, st>>>(b);
+    else if (inverse) ntt_inv_cluster<LOGN, false><<<grid, C::T, smem, st>>>(b);
+    else if (fpo && a.pro == 0 && a.epi == 3) ntt_fwd_cluster<LOGN, 0, 3, true><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 1 && a.epi == 1) ntt_fwd_cluster<LOGN, 1, 1><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 2 && a.epi == 2) ntt_fwd_cluster<LOGN, 2, 2><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 2 && a.epi == 0) ntt_fwd_cluster<LOGN, 2, 0><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 2 && a.epi == 3) ntt_fwd_cluster<LOGN, 2, 3><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 0 && a.epi == 2) ntt_fwd_cluster<LOGN, 0, 2><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 1 && a.epi == 2) ntt_fwd_cluster<LOGN, 1, 2><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 0 && a.epi == 4) ntt_fwd_cluster<LOGN, 0, 4><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 1 && a.epi == 4) ntt_fwd_cluster<LOGN, 1, 4><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 0 && a.epi == 3) ntt_fwd_cluster<LOGN, 0, 3><<<grid, C::T, smem, st>>>(b);
+    else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(b);
     return launched();
 }
 
