@@ -275,12 +275,13 @@ struct FQ {                     // per-prime FP64 constants
 // FP64 lazy-reduction schedule.  Twiddles are stored signed, |w| <= q/2, so
 // fmm(a, w) only needs |a| < 4q (quotient |a w / q| < 2^51) and returns
 // |v| <= 0.5q + |a| 2^-55 <= 0.63q.
-//   forward (CT): u is reduced on stages s = 3 mod 4; starting from
-//     canonical input every value stays <= 1.13q + 3 * 0.63q < 3.1q (< 4q);
+//   forward (CT): u is reduced on stages s = 4 mod 5; starting from
+//     canonical input (or a reduced stage, <= 1.13q) every value stays
+//     <= 1.13q + 4 * 0.63q < 3.7q (< 4q: fmm's input bound; < 8q: exact);
 //   inverse (GS): the sum is reduced on every other stage counted from the
 //     first (t = LOGN-1-s odd); every value stays <= 2q before a reduced
 //     stage and <= 1.25q after it, so u - v stays < 4q.
-__device__ __forceinline__ constexpr bool fwd_fred(int s) { return (s & 3) == 3; }
+__device__ __forceinline__ constexpr bool fwd_fred(int s) { return s % 5 == 4; }
 template <int LOGN> __device__ __forceinline__ constexpr bool inv_fred(int s) { return ((LOGN - 1 - s) & 1) == 1; }
 
 // pass A: the loads (issued before the cluster barrier that guards the
