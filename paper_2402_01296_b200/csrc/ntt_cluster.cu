@@ -458,20 +458,25 @@ __device__ __forceinline__ void dinv_pass(double* x, const u64* __restrict__ gin
     const int base = gi * (C::N >> S0) + (b % TL);
     const int lbase = base - rank * C::PART;
     if constexpr (FIRST) {
-        // coalesced HBM reads into SMEM, then the per-thread contiguous runs from SMEM
+        // coalesced HBM reads straight into SMEM (cp.async: no register staging),
+        // then the per-thread contiguous runs from SMEM
         static_assert(TL == 1, "first inverse pass is contiguous");
         const int j0 = rank * C::PART;
+        u64* su = reinterpret_cast<u64*>(sm);
 #pragma unroll
-        for (int m = 0; m < C::PART / (2 * C::T); m++) {
-            const int e = 2 * tid + m * 2 * C::T;
-            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gin + j0 + e);
-            sm[cswz(e)] = fload(v.x);
-            sm[cswz(e + 1)] = fload(v.y);
+        for (int m = 0; m < C::PART / C::T; m++) {
+            const int e = tid + m * C::T;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(su + cswz(e))), "l"(gin + j0 + e)
+                         : "memory");
         }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         __syncthreads();
-    }
 #pragma unroll
-    for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+        for (int k = 0; k < BS; k++) x[k] = fload(su[cswz(lbase + k)]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < BS; k++) x[k] = sm[cswz(lbase + k * TL)];
+    }
 #pragma unroll
     for (int ls = R - 1; ls >= 0; ls--) {
         const int h = BS >> (ls + 1);
