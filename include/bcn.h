@@ -62,13 +62,28 @@ int bcn_ctx_set_fft(bcn_ctx *ctx, const double *re, const double *im);
 int bcn_ctx_destroy(bcn_ctx *ctx);
 /* bytes of device memory held by tables + keys + scratch */
 int bcn_ctx_memory(bcn_ctx *ctx, uint64_t *bytes);
-/* drop the scratch arena (between workloads) */
+/* drop the scratch arena (between workloads); BCN_ERR_USAGE while frozen */
 int bcn_ctx_trim(bcn_ctx *ctx);
+/* freeze (delta = +1) / release (delta = -1) the context's arenas.  A CUDA
+ * graph captured over this context replays raw pointers into its scratch
+ * arenas and pointer tables; while any graph holds the context (freeze count
+ * > 0) a call that would grow or free an arena fails with BCN_ERR_USAGE
+ * instead of moving memory under the graph.  No reference counterpart: the
+ * reference has no device memory (graphs.py). */
+int bcn_ctx_freeze(bcn_ctx *ctx, int delta);
 
 /* ---- K1/K2: negacyclic NTT / INTT, in place.
  * data: u64[npoly][nlimb][N]; limb t is modulo basis prime (prime0 + t). */
 int bcn_ntt_fwd(bcn_ctx *ctx, uint64_t *data, int npoly, int nlimb, int prime0, void *stream);
 int bcn_ntt_inv(bcn_ctx *ctx, uint64_t *data, int npoly, int nlimb, int prime0, void *stream);
+/* Measurement only (bench.py roofline): while enabled, every NTT/INTT launch
+ * of every context is bracketed by a CUDA event pair on its stream.
+ * bcn_ntt_timing(1) clears and starts recording, (0) stops.
+ * bcn_ntt_timing_read syncs and fills 4 classes {plain fwd, plain inv,
+ * fused fwd, fused inv}: summed launch ms, algorithmic bytes (16 B per
+ * coefficient) and launch counts.  Never used inside a CUDA-graph capture. */
+int bcn_ntt_timing(int enable);
+int bcn_ntt_timing_read(double *ms, uint64_t *bytes, uint64_t *launches);
 
 /* ---- K9: encode_plain (sim.py:172-181) + CKKS canonical embedding.
  * vals: f64[nplain][vstride] (first vlen used, rest zero).  out:

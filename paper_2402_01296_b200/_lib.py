@@ -42,8 +42,11 @@ SIGNATURES = {
     "bcn_ctx_destroy": [_P],
     "bcn_ctx_memory": [_P, ctypes.POINTER(_U64)],
     "bcn_ctx_trim": [_P],
+    "bcn_ctx_freeze": [_P, _I],
     "bcn_ntt_fwd": [_P, _P, _I, _I, _I, _P],
     "bcn_ntt_inv": [_P, _P, _I, _I, _I, _P],
+    "bcn_ntt_timing": [_I],
+    "bcn_ntt_timing_read": [ctypes.POINTER(_D), ctypes.POINTER(_U64), ctypes.POINTER(_U64)],
     "bcn_encode": [_P, _P, _I, _I, _I, _D, _I, _I, _P, _P],
     "bcn_encrypt": [_P, _P, _I, _I, _I, _I, _D, _U64, _P, _P],
     "bcn_encrypt_devctr": [_P, _P, _I, _I, _I, _I, _D, _P, _P, _P],
@@ -128,3 +131,19 @@ def launch_count() -> int:
     v = ctypes.c_uint64()
     call("bcn_launch_count", ctypes.byref(v))
     return int(v.value)
+
+
+NTT_CLASSES = ("plain_fwd", "plain_inv", "fused_fwd", "fused_inv")
+
+
+def ntt_timing(enable: bool) -> None:
+    """Bracket every NTT launch with CUDA events (measurement only, bcn.h)."""
+    call("bcn_ntt_timing", int(bool(enable)))
+
+
+def ntt_timing_read() -> dict:
+    ms = (ctypes.c_double * 4)()
+    nb = (_U64 * 4)()
+    nl = (_U64 * 4)()
+    call("bcn_ntt_timing_read", ms, nb, nl)
+    return {c: {"ms": ms[i], "bytes": int(nb[i]), "launches": int(nl[i])} for i, c in enumerate(NTT_CLASSES)}

@@ -1,14 +1,19 @@
-"""In-tree build of libbcn.so (sm_100a) -- plain nvcc, no torch types in the ABI."""
+"""In-tree build of libbcn.so (sm_100a) -- plain nvcc, no torch types in the ABI.
+
+Each .cu is compiled to its own object in parallel (no relocatable device
+code: the translation units share only host-side symbols), then linked."""
 
 from __future__ import annotations
 
 import glob
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbcn.so")
+OBJ = os.path.join(HERE, "..", "build", "bcn_obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -17,7 +22,6 @@ FLAGS = [
     "-fmad=false",              # float64 embedding: same IEEE op order as the oracle
     "-Xcompiler", "-fPIC,-O3",
     "-Xptxas", "-O3",
-    "-shared", "-cudart", "shared",
 ]
 
 
@@ -25,22 +29,43 @@ def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _deps() -> list[str]:
+    return glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(HERE, "..", "include", "bcn.h")]
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [
-        os.path.join(HERE, "..", "include", "bcn.h")]
-    return any(os.path.getmtime(p) > t for p in deps)
+    return any(os.path.getmtime(p) > t for p in sources() + _deps())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     extra = os.environ.get("BCN_NVCC_EXTRA", "").split()   # experiments: e.g. -DBCN_CNTT_MINB=1
-    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"), *sources(), "-o", LIB + ".tmp"]
+    os.makedirs(OBJ, exist_ok=True)
+    inc = ["-I", os.path.join(HERE, "..", "include")]
+    newest_dep = max(os.path.getmtime(p) for p in _deps())
+
+    def compile_one(src: str) -> str:
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        if (not force and not extra and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(src), newest_dep)):
+            return obj
+        cmd = [NVCC, *FLAGS, *extra, *inc, "-c", src, "-o", obj + ".tmp"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "shared", *objs,
+           "-o", LIB + ".tmp"]
     if verbose:
-        print(" ".join(cmd))
+        print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

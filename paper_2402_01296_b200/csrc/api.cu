@@ -109,6 +109,7 @@ struct bcn_ctx {
     size_t scratch2_bytes = 0;
     void* ptr_dev = nullptr;  // device copy of a host pointer table (plane packing)
     size_t ptr_cap = 0;
+    int frozen = 0;           // > 0 while a captured CUDA graph holds pointers into the arenas (bcn_ctx_freeze)
     size_t table_bytes = 0, key_bytes = 0;
     u64 q0inv_q1 = 0, q0inv_q1_p = 0;
     u64* md_scale = nullptr;  // [4K] {n^-1 h_k, shoup, w1 n^-1 h_k, shoup}: ModDown INTT outputs y_k directly
@@ -122,9 +123,13 @@ static cudaError_t dmalloc(void** p, size_t bytes, size_t* acc) {
     return e;
 }
 
+static const char* kFrozen = "context arenas are frozen by a captured CUDA graph (bcn_ctx_freeze): "
+                             "this call needs a larger arena; use another context";
+
 static u64* scratch_get(bcn_ctx* c, size_t words, int* err) {
     size_t bytes = words * sizeof(u64);
     if (bytes > c->scratch_bytes) {
+        if (c->frozen) { *err = fail(BCN_ERR_USAGE, kFrozen); return nullptr; }
         if (c->scratch) cudaFree(c->scratch);   // synchronising: in-flight users are done
         c->scratch = nullptr;
         size_t nb = bytes + bytes / 4;
@@ -142,6 +147,7 @@ static u64* scratch_get(bcn_ctx* c, size_t words, int* err) {
 static u64* scratch2_get(bcn_ctx* c, size_t words, int* err) {
     size_t bytes = words * sizeof(u64);
     if (bytes > c->scratch2_bytes) {
+        if (c->frozen) { *err = fail(BCN_ERR_USAGE, kFrozen); return nullptr; }
         if (c->scratch2) cudaFree(c->scratch2);
         c->scratch2 = nullptr;
         if (cudaMalloc(&c->scratch2, bytes) != cudaSuccess) {
@@ -638,7 +644,14 @@ int bcn_ctx_memory(bcn_ctx* c, uint64_t* bytes) {
     return BCN_OK;
 }
 
+int bcn_ctx_freeze(bcn_ctx* c, int delta) {
+    if (c->frozen + delta < 0) return fail(BCN_ERR_USAGE, "bcn_ctx_freeze: unbalanced release");
+    c->frozen += delta;
+    return BCN_OK;
+}
+
 int bcn_ctx_trim(bcn_ctx* c) {
+    if (c->frozen) return fail(BCN_ERR_USAGE, kFrozen);
     if (c->scratch || c->scratch2) cudaDeviceSynchronize();
     if (c->scratch) cudaFree(c->scratch);
     if (c->scratch2) cudaFree(c->scratch2);
@@ -937,6 +950,7 @@ int bcn_pack_planes(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const u
     cudaStream_t st = (cudaStream_t)stream;
     const size_t np = (size_t)n_out * n_terms;
     if (np > c->ptr_cap) {
+        if (c->frozen) return fail(BCN_ERR_USAGE, kFrozen);
         if (c->ptr_dev) cudaFree(c->ptr_dev);
         c->ptr_dev = nullptr;
         c->ptr_cap = 0;
@@ -975,6 +989,7 @@ int bcn_pack_planes_ext(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, con
     const size_t np = (size_t)n_out * n_terms;
     const size_t bytes = np * sizeof(u64*) + (size_t)n_terms * sizeof(int);
     if (bytes > c->ptr_cap * sizeof(u64*)) {
+        if (c->frozen) return fail(BCN_ERR_USAGE, kFrozen);
         if (c->ptr_dev) cudaFree(c->ptr_dev);
         c->ptr_dev = nullptr;
         c->ptr_cap = 0;

@@ -267,6 +267,18 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
 namespace bcn {
 extern std::atomic<unsigned long long> g_launches;
 }
+// Kernel attributes (max dynamic SMEM) are per device: `mask` (a static at
+// the call site) records the devices already configured, so a second
+// context on another device in the same process configures its own.
+static inline bool first_on_device(unsigned long long* mask, unsigned long long* bit) {
+    int d = 0;
+    cudaGetDevice(&d);
+    *bit = 1ull << (d & 63);
+    return (*mask & *bit) == 0;
+}
+#define BCN_SMEM_ATTR(err, fn, bytes) \
+    do { if ((err) == cudaSuccess) (err) = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes)); } while (0)
+
 static inline cudaError_t launched() {
     bcn::g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();

@@ -70,8 +70,14 @@ cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long
     if (!nplain) return cudaSuccess;
     const int N = 1 << logn;
     const size_t smem = (size_t)N * sizeof(double);
-    static bool cfg = false;
-    if (!cfg) { cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+    static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (encode_kernel), 200 * 1024);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
+    }
     int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
     encode_kernel<<<nplain, tpb, smem, st>>>(out, os, vals, vlen, vs, scale, logn, limbs, pr, ft, add_err, seed,
                                              id_base, id_dev);
@@ -152,8 +158,14 @@ cudaError_t decode_op(double* out, int nout, const u64* poly, long long ps, int 
     if (!npoly) return cudaSuccess;
     const int N = 1 << logn;
     const size_t smem = (size_t)N * sizeof(double);
-    static bool cfg = false;
-    if (!cfg) { cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+    static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (decode_kernel), 200 * 1024);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
+    }
     int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
     decode_kernel<<<npoly, tpb, smem, st>>>(out, nout, poly, ps, k, scale, logn, pr, ft, q0inv_mod_q1, q0inv_p);
     return launched();

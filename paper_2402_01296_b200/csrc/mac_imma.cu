@@ -434,10 +434,13 @@ cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const 
     if (gcnt <= 0 || m.n_terms <= 0 || m.n_out <= 0) return cudaSuccess;
     const int nch = (m.n_terms + 31) / 32;
     const size_t smem = mac_imma_smem();
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(mac_imma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
+    static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (mac_imma_kernel), (int)smem);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
     }
     const int oblocks = (opad + 31) / 32;
     const int mt = opad >= 32 ? 2 : 1;

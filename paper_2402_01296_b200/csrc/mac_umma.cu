@@ -443,10 +443,13 @@ cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, 
     if (gcnt <= 0 || n_terms <= 0 || n_out <= 0) return cudaSuccess;
     if (gcnt > UM_COLS / 2) return cudaErrorInvalidValue;
     const int nch = (n_terms + 31) / 32;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(mac_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UM_SMEM);
-        configured = true;
+    static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (mac_umma_kernel), (int)UM_SMEM);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -14,6 +14,8 @@
 // coefficients and folds N^-1 into its final stage.
 #include <cstdlib>
 
+#include <vector>
+
 #include "common.cuh"
 #include "ops.cuh"
 
@@ -213,11 +215,14 @@ template <int LOGN>
 static cudaError_t launch_one(bool inverse, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
     using C = NttCfg<LOGN>;
     const size_t smem = (size_t)C::N * sizeof(u64);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(ntt_fwd_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_inv_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
+    static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (ntt_fwd_kernel<LOGN>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_inv_kernel<LOGN>), (int)smem);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
     }
     dim3 grid(nlimbs, npolys);
     if (inverse) ntt_inv_kernel<LOGN><<<grid, C::T, smem, st>>>(a);
@@ -234,8 +239,8 @@ static int cluster_mode() {
     return mode;
 }
 
-cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
-    if (nlimbs <= 0 || npolys <= 0) return cudaSuccess;
+static cudaError_t ntt_launch_impl(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys,
+                                   cudaStream_t st) {
     // fused prologue / epilogue / copy forms exist only in the cluster kernels
     const bool fused = a.pro || a.epi || a.copy_src || a.inv_scale;
     if ((logn == 13 || logn == 14) && (cluster_mode() || fused))
@@ -257,4 +262,64 @@ cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int
     }
 }
 
+// ---- in-step NTT timing (bcn_ntt_timing): a CUDA event pair around every
+// NTT launch on its own stream, so bench.py can report the byte-weighted
+// roofline fraction of all NTT launches of a real forward step.  Classes:
+// 0 plain forward, 1 plain inverse, 2 fused forward, 3 fused inverse
+// (fused = prologue / epilogue / out-of-place forms).  Algorithmic bytes:
+// 16 B per coefficient (one u64 read + one u64 write), whatever the fusion
+// reads on top -- a lower bound on the bytes such a launch moves.
+struct NttTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;     // 2 per record
+    std::vector<int> cls;
+    std::vector<unsigned long long> bytes;
+    size_t used = 0;
+};
+static NttTimer g_ntt_timer;
+
+cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
+    if (nlimbs <= 0 || npolys <= 0) return cudaSuccess;
+    NttTimer& T = g_ntt_timer;
+    if (!T.on) return ntt_launch_impl(inverse, logn, a, nlimbs, npolys, st);
+    if (T.used == T.cls.size()) {
+        cudaEvent_t e0, e1;
+        cudaError_t e = cudaEventCreate(&e0);
+        if (e == cudaSuccess) e = cudaEventCreate(&e1);
+        if (e != cudaSuccess) return e;
+        T.ev.push_back(e0);
+        T.ev.push_back(e1);
+        T.cls.push_back(0);
+        T.bytes.push_back(0);
+    }
+    const size_t i = T.used++;
+    const bool fused = a.pro || a.epi || a.copy_src || a.inv_scale || a.src;
+    T.cls[i] = (fused ? 2 : 0) + (inverse ? 1 : 0);
+    T.bytes[i] = 16ull * (1ull << logn) * (unsigned long long)nlimbs * (unsigned long long)npolys;
+    cudaEventRecord(T.ev[2 * i], st);
+    cudaError_t e = ntt_launch_impl(inverse, logn, a, nlimbs, npolys, st);
+    cudaEventRecord(T.ev[2 * i + 1], st);
+    return e;
+}
+
 }  // namespace bcn
+
+extern "C" int bcn_ntt_timing(int enable) {
+    bcn::g_ntt_timer.on = enable != 0;
+    if (enable) bcn::g_ntt_timer.used = 0;
+    return 0;
+}
+
+extern "C" int bcn_ntt_timing_read(double* ms, uint64_t* bytes, uint64_t* launches) {
+    bcn::NttTimer& T = bcn::g_ntt_timer;
+    for (int k = 0; k < 4; k++) { ms[k] = 0.0; bytes[k] = 0; launches[k] = 0; }
+    for (size_t i = 0; i < T.used; i++) {
+        if (cudaEventSynchronize(T.ev[2 * i + 1]) != cudaSuccess) return 4;
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, T.ev[2 * i], T.ev[2 * i + 1]) != cudaSuccess) return 4;
+        ms[T.cls[i]] += t;
+        bytes[T.cls[i]] += T.bytes[i];
+        launches[T.cls[i]] += 1;
+    }
+    return 0;
+}

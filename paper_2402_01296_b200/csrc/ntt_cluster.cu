@@ -838,22 +838,25 @@ template <int LOGN>
 static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
     using C = CCfg<LOGN>;
     const size_t smem = (size_t)C::PART * sizeof(u64);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_fwd_cluster<LOGN, 0, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_inv_cluster<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(ntt_inv_cluster<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
+    static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 0>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 1, 1>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 2, 2>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 2, 0>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 2, 3>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 2>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 1, 2>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 4>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 1, 4>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 3>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 3, true>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_inv_cluster<LOGN, false>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_inv_cluster<LOGN, true>), (int)smem);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
     }
     static const bool pm_env = getenv("BCN_NTT_POLY_MAJOR") && getenv("BCN_NTT_POLY_MAJOR")[0] == '1';
     NttArgs b = a;

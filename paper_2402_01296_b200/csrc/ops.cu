@@ -309,10 +309,13 @@ template <int OT, int S, bool FULL>
 static cudaError_t launch_mac_multi_tma(u64* out, long long out_stride, const MacMulti& m, int G, int nlimb, int logn,
                                         const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st) {
     const size_t smem = (size_t)S * (2 + OT) * MM_NB * sizeof(u64);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(mac_multi_tma_kernel<OT, S, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
+    static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (mac_multi_tma_kernel<OT, S, FULL>), (int)smem);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
     }
     dim3 grid(G, (1 << logn) / MM_NB, nlimb);
     mac_multi_tma_kernel<OT, S, FULL>
@@ -605,8 +608,14 @@ cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int lo
     if (N >= 1024) {
         constexpr int BLK = 1024;
         size_t smem = (size_t)ndig * BLK * sizeof(u64);
-        static bool cfg = false;
-        if (!cfg) { cudaFuncSetAttribute(inner_kernel<BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+        static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (inner_kernel<BLK>), 200 * 1024);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
+    }
         dim3 grid(N / BLK, tcnt, npoly);
         inner_kernel<BLK><<<grid, 256, smem, st>>>(A, U, next, ndig, logn, g, key, key_digit_stride,
                                                    key_comp_stride, ext, keyl, pr, t0);
@@ -899,8 +908,14 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
     if (N >= 1024) {
         constexpr int BLK = 1024;
         const size_t smem = (size_t)(ndig + 1) * BLK * sizeof(u64);
-        static bool cfg = false;
-        if (!cfg) { cudaFuncSetAttribute(rotsum_kernel<BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); cfg = true; }
+        static unsigned long long smem_cfg = 0;
+    unsigned long long smem_bit = 0;
+    if (first_on_device(&smem_cfg, &smem_bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (rotsum_kernel<BLK>), 200 * 1024);
+        if (ae != cudaSuccess) return ae;
+        smem_cfg |= smem_bit;
+    }
         dim3 grid(G, N / BLK, next);
         rotsum_kernel<BLK><<<grid, BLK, smem, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, kds, kcs, ext, pr,
                                                     flags, c0_ostride);

@@ -9,6 +9,7 @@ back to the host: a missing library or device raises DeviceError.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -18,6 +19,28 @@ from .errors import CapacityError, DeviceError, ParameterError
 from .params import HeParams, fft_table, galois_element
 
 RELIN_KEY_ID = 2
+RANK_ID_SHIFT = 40      # encryption ids of rank r start at 1 + (r << 40)
+
+
+def process_rank() -> int:
+    """This process's rank in a multi-GPU job (torch.distributed if it is
+    initialised, else the launcher's RANK variable, else 0)."""
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return int(dist.get_rank())
+    except (ImportError, RuntimeError):
+        pass
+    return int(os.environ.get("RANK", "0") or 0)
+
+
+def counter_base(rank: int) -> int:
+    """First Philox encryption id of a rank.  Every rank derives the same keys
+    from the shared seed, so the ids (the per-ciphertext randomness `a`, `e`)
+    must not overlap across ranks: 2^40 ids per rank."""
+    if rank < 0 or rank >= (1 << (64 - RANK_ID_SHIFT)):
+        raise ParameterError(f"rank {rank} outside [0, 2^{64 - RANK_ID_SHIFT})")
+    return 1 + (rank << RANK_ID_SHIFT)
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -52,7 +75,7 @@ class Engine:
         re, im = fft_table(self.N)
         _lib.call("bcn_ctx_set_fft", h, re.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                   im.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
-        self._counter = 1   # Philox id of the next encryption
+        self._counter = counter_base(process_rank())   # Philox id of the next encryption
         self.graph_counter: torch.Tensor | None = None   # device-side id base (CUDA-graph replays)
 
     def __del__(self):
@@ -94,6 +117,8 @@ class Engine:
     def next_counter(self, n: int = 1) -> int:
         c = self._counter
         self._counter += n
+        if (self._counter - 1) >> RANK_ID_SHIFT != (c - 1) >> RANK_ID_SHIFT:
+            raise ParameterError("encryption id range of this rank exhausted")
         return c
 
     # ---------------------------------------------------------- K1 / K2
@@ -391,6 +416,14 @@ class Engine:
         out = torch.empty_like(x)
         _lib.call("bcn_automorph", self._h, _ptr(out), _ptr(x), npoly, nlimb, g, _stream())
         return out
+
+    def freeze(self, delta: int) -> None:
+        """+1: a CUDA graph now holds pointers into this context's arenas (growth /
+        trim fail with UsageError until released); -1: release."""
+        _lib.call("bcn_ctx_freeze", self._h, int(delta))
+
+    def trim(self) -> None:
+        _lib.call("bcn_ctx_trim", self._h)
 
     def memory_bytes(self) -> int:
         b = ctypes.c_uint64()

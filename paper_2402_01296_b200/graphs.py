@@ -9,6 +9,13 @@ op, decryption of the logits -- one graph launch.  The OpRecorder counts of
 the captured forward are kept so each replay still reports the reference's
 op counts.  This replaces a tracing compiler: the capture is of the real
 library launches, nothing is re-implemented.
+
+The graph replays raw device pointers: into the context's scratch arenas and
+pointer tables, and into the HBM plaintext cache.  So after capture the
+context is frozen (`bcn_ctx_freeze`: a later call that would grow or free an
+arena raises UsageError instead of moving memory under the graph) and the
+cache entries the forward used are pinned by strong references here (an LRU
+eviction then only drops the cache's own reference).  `close()` releases both.
 """
 
 from __future__ import annotations
@@ -17,12 +24,14 @@ import numpy as np
 import torch
 
 from .network import forward_bicrypto
+from .errors import UsageError
 from .sim import HeContext
 
 
 class GraphedForward:
     def __init__(self, net, weights, ctx: HeContext, sens_shape, full_shape, *, strategy: str = "hw",
                  group_size: int | None = None, warmup: int = 2):
+        self._frozen = False
         eng = ctx.engine
         self.ctx, self.eng = ctx, eng
         dev = eng.device
@@ -49,13 +58,30 @@ class GraphedForward:
                     self.slots = eng.decrypt(ct.data, ct.level, ct.scale)
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize()
+            eng.freeze(+1)
+            self._frozen = True
         finally:
             eng.graph_counter = None
+        self._pinned = list(ctx._pt_cache.values())      # every plaintext / plane / key the graph reads
         self.result = res
         idx = np.arange(res.tiles)[:, None] * res.tile_step + np.arange(res.n_outputs)[None, :]
         self._idx = torch.as_tensor(idx.ravel(), device=dev)
         self.n_images = n_img
         self.recorder = res.recorder
+
+    def close(self) -> None:
+        """Drop the graph and release the context (arenas may move again)."""
+        if getattr(self, "_frozen", False):
+            self._frozen = False
+            self.graph = None
+            self._pinned = []
+            self.eng.freeze(-1)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def _next_counter(self):
         self.counter.fill_(self.eng.next_counter(self._ids_per_call))
@@ -64,6 +90,8 @@ class GraphedForward:
         """Run one request: host (or device) inputs -> decrypted logits on the host."""
         self.sens.copy_(torch.as_tensor(sens), non_blocking=True)
         self.full.copy_(torch.as_tensor(full), non_blocking=True)
+        if not self._frozen:
+            raise UsageError("GraphedForward was closed")
         self._next_counter()
         self.graph.replay()
         return self.slots[:, self._idx].reshape(-1, self.result.n_outputs)[:self.n_images].cpu().numpy()

@@ -76,3 +76,17 @@ def decomposed(sens, full, region=None):
     from paper_2402_01296_b200.network import DecomposedInput
 
     return [DecomposedInput(s, f, region or (0, 0, s.shape[-2], s.shape[-1])) for s, f in zip(sens, full)]
+
+
+def cfg4_set_inputs(set_ids, seed: int = 500, per_set: int = 32):
+    """Config-5 inputs: slot set s (32 images) drawn from its own seeded
+    stream (seed, s), so any rank can produce exactly its shard of the fixed
+    65,536-image job, independent of the world size."""
+    sens, full = [], []
+    for s in set_ids:
+        a, b = cfg4_inputs(per_set, seed=(seed, int(s)))
+        sens.append(a)
+        full.append(b)
+    if not sens:
+        return np.zeros((0, 3, 16, 16)), np.zeros((0, 3, 32, 32))
+    return np.concatenate(sens), np.concatenate(full)

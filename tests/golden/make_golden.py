@@ -116,6 +116,29 @@ def cifar3_cfg4(n=8):
           meta=json.dumps(meta), **{f"w::{k}": v for k, v in w.items()})
 
 
+def cifar3_cfg4_sets(n_sets=2):
+    """Two FULL slot sets (32 images each, 32 x 16 x 16 = 8192 slots) of config-4
+    inputs: reference_forward over all 64 images, the simulator's
+    forward_bicrypto run set by set (one ciphertext set holds 32 images)."""
+    bundle = C.get("cifar3")
+    w = synthetic.weights_for(synthetic.tensor_shapes(bundle), 0.05, seed=3)
+    sens, full = synthetic.cfg4_inputs(32 * n_sets, seed=9)
+    dec = [RDec(s, f, (0, 0, 16, 16)) for s, f in zip(sens, full)]
+    net = _ref_cifar3()
+    warch = RArchive(dict(w))
+    ctx = R.make_context(1 << 14, 14, 2.0 ** 30)
+    ref = R.reference_forward(net, dec, warch)
+    sims, recs = [], []
+    for g in range(n_sets):
+        sim, rec = _run(net, dec[32 * g:32 * (g + 1)], warch, ctx, "bhw")
+        sims.append(sim)
+        recs.append(rec.snapshot())
+    assert all(r == recs[0] for r in recs)
+    meta = {"counts_bhw": recs[0]}
+    _pack(os.path.join(HERE, "cifar3_cfg4_sets.npz"), sens=sens, full=full, logits_ref=ref,
+          logits_sim=np.concatenate(sims), meta=json.dumps(meta), **{f"w::{k}": v for k, v in w.items()})
+
+
 def cnn3_backbone():
     """The single-chain cnn3 run fully encrypted by the reference's
     forward_backbone (network.py:510-582) on one whole image (the reference's

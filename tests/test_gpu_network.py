@@ -161,3 +161,114 @@ def test_fc_bsgs_matches_direct_and_plain(n1, n2, tiles, monkeypatch):
         assert counts["Add_CC"] == n1 + n2 - 2 and counts["Add_PC"] == 1
         assert level == ctx.max_level - 1
     assert res["1"][1] == res["0"][1]
+
+
+@pytest.mark.parametrize("G,layout", [(8, 0), (64, 1)])
+def test_cifar3_at_benchmarked_slot_set_counts(G, layout):
+    """The conv paths the benchmark takes: G >= BCN_CONV_TC_MIN_G slot sets run
+    the key-switch-fused conv MAC (materialize_conv -> conv_ks_mac) on the
+    integer tensor cores -- mma.sync IMMA planes for G < 64, tcgen05 (UMMA,
+    TMEM accumulators) for G >= 64 -- with the merged ModDown+rescale tail.
+    Logits of every image vs the float64 reference_forward, counts and
+    per-layer tables vs the reference's golden integers (one op set per G)."""
+    import synthetic
+    from paper_2402_01296_b200 import sim
+
+    assert sim._conv_layout(G) == layout
+    d, w, _, meta = _load("cifar3_cfg4")
+    bundle = B.get("cifar3")
+    sens, full = synthetic.cfg4_inputs(32 * G, seed=40 + G)
+    ctx = B.make_context(1 << 14, B.required_levels(bundle) + 1, 2.0 ** 50)
+    sim.reset_stats()
+    res = B.forward_bicrypto(bundle.bi, (sens, full), w, ctx, strategy="bhw", group_size=32)
+    assert res.logits_ct.batch == G
+    assert res.recorder.snapshot() == meta["counts_bhw"]
+    assert [list(x) for x in res.recorder.layer_table()] == meta["layer_table"]
+    assert sim.STATS["keyswitch_lazy"] > 0 and sim.STATS["mac_launch"] > 0
+    logits = res.decrypt_logits()
+    assert logits.shape == (32 * G, 10)
+    ref = B.reference_forward(bundle.bi, synthetic.decomposed(sens, full), w)
+    _check(logits, ref)
+
+
+def test_cifar3_two_full_slot_sets_match_reference_golden():
+    """64 images = 2 full slot sets (32 x 16 x 16 = 8192 slots each): logits vs
+    the unmodified reference's reference_forward AND its simulator, run set by
+    set (tests/golden/make_golden.py::cifar3_cfg4_sets)."""
+    d = np.load(os.path.join(GOLD, "cifar3_cfg4_sets.npz"))
+    meta = json.loads(str(d["meta"]))
+    w = TensorArchive({k[3:]: d[k] for k in d.files if k.startswith("w::")})
+    bundle = B.get("cifar3")
+    ctx = B.make_context(1 << 14, B.required_levels(bundle) + 1, 2.0 ** 50)
+    res = B.forward_bicrypto(bundle.bi, (d["sens"], d["full"]), w, ctx, strategy="bhw", group_size=32)
+    assert res.recorder.snapshot() == meta["counts_bhw"]
+    logits = res.decrypt_logits()
+    _check(logits, d["logits_ref"])
+    _check(logits, d["logits_sim"], tol=1e-6)
+
+
+def _shard_worker(rank, world, port, n_sets, out_q):
+    """One rank of the sharded config-4/5 forward: its contiguous slot sets,
+    keys regenerated from the shared seed, logits ciphertexts gathered to
+    rank 0 (gloo here: CPU copies) and decrypted there."""
+    import torch
+    import torch.distributed as dist
+
+    import synthetic
+    from paper_2402_01296_b200.shard import gather_to_root, shard_range
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        d, w, _, meta = _load("cifar3_cfg4")
+        bundle = B.get("cifar3")
+        ctx = B.make_context(1 << 14, B.required_levels(bundle) + 1, 2.0 ** 50)
+        sets = shard_range(n_sets, rank, world)
+        sens, full = synthetic.cfg4_set_inputs(sets, seed=77)
+        res = B.forward_bicrypto(bundle.bi, (sens, full), w, ctx, strategy="bhw", group_size=32)
+        assert res.recorder.snapshot() == meta["counts_bhw"]
+        data = res.logits_ct.data
+        c1_head = data[0, 1, 0, :64].cpu().numpy()
+        got = gather_to_root(data.cpu(), n_sets)
+        c1s = [None] * world
+        dist.all_gather_object(c1s, c1_head)
+        if rank == 0:
+            slots = ctx.engine.decrypt(got.cuda(), res.logits_ct.level, res.logits_ct.scale).cpu().numpy()
+            idx = np.arange(32)[:, None] * res.tile_step + np.arange(10)[None, :]
+            out_q.put((slots[:, idx].reshape(-1, 10), c1s))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_forward_two_ranks_gather_matches_reference():
+    """Two ranks (processes) on one GPU, each with its own shard of 4 slot sets
+    (128 images): the gathered, rank-0-decrypted logits equal the reference
+    for every image, and the ranks' ciphertexts carry distinct encryption
+    randomness (Philox ids partitioned by rank)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    import synthetic
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    n_sets = 4
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    ps = [ctxm.Process(target=_shard_worker, args=(r, 2, port, n_sets, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    logits, c1s = q.get(timeout=600)
+    for p in ps:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    d, w, _, _ = _load("cifar3_cfg4")
+    sens, full = synthetic.cfg4_set_inputs(range(n_sets), seed=77)
+    ref = B.reference_forward(B.get("cifar3").bi, synthetic.decomposed(sens, full), w)
+    assert logits.shape == (32 * n_sets, 10)
+    _check(logits, ref)
+    assert not np.array_equal(c1s[0], c1s[1])

@@ -505,3 +505,126 @@ def test_single_special_prime_moddown_matches_oracle(N, L, dnum, monkeypatch):
         outs.append([to_numpy_u64(rot), to_numpy_u64(sq)])
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+# ------------------------------------------------- BASELINE configs 2 and 3 at their real shapes
+def _worst_cases(basis, N, rng):
+    qs = np.array(basis, dtype=np.uint64)[:, None]
+    alt = np.where(np.arange(N) % 2 == 0, 0, 1).astype(np.uint64)[None] * (qs - np.uint64(1))
+    spike = np.zeros((len(basis), N), np.uint64)
+    spike[:, N // 3] = (qs[:, 0] - np.uint64(1))
+    top = np.broadcast_to(qs - np.uint64(1), (len(basis), N))
+    uni = np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in basis])
+    near = np.stack([q - np.uint64(1) - rng.integers(0, 4, N, dtype=np.uint64) for q in basis])
+    return np.stack([top, alt, spike, uni, near])
+
+
+@pytest.mark.parametrize("logn", [13, 14])
+def test_ntt_60bit_cluster_matches_oracle(logn):
+    """BASELINE config 2's NTT: ~60-bit primes (all >= 2^50, so the integer
+    Shoup/Harvey butterflies of the cluster kernel, with lazy reduction up to
+    4q < 2^62) at N = 8192 and 16384 -- worst-case residues (all q-1, q-1
+    alternating with 0, a spike, near-q noise) and uniform ones, forward and
+    inverse, bit for bit against the oracle."""
+    N = 1 << logn
+    eng, orc, hp = _pair(N, 3, 60, dnum=1)
+    basis = list(hp.q) + list(hp.p)
+    assert all(q >= (1 << 59) for q in basis)
+    x = _worst_cases(basis, N, np.random.default_rng(logn))
+    t = torch.from_numpy(x.view(np.int64).copy()).cuda()
+    eng.ntt(t, 0)
+    got = to_numpy_u64(t)
+    exp = np.stack([O.ntt(x[i], basis) for i in range(len(x))])
+    np.testing.assert_array_equal(got, exp)
+    y = torch.from_numpy(exp.view(np.int64).copy()).cuda()
+    eng.ntt(y, 0, inverse=True)
+    np.testing.assert_array_equal(to_numpy_u64(y), x)
+
+
+def test_config2_mac_matches_oracle():
+    """BASELINE config 2's MAC at its real shape: N = 8192, 4 limbs of ~60-bit
+    primes, Y_g = sum_{t<25} ct_{25g+t} (x) pt_{25g+t}; 60 ciphertexts -> groups
+    of 25, 25 and a ragged last group of 10; all-(q-1) operands in one group."""
+    N, limbs, n_ct, group = 8192, 4, 60, 25
+    hp = make_params(N, limbs - 1, 60, dnum=1, n_special=1)
+    eng = Engine(hp)
+    q = list(hp.q)
+    cts = eng.sample_uniform(n_ct * 2, limbs, 0, seed=1, id0=0).view(n_ct, 2, limbs, N)
+    pts = eng.sample_uniform(n_ct, limbs, 0, seed=2, id0=0)
+    qcol = torch.from_numpy((np.array(q, dtype=np.uint64) - np.uint64(1)).view(np.int64)).cuda()[:, None]
+    cts[25:50] = qcol                                 # worst case: every operand q-1 in group 1
+    pts[25:50] = qcol
+    got = to_numpy_u64(eng.mac(cts, eng.to_montgomery(pts), group))
+    c_np, p_np = to_numpy_u64(cts), to_numpy_u64(pts)
+    assert got.shape == (3, 2, limbs, N)
+    for g in range(3):
+        for comp in range(2):
+            acc = np.zeros((limbs, N), np.uint64)
+            for k in range(g * group, min(n_ct, (g + 1) * group)):
+                acc = O.add(acc, O.mul(c_np[k, comp], p_np[k], q), q)
+            np.testing.assert_array_equal(got[g, comp], acc)
+
+
+def test_config3_relin_no_rescale_and_rotation_match_oracle():
+    """BASELINE config 3 at its real shape: N = 16384, 8 limbs of 50-bit
+    primes, K = 1 special prime, dnum = 2.  Stage A: ct x ct + relinearise
+    WITHOUT rescale (mul_cc(rescale=False)); stage B: a hoisted rotation by
+    +-2^k of the result -- both bit for bit against the oracle."""
+    N, L = 16384, 7
+    hp = make_params(N, L, 50, dnum=2, n_special=1, seed=5)
+    op = O.make_params(N, L, 50, dnum=2, n_special=1, seed=5)
+    assert list(hp.q) == op.q and list(hp.p) == op.p and hp.K == 1
+    eng, orc = Engine(hp), O.Oracle(op)
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal((2, N // 2)) * 0.5
+    ct = eng.encrypt(v, counter=21)
+    oc = [orc.encrypt(v[0], 21), orc.encrypt(v[1], 22)]
+    sq = eng.mul_cc(ct, ct, L, rescale=False)
+    osq = [orc.mul_cc(o, o, rescale=False) for o in oc]
+    _assert_ct(sq, osq)
+    U = eng.modup(sq, L)
+    for r in (1, -64):
+        _assert_ct(eng.rotate(sq, r, L, U=U), [orc.rotate(o, r) for o in osq])
+
+
+def test_encryption_ids_are_partitioned_by_rank(monkeypatch):
+    """Every rank derives the same keys from the shared seed, so two ranks must
+    never draw the same Philox encryption randomness: rank r's ids start at
+    1 + (r << 40).  Equal plaintexts on ranks 0 and 1 give different c1 (the
+    uniform `a`) and both decrypt correctly."""
+    from paper_2402_01296_b200.engine import counter_base
+
+    N = 1024
+    hp = make_params(N, 2, 40, dnum=1)
+    v = np.random.default_rng(0).standard_normal((1, N // 2))
+    cts = []
+    for rank in (0, 1):
+        monkeypatch.setenv("RANK", str(rank))
+        eng = Engine(hp)
+        assert eng._counter == counter_base(rank)
+        ct = eng.encrypt(v)
+        cts.append(to_numpy_u64(ct)[0])
+        assert np.abs(eng.decrypt(ct, hp.max_level, hp.scale).cpu().numpy()[0] - v[0]).max() < 1e-6
+    assert not np.array_equal(cts[0][1], cts[1][1])
+    assert not np.array_equal(cts[0][0], cts[1][0])
+
+
+def test_context_freeze_blocks_arena_moves():
+    """bcn_ctx_freeze: while a captured graph holds a context, a call that would
+    grow or free its scratch arena raises UsageError instead of moving memory."""
+    from paper_2402_01296_b200.errors import UsageError
+
+    eng, orc, hp = _pair(1024, 3, 40, dnum=2)
+    rng = np.random.default_rng(0)
+    ct = eng.encrypt(rng.standard_normal((1, 512)), counter=3)
+    eng.mul_cc(ct, ct, hp.max_level)                    # sizes the arena for G = 1
+    eng.freeze(+1)
+    eng.mul_cc(ct, ct, hp.max_level)                    # fits: fine
+    big = eng.encrypt(rng.standard_normal((64, 512)), counter=10)
+    with pytest.raises(UsageError):
+        eng.mul_cc(big, big, hp.max_level)              # would grow the arena
+    with pytest.raises(UsageError):
+        eng.trim()
+    eng.freeze(-1)
+    eng.mul_cc(big, big, hp.max_level)
+    eng.trim()

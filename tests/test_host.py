@@ -134,7 +134,8 @@ def test_required_levels_pins():
 
 # ---------------------------------------------------------------- network (host parts)
 def test_clear_forward_matches_reference_golden():
-    for name, arch in (("cnn3_fixture", "cnn3"), ("cnn3_cfg1", "cnn3"), ("cifar3_cfg4", "cifar3")):
+    for name, arch in (("cnn3_fixture", "cnn3"), ("cnn3_cfg1", "cnn3"), ("cifar3_cfg4", "cifar3"),
+                      ("cifar3_cfg4_sets", "cifar3")):
         d, w, dec, _ = _gold(name)
         got = B.reference_forward(catalog.get(arch).bi, dec, w)
         assert np.abs(got - d["logits_ref"]).max() <= 1e-12 * max(1.0, np.abs(d["logits_ref"]).max())
@@ -207,9 +208,14 @@ def _worker(rank, world, port, n_items, out_q):
     import torch
     import torch.distributed as dist
 
+    from paper_2402_01296_b200.engine import counter_base, process_rank
     from paper_2402_01296_b200.shard import gather_to_root, shard_range
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    assert process_rank() == rank                 # the engine's encryption-id base follows the job rank
+    bases = [None] * world
+    dist.all_gather_object(bases, counter_base(process_rank()))
+    assert len(set(bases)) == world
     mine = shard_range(n_items, rank, world)
     local = torch.stack([torch.full((2, 3), float(i)) for i in mine]) if len(mine) else torch.zeros((0, 2, 3))
     got = gather_to_root(local, n_items)
@@ -237,6 +243,17 @@ def test_sharded_gather_world2_gloo(n_items):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert np.array_equal(got[:, 0, 0], np.arange(n_items, dtype=float))
+
+
+def test_encryption_id_ranges_are_disjoint_per_rank():
+    """Philox encryption ids: rank r owns [1 + r 2^40, 1 + (r+1) 2^40)."""
+    from paper_2402_01296_b200.engine import RANK_ID_SHIFT, counter_base
+
+    assert counter_base(0) == 1
+    assert counter_base(1) - counter_base(0) == 1 << RANK_ID_SHIFT
+    assert len({counter_base(r) for r in range(8)}) == 8
+    with pytest.raises(Exception):
+        counter_base(-1)
 
 
 def test_latency_table_has_the_reference_cost_model_format():
