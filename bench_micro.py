@@ -63,6 +63,42 @@ def config2(steps=10, warmup=3, n_ct=4096, limbs=4, N=8192):
     return res
 
 
+def config2_fused(steps=10, warmup=3, n_ct=4096, limbs=4, N=8192, group=25):
+    """Config 2 as ONE pass (bcn_ntt_mac_rescale / bcn32_ntt_mac_rescale,
+    SURVEY.md 8(f) item 2): coefficient-domain ciphertexts -> NTT -> (.) pt ->
+    sum of 25 -> rescale, in u64 words (BASELINE's ~60-bit primes) and in the
+    32-bit-limb variant (primes < 2^30).  Algorithmic bytes: every ciphertext
+    and plaintext word read once, the rescaled outputs written once."""
+    from paper_2402_01296_b200.limb32 import Engine32, primes32
+
+    n_out = -(-n_ct // group)
+    res = {}
+    hp = make_params(N, limbs - 1, 60, dnum=1, n_special=1)
+    eng = Engine(hp)
+    cts = eng.sample_uniform(n_ct * 2, limbs, 0, seed=1, id0=0).view(n_ct, 2, limbs, N)
+    pts = eng.to_montgomery(eng.sample_uniform(n_ct, limbs, 0, seed=2, id0=0))
+    nbytes = (cts.numel() + pts.numel() + n_out * 2 * (limbs - 1) * N) * 8
+    ms = time_region(lambda: eng.ntt_mac_rescale(cts, pts, group), steps, warmup)
+    res["u64"] = {"ms": ms, "bytes": nbytes, "GBps": nbytes / ms / 1e6, "primes_bits": 60}
+    del eng, cts, pts
+    torch.cuda.empty_cache()
+    e32 = Engine32(N, primes32(N, limbs))
+    cts = e32.uniform((n_ct, 2, limbs, N), seed=1)
+    pts = e32.to_montgomery(e32.uniform((n_ct, limbs, N), seed=2))
+    nbytes = (cts.numel() + pts.numel() + n_out * 2 * (limbs - 1) * N) * 4
+    ms = time_region(lambda: e32.ntt_mac_rescale(cts, pts, group), steps, warmup)
+    res["u32"] = {"ms": ms, "bytes": nbytes, "GBps": nbytes / ms / 1e6, "primes_bits": 30}
+    data = cts.view(n_ct * 2, limbs, N)
+    nb = 2 * data.numel() * 4
+    ms = time_region(lambda: e32.ntt(data), steps, warmup)
+    res["u32_ntt"] = {"ms": ms, "bytes": nb, "GBps": nb / ms / 1e6}
+    ms = time_region(lambda: e32.ntt(data, inverse=True), steps, warmup)
+    res["u32_intt"] = {"ms": ms, "bytes": nb, "GBps": nb / ms / 1e6}
+    del e32, cts, pts, data
+    torch.cuda.empty_cache()
+    return res
+
+
 def ntt14(steps=10, warmup=3, npoly=128, limbs=12):
     """The workload's NTT: N = 2^14 cluster kernels (ntt_fwd_cluster<14,0,0> /
     ntt_inv_cluster<14>) over a ModDown-shaped batch of 128 polys x 12 limbs of
@@ -124,6 +160,10 @@ def config3(steps=3, warmup=1, n_ct=1024, N=16384, limbs=8, batch=128):
 if __name__ == "__main__":
     import json
     t0 = time.time()
+    import sys
+    if "fused" in sys.argv:
+        print(json.dumps({"config2_fused": config2_fused()}, indent=1))
+        raise SystemExit(0)
     print(json.dumps({"config2": config2()}, indent=1))
     print(json.dumps({"config3": config3()}, indent=1))
     print("wall", time.time() - t0)

@@ -209,6 +209,17 @@ int bcn_premul_key(bcn_ctx *ctx, uint64_t *out, uint64_t g, const uint64_t *pt, 
 int bcn_mac(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, const uint64_t *pt_mont, int n_items, int group,
             int nlimb, void *stream);
 
+/* ---- K1+K4+K5 fused (BASELINE config 2 in ONE pass):
+ * out[g] = Rescale( sum_{t < group} NTT(ct[g group + t]) (.) pt[g group + t] )
+ * -- the RNS form of one packed conv output (conv_accumulate,
+ * pkg/src/bibranch/layers.py:149-172: plaintext products summed, then one
+ * rescale, sim.py:221-248).  ct: u64[n_items][2][nlimb][N] in the
+ * COEFFICIENT domain (limb t mod q_t); pt_mont: u64[n_items][nlimb][N], NTT
+ * domain, Montgomery; out: u64[ceil(n_items/group)][2][nlimb-1][N], NTT
+ * domain.  2 <= nlimb <= 8, 2^10 <= N <= 2^13. */
+int bcn_ntt_mac_rescale(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, const uint64_t *pt_mont, int n_items,
+                        int group, int nlimb, void *stream);
+
 /* ---- K5: rescale by q_level: in u64[G][2][in_nlimb][N] -> out u64[G][2][level][N] */
 int bcn_rescale(bcn_ctx *ctx, uint64_t *out, const uint64_t *in, int in_nlimb, int G, int level, void *stream);
 
@@ -242,6 +253,28 @@ int bcn_sample_uniform(bcn_ctx *ctx, uint64_t *out, int npoly, int nlimb, int pr
 int bcn_to_montgomery(bcn_ctx *ctx, uint64_t *out, const uint64_t *in, int npoly, int nlimb, int prime0,
                       void *stream);
 int bcn_automorph(bcn_ctx *ctx, uint64_t *out, const uint64_t *in, int npoly, int nlimb, uint64_t g, void *stream);
+
+/* ==== 32-bit-limb variant ========================
+ * Residues are u32 modulo primes q < 2^30 (q = 1 mod 2N), Delta = 2^30 -- the
+ * reference's default scale (pkg/src/bibranch/cli.py:66) -- so every word is
+ * half the HBM bytes of the u64 engine and every product a native 32-bit
+ * multiply.  Own context: nlimb primes q[0..nlimb-1], 2 <= nlimb <= 8,
+ * N = 2^logn, 2^10 <= N <= 2^14.  Same layouts and ordering as the u64
+ * entry points above with uint32_t words; Montgomery form is x 2^32 mod q. */
+typedef struct bcn32_ctx bcn32_ctx;
+const char *bcn32_last_error(void);
+int bcn32_ctx_create(bcn32_ctx **out, int logn, int nlimb, const uint32_t *q, int device);
+int bcn32_ctx_destroy(bcn32_ctx *ctx);
+/* in-place NTT / INTT of u32[npoly][nlimb][N] (limb t mod q_t) -- K1/K2 */
+int bcn32_ntt_fwd(bcn32_ctx *ctx, uint32_t *data, int npoly, void *stream);
+int bcn32_ntt_inv(bcn32_ctx *ctx, uint32_t *data, int npoly, void *stream);
+/* out = in 2^32 mod q_t over u32[npoly][nlimb][N] */
+int bcn32_to_montgomery(bcn32_ctx *ctx, uint32_t *out, const uint32_t *in, int npoly, void *stream);
+/* bcn_ntt_mac_rescale with u32 words: ct u32[n_items][2][nlimb][N]
+ * (coefficient domain), pt_mont u32[n_items][nlimb][N] (NTT domain,
+ * Montgomery), out u32[ceil(n_items/group)][2][nlimb-1][N] (NTT domain) */
+int bcn32_ntt_mac_rescale(bcn32_ctx *ctx, uint32_t *out, const uint32_t *ct, const uint32_t *pt_mont, int n_items,
+                          int group, void *stream);
 
 #ifdef __cplusplus
 }

@@ -89,6 +89,14 @@ SIGNATURES = {
     "bcn_sample_uniform": [_P, _P, _I, _I, _I, _U64, _U64, _P],
     "bcn_to_montgomery": [_P, _P, _P, _I, _I, _I, _P],
     "bcn_automorph": [_P, _P, _P, _I, _I, _U64, _P],
+    "bcn_ntt_mac_rescale": [_P, _P, _P, _P, _I, _I, _I, _P],
+    # 32-bit-limb variant (own context, bcn32_last_error)
+    "bcn32_ctx_create": [ctypes.POINTER(_P), _I, _I, ctypes.POINTER(ctypes.c_uint32), _I],
+    "bcn32_ctx_destroy": [_P],
+    "bcn32_ntt_fwd": [_P, _P, _I, _P],
+    "bcn32_ntt_inv": [_P, _P, _I, _P],
+    "bcn32_to_montgomery": [_P, _P, _P, _I, _P],
+    "bcn32_ntt_mac_rescale": [_P, _P, _P, _P, _I, _I, _P],
 }
 
 _lib = None
@@ -105,6 +113,8 @@ def load():
         lib.bcn_last_error.restype = ctypes.c_char_p
         lib.bcn_last_error.argtypes = []
         lib.bcn_version.restype = _I
+        lib.bcn32_last_error.restype = ctypes.c_char_p
+        lib.bcn32_last_error.argtypes = []
         for name, argt in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = _I
@@ -114,12 +124,13 @@ def load():
 
 
 def exported_symbols() -> list[str]:
-    return ["bcn_last_error", "bcn_version", *SIGNATURES]
+    return ["bcn_last_error", "bcn_version", "bcn32_last_error", *SIGNATURES]
 
 
 def check(code: int, what: str = "") -> None:
     if code != BCN_OK:
-        msg = load().bcn_last_error().decode(errors="replace")
+        last = load().bcn32_last_error if what.startswith("bcn32_") else load().bcn_last_error
+        msg = last().decode(errors="replace")
         raise _ERRORS.get(code, DeviceError)(f"{what}: {msg}" if what else msg)
 
 

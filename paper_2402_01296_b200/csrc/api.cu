@@ -1189,6 +1189,40 @@ int bcn_mac(bcn_ctx* c, uint64_t* out, const uint64_t* ct, const uint64_t* pt_mo
     return BCN_OK;
 }
 
+// config 2 in one pass: out[g] = Rescale(sum_t NTT(ct_t) (.) pt_t), the
+// ciphertexts in the coefficient domain (ntt_mac_rescale.cu)
+int bcn_ntt_mac_rescale(bcn_ctx* c, uint64_t* out, const uint64_t* ct, const uint64_t* pt_mont, int n_items,
+                        int group, int nlimb, void* stream) {
+    if (nlimb < 2 || nlimb > 8 || nlimb > c->nq || group < 1 || n_items < 0)
+        return fail(BCN_ERR_PARAM, "bad fused MAC shape (2 <= nlimb <= min(8, max_level + 1))");
+    if (c->logn < 10 || c->logn > 13) return fail(BCN_ERR_PARAM, "fused NTT+MAC+rescale needs 2^10 <= N <= 2^13 (u64)");
+    NmrArgs<u64> a;
+    a.ct = (const u64*)ct; a.pt = (const u64*)pt_mont; a.out = (u64*)out; a.tw = c->tw;
+    a.n_items = n_items; a.group = group; a.nlimb = nlimb;
+    memset(&a.k, 0, sizeof(a.k));
+    const int top = nlimb - 1;
+    const u64 qt = c->primes[top];
+    for (int t = 0; t < nlimb; t++) {
+        const PrimeInfo& P = c->hpr[t];
+        const u64 qi = P.q;
+        a.k.q[t] = qi;
+        a.k.qneg[t] = P.qinv_neg;
+        a.k.ninv[t] = P.pad[0];
+        a.k.ninv_p[t] = P.pad[1];
+        a.k.wn[t] = c->wn_host[t];
+        a.k.wn_p[t] = shoup_h(c->wn_host[t], qi);
+        a.k.inv1[t] = P.pad[2];
+        if (t < top) {
+            const u64 li = inv_h(qt % qi, qi);
+            a.k.qlinv[t] = li;
+            a.k.qlinv_p[t] = shoup_h(li, qi);
+            a.k.qlmod[t] = qt % qi;
+        }
+    }
+    CUDA_TRY(ntt_mac_rescale_launch<u64>(a, c->logn, (cudaStream_t)stream));
+    return BCN_OK;
+}
+
 // -------------------------------------------------------- key switching
 static u64* key_ptr(bcn_ctx* c, u64 id) {
     auto it = c->keys.find(id);

@@ -94,6 +94,24 @@ struct NttArgs {
     long long copy_stride;
 };
 
+// fused NTT -> MAC -> rescale (ntt_mac_rescale.cu), word W = u32 or u64;
+// per-limb constants (limb t = prime t of the chain q_0..q_{nlimb-1})
+template <class W> struct NmrConst {
+    W q[8], qneg[8], ninv[8], ninv_p[8], wn[8], wn_p[8];
+    W qlinv[8], qlinv_p[8];   // q_top^-1 mod q_t (Shoup), t < top
+    W qlmod[8];               // q_top mod q_t
+    W inv1[8];                // floor(2^bits / q_t): reduction of any word by a Shoup multiply by 1
+};
+template <class W> struct NmrArgs {
+    const W* ct;      // [n_items][2][nlimb][N], coefficient domain
+    const W* pt;      // [n_items][nlimb][N], NTT domain, Montgomery
+    W* out;           // [n_groups][2][nlimb-1][N], NTT domain
+    const void* tw;   // {w, shoup} pairs of W; limb t at t * 2N (forward N entries, then inverse N entries)
+    int n_items, group, nlimb;
+    NmrConst<W> k;
+};
+template <class W> cudaError_t ntt_mac_rescale_launch(const NmrArgs<W>& a, int logn, cudaStream_t st);
+
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
 cudaError_t ntt_cluster_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st);
 

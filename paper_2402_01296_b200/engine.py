@@ -400,6 +400,18 @@ class Engine:
         _lib.call("bcn_mac", self._h, _ptr(out), _ptr(ct), _ptr(pt_mont), n_items, group, nl, _stream())
         return out
 
+    def ntt_mac_rescale(self, ct_coef: torch.Tensor, pt_mont: torch.Tensor, group: int) -> torch.Tensor:
+        """BASELINE config 2 in one pass (bcn_ntt_mac_rescale): ct_coef
+        (n_items, 2, nlimb, N) in the coefficient domain, pt_mont
+        (n_items, nlimb, N) NTT domain / Montgomery -> (n_groups, 2, nlimb-1, N)
+        = Rescale(sum over each group of NTT(ct) * pt), NTT domain."""
+        n_items, _, nl, N = ct_coef.shape
+        ng = -(-n_items // group)
+        out = torch.empty((ng, 2, nl - 1, N), dtype=torch.int64, device=self.device)
+        _lib.call("bcn_ntt_mac_rescale", self._h, _ptr(out), _ptr(ct_coef), _ptr(pt_mont), n_items, group, nl,
+                  _stream())
+        return out
+
     def sample_uniform(self, npoly: int, nlimb: int, prime0: int = 0, seed: int = 0, id0: int = 0) -> torch.Tensor:
         out = torch.empty((npoly, nlimb, self.N), dtype=torch.int64, device=self.device)
         _lib.call("bcn_sample_uniform", self._h, _ptr(out), npoly, nlimb, prime0, seed, id0, _stream())

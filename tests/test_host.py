@@ -187,7 +187,7 @@ def test_library_exports_every_header_symbol():
     from paper_2402_01296_b200 import _lib
 
     header = open(os.path.join(ROOT, "include", "bcn.h")).read()
-    declared = set(re.findall(r"\b(bcn_[a-z0-9_]+)\s*\(", header))
+    declared = set(re.findall(r"\b(bcn(?:32)?_[a-z0-9_]+)\s*\(", header))
     assert declared == set(_lib.exported_symbols())
     lib = _lib.load()          # loads without a GPU; no compute call here
     for name in declared:

@@ -190,3 +190,32 @@ def test_default_chains_are_fp64_eligible(N, L, dnum, K):
     # a scale above 2^50 keeps q0 / specials at least as wide as the rescale primes
     wide = make_params(N, 4, 55, dnum=dnum)
     assert all(q.bit_length() == 55 for q in list(wide.q) + list(wide.p))
+
+
+@pytest.mark.parametrize("bits,L", [(30, 3), (60, 4)])
+def test_ntt_mac_rescale_restatement_is_the_coefficient_definition(bits, L):
+    """Pin of oracle.ntt_mac_rescale (config 2, 8(f) item 2) against its
+    definition in the coefficient domain with the schoolbook negacyclic
+    product: Y = round((sum_t ct_t * p_t) / q_top) per limb, i.e.
+    (c_i - centred(c_top)) q_top^-1 mod q_i -- for 30-bit (32-bit-limb
+    variant) and 60-bit (config 2) primes, a ragged last group."""
+    N, n, group = 16, 5, 2
+    primes = O.ntt_primes(bits, L, N)
+    rng = np.random.default_rng(bits)
+    cts = np.stack([np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in primes])
+                              for _ in range(2)]) for _ in range(n)])
+    pc = np.stack([np.stack([rng.integers(0, q, N, dtype=np.uint64) for q in primes]) for _ in range(n)])
+    pts = np.stack([O.ntt(pc[k], primes) for k in range(n)])
+    got = O.ntt_mac_rescale(cts, pts, primes, group)
+    qt = primes[-1]
+    for g, g0 in enumerate(range(0, n, group)):
+        for comp in range(2):
+            acc = [[0] * N for _ in primes]
+            for k in range(g0, min(n, g0 + group)):
+                for i, q in enumerate(primes):
+                    prod = O.negacyclic_mul_naive(cts[k, comp, i], pc[k, i], q)
+                    acc[i] = [(a + int(b)) % q for a, b in zip(acc[i], prod)]
+            top = [v - qt if v > qt // 2 else v for v in acc[-1]]
+            want = np.stack([np.array([((acc[i][j] - top[j]) * pow(qt, -1, q)) % q for j in range(N)],
+                                      dtype=np.uint64) for i, q in enumerate(primes[:-1])])
+            np.testing.assert_array_equal(O.intt(got[g, comp], primes[:-1]), want)
