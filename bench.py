@@ -415,6 +415,35 @@ def cpu_reference_forward(cores: int, weights: dict, target_s: float, steps: int
     return ref_arm.time_forward(cores, steps, warmup)
 
 
+def ks_compute_bound(c3: dict, n14: dict) -> dict:
+    """Compute-aware floor of config 3 next to its HBM fraction (SURVEY.md
+    8(d)'s compute reference): limb-transforms x the N = 2^14 NTT time per
+    limb-poly measured in this run (bench_micro.ntt14), plus the inner
+    products at the measured 64-bit MAC rate of the IMAD pipe (Acc4, 5.5
+    MAC/clk/SM, tools/micro/mac_bench.cu).  Per key switch at level l with
+    l+1 = 8 limbs, K = 1, alpha = 4, dnum = 2: ModUp = (l+1) INTT + dnum (l+1+K-alpha)
+    NTT; ModDown = 2K INTT + 2(l+1) NTT; inner product 2 dnum (l+1+K) N MACs.
+    Stage A: 1024 full key switches; stage B: 1024 ModUps + 14 x 1024
+    (inner product + ModDown)."""
+    n_ct, limbs, K, alpha, dnum, N, rots = 1024, 8, 1, 4, 2, 16384, 14
+    us_fwd = n14["fwd"]["ms"] * 1e3 / n14["limb_polys"]
+    us_inv = n14["inv"]["ms"] * 1e3 / n14["limb_polys"]
+    modup = limbs * us_inv + dnum * (limbs + K - alpha) * us_fwd
+    moddown = 2 * K * us_inv + 2 * limbs * us_fwd
+    mac_rate = 5.5 * 148 * 1.965e9                      # 64-bit modular MACs / s
+    inner_ms = 2 * dnum * (limbs + K) * N / mac_rate * 1e3
+    a_ms = n_ct * (modup + moddown) / 1e3 + n_ct * inner_ms
+    b_ms = n_ct * modup / 1e3 + n_ct * rots * (moddown / 1e3 + inner_ms)
+    return {"relin": {"bound_ms": a_ms, "measured_ms": c3["relin"]["ms"], "frac": a_ms / c3["relin"]["ms"]},
+            "rotations": {"bound_ms": b_ms, "measured_ms": c3["rotations"]["ms"],
+                          "frac": b_ms / c3["rotations"]["ms"]},
+            "ntt_us_per_limb_poly": {"fwd": us_fwd, "inv": us_inv},
+            "limb_transforms": {"relin_per_ct": limbs + dnum * (limbs + K - alpha) + 2 * K + 2 * limbs,
+                                "rotations_per_ct": limbs + dnum * (limbs + K - alpha) + rots * (2 * K + 2 * limbs)},
+            "note": "floor = NTT limb-transforms at this run's measured us/limb-poly + inner-product MACs at "
+                    "the IMAD-pipe rate; frac = floor / measured"}
+
+
 def cpu_oracle_columns() -> dict:
     """Configs 2 and 3 have no reference counterpart (the reference does no
     cryptography): the C/numpy RNS-CKKS oracle port on the same shapes, on a
@@ -445,8 +474,19 @@ def cpu_oracle_columns() -> dict:
                 acc = O.add(acc, O.mul(cts[(g * 25 + t) % 50], pts[t], p2.q), p2.q)
     t_mac = (time.perf_counter() - t0) / 2 * 164
     scale = 32768 / sub
-    out["config2"] = {"ntt_ms": t_ntt * scale * 1e3, "intt_ms": t_intt * scale * 1e3, "mac_ms": t_mac * 1e3,
-                      "sample": f"{sub} of 32768 limb-polys (NTT/INTT), 2 of 164 MAC groups; scaled linearly",
+    # config 2 fused (NTT -> MAC -> rescale, oracle.ntt_mac_rescale) on 2 of the 164 groups, u64 and u32 primes
+    fused = {}
+    for tag, bits in (("u64", 60), ("u32", 30)):
+        primes = O.ntt_primes(bits, 4, 8192)
+        fc = np.stack([np.stack([np.stack([rng.integers(0, q, 8192, dtype=np.uint64) for q in primes])
+                                 for _ in range(2)]) for _ in range(50)])
+        fp = np.stack([np.stack([rng.integers(0, q, 8192, dtype=np.uint64) for q in primes]) for _ in range(50)])
+        t0 = time.perf_counter()
+        O.ntt_mac_rescale(fc, fp, primes, 25)
+        fused[tag + "_ms"] = (time.perf_counter() - t0) / 2 * 164 * 1e3
+    out["config2"] = {**{"fused_" + k: v for k, v in fused.items()}, "ntt_ms": t_ntt * scale * 1e3, "intt_ms": t_intt * scale * 1e3, "mac_ms": t_mac * 1e3,
+                      "sample": f"{sub} of 32768 limb-polys (NTT/INTT), 2 of 164 MAC groups, 2 of 164 fused "
+                                "NTT+MAC+rescale groups (u64: 60-bit, u32: 30-bit primes); scaled linearly",
                       "kind": "port", "cores": int(os.environ.get("OMP_NUM_THREADS", cores_available()))}
     # config 3: one ct x ct + relinearisation (merged with rescale) and 2 of the 14 hoisted rotations of one
     # ciphertext (N = 16384, 8 limbs, K = 1, dnum = 2); scaled to 1024 ciphertexts x 14 rotations
@@ -569,9 +609,11 @@ def main():
         import bench_micro
         extras["latency_1img"] = latency_cfg1()
         c2 = bench_micro.config2()
+        c2f = bench_micro.config2_fused()
         c3 = bench_micro.config3()
         n14 = bench_micro.ntt14()
-        extras["micro"] = {"config2": c2, "config3": c3, "ntt14": n14}
+        extras["micro"] = {"config2": c2, "config2_fused": c2f, "config3": c3, "ntt14": n14,
+                           "ks_bound": ks_compute_bound(c3, n14)}
         peak, peak_kind = _peaks()
         extras["roofline"] = ntt_roofline(res["ntt_step"], peak, peak_kind)
         extras["roofline_micro"] = {
@@ -582,6 +624,9 @@ def main():
             extras["roofline_micro"]["cfg2_" + name] = {"achieved": c2[name]["GBps"], "frac": c2[name]["GBps"] / peak}
         for name in ("relin", "rotations"):
             extras["roofline_micro"]["ks_" + name] = {"achieved": c3[name]["GBps"], "frac": c3[name]["GBps"] / peak}
+        for name in ("u64", "u32", "u32_ntt", "u32_intt"):
+            extras["roofline_micro"]["cfg2_fused_" + name] = {"achieved": c2f[name]["GBps"],
+                                                              "frac": c2f[name]["GBps"] / peak}
         _, weights = cifar3_weights()
         cores = cores_available()
         cpu = cpu_reference_forward(cores, weights, 20.0)
