@@ -398,7 +398,10 @@ def ntt_roofline(ntt_step: dict, peak: float, peak_kind: str) -> dict:
         "peak_kind": peak_kind, "traffic": _traffic().get("ntt14_fwd"),
         "algorithmic_bytes_per_step": tot_b, "ntt_ms_per_step": tot_ms,
         "algorithmic_bytes_per_unit": "16 B per coefficient of each limb-poly transformed (one u64 read + one u64 "
-                                      "write); fused prologue/epilogue reads are not counted (lower bound)",
+                                      "write) plus the operands a fused prologue/epilogue reads once (rescale-lift "
+                                      "top limb per poly, combine inputs c/A/B, ModDown addend sigma(c0), "
+                                      "epilogue-4 U digits); keys and twiddles excluded (csrc/ntt.cu "
+                                      "ntt_algorithmic_bytes)",
         "launches": sum(v["launches"] for v in ntt_step.values()), "by_class": per,
         "timing": "CUDA event pair around every NTT launch on its stream (bcn_ntt_timing), one untimed step "
                   "after the timed region"}

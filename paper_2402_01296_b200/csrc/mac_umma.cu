@@ -50,7 +50,9 @@ typedef unsigned char u8;
 #ifndef UM_RS
 #define UM_RS 2                                   // raw stages (bulk copy -> transposers)
 #endif
-#define UM_TR 4                                   // transposer warps: one thread per column
+#ifndef UM_TR
+#define UM_TR 8                                   // transposer warps: one thread per (column, k-half); 4: per column
+#endif
 #define UM_W_COPY UM_TR                           // bulk-copy issuer warp
 #define UM_W_MMA (UM_TR + 1)                      // MMA issuer warp (also owns TMEM)
 #define UM_W_EPI (UM_TR + 2)                      // first of the epilogue warps
@@ -289,7 +291,15 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                     const u32 sb = (u32)kmax * UM_COLS * 8, pb = (u32)nbo * 16 * 256;
                     unsigned char* dst = raw + (size_t)rs * UM_RBYTES;
                     mbar_expect_tx(&rfull[rs], sb + pb);
-                    bulk_load(dst, S + (bl * n_terms + c * 32) * UM_COLS, sb, &rfull[rs]);
+#ifndef UM_SPLIT
+#define UM_SPLIT 1
+#endif
+#pragma unroll
+                    for (int sp = 0; sp < UM_SPLIT; sp++)    // UM_SPLIT concurrent bulk copies per chunk
+                        bulk_load(dst + sp * (sb / UM_SPLIT),
+                                  reinterpret_cast<const unsigned char*>(S + (bl * n_terms + c * 32) * UM_COLS) +
+                                      sp * (sb / UM_SPLIT),
+                                  sb / UM_SPLIT, &rfull[rs]);
                     bulk_load(dst + UM_COLS * 32 * 8, planes + ((b * nch + c) * opad + ob * 32) * 256, pb, &rfull[rs]);
                 }
             }
@@ -299,7 +309,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
         // thread = one column; per k-half it reads 16 words (lanes: 32 consecutive
         // columns, conflict-free) and writes one 16-byte core-matrix row per plane
         // (lanes: 512 contiguous bytes, conflict-free)
-        const int col = threadIdx.x;                     // 0 .. 127
+        const int col = threadIdx.x & (UM_COLS - 1);     // 0 .. 127
+        constexpr int KH = UM_TR * 32 / UM_COLS;         // k-halves per thread's column split: 1 or 2 threads
+        const int kh0 = (UM_TR == 8) ? (threadIdx.x >> 7) : 0;
         u32 it = 0;
         for (long long item = i_lo; item < i_hi; item += i_step) {
             const long long bl = item / nob;
@@ -314,7 +326,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                 u8* As = um_smem + (size_t)stage * UM_SBYTES;
                 u8* Bs = As + UM_ABYTES;
 #pragma unroll
-                for (int kh = 0; kh < 2; kh++) {
+                for (int kx = 0; kx < 2 / KH; kx++) {
+                    const int kh = kh0 + kx;
                     u32 pl[8][4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
@@ -332,7 +345,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                         *reinterpret_cast<uint4*>(dst + j * UM_APLANE) = make_uint4(pl[j][0], pl[j][1], pl[j][2], pl[j][3]);
                 }
                 // B: piece (output, k-half, plane) -> its strip row 7 + plane
-                for (int p = col; p < nbo * 256; p += UM_TR * 32) {
+                for (int p = threadIdx.x; p < nbo * 256; p += UM_TR * 32) {
                     const int o = p >> 4, kh = (p >> 3) & 1, i = p & 7;
                     *reinterpret_cast<uint4*>(Bs + kh * UM_BHALF + (o * 16 + 7 + i) * 16) = rp[p];
                 }

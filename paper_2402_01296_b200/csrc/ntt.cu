@@ -267,8 +267,8 @@ static cudaError_t ntt_launch_impl(bool inverse, int logn, const NttArgs& a, int
 // roofline fraction of all NTT launches of a real forward step.  Classes:
 // 0 plain forward, 1 plain inverse, 2 fused forward, 3 fused inverse
 // (fused = prologue / epilogue / out-of-place forms).  Algorithmic bytes:
-// 16 B per coefficient (one u64 read + one u64 write), whatever the fusion
-// reads on top -- a lower bound on the bytes such a launch moves.
+// ntt_algorithmic_bytes() below (16 B per coefficient plus the fused
+// operands); the 16-B-only count is kept alongside for comparison.
 struct NttTimer {
     bool on = false;
     std::vector<cudaEvent_t> ev;     // 2 per record
@@ -277,6 +277,26 @@ struct NttTimer {
     size_t used = 0;
 };
 static NttTimer g_ntt_timer;
+
+// Algorithmic bytes of one launch (distinct inputs read once,
+// outputs written once): 16 B per coefficient of every limb-poly transformed,
+// plus the operands a fused prologue / epilogue reads -- the rescale lift's
+// top limb (once per poly), the combine inputs c / A / B, the ModDown addend
+// sigma(c0), the K special limbs converted in prologue 2, epilogue 4's U
+// digits (shared by the two components of a ciphertext).  Key words and
+// twiddles are excluded (L2-resident, amortised over the batch).
+static unsigned long long ntt_algorithmic_bytes(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys) {
+    const unsigned long long unit = 8ull << logn, nl = (unsigned long long)nlimbs, np = (unsigned long long)npolys;
+    unsigned long long b = 2 * unit * nl * np;
+    if (inverse) return b;
+    if (a.pro == 1) b += unit * np;
+    if (a.pro == 2 && a.pro_dnum == 0) b += unit * np * (unsigned long long)a.pro_K;
+    if (a.epi == 1) b += unit * nl * np;
+    if (a.epi == 2 || a.epi == 3) b += unit * nl * np;
+    if (a.epi == 4) b += unit * nl * (np / 2) * (unsigned long long)a.epi_ndig;
+    if ((a.epi == 2 || a.epi == 3 || a.epi == 4) && a.epi_add) b += unit * nl * (a.epi_add_c1 ? np : (np + 1) / 2);
+    return b;
+}
 
 cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int npolys, cudaStream_t st) {
     if (nlimbs <= 0 || npolys <= 0) return cudaSuccess;
@@ -295,7 +315,7 @@ cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int
     const size_t i = T.used++;
     const bool fused = a.pro || a.epi || a.copy_src || a.inv_scale || a.src;
     T.cls[i] = (fused ? 2 : 0) + (inverse ? 1 : 0);
-    T.bytes[i] = 16ull * (1ull << logn) * (unsigned long long)nlimbs * (unsigned long long)npolys;
+    T.bytes[i] = ntt_algorithmic_bytes(inverse, logn, a, nlimbs, npolys);
     cudaEventRecord(T.ev[2 * i], st);
     cudaError_t e = ntt_launch_impl(inverse, logn, a, nlimbs, npolys, st);
     cudaEventRecord(T.ev[2 * i + 1], st);

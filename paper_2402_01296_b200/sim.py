@@ -79,6 +79,16 @@ class OpRecorder:
         self.per_layer: list[tuple[str, dict]] = []
         self._open: list[tuple[str, dict]] = []
         self._unscoped = _zeros()
+        self._timing = False
+        self._events: list[tuple[str, object, object]] = []
+
+    def enable_timing(self, on: bool = True) -> None:
+        """Device time per layer scope (no reference counterpart; tracing aid):
+        every scope records a CUDA event pair on the current stream and an
+        NVTX range, read back by layer_times().  Lazily evaluated terms run in
+        the scope that first uses them, so a layer's time is the device work
+        issued while it is open."""
+        self._timing = on
 
     def bump(self, key: str, n: int = 1) -> None:
         self.counters[key] += n
@@ -108,6 +118,14 @@ class OpRecorder:
     def snapshot(self) -> dict:
         return dict(self.counters)
 
+    def layer_times(self) -> list[tuple[str, float]]:
+        """(scope, device ms) in scope-exit order; synchronises the events."""
+        out = []
+        for name, e0, e1 in self._events:
+            e1.synchronize()
+            out.append((name, e0.elapsed_time(e1)))
+        return out
+
 
 class _Scope:
     __slots__ = ("rec", "name")
@@ -117,11 +135,24 @@ class _Scope:
 
     def __enter__(self):
         self.rec._open.append((self.name, _zeros()))
+        if self.rec._timing:
+            import torch
+            torch.cuda.nvtx.range_push(self.name)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.rec._open[-1] = (self.name, self.rec._open[-1][1], ev)
         return self.rec
 
     def __exit__(self, *exc):
-        name, delta = self.rec._open.pop()
+        entry = self.rec._open.pop()
+        name, delta = entry[0], entry[1]
         self.rec.per_layer.append((name, delta))
+        if len(entry) > 2:
+            import torch
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            torch.cuda.nvtx.range_pop()
+            self.rec._events.append((name, entry[2], ev))
         return False
 
 

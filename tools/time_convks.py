@@ -1,0 +1,43 @@
+"""A/B timing of the conv layer with lazy ModDown on the tensor cores
+(bcn_conv_ks_mac: slot_major_ks + mac_umma + merged ModDown/rescale tails)
+at cifar3 conv2's shape: 16 sources x 9 taps = 144 terms, 32 outputs,
+level 11, G slot sets (default 128).  Prints ms per call (CUDA events)."""
+import ctypes
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2402_01296_b200 import _lib  # noqa: E402
+from paper_2402_01296_b200.engine import Engine  # noqa: E402
+from paper_2402_01296_b200.params import galois_element as ge, make_params  # noqa: E402
+
+G = int(os.environ.get("PROF_G", "128"))
+hp = make_params(16384, 14, 50, dnum=3)
+eng = Engine(hp)
+lvl, O = 11, 32
+srcs = [eng.sample_uniform(2 * G, lvl + 1, 0, seed=9 + i).view(G, 2, lvl + 1, 16384) for i in range(16)]
+Us = [eng.modup(x, lvl) for x in srcs]
+rots = [0, 1, 2, 16, 17, 18, 32, 33, 34]
+terms = [(srcs[c], Us[c], ge(r, 16384) if r else 1) for c in range(16) for r in rots]
+nb = ctypes.c_uint64()
+_lib.call("bcn_planes_ext_bytes", eng._h, O, len(terms), lvl, ctypes.byref(nb))
+planes = torch.randint(0, 256, (int(nb.value),), dtype=torch.uint8, device="cuda")
+
+
+def run():
+    return eng.conv_ks_mac([t[0] for t in terms], [t[1] if t[2] != 1 else None for t in terms],
+                           [t[2] for t in terms], planes, O, lvl, 1)
+
+
+out = run()
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(3):
+    out = run()
+e.record()
+torch.cuda.synchronize()
+print(f"{os.environ.get('BCN_LIB', 'default')}: conv_ks_mac G={G} {s.elapsed_time(e) / 3:.3f} ms "
+      f"checksum {int(out.view(-1)[::9973].sum())}")
