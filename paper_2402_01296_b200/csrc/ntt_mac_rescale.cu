@@ -87,16 +87,30 @@ template <int LOGN> struct NmrCfg {
     static constexpr int R0 = (LOGN % LOGE) ? (LOGN % LOGE) : LOGE;
 };
 
-// SMEM swizzle: low 4 bits ^= bits 4..7, bit 4 ^= bit 8 -- every pass of the
-// E = 16 schedule is bank-conflict free for 4-byte words (and for 8-byte
-// words, whose bank does not depend on bit 4)
-template <int LOGN> __device__ __forceinline__ int sw(int j) { return j ^ ((j >> 4) & 15) ^ (((j >> 8) & 1) << 4); }
+// SMEM layout: one pad word per 32 (index j lives at j + j / 32).  For every
+// pass of the E = 16 schedule the address is affine in the unrolled element
+// index (immediate offsets from one per-thread base: no per-access ALU), and
+// the 32 lanes of a warp hit 32 distinct banks with 4-byte words: runs of 32
+// consecutive columns (strides >= 32), stride-16 runs in the last pass, and
+// in the stride-16 pass the two half-warps take block rows 2 apart (bits 4
+// and 5 of the block index swapped, blk()), which the padding puts 16 banks
+// apart.
+template <int LOGN> __device__ __forceinline__ int sw(int j) { return j + (j >> 5); }
+template <int LOGN> struct Pad { static constexpr int NP = (1 << LOGN) + ((1 << LOGN) >> 5); };
+// padded address of element base + k TL as (per-thread base) + (compile-time offset)
+template <int TL, int BS>
+__device__ __forceinline__ int pad_at(int pbase, int base, int k) {
+    if constexpr (TL % 32 == 0) return pbase + k * TL + ((k * TL) >> 5);
+    else if constexpr (TL == 16) return pbase + 16 * k + (k >> 1);      // base % 32 < 16
+    else if constexpr (TL == 1 && BS == 16) return pbase + k;           // base % 16 == 0
+    else return (base + k * TL) + ((base + k * TL) >> 5);
+}
+// block index of thread slot b in a pass with element stride TL
+template <int TL> __device__ __forceinline__ int blk(int b) {
+    if constexpr (TL == 16) return (b & ~0x30) | ((b & 0x10) << 1) | ((b & 0x20) >> 1);
+    else return b;
+}
 
-// ---- forward pass: S0 stages done, R more.  FIRST reads via ld(j) -- every
-// load of the pass is issued before a barrier, so ld may read the very array
-// the pass then writes (the NTT runs in place in its input ring slot); other
-// passes read / write the swizzled array `sm`; LAST leaves the canonical
-// result in x (thread owns words (tid + i T) BS + k).
 struct NoHook { __device__ void operator()() const {} };
 
 template <class W, int LOGN, int S0, int R, bool FIRST, bool LAST, class Ld, class Hook = NoHook>
@@ -107,10 +121,12 @@ __device__ __forceinline__ void fpass(W* x, W* sm, const typename Ar<W>::TW* __r
     const W q2 = 2 * q;
 #pragma unroll
     for (int i = 0; i < NB; i++) {
-        const int b = tid + i * C::T;
+        const int b = blk<TL>(tid + i * C::T);
         const int base = (b / TL) * (C::N >> S0) + (b % TL);
+        const int pbase = base + (base >> 5);
 #pragma unroll
-        for (int k = 0; k < BS; k++) x[i * BS + k] = FIRST ? ld(base + k * TL) : sm[sw<LOGN>(base + k * TL)];
+        for (int k = 0; k < BS; k++)
+            x[i * BS + k] = FIRST ? ld(base + k * TL) : sm[pad_at<TL, BS>(pbase, base, k)];
     }
     if (FIRST) {
         __syncthreads();
@@ -118,17 +134,19 @@ __device__ __forceinline__ void fpass(W* x, W* sm, const typename Ar<W>::TW* __r
     }
 #pragma unroll
     for (int i = 0; i < NB; i++) {
-        const int b = tid + i * C::T;
+        const int b = blk<TL>(tid + i * C::T);
         const int gi = b / TL;
         const int base = gi * (C::N >> S0) + (b % TL);
+        const int pbase = base + (base >> 5);
 #pragma unroll
         for (int ls = 0; ls < R; ls++) {
             const int h = BS >> (ls + 1);
             const int s = S0 + ls;
+            const typename Ar<W>::TW* __restrict__ ws = Wt + (1 << s) + (gi << ls);   // + compile-time offsets
 #pragma unroll
             for (int k = 0; k < BS; k++) {
                 if (k & h) continue;
-                const typename Ar<W>::TW w = Wt[(1 << s) + (gi << ls) + (k >> (R - ls))];
+                const typename Ar<W>::TW w = ws[k >> (R - ls)];
                 W u = x[i * BS + k];
                 if (!(FIRST && ls == 0)) u = csubw<W>(u, q2);
                 const W v = Ar<W>::shoup_lazy(x[i * BS + k + h], w.x, w.y, q);
@@ -139,29 +157,33 @@ __device__ __forceinline__ void fpass(W* x, W* sm, const typename Ar<W>::TW* __r
 #pragma unroll
         for (int k = 0; k < BS; k++) {
             if (LAST) x[i * BS + k] = csubw<W>(csubw<W>(x[i * BS + k], q2), q);
-            else sm[sw<LOGN>(base + k * TL)] = x[i * BS + k];
+            else sm[pad_at<TL, BS>(pbase, base, k)] = x[i * BS + k];
         }
     }
 }
 
-template <class W, int LOGN, int S0>
-__device__ __forceinline__ void frest(W* x, W* sm, const typename Ar<W>::TW* __restrict__ Wt, W q, int tid) {
+template <class W, int LOGN, int S0, class Hook2>
+__device__ __forceinline__ void frest(W* x, W* sm, const typename Ar<W>::TW* __restrict__ Wt, W q, int tid,
+                                      Hook2 last_hook) {
     using C = NmrCfg<LOGN>;
     if constexpr (S0 < LOGN) {
         __syncthreads();
+        if constexpr (S0 + C::LOGE >= LOGN) last_hook();
         fpass<W, LOGN, S0, C::LOGE, false, (S0 + C::LOGE >= LOGN)>(x, sm, Wt, q, tid, [](int) { return W(0); });
-        frest<W, LOGN, S0 + C::LOGE>(x, sm, Wt, q, tid);
+        frest<W, LOGN, S0 + C::LOGE>(x, sm, Wt, q, tid, last_hook);
     }
 }
 
 // full forward NTT: input via ld(j), result canonical in x (no trailing
-// barrier); hook() runs on every thread right after the first barrier
-template <class W, int LOGN, class Ld, class Hook = NoHook>
+// barrier); hook() runs on every thread right after the first barrier,
+// last_hook() right before the last pass (e.g. to issue the loads the code
+// after the transform consumes)
+template <class W, int LOGN, class Ld, class Hook = NoHook, class Hook2 = NoHook>
 __device__ __forceinline__ void fwd_ntt(W* x, W* sm, const typename Ar<W>::TW* __restrict__ Wt, W q, int tid, Ld ld,
-                                        Hook hook = Hook()) {
+                                        Hook hook = Hook(), Hook2 last_hook = Hook2()) {
     using C = NmrCfg<LOGN>;
     fpass<W, LOGN, 0, C::R0, true, (C::R0 >= LOGN)>(x, sm, Wt, q, tid, ld, hook);
-    frest<W, LOGN, C::R0>(x, sm, Wt, q, tid);
+    frest<W, LOGN, C::R0>(x, sm, Wt, q, tid, last_hook);
 }
 
 // the words the last forward pass leaves in x[e] of thread tid
@@ -205,23 +227,37 @@ __device__ __forceinline__ void store_own(W* dst, const W* x, int tid) {
 
 // ---- inverse (Gentleman-Sande) in place on the swizzled array `a`; the last
 // stage folds N^-1; output canonical in `a` (swizzled).  Ends with a barrier.
-template <class W, int LOGN, int S0, int R, bool LAST>
+template <class W, int LOGN, int S0, int R, bool LAST, bool GIN = false, bool GOUT = false>
 __device__ __forceinline__ void ipass(W* x, W* a, const typename Ar<W>::TW* __restrict__ Wi, W q, W ninv, W ninv_p,
-                                      W wn, W wn_p, int tid) {
+                                      W wn, W wn_p, int tid, const W* __restrict__ gin = nullptr,
+                                      W* __restrict__ gout = nullptr) {
     using C = NmrCfg<LOGN>;
     constexpr int BS = 1 << R, NB = C::E / BS, TL = C::N >> (S0 + R);
     const W q2 = 2 * q;
 #pragma unroll
     for (int i = 0; i < NB; i++) {
-        const int b = tid + i * C::T;
+        const int b = blk<TL>(tid + i * C::T);
         const int gi = b / TL;
         const int base = gi * (C::N >> S0) + (b % TL);
+        const int pbase = base + (base >> 5);
 #pragma unroll
-        for (int k = 0; k < BS; k++) x[i * BS + k] = a[sw<LOGN>(base + k * TL)];
+        if constexpr (GIN) {                            // first pass straight from HBM: contiguous 16-word runs
+            static_assert(TL == 1 && BS == 16, "global input needs a contiguous first pass");
+            constexpr int PER = 16 / sizeof(W);
+#pragma unroll
+            for (int v = 0; v < BS / PER; v++) {
+                const uint4 r = __ldg(reinterpret_cast<const uint4*>(gin + base) + v);
+                memcpy(&x[i * BS + v * PER], &r, 16);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < BS; k++) x[i * BS + k] = a[pad_at<TL, BS>(pbase, base, k)];
+        }
 #pragma unroll
         for (int ls = R - 1; ls >= 0; ls--) {
             const int h = BS >> (ls + 1);
             const int s = S0 + ls;
+            const typename Ar<W>::TW* __restrict__ ws = Wi + (1 << s) + (gi << ls);
 #pragma unroll
             for (int k = 0; k < BS; k++) {
                 if (k & h) continue;
@@ -230,53 +266,63 @@ __device__ __forceinline__ void ipass(W* x, W* a, const typename Ar<W>::TW* __re
                     x[i * BS + k] = shoupw<W>(u + v, ninv, ninv_p, q);
                     x[i * BS + k + h] = shoupw<W>(u - v + q2, wn, wn_p, q);
                 } else {
-                    const typename Ar<W>::TW w = Wi[(1 << s) + (gi << ls) + (k >> (R - ls))];
+                    const typename Ar<W>::TW w = ws[k >> (R - ls)];
                     x[i * BS + k] = csubw<W>(u + v, q2);
                     x[i * BS + k + h] = Ar<W>::shoup_lazy(u - v + q2, w.x, w.y, q);
                 }
             }
         }
 #pragma unroll
-        for (int k = 0; k < BS; k++) a[sw<LOGN>(base + k * TL)] = x[i * BS + k];
+        for (int k = 0; k < BS; k++) {
+            if constexpr (GOUT) gout[base + k * TL] = x[i * BS + k];   // last pass straight to HBM (coalesced)
+            else a[pad_at<TL, BS>(pbase, base, k)] = x[i * BS + k];
+        }
     }
-    __syncthreads();
+    if constexpr (!GOUT) __syncthreads();
 }
 
-template <class W, int LOGN, int S0>
+template <class W, int LOGN, int S0, bool GIN = false>
 __device__ __forceinline__ void irest(W* x, W* a, const typename Ar<W>::TW* __restrict__ Wi, W q, W ninv, W ninv_p,
-                                      W wn, W wn_p, int tid) {
+                                      W wn, W wn_p, int tid, const W* gin = nullptr) {
     using C = NmrCfg<LOGN>;
     if constexpr (S0 >= C::R0) {
-        ipass<W, LOGN, S0, C::LOGE, false>(x, a, Wi, q, ninv, ninv_p, wn, wn_p, tid);
+        ipass<W, LOGN, S0, C::LOGE, false, GIN>(x, a, Wi, q, ninv, ninv_p, wn, wn_p, tid, gin);
         irest<W, LOGN, S0 - C::LOGE>(x, a, Wi, q, ninv, ninv_p, wn, wn_p, tid);
     }
 }
 
-template <class W, int LOGN>
+// inverse NTT: in place on the padded SMEM array `a`, or (GIO) from gio in HBM
+// back to gio, with `a` as the exchange buffer
+template <class W, int LOGN, bool GIO = false>
 __device__ __forceinline__ void inv_ntt_smem(W* x, W* a, const typename Ar<W>::TW* __restrict__ Wi, W q, W ninv,
-                                             W ninv_p, W wn, W wn_p, int tid) {
+                                             W ninv_p, W wn, W wn_p, int tid, W* gio = nullptr) {
     using C = NmrCfg<LOGN>;
-    irest<W, LOGN, LOGN - C::LOGE>(x, a, Wi, q, ninv, ninv_p, wn, wn_p, tid);
-    ipass<W, LOGN, 0, C::R0, true>(x, a, Wi, q, ninv, ninv_p, wn, wn_p, tid);
+    static_assert(!GIO || LOGN - C::LOGE >= C::R0, "global in/out needs at least two passes");
+    irest<W, LOGN, LOGN - C::LOGE, GIO>(x, a, Wi, q, ninv, ninv_p, wn, wn_p, tid, gio);
+    ipass<W, LOGN, 0, C::R0, true, false, GIO>(x, a, Wi, q, ninv, ninv_p, wn, wn_p, tid, nullptr, gio);
 }
 
 // ---- the fused kernel --------------------------------------------------
 // Cluster = 2 nlimb CTAs: rank = component * nlimb + limb.  SMEM per CTA:
-// ring[2][N] (bulk-copied ciphertext limb-polys; each NTT runs in place in
-// its slot) | pts[N] (the term's plaintext limb, bulk-copied while the NTT
-// runs) | 3 mbarriers: 3 N words = 96 KiB (u32: 2 CTAs per SM) / 192 KiB
-// (u64) at N = 8192.  The running sum lives in registers: the words the last
-// NTT pass leaves in a thread are the words it accumulates.
-template <class W, int LOGN> struct NmrOcc { static constexpr int MINB = (sizeof(W) == 4 && LOGN <= 13) ? 2 : 1; };
+// ring[2][33 N / 32] (bulk-copied ciphertext limb-polys; each NTT runs in
+// place in its slot, padded) | 2 mbarriers: 66 KiB (u32) / 132 KiB (u64) at
+// N = 8192.  The running sum lives in registers: the words the last NTT pass
+// leaves in a thread are the words it accumulates, and its plaintext words
+// (16 consecutive) come straight from HBM/L2 with 16-byte loads issued
+// before the last pass.
+#ifndef NMR_MINB32
+#define NMR_MINB32 2
+#endif
+template <class W, int LOGN> struct NmrOcc { static constexpr int MINB = (sizeof(W) == 4 && LOGN <= 13) ? NMR_MINB32 : 1; };
 
 template <class W, int LOGN>
 __global__ void __launch_bounds__(NmrCfg<LOGN>::T, (NmrOcc<W, LOGN>::MINB)) ntt_mac_rescale_kernel(NmrArgs<W> a) {
     using C = NmrCfg<LOGN>;
     using O = Own<LOGN>;
     extern __shared__ __align__(16) unsigned char smraw[];
+    constexpr int NP = Pad<LOGN>::NP;                  // padded slot (the in-place NTT writes j + j / 32)
     W* ring = reinterpret_cast<W*>(smraw);
-    W* pts = ring + 2 * C::N;
-    u64* bar = reinterpret_cast<u64*>(pts + C::N);     // [0], [1] ring slots, [2] plaintext
+    u64* bar = reinterpret_cast<u64*>(ring + 2 * NP);  // [0], [1] ring slots
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     const int comp = rank / a.nlimb, t = rank - comp * a.nlimb;
@@ -291,14 +337,15 @@ __global__ void __launch_bounds__(NmrCfg<LOGN>::T, (NmrOcc<W, LOGN>::MINB)) ntt_
     auto src_of = [&](int s) { return a.ct + (((size_t)(k0 + s) * 2 + comp) * a.nlimb + t) * C::N; };
     auto pt_of = [&](int s) { return a.pt + ((size_t)(k0 + s) * a.nlimb + t) * C::N; };
     if (tid == 0) {
-        for (int i = 0; i < 3; i++) mbar_init(&bar[i], 1);
+        for (int i = 0; i < 2; i++) mbar_init(&bar[i], 1);
         fence_barrier_init();
         for (int s = 0; s < 2 && s < nterm; s++) {
             mbar_expect_tx(&bar[s], BYTES);
-            bulk_load(ring + s * C::N, src_of(s), BYTES, &bar[s]);
+            bulk_load(ring + s * NP, src_of(s), BYTES, &bar[s]);
         }
     }
     W x[C::E];
+    W p[C::E];
     W acc[C::E];
 #pragma unroll
     for (int e = 0; e < C::E; e++) acc[e] = 0;
@@ -307,25 +354,21 @@ __global__ void __launch_bounds__(NmrCfg<LOGN>::T, (NmrOcc<W, LOGN>::MINB)) ntt_
     for (int s = 0; s < nterm; s++) {
         const int slot = s & 1;
         mbar_wait(&bar[slot], (u32)((s >> 1) & 1));
-        W* in = ring + slot * C::N;
-        fwd_ntt<W, LOGN>(x, in, Wt, q, tid, [&](int j) { return in[j]; }, [&]() {
-            if (tid == 0) {                             // every thread is done with pts of term s - 1
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&bar[2], BYTES);
-                bulk_load(pts, pt_of(s), BYTES, &bar[2]);
-            }
-        });
+        W* in = ring + slot * NP;
+        // the plaintext words this thread multiplies (its 16 output words, 4 x 16-byte
+        // loads) are issued right before the last pass, whose butterflies hide them
+        fwd_ntt<W, LOGN>(x, in, Wt, q, tid, [&](int j) { return in[j]; }, NoHook(),
+                         [&]() { load_own<W, LOGN>(p, pt_of(s), tid); });
         __syncthreads();                                // every thread is done with ring[slot]
         if (tid == 0 && s + 2 < nterm) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&bar[slot], BYTES);
             bulk_load(in, src_of(s + 2), BYTES, &bar[slot]);
         }
-        mbar_wait(&bar[2], (u32)(s & 1));
 #pragma unroll
-        for (int e = 0; e < C::E; e++) acc[e] = csubw<W>(acc[e] + Ar<W>::mont(x[e], pts[O::word(tid, e)], q, qneg), q);
+        for (int e = 0; e < C::E; e++) acc[e] = csubw<W>(acc[e] + Ar<W>::mont(x[e], p[e], q, qneg), q);
     }
-    __syncthreads();                                    // ring / pts free
+    __syncthreads();                                    // ring free
     // ---- rescale by q_top: the top limb's sums go through SMEM (ring slot 0)
     W* sums = ring;
     if (t == top) {
@@ -340,7 +383,7 @@ __global__ void __launch_bounds__(NmrCfg<LOGN>::T, (NmrOcc<W, LOGN>::MINB)) ntt_
         const W qt = a.k.q[top], half = qt >> 1;
         const W inv1 = a.k.inv1[t], qlm = a.k.qlmod[t];
         const W qli = a.k.qlinv[t], qlip = a.k.qlinv_p[t];
-        fwd_ntt<W, LOGN>(x, ring + C::N, Wt, q, tid, [&](int j) {
+        fwd_ntt<W, LOGN>(x, ring + NP, Wt, q, tid, [&](int j) {
             const W v = rs[sw<LOGN>(j)];
             const W r = shoupw<W>(v, W(1), inv1, q);                   // v mod q_t
             return v > half ? (r >= qlm ? r - qlm : r + q - qlm) : r;  // centred lift: v - q_top
@@ -353,7 +396,7 @@ __global__ void __launch_bounds__(NmrCfg<LOGN>::T, (NmrOcc<W, LOGN>::MINB)) ntt_
 }
 
 template <class W, int LOGN>
-static size_t nmr_smem() { return (size_t)3 * NmrCfg<LOGN>::N * sizeof(W) + 24; }
+static size_t nmr_smem() { return (size_t)2 * Pad<LOGN>::NP * sizeof(W) + 16; }
 
 template <class W, int LOGN>
 static cudaError_t nmr_launch_t(const NmrArgs<W>& a, int n_groups, cudaStream_t st) {
@@ -416,14 +459,9 @@ __global__ void __launch_bounds__(NmrCfg<LOGN>::T) ntt_w_kernel(W* data, const t
     W x[C::E];
     if constexpr (!INV) {
         fwd_ntt<W, LOGN>(x, sm, Wt, q, tid, [&](int j) { return g[j]; });
-        constexpr int BSL = 1 << ((C::R0 >= LOGN) ? C::R0 : C::LOGE);
-#pragma unroll
-        for (int e = 0; e < C::E; e++) g[(tid + (e / BSL) * C::T) * BSL + (e % BSL)] = x[e];
+        store_own<W, LOGN>(g, x, tid);
     } else {
-        for (int j = tid; j < C::N; j += C::T) sm[sw<LOGN>(j)] = g[j];
-        __syncthreads();
-        inv_ntt_smem<W, LOGN>(x, sm, Wt + C::N, q, k.ninv[t], k.ninv_p[t], k.wn[t], k.wn_p[t], tid);
-        for (int j = tid; j < C::N; j += C::T) g[j] = sm[sw<LOGN>(j)];
+        inv_ntt_smem<W, LOGN, true>(x, sm, Wt + C::N, q, k.ninv[t], k.ninv_p[t], k.wn[t], k.wn_p[t], tid, g);
     }
 }
 
@@ -431,7 +469,7 @@ template <class W, int LOGN>
 static cudaError_t ntt_w_launch_t(bool inv, W* data, const typename Ar<W>::TW* tw, const NmrConst<W>& k, int nlimb,
                                   int npoly, cudaStream_t st) {
     using C = NmrCfg<LOGN>;
-    const size_t smem = (size_t)C::N * sizeof(W);
+    const size_t smem = (size_t)Pad<LOGN>::NP * sizeof(W);
     static unsigned long long cfg = 0;
     unsigned long long bit = 0;
     if (first_on_device(&cfg, &bit)) {
