@@ -247,6 +247,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, u32 bytes,
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
 }
+// L2 prefetch of a contiguous range by the TMA engine (no registers, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, u32 bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
     u32 done;
     do {

@@ -120,6 +120,31 @@ struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top
     long long uds = 0, kds = 0;
     int ndig = 0;
     u64 qinv_neg = 0, inv1 = 0;
+    // issue L2 bulk prefetches of everything operator() will read for the
+    // words [j0, j0 + part) of this CTA, so those loads overlap the transform
+    // instead of following it.  Under X -> X^g an aligned 32-block is the image
+    // of one aligned 32-block, so a gathered operand is 256-byte runs.
+    __device__ __forceinline__ void prefetch(int j0, int part, int tid, int nthr) const {
+        if constexpr (MODE == 0) {
+            return;
+        } else {
+            constexpr u32 RUN = 32 * sizeof(u64);
+            const bool gather = (MODE == 2 || MODE == 4) && g != 1u;
+            for (int b = tid; b < part / 32; b += nthr) {
+                const int j = j0 + 32 * b;
+                const int sj = gather ? ((int)automorph_src((u32)j, g, logn) & ~31) : j;
+                if constexpr (MODE == 4) {
+                    for (int d = 0; d < ndig; d++) {
+                        bulk_prefetch_l2(U + d * uds + sj, RUN);
+                        bulk_prefetch_l2(kp + d * kds + j, RUN);
+                    }
+                } else {
+                    bulk_prefetch_l2(c + j, RUN);
+                }
+                if (add) bulk_prefetch_l2(add + (MODE == 3 ? j : sj), RUN);
+            }
+        }
+    }
     __device__ __forceinline__ u64 operator()(int j, u64 v) const {
         if constexpr (MODE == 0) {
             return v;
@@ -642,6 +667,9 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
         epi.w = epi.wp = 0;
     }
     const int tid = threadIdx.x;
+    if constexpr (EM != 0) {
+        if (a.epi_pf) epi.prefetch(rank * C::PART, C::PART, tid, C::T);
+    }
     if (a.twf && q < (1ull << 50)) {         // FP64 butterflies (uniform per cluster: one limb)
         double* dpeers[C::CS];
 #pragma unroll
@@ -861,6 +889,10 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     static const bool pm_env = getenv("BCN_NTT_POLY_MAJOR") && getenv("BCN_NTT_POLY_MAJOR")[0] == '1';
     NttArgs b = a;
     b.grid_pm = (pm_env || npolys > 65535) ? 1 : 0;
+    // BCN_EPI_PREFETCH=1: L2 bulk prefetch of the fused epilogue's operands at kernel
+    // start -- measured slower (config-3 rotations 65.8 -> 70.2 ms, cifar3 step unchanged)
+    static const bool pf_on = getenv("BCN_EPI_PREFETCH") && getenv("BCN_EPI_PREFETCH")[0] == '1';
+    b.epi_pf = pf_on ? 1 : 0;
     const dim3 grid = b.grid_pm ? dim3(C::CS * npolys, nlimbs) : dim3(C::CS * nlimbs, npolys);
     // FP64-only instantiations where they measured faster (the inverse, the merged tails
     // <0,3>: 74.8 -> 70.9 ms per cifar3 forward); the plain forward <0,0> measured slower

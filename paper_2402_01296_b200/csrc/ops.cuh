@@ -40,6 +40,7 @@ struct NttArgs {
     const ulonglong2* twt;   // cluster NTT (logn 13/14): tw with the pass-transposed layout of twf
     const double2* twf;
     int fp_all;              // every limb of the launch is below 2^50 (FP64-only kernel variants)
+    int epi_pf;              // cluster NTT: L2-prefetch the fused epilogue's operands at kernel start (set by the launcher)
     int grid_pm;             // cluster NTT grid order: 0 limb fastest (default), 1 poly fastest (set by the launcher)      // same layout, {w, w/q} in FP64 (cluster NTT, q < 2^50); nullptr: integer only
     const PrimeInfo* pr;
     int skip_alpha;          // ModUp: skip limb t of digit d when t/alpha == d and t <= skip_level
