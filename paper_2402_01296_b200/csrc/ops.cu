@@ -879,6 +879,71 @@ __global__ void __launch_bounds__(256, BCN_RS2_MINB) rotsum2_kernel(
     }
 }
 
+// rotsum3: rotsum2 for the common case -- every term's key already carries its
+// multiplier (fused, bcn_premul_key) and no plaintext is batched per slot set.
+// Straight-line term loop: the per-term state is the Galois element and four
+// pointers from the parameter bank, the block coordinates are hoisted, and
+// the high halves fold every 32 / ND terms at a uniform counter instead of a
+// per-term check (ISA: ~90 instead of ~210 instructions per term at ND = 2).
+#ifndef BCN_RS3_MINB
+#define BCN_RS3_MINB 6
+#endif
+template <int ND>
+__global__ void __launch_bounds__(256, BCN_RS3_MINB) rotsum3_kernel(
+        u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T, long long c0_gstride, int nq, int next,
+        int logn, long long kds, long long kcs, Limbs ext, const PrimeInfo* __restrict__ pr, int acc_flags,
+        long long c0_ostride) {
+    constexpr int FOLD = 32 / ND;
+    const int N = 1 << logn;
+    const int n = blockIdx.x * 256 + threadIdx.x;
+    const int t = blockIdx.y;
+    const long long p = blockIdx.z;
+    const int kt = ext.prime[t];
+    const PrimeInfo& P = pr[kt];
+    const u64 q = P.q, qn = P.qinv_neg, one_m = P.r1, inv1 = P.pad[2];
+    const bool has_c0 = t < nq;
+    const u32 dstr = (u32)next * (u32)N;
+    const u32 uoff = ((u32)p * ND * next + t) * (u32)N;
+    const u32 coff = (u32)(p * c0_gstride) + (u32)t * N;
+    const u32 koff = (u32)kt * N + n;
+    const u32 poff = (u32)t * N + n;
+    const u32 kds32 = (u32)kds, kcs32 = (u32)kcs;
+    Acc4 b0, b1, cc;
+    b0.zero(); b1.zero(); cc.zero();
+    int kf = 0;
+    for (int k = 0; k < T.n; k++) {
+        const u32 sn = automorph_src((u32)n, T.g[k], logn);
+        const u64* __restrict__ Uk = T.U[k] + (uoff + sn);
+        const u64* __restrict__ kp = T.key[k] + koff;
+#pragma unroll
+        for (int j = 0; j < ND; j++) {
+            const u64 u = __ldg(Uk + j * dstr);
+            b0.mac(u, __ldg(kp + j * kds32));
+            b1.mac(u, __ldg(kp + j * kds32 + kcs32));
+        }
+        if (has_c0) {
+            const u64* pk = T.pt[k];
+            const u64 w = pk ? __ldg(pk + poff) : one_m;
+            cc.mac(__ldg(T.c0[k] + (coff + sn)), w);
+            if ((k & 31) == 31) cc.fold_hi(q, inv1);
+        }
+        if (++kf == FOLD) { b0.fold_hi(q, inv1); b1.fold_hi(q, inv1); kf = 0; }
+    }
+    const int accumulate = acc_flags & 1, c0_acc = (acc_flags >> 1) & 1;
+    u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
+    u64* o1 = o0 + (long long)next * N;
+    u64 r0 = b0.reduce(q, qn, inv1), r1 = b1.reduce(q, qn, inv1);
+    if (accumulate) { r0 = add_mod(r0, *o0, q); r1 = add_mod(r1, *o1, q); }
+    *o0 = r0;
+    *o1 = r1;
+    if (has_c0) {
+        u64* oc = C0 + p * c0_ostride + (long long)t * N + n;
+        u64 rc = cc.reduce(q, qn, inv1);
+        if (c0_acc) rc = add_mod(rc, *oc, q);
+        *oc = rc;
+    }
+}
+
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
                       int accumulate, cudaStream_t st, long long c0_ostride, int c0_accumulate) {
@@ -892,6 +957,18 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
         return cudaErrorInvalidValue;                 // kernel offsets are 32-bit
     if (N >= 256 && !getenv("BCN_ROTSUM_STAGED")) {
         dim3 grid(N / 256, next, G);
+        static const bool rs3_off = getenv("BCN_ROTSUM3") && getenv("BCN_ROTSUM3")[0] == '0';
+        bool simple = !rs3_off && ndig >= 1 && ndig <= 4;
+        for (int k = 0; k < terms.n && simple; k++) simple = terms.fused[k] && !terms.pt_batched[k];
+        if (simple) {
+            switch (ndig) {
+#define BCN_RS3(D) case D: rotsum3_kernel<D><<<grid, 256, 0, st>>>(B, C0, terms, c0_gstride, nq, next, logn, kds, kcs, \
+                                                                 ext, pr, flags, c0_ostride); break;
+                BCN_RS3(1) BCN_RS3(2) BCN_RS3(3) BCN_RS3(4)
+#undef BCN_RS3
+            }
+            return launched();
+        }
         switch (ndig) {
 #define BCN_RS2(D) case D: rotsum2_kernel<D><<<grid, 256, 0, st>>>(B, C0, terms, c0_gstride, nq, next, ndig, logn, \
                                                                  kds, kcs, ext, pr, flags, c0_ostride); break;
