@@ -50,8 +50,11 @@ typedef unsigned char u8;
 #ifndef UM_RS
 #define UM_RS 2                                   // raw stages (bulk copy -> transposers)
 #endif
+#ifndef UM_PAIR_MAXO
+#define UM_PAIR_MAXO 32                           // widest output count stored as slot pairs
+#endif
 #ifndef UM_TR
-#define UM_TR 8                                   // transposer warps: one thread per (column, k-half); 4: per column
+#define UM_TR 4                                   // transposer warps: one thread per column (8: per column and k-half, no gain; 4 leaves the epilogue registers for slot pairs)
 #endif
 #define UM_W_COPY UM_TR                           // bulk-copy issuer warp
 #define UM_W_MMA (UM_TR + 1)                      // MMA issuer warp (also owns TMEM)
@@ -273,13 +276,22 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
     const long long tstart = clock64();
     // items strided over the CTAs: at any moment the GPU streams adjacent slots,
     // i.e. one contiguous region of S (a contiguous run per CTA is 2x slower)
-    const long long i_lo = blockIdx.x, i_hi = items, i_step = gridDim.x;
+    const long long i_hi = items;
+    // item sequence of this CTA: items strided over the CTAs; with one item per
+    // slot (<= 32 outputs) in pairs of adjacent slots, so the epilogue can hold a
+    // pair's words and store them as 16-byte runs (half the store requests of
+    // the 32-lines-per-instruction 8-byte stores)
+    const bool paired = nob == 1 && opad <= UM_PAIR_MAXO && !(dbg & 16);
+    auto item_at = [&](long long k) -> long long {
+        return paired ? 2 * ((long long)blockIdx.x + (k >> 1) * gridDim.x) + (k & 1)
+                      : (long long)blockIdx.x + k * gridDim.x;
+    };
 
     if (warp == UM_W_COPY) {
         // ------------------------------------------------ bulk-copy issuer (one lane)
         if (lane == 0) {
             u32 it = 0;
-            for (long long item = i_lo; item < i_hi; item += i_step) {
+            for (long long kk = 0, item = item_at(0); item < i_hi; item = item_at(++kk)) {
                 const long long bl = item / nob;
                 const int ob = (int)(item - bl * nob);
                 const int nbo = min(2, (opad - ob * 32) >> 4);
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
         constexpr int KH = UM_TR * 32 / UM_COLS;         // k-halves per thread's column split: 1 or 2 threads
         const int kh0 = (UM_TR == 8) ? (threadIdx.x >> 7) : 0;
         u32 it = 0;
-        for (long long item = i_lo; item < i_hi; item += i_step) {
+        for (long long kk = 0, item = item_at(0); item < i_hi; item = item_at(++kk)) {
             const long long bl = item / nob;
             const int ob = (int)(item - bl * nob);
             const int nbo = min(2, (opad - ob * 32) >> 4);
@@ -357,7 +369,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
     } else if (warp == UM_W_MMA) {
         // ------------------------------------------------ MMA issuer
         u32 it = 0, use[2] = {0, 0};
-        for (long long item = i_lo; item < i_hi; item += i_step) {
+        for (long long kk = 0, item = item_at(0); item < i_hi; item = item_at(++kk)) {
             const int ob = (int)(item % nob);
             const int nbo = min(2, (opad - ob * 32) >> 4);
             for (int c = 0; c < nch; c++, it++) {
@@ -394,7 +406,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
         const int col = quarter * 32 + lane;
         const bool live_col = col < 2 * gcnt;
         u32 use[2] = {0, 0};
-        for (long long item = i_lo; item < i_hi; item += i_step) {
+        u64 hold[16];                                    // paired mode: the even slot's words [nb][og][x]
+#pragma unroll
+        for (int x = 0; x < 16; x++) hold[x] = 0;
+        for (long long kk = 0, item = item_at(0); item < i_hi; item = item_at(++kk)) {
             const long long bl = item / nob;
             const int ob = (int)(item - bl * nob);
             const int nbo = min(2, (opad - ob * 32) >> 4);
@@ -410,6 +425,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
 #pragma unroll 1
                 for (int og = 0; og < 2; og++) {
                     u32 d[4][16];
+                    const bool hold_it = paired && (kk & 1) == 0;     // even slot of a pair: keep
+                    const bool pair_st = paired && (kk & 1) == 1;     // odd slot: store both
 #pragma unroll
                     for (int x = 0; x < 4; x++)
                         tmem_ld16(tmem + ((u32)(quarter * 32) << 16) + nb * 256 + (ohalf * 8 + og * 4 + x) * 16, d[x]);
@@ -424,10 +441,26 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
 #pragma unroll
                     for (int x = 0; x < 4; x++) {
                         const int o = ob * 32 + nb * 16 + ohalf * 8 + og * 4 + x;
-                        if (live_col && o < n_out && !(dbg & 1)) {
+                        if (hold_it) {                            // static register indices
+                            if (nb == 0) { if (og == 0) hold[x] = r[x]; else hold[4 + x] = r[x]; }
+                            else { if (og == 0) hold[8 + x] = r[x]; else hold[12 + x] = r[x]; }
+                        } else if (live_col && o < n_out && !(dbg & 1)) {
                             u64* po = obase + (long long)o * ostride;
-                            const u64 v = accumulate ? add_mod(r[x], *po, P.q) : r[x];
-                            if (!(dbg & 8) || v == 12345ull) *po = v;
+                            if (pair_st) {                        // slots b - 1, b: one 16-byte store
+                                ulonglong2* pp = reinterpret_cast<ulonglong2*>(po - 1);
+                                const u64 h = nb == 0 ? (og == 0 ? hold[x] : hold[4 + x])
+                                                      : (og == 0 ? hold[8 + x] : hold[12 + x]);
+                                ulonglong2 v = make_ulonglong2(h, r[x]);
+                                if (accumulate) {
+                                    const ulonglong2 a = *pp;
+                                    v.x = add_mod(v.x, a.x, P.q);
+                                    v.y = add_mod(v.y, a.y, P.q);
+                                }
+                                *pp = v;
+                            } else {
+                                const u64 v = accumulate ? add_mod(r[x], *po, P.q) : r[x];
+                                if (!(dbg & 8) || v == 12345ull) *po = v;
+                            }
                         }
                     }
                 }

@@ -1,7 +1,7 @@
 """A/B timing of the conv layer with lazy ModDown on the tensor cores
 (bcn_conv_ks_mac: slot_major_ks + mac_umma + merged ModDown/rescale tails)
 at cifar3 conv2's shape: 16 sources x 9 taps = 144 terms, 32 outputs,
-level 11, G slot sets (default 128).  Prints ms per call (CUDA events)."""
+level 11, G slot sets (default 128); conv1: PROF_SRC=3 PROF_OUT=16 PROF_LVL=14.  Prints ms per call (CUDA events)."""
 import ctypes
 import os
 import sys
@@ -16,11 +16,12 @@ from paper_2402_01296_b200.params import galois_element as ge, make_params  # no
 G = int(os.environ.get("PROF_G", "128"))
 hp = make_params(16384, 14, 50, dnum=3)
 eng = Engine(hp)
-lvl, O = 11, 32
-srcs = [eng.sample_uniform(2 * G, lvl + 1, 0, seed=9 + i).view(G, 2, lvl + 1, 16384) for i in range(16)]
+lvl, O = int(os.environ.get("PROF_LVL", "11")), int(os.environ.get("PROF_OUT", "32"))   # conv1: 14, 16, 3 sources
+nsrc = int(os.environ.get("PROF_SRC", "16"))
+srcs = [eng.sample_uniform(2 * G, lvl + 1, 0, seed=9 + i).view(G, 2, lvl + 1, 16384) for i in range(nsrc)]
 Us = [eng.modup(x, lvl) for x in srcs]
 rots = [0, 1, 2, 16, 17, 18, 32, 33, 34]
-terms = [(srcs[c], Us[c], ge(r, 16384) if r else 1) for c in range(16) for r in rots]
+terms = [(srcs[c], Us[c], ge(r, 16384) if r else 1) for c in range(nsrc) for r in rots]
 nb = ctypes.c_uint64()
 _lib.call("bcn_planes_ext_bytes", eng._h, O, len(terms), lvl, ctypes.byref(nb))
 planes = torch.randint(0, 256, (int(nb.value),), dtype=torch.uint8, device="cuda")
