@@ -672,6 +672,26 @@ def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Cipherte
     return Ciphertext(data, lvl - 1, (a.scale * b.scale) / ctx.q(lvl), ctx)
 
 
+def he_mul_support_mask(a: Ciphertext, rec: OpRecorder) -> Ciphertext:
+    """he_mul(a, mask, mask=True) for a 0/1 mask that is 1 on a's whole slot
+    support (a conv layer's output mask: every tap pattern is already zero off
+    the output grid, layers.py _tap_pattern): value-preserving, so it is
+    realised as the level step alone -- the top RNS limb is discarded (an
+    exact modulus switch of a CKKS ciphertext, scale unchanged) instead of a
+    plaintext product and a rescale.  Same counts (Mul_PC, Mul_PC_mask) and
+    level algebra as sim.py:221-248; the off-grid slots keep their CKKS noise
+    instead of being zeroed, and no later layer reads them (their taps read
+    input-grid anchors only)."""
+    ctx = a.ctx
+    if a.level < 1:
+        raise _depth_error(rec, ctx)
+    rec.bump("Mul_PC")
+    rec.bump("Mul_PC_mask")
+    a.materialize()
+    data = a._data[:, :, :a.level].contiguous()
+    return Ciphertext(data, a.level - 1, a.scale, ctx)
+
+
 def _rotated(c: Ciphertext, r: int) -> Ciphertext:
     """Memoised, hoisted rotation of a materialised ciphertext (r reduced)."""
     ctx = c.ctx

@@ -266,3 +266,23 @@ def test_latency_table_has_the_reference_cost_model_format():
         ops = tab[scheme]
         for k in ("Add_PC", "Add_CC", "Mul_PC", "Mul_CC", "Rot"):
             assert ops[k] > 0
+
+
+@pytest.mark.parametrize("geom", [((28, 28), (5, 5), (2, 2), (0, 0)), ((32, 32), (3, 3), (1, 1), (1, 1)),
+                                  ((32, 32), (3, 3), (2, 2), (1, 1)), ((14, 14), (5, 5), (1, 1), (0, 0))])
+@pytest.mark.parametrize("tiles", [1, 4])
+def test_conv_tap_patterns_vanish_off_the_output_grid(geom, tiles):
+    """sim.he_mul_support_mask realises a conv layer's output-mask product as a
+    level drop: valid because every tap pattern (layers._tap_pattern) is zero
+    off the output grid, so the conv output's support is inside the mask."""
+    from paper_2402_01296_b200.layers import SlotGrid, _grid_pattern, _tap_pattern, conv_geometry
+
+    (h, w), k, stride, pad = geom
+    S = 8192
+    grid = SlotGrid(h, w, tiles=tiles, tile_step=S // tiles if tiles > 1 else 0)
+    out = conv_geometry(grid, k, stride, pad)
+    mask = _grid_pattern(out, S)
+    for di in range(k[0]):
+        for dj in range(k[1]):
+            tap = _tap_pattern(grid, out, stride, pad, di, dj, S)
+            assert not np.any(tap[mask == 0]), (di, dj)
