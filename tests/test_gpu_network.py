@@ -163,6 +163,42 @@ def test_fc_bsgs_matches_direct_and_plain(n1, n2, tiles, monkeypatch):
     assert res["1"][1] == res["0"][1]
 
 
+@pytest.mark.parametrize("n1,n2,tiles,parts", [(256, 10, 4, 2), (64, 3, 1, 1), (128, 16, 2, 3)])
+def test_fc_hybrid_matches_direct_at_output_slots(n1, n2, tiles, parts, monkeypatch):
+    """fc_forward_multi with offgrid_free=True (layers.fc_hybrid: padded-row
+    diagonals as one lazy rotation sum + rotate-and-add, the fc1 evaluation of
+    forward_bicrypto) vs the direct per-diagonal sum: same values at the output
+    slots of every tile (to CKKS noise), identical reference counts and level;
+    cifar3's own shape (two 256-wide blocks, 10 outputs, full 256-slot tiles)
+    included."""
+    from paper_2402_01296_b200.layers import fc_forward_multi
+
+    rng = np.random.default_rng(n1 + 7 * n2 + parts)
+    ctx = B.make_context(2048 if tiles * 256 <= 1024 else 4096, 3, 2.0 ** 50)
+    S = ctx.slot_count
+    step = 256 if tiles > 1 else 0
+    xs = rng.standard_normal((parts, tiles, n1))
+    Ws = [rng.standard_normal((n1, n2)) / np.sqrt(n1 * parts) for _ in range(parts)]
+    kb = rng.standard_normal(n2)
+    res = {}
+    for hybrid in (True, False):
+        rec = B.OpRecorder()
+        blocks = []
+        for pi in range(parts):
+            slots = np.zeros(S)
+            for tt in range(tiles):
+                slots[tt * step:tt * step + n1] = xs[pi, tt]
+            blocks.append((B.encrypt_vector(slots, ctx), Ws[pi]))
+        out = fc_forward_multi(blocks, kb, ctx, rec, tiles=tiles, tile_step=step, offgrid_free=hybrid)
+        dec = B.decrypt_vector(out, ctx)
+        res[hybrid] = (np.stack([dec[tt * step:tt * step + n2] for tt in range(tiles)]), rec.snapshot(), out.level)
+    want = sum(xs[pi] @ Ws[pi] for pi in range(parts)) + kb
+    for hybrid, (got, counts, level) in res.items():
+        assert np.abs(got - want).max() < 1e-8, hybrid
+        assert level == ctx.max_level - 1
+    assert res[True][1] == res[False][1]
+
+
 @pytest.mark.parametrize("G,layout", [(8, 0), (64, 1)])
 def test_cifar3_at_benchmarked_slot_set_counts(G, layout):
     """The conv paths the benchmark takes: G >= BCN_CONV_TC_MIN_G slot sets run
