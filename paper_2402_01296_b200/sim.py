@@ -682,14 +682,26 @@ def he_mul_support_mask(a: Ciphertext, rec: OpRecorder) -> Ciphertext:
     level algebra as sim.py:221-248; the off-grid slots keep their CKKS noise
     instead of being zeroed, and no later layer reads them (their taps read
     input-grid anchors only)."""
-    ctx = a.ctx
     if a.level < 1:
-        raise _depth_error(rec, ctx)
+        raise _depth_error(rec, a.ctx)
     rec.bump("Mul_PC")
     rec.bump("Mul_PC_mask")
+    return he_drop_levels(a, 1, rec)
+
+
+def he_drop_levels(a: Ciphertext, n: int, rec: OpRecorder) -> Ciphertext:
+    """a at level - n with the same value and scale: the top n RNS limbs are
+    discarded (an exact modulus switch of a CKKS ciphertext, no rescale).  The
+    engine's stand-in for reference ops whose level step it realises without
+    work (he_mul_support_mask, layers.flatten_packed); DepthBudgetError as
+    he_mul would raise it."""
+    ctx = a.ctx
+    if a.level < n:
+        raise _depth_error(rec, ctx)
     a.materialize()
-    data = a._data[:, :, :a.level].contiguous()
-    return Ciphertext(data, a.level - 1, a.scale, ctx)
+    if n == 0:
+        return a
+    return Ciphertext(a._data[:, :, :a.level + 1 - n].contiguous(), a.level - n, a.scale, ctx)
 
 
 def _rotated(c: Ciphertext, r: int) -> Ciphertext:
