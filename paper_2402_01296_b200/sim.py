@@ -399,9 +399,11 @@ def _as_plain_rows(v, ctx: HeContext):
     return arr
 
 
-def encrypt_vector(v: PlainLike, ctx: HeContext) -> Ciphertext:
+def encrypt_vector(v: PlainLike, ctx: HeContext, *, level: int | None = None) -> Ciphertext:
     """Encrypt <= slot_count reals (zero-padded) at max_level (sim.py:184-189).
-    A 2-D (G, n) input encrypts G independent slot sets in one batch."""
+    A 2-D (G, n) input encrypts G independent slot sets in one batch.
+    level (engine-internal, forward_bicrypto's prepaid level steps): encrypt
+    at a lower level instead."""
     rows = _as_plain_rows(v, ctx)
     if isinstance(rows, np.ndarray):
         if not np.all(np.isfinite(rows)):
@@ -412,8 +414,11 @@ def encrypt_vector(v: PlainLike, ctx: HeContext) -> Ciphertext:
         if not torch.cuda.is_current_stream_capturing() and not bool(torch.isfinite(rows).all()):
             raise ParameterError("plaintext vector must contain only finite values")
     eng = ctx.engine
-    data = eng.encrypt(rows, ctx.max_level, ctx.delta)
-    return Ciphertext(data, ctx.max_level, ctx.delta, ctx)
+    lv = ctx.max_level if level is None else int(level)
+    if not 0 <= lv <= ctx.max_level:
+        raise ParameterError(f"level {lv} outside [0, {ctx.max_level}]")
+    data = eng.encrypt(rows, lv, ctx.delta)
+    return Ciphertext(data, lv, ctx.delta, ctx)
 
 
 def _decrypt(c: Ciphertext) -> np.ndarray:
@@ -672,7 +677,7 @@ def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Cipherte
     return Ciphertext(data, lvl - 1, (a.scale * b.scale) / ctx.q(lvl), ctx)
 
 
-def he_mul_support_mask(a: Ciphertext, rec: OpRecorder) -> Ciphertext:
+def he_mul_support_mask(a: Ciphertext, rec: OpRecorder, *, drop: bool = True) -> Ciphertext:
     """he_mul(a, mask, mask=True) for a 0/1 mask that is 1 on a's whole slot
     support (a conv layer's output mask: every tap pattern is already zero off
     the output grid, layers.py _tap_pattern): value-preserving, so it is
@@ -681,11 +686,14 @@ def he_mul_support_mask(a: Ciphertext, rec: OpRecorder) -> Ciphertext:
     plaintext product and a rescale.  Same counts (Mul_PC, Mul_PC_mask) and
     level algebra as sim.py:221-248; the off-grid slots keep their CKKS noise
     instead of being zeroed, and no later layer reads them (their taps read
-    input-grid anchors only)."""
-    if a.level < 1:
-        raise _depth_error(rec, a.ctx)
+    input-grid anchors only).  drop=False: the level step was taken in advance
+    (forward_bicrypto's prepaid levels) -- counts only."""
     rec.bump("Mul_PC")
     rec.bump("Mul_PC_mask")
+    if not drop:                 # the level step was prepaid (forward_bicrypto encrypted lower)
+        return a.materialize()
+    if a.level < 1:
+        raise _depth_error(rec, a.ctx)
     return he_drop_levels(a, 1, rec)
 
 
