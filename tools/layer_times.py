@@ -17,7 +17,8 @@ G = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 bundle, weights = bench.cifar3_weights()
 sens, full = bench.rank_inputs("cfg4", 32 * G, 0, 1)
 w = TensorArchive(weights)
-ctx = BCN.make_context(1 << 14, BCN.required_levels(bundle) + 1, bench.SCALE)
+dnum = int(os.environ["BCN_DNUM"]) if os.environ.get("BCN_DNUM") else None   # A/B of the key-switch digits
+ctx = BCN.make_context(1 << 14, BCN.required_levels(bundle) + 1, bench.SCALE, dnum=dnum)
 dev = torch.device("cuda", 0)
 inp = (torch.as_tensor(sens, device=dev), torch.as_tensor(full, device=dev))
 for _ in range(2):
