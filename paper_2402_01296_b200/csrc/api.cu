@@ -1065,7 +1065,8 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
     const bool tc05 = layout == BCN_PLANES_TCGEN05;
     const int spitch = tc05 ? 128 : 64;
     const size_t per_limb = (size_t)N * n_terms * spitch * sizeof(u64);
-    const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(next, ((size_t)4 << 30) / per_limb));
+    static const size_t stage_bytes = (size_t)(getenv("BCN_STAGE_GB") ? atof(getenv("BCN_STAGE_GB")) : 4.0) * (1ull << 30);
+    const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(next, stage_bytes / per_limb));
     u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * spitch, &err);
     if (!S) return err;
     const int GB = tc05 ? 64 : imma_gblock();
