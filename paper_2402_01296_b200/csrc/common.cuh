@@ -134,14 +134,16 @@ __device__ __forceinline__ uint4 draw(u64 seed, u32 domain, u32 limb, u64 id, u3
     return philox4x32_10(c, k);
 }
 
-// ((o1:o0) * 2^64 + (o3:o2)) mod q  ==  x*(2^64 mod q) + y  mod q
+// ((o1:o0) * 2^64 + (o3:o2)) mod q  ==  x*(2^64 mod q) + y  mod q; the two
+// 64-bit reductions are Shoup multiplies by 1 (pad[2] = floor(2^64 / q)):
+// exact for any 64-bit word, the same residues as x % q
 __device__ __forceinline__ u64 uniform_mod(uint4 o, const PrimeInfo& p) {
     u64 x = ((u64)o.y << 32) | o.x;
     u64 y = ((u64)o.w << 32) | o.z;
     u64 q = p.q;
-    u64 xr = x % q;  // cold path (keygen / encrypt only)
+    u64 xr = shoup(x, 1ull, p.pad[2], q);
     u64 t = shoup(xr, p.r1, p.r1_shoup, q);
-    u64 yr = y % q;
+    u64 yr = shoup(y, 1ull, p.pad[2], q);
     return add_mod(t, yr, q);
 }
 

@@ -39,7 +39,11 @@ class GraphedForward:
         self.full = torch.zeros(full_shape, dtype=torch.float64, device=dev)
         self.counter = torch.zeros(1, dtype=torch.int64, device=dev)
         n_img = sens_shape[0]
-        self._ids_per_call = n_img * sens_shape[1] + 1     # >= ciphertexts encrypted per forward
+        # >= ciphertexts encrypted per forward: every input channel, plus the first
+        # conv's pre-rotated copies (network._encrypt_channels)
+        first = net.cipher_layers[0] if getattr(net, "cipher_layers", None) else None
+        taps = first.kernel[0] * first.kernel[1] if first is not None and first.kind == "conv" else 1
+        self._ids_per_call = n_img * sens_shape[1] * taps + 1
         eng.graph_counter = self.counter
         try:
             kw = dict(strategy=strategy, group_size=group_size)

@@ -879,6 +879,8 @@ def materialize_conv(accs: list) -> bool:
     first = lazy[0]
     if not first._scaled or len(first._terms) > 256:
         return False
+    if not any(t[0] == "rot" for t in first._terms):
+        return False                       # no key switching at all: the multi-output MAC (materialize_group)
 
     def sig(t):
         return (id(t[1]), t[2]) if t[0] == "rot" else (id(t[1]), 1)
