@@ -1070,6 +1070,9 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
     u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * spitch, &err);
     if (!S) return err;
     const int GB = tc05 ? 64 : imma_gblock();
+    // every basis prime below 2^56: byte plane 7 of every staged word and plaintext is zero
+    bool planes7 = !getenv_flag_off("BCN_UMMA_7PLANES");
+    for (int t = 0; t < next && planes7; t++) planes7 = c->primes[ext.prime[t]] < (1ull << 56);
     for (int g0 = 0; g0 < G; g0 += GB) {
         const int gcnt = std::min(GB, G - g0);
         for (int t0 = 0; t0 < next; t0 += tcnt) {
@@ -1079,7 +1082,7 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
                                       c->fp_conv ? c->fq : nullptr));
             if (tc05)
                 CUDA_TRY(mac_umma_op(acc, cw, n_out, n_terms, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad,
-                                     next, c->logn, ext, c->pr, 0, st));
+                                     next, c->logn, ext, c->pr, 0, st, planes7 ? 7 : 8));
             else
                 CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, next,
                                      c->logn, ext, c->pr, 0, st));

@@ -224,7 +224,7 @@ __device__ __forceinline__ u64 partials_redc(const u32 (&d)[16], const RedcK& P)
 __global__ void __launch_bounds__(UM_THREADS, 1)
     mac_umma_kernel(u64* __restrict__ out, long long ostride, int n_out, int n_terms, const u8* __restrict__ planes,
                     const u64* __restrict__ S, int g0, int gcnt, int t0, int tcnt, int opad, int nch, int nlimb,
-                    int logn, Limbs limbs, const PrimeInfo* __restrict__ pr, int accumulate, int dbg) {
+                    int logn, Limbs limbs, const PrimeInfo* __restrict__ pr, int accumulate, int dbg, int nplanes) {
     extern __shared__ __align__(1024) unsigned char um_smem[];
     unsigned char* raw = um_smem + (size_t)UM_ST * UM_SBYTES;                  // [UM_RS] raw chunk images
     u64* bars = reinterpret_cast<u64*>(raw + (size_t)UM_RS * UM_RBYTES);
@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                             tc_fence_after();
                         }
 #pragma unroll
-                        for (int j = 0; j < 8; j++) {
+                        for (int j = 0; j < 8; j++) {             // byte planes of the staged words
+                            if (j >= nplanes) break;              // every prime < 2^56: byte 7 is zero
                             const u64 ad = umma_sdesc(a0 + j * UM_APLANE, UM_COLS * 16, 128);
                             const u64 bd = umma_sdesc(b0 + (nb * 256 + 7 - j) * 16, UM_BHALF, 128);
                             if (!(dbg & 4)) umma_i8(tmem + nb * 256, ad, bd, (c > 0 || j > 0) ? 1u : 0u);
@@ -485,9 +486,9 @@ size_t mac_umma_smem() { return UM_SMEM; }
 
 cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, const u8* planes, const u64* S,
                         int g0, int gcnt, int t0, int tcnt, int opad, int nlimb, int logn, const Limbs& limbs,
-                        const PrimeInfo* pr, int accumulate, cudaStream_t st) {
+                        const PrimeInfo* pr, int accumulate, cudaStream_t st, int nplanes) {
     if (gcnt <= 0 || n_terms <= 0 || n_out <= 0) return cudaSuccess;
-    if (gcnt > UM_COLS / 2) return cudaErrorInvalidValue;
+    if (gcnt > UM_COLS / 2 || nplanes < 7 || nplanes > 8) return cudaErrorInvalidValue;
     const int nch = (n_terms + 31) / 32;
     static unsigned long long smem_cfg = 0;
     unsigned long long smem_bit = 0;
@@ -504,7 +505,7 @@ cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, 
     const int grid = (int)std::min<long long>(items, sms);
     static const int dbg = getenv("BCN_UMMA_DBG") ? atoi(getenv("BCN_UMMA_DBG")) : 0;   // experiments only
     mac_umma_kernel<<<grid, UM_THREADS, UM_SMEM, st>>>(out, out_stride, n_out, n_terms, planes, S, g0, gcnt, t0, tcnt,
-                                                       opad, nch, nlimb, logn, limbs, pr, accumulate, dbg);
+                                                       opad, nch, nlimb, logn, limbs, pr, accumulate, dbg, nplanes);
     return launched();
 }
 

@@ -201,7 +201,7 @@ cudaError_t pack_planes_umma_op(unsigned char* planes, const u64* const* pts_dev
                                 int nch, int nl, int logn, cudaStream_t st, const int* tlimbs_dev = nullptr);
 cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, const unsigned char* planes,
                         const u64* S, int g0, int gcnt, int t0, int tcnt, int opad, int nlimb, int logn,
-                        const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st);
+                        const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st, int nplanes = 8);
 // slot-major staging of a g-block x limb-block of the ct terms: S[(tl N + n) K + k][64]
 cudaError_t slot_major_op(u64* S, const MacImma& m, int g0, int gcnt, int t0, int tcnt, int nlimb, int logn,
                           cudaStream_t st);
