@@ -210,17 +210,47 @@ def run_ours(args, rank: int, world: int, dist_on: bool, pool):
     sens_h = torch.as_tensor(sens_np).pin_memory()
     full_h = torch.as_tensor(full_np).pin_memory()
 
-    def step(device_inputs: bool):
+    # e2e inputs: every step copies its inputs from pinned host memory on a copy
+    # stream into one of two device buffers; step k+1's copy is issued when step k
+    # starts, so it overlaps step k's compute (each copy is still inside the timed
+    # region, and a step waits for its own copy)
+    copy_stream = torch.cuda.Stream(device=dev)
+    in_bufs = [(torch.empty_like(sens_d), torch.empty_like(full_d)) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    for ev in consumed:
+        ev.record()
+
+    def issue_copy(slot: int):
+        copy_stream.wait_event(consumed[slot])          # the step that last read this buffer is done
+        with torch.cuda.stream(copy_stream):
+            in_bufs[slot][0].copy_(sens_h, non_blocking=True)
+            in_bufs[slot][1].copy_(full_h, non_blocking=True)
+            ready[slot].record(copy_stream)
+
+    def step(device_inputs: bool, slot: int = 0):
         outs = []
+        if not device_inputs:
+            torch.cuda.current_stream().wait_event(ready[slot])
+        src = (sens_d, full_d) if device_inputs else in_bufs[slot]
         for s0 in range(0, n_img, chunk_imgs):
             s1 = min(n_img, s0 + chunk_imgs)
-            if device_inputs:
-                inp = (sens_d[s0:s1], full_d[s0:s1])
-            else:
-                inp = (sens_h[s0:s1].to(dev, non_blocking=True), full_h[s0:s1].to(dev, non_blocking=True))
+            inp = (src[0][s0:s1], src[1][s0:s1])
             res = BCN.forward_bicrypto(bundle.bi, inp, w, ctx, strategy="bhw", group_size=IMAGES_PER_SET)
             outs.append(res)
         return outs
+
+    def run_steps(device_inputs: bool, to_host: bool, n: int):
+        last = None
+        if not device_inputs:
+            issue_copy(0)
+        for k in range(n):
+            if not device_inputs and k + 1 < n:
+                issue_copy((k + 1) % 2)
+            last = finish(step(device_inputs, k % 2), to_host)
+            if not device_inputs:
+                consumed[k % 2].record()
+        return last
 
     def finish(outs, to_host: bool):
         """gather logits ciphertexts to rank 0 and decrypt there."""
@@ -238,8 +268,7 @@ def run_ours(args, rank: int, world: int, dist_on: bool, pool):
         return logits.cpu() if to_host else logits
 
     def timed(device_inputs: bool, to_host: bool, K: int, W: int, rec_clocks: bool):
-        for _ in range(W):
-            finish(step(device_inputs), to_host)
+        run_steps(device_inputs, to_host, W)
         if dist_on:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -250,9 +279,7 @@ def run_ours(args, rank: int, world: int, dist_on: bool, pool):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.nvtx.range_push("timed_e2e" if to_host else "timed")   # ncu --nvtx-include timed/
         s.record()
-        last = None
-        for _ in range(K):
-            last = finish(step(device_inputs), to_host)
+        last = run_steps(device_inputs, to_host, K)
         e.record()
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
@@ -315,7 +342,10 @@ def run_ours(args, rank: int, world: int, dist_on: bool, pool):
     d2h = total_images * 10 * 8 if rank == 0 else 0
     return {
         "value": value, "ms_per_step": ms, "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": h2d,
-                                                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                                                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                                                    "note": "every step copies its inputs from pinned host memory "
+                                                            "(copy stream, double buffer: step k+1's copy overlaps "
+                                                            "step k) and reads its logits back to the host"},
         "gpu_launches": launches, "clocks": clocks, "counts_per_forward": counts, "keys_agree_across_ranks": keys_agree,
         "device_work_per_forward": dev_work, "parity": parity, "ctx": ctx, "ntt_step": ntt_step,
         "total_images": total_images,
