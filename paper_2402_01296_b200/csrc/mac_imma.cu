@@ -101,6 +101,9 @@ template <int ND>    // digits (1..4); 0: any count, key words re-read from L1
 #ifndef BCN_SMKS_MINB
 #define BCN_SMKS_MINB 4
 #endif
+#ifndef BCN_SMKS_FP64_BOTH
+#define BCN_SMKS_FP64_BOTH 1      // both components on the FP64 pipe (0: component 1 on IMAD; A/B conv2 101 vs 108 ms)
+#endif
 __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* __restrict__ S, const KsTerms T, int g0, int gcnt,
                                                             int t0, int nq, int next, int ndig, int logn,
                                                             int spitch, long long kds, long long kcs, Limbs ext,
@@ -156,6 +159,15 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                     kd[j] = fload(redc(0ull, k0[j], q, P.qinv_neg));
                     kq[j] = __dmul_rn(kd[j], f.y);
                 }
+#if BCN_SMKS_FP64_BOTH
+                // component 1 on the FP64 pipe as well: the converted U words feed both sums
+                double kd1[ND], kq1[ND];
+#pragma unroll
+                for (int j = 0; j < ND; j++) {
+                    kd1[j] = fload(redc(0ull, k1[j], q, P.qinv_neg));
+                    kq1[j] = __dmul_rn(kd1[j], f.y);
+                }
+#endif
                 // P sigma(c0) joins component 0's FP64 sum as one more two-product term
                 // (|sum| < (ND + 1) 0.63 q < 2^53: exact), so no 64-bit Shoup product;
                 // the operand pointers advance by constant strides (no per-slot-set
@@ -166,9 +178,20 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                 const u64* Cp = src + (long long)(g0 + w0) * 2 * LNs + sn;
 #pragma unroll 2
                 for (int gi = w0; gi < gcnt; gi += nw, Up += ustep, Cp += cstep) {
+                    double acc = qlimb ? fmm(fload(__ldg(Cp)), pd, pq, f.x) : 0.0;
+#if BCN_SMKS_FP64_BOTH
+                    double acc1 = 0.0;
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const double ud = fload(__ldg(Up + j * dstr));
+                        acc = __dadd_rn(acc, fmm(ud, kd[j], kq[j], f.x));
+                        acc1 = __dadd_rn(acc1, fmm(ud, kd1[j], kq1[j], f.x));
+                    }
+                    tile[2 * gi][nn] = fcanon(acc, f.y, f.x);
+                    tile[2 * gi + 1][nn] = fcanon(acc1, f.y, f.x);
+#else
                     Acc4 a1;
                     a1.zero();
-                    double acc = qlimb ? fmm(fload(__ldg(Cp)), pd, pq, f.x) : 0.0;
 #pragma unroll
                     for (int j = 0; j < ND; j++) {
                         const u64 u = __ldg(Up + j * dstr);
@@ -177,6 +200,7 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                     }
                     tile[2 * gi][nn] = fcanon(acc, f.y, f.x);
                     tile[2 * gi + 1][nn] = a1.reduce(q, P.qinv_neg, P.pad[2]);
+#endif
                 }
             }
         }
