@@ -152,6 +152,13 @@ int bcn_pack_planes(bcn_ctx *ctx, uint8_t *planes, int n_out, int n_terms, const
                     void *stream);
 int bcn_mac_multi_planes(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *cts,
                          const uint8_t *planes, int G, int level, int rescale, void *stream);
+/* the same with the byte planes in `layout` (BCN_PLANES_IMMA / BCN_PLANES_TCGEN05):
+ * the tcgen05 layout runs the tensor-core MAC on tcgen05.mma with TMEM accumulators
+ * (blocks of 64 slot sets); planes from bcn_pack_planes_layout with the same layout */
+int bcn_pack_planes_layout(bcn_ctx *ctx, uint8_t *planes, int n_out, int n_terms, const uint64_t *const *pts,
+                           int level, int layout, void *stream);
+int bcn_mac_multi_planes_layout(bcn_ctx *ctx, uint64_t *out, int n_out, int n_terms, const uint64_t *const *cts,
+                                const uint8_t *planes, int G, int level, int rescale, int layout, void *stream);
 /* Conv layer with lazy ModDown: out[o] = Rescale(sum_k pt[o][k]
  * (x) rot_{g_k}(src_k)) with the key-switch inner products computed on the
  * fly into the tensor-core MAC over the extended basis and ONE merged

@@ -62,6 +62,8 @@ SIGNATURES = {
     "bcn_planes_bytes": [_P, _I, _I, _I, ctypes.POINTER(_U64)],
     "bcn_pack_planes": [_P, _P, _I, _I, ctypes.POINTER(_U64), _I, _P],
     "bcn_mac_multi_planes": [_P, _P, _I, _I, ctypes.POINTER(_U64), _P, _I, _I, _I, _P],
+    "bcn_pack_planes_layout": [_P, _P, _I, _I, ctypes.POINTER(_U64), _I, _I, _P],
+    "bcn_mac_multi_planes_layout": [_P, _P, _I, _I, ctypes.POINTER(_U64), _P, _I, _I, _I, _I, _P],
     "bcn_mac_terms_acc": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],
     "bcn_rotsum": [_P, _P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64),
                    ctypes.POINTER(_U64), ctypes.POINTER(_I), _I, _I, _P],

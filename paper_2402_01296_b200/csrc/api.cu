@@ -942,6 +942,12 @@ int bcn_planes_bytes(bcn_ctx* c, int n_out, int n_terms, int level, uint64_t* by
 
 int bcn_pack_planes(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const uint64_t* const* pts, int level,
                     void* stream) {
+    return bcn_pack_planes_layout(c, planes, n_out, n_terms, pts, level, BCN_PLANES_IMMA, stream);
+}
+
+int bcn_pack_planes_layout(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const uint64_t* const* pts,
+                           int level, int layout, void* stream) {
+    if (layout != BCN_PLANES_IMMA && layout != BCN_PLANES_TCGEN05) return fail(BCN_ERR_PARAM, "unknown planes layout");
     int e = check_level(c, level);
     if (e) return e;
     int opad, nch;
@@ -958,8 +964,12 @@ int bcn_pack_planes(bcn_ctx* c, uint8_t* planes, int n_out, int n_terms, const u
         c->ptr_cap = np;
     }
     CUDA_TRY(cudaMemcpyAsync(c->ptr_dev, pts, np * sizeof(u64*), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(pack_planes_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch, level + 1, c->logn,
-                            st));
+    if (layout == BCN_PLANES_TCGEN05)
+        CUDA_TRY(pack_planes_umma_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch, level + 1,
+                                     c->logn, st));
+    else
+        CUDA_TRY(pack_planes_op(planes, (const u64* const*)c->ptr_dev, n_out, n_terms, opad, nch, level + 1,
+                                c->logn, st));
     CUDA_TRY(cudaStreamSynchronize(st));          // the host pointer table may go away after return
     return BCN_OK;
 }
@@ -1094,6 +1104,13 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
 
 int bcn_mac_multi_planes(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* cts,
                          const uint8_t* planes, int G, int level, int rescale, void* stream) {
+    return bcn_mac_multi_planes_layout(c, out, n_out, n_terms, cts, planes, G, level, rescale, BCN_PLANES_IMMA,
+                                       stream);
+}
+
+int bcn_mac_multi_planes_layout(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* cts,
+                                const uint8_t* planes, int G, int level, int rescale, int layout, void* stream) {
+    if (layout != BCN_PLANES_IMMA && layout != BCN_PLANES_TCGEN05) return fail(BCN_ERR_PARAM, "unknown planes layout");
     int e = check_level(c, level);
     if (e) return e;
     int opad, nch;
@@ -1115,19 +1132,28 @@ int bcn_mac_multi_planes(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, cons
     M.n_terms = n_terms;
     M.n_out = n_out;
     for (int k = 0; k < n_terms; k++) M.ct[k] = (const u64*)cts[k];
-    // stage blocks of <= 32 slot sets x tcnt limbs slot-major (<= ~4 GiB), then multiply
-    const size_t per_limb = (size_t)N * n_terms * 64 * sizeof(u64);
+    // stage blocks of slot sets x tcnt limbs slot-major (<= ~4 GiB), then multiply:
+    // tcgen05 blocks of 64 slot sets (M = 128 columns), IMMA blocks of IMMA_GB
+    const bool tc05 = layout == BCN_PLANES_TCGEN05;
+    const int spitch = tc05 ? 128 : 64;
+    const size_t per_limb = (size_t)N * n_terms * spitch * sizeof(u64);
     const int tcnt = (int)std::max<size_t>(1, std::min<size_t>(nl, ((size_t)4 << 30) / per_limb));
-    u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * 64, &err);
+    u64* S = scratch2_get(c, (size_t)tcnt * N * n_terms * spitch, &err);
     if (!S) return err;
-    const int GB = imma_gblock();
+    bool planes7 = !getenv_flag_off("BCN_UMMA_7PLANES");
+    for (int t = 0; t < nl && planes7; t++) planes7 = c->primes[t] < (1ull << 56);
+    const int GB = tc05 ? 64 : imma_gblock();
     for (int g0 = 0; g0 < G; g0 += GB) {
         const int gcnt = std::min(GB, G - g0);
         for (int t0 = 0; t0 < nl; t0 += tcnt) {
             const int tc = std::min(tcnt, nl - t0);
-            CUDA_TRY(slot_major_op(S, M, g0, gcnt, t0, tc, nl, c->logn, st));
-            CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, nl, c->logn,
-                                 l, c->pr, 0, st));
+            CUDA_TRY(slot_major_op(S, M, g0, gcnt, t0, tc, nl, c->logn, st, spitch));
+            if (tc05)
+                CUDA_TRY(mac_umma_op(acc, cw, n_out, n_terms, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad,
+                                     nl, c->logn, l, c->pr, 0, st, planes7 ? 7 : 8));
+            else
+                CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, nl,
+                                     c->logn, l, c->pr, 0, st));
         }
     }
     if (!rescale) return BCN_OK;

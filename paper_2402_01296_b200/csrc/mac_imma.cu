@@ -263,8 +263,8 @@ cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0,
 // CTA = (k, limb, 32 coefficients): 64 coalesced 256-byte row reads, 32
 // coalesced 512-byte row writes through a padded SMEM tile.
 __global__ void __launch_bounds__(256) slot_major_kernel(u64* __restrict__ S, const MacImma m, int g0, int gcnt,
-                                                         int t0, int nlimb, int logn) {
-    __shared__ u64 tile[64][33];
+                                                         int t0, int nlimb, int logn, int spitch) {
+    __shared__ u64 tile[128][33];
     const int N = 1 << logn;
     const long long LN = (long long)nlimb << logn;
     const int n0 = blockIdx.x * 32, tl = blockIdx.y, k = blockIdx.z;
@@ -275,10 +275,10 @@ __global__ void __launch_bounds__(256) slot_major_kernel(u64* __restrict__ S, co
         tile[col][nn] = __ldg(src + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN + nn);
     }
     __syncthreads();
-    u64* dst = S + (((long long)tl * N + n0) * m.n_terms + k) * 64;
+    u64* dst = S + (((long long)tl * N + n0) * m.n_terms + k) * spitch;
     const int lane = threadIdx.x & 31;
     for (int r = threadIdx.x >> 5; r < 32; r += blockDim.x >> 5)
-        for (int col = lane; col < ncol; col += 32) dst[(long long)r * m.n_terms * 64 + col] = tile[col][r];
+        for (int col = lane; col < ncol; col += 32) dst[(long long)r * m.n_terms * spitch + col] = tile[col][r];
 }
 
 // ---------------------------------------------------------------- kernel
@@ -448,10 +448,11 @@ __global__ void __launch_bounds__(512, 1)
 size_t mac_imma_smem() { return IM_ST * (8 * 32 * 32 + 32 * IM_BP * 8); }
 
 cudaError_t slot_major_op(u64* S, const MacImma& m, int g0, int gcnt, int t0, int tcnt, int nlimb, int logn,
-                          cudaStream_t st) {
+                          cudaStream_t st, int spitch) {
     const int N = 1 << logn;
+    if (2 * gcnt > spitch || spitch > 128) return cudaErrorInvalidValue;
     dim3 grid(N / 32, tcnt, m.n_terms);
-    slot_major_kernel<<<grid, 256, 0, st>>>(S, m, g0, gcnt, t0, nlimb, logn);
+    slot_major_kernel<<<grid, 256, 0, st>>>(S, m, g0, gcnt, t0, nlimb, logn, spitch);
     return launched();
 }
 

@@ -204,7 +204,7 @@ cudaError_t mac_umma_op(u64* out, long long out_stride, int n_out, int n_terms, 
                         const Limbs& limbs, const PrimeInfo* pr, int accumulate, cudaStream_t st, int nplanes = 8);
 // slot-major staging of a g-block x limb-block of the ct terms: S[(tl N + n) K + k][64]
 cudaError_t slot_major_op(u64* S, const MacImma& m, int g0, int gcnt, int t0, int tcnt, int nlimb, int logn,
-                          cudaStream_t st);
+                          cudaStream_t st, int spitch = 64);
 cudaError_t mac_imma_op(u64* out, long long out_stride, const MacImma& m, const unsigned char* planes, const u64* S,
                         int g0, int gcnt, int t0, int tcnt, int opad, int nlimb, int logn, const Limbs& limbs,
                         const PrimeInfo* pr, int accumulate, cudaStream_t st);

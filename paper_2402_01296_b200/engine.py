@@ -349,27 +349,30 @@ class Engine:
         _lib.call("bcn_mac_multi", self._h, _ptr(out), O, K, c_arr, p_arr, G, level, int(rescale), _stream())
         return out
 
-    def pack_planes(self, pts, level: int) -> torch.Tensor:
+    def pack_planes(self, pts, level: int, layout: int = 0) -> torch.Tensor:
         """Byte-plane pack of an O x K plaintext matrix (Montgomery u64[1,level+1,N]
-        each) for mac_multi_planes; K <= 256.  Done once per layer."""
+        each) for mac_multi_planes; K <= 256.  Done once per layer.
+        layout: 0 mma.sync IMMA, 1 tcgen05 (the MAC must use the same)."""
         O, K = len(pts), len(pts[0])
         nb = ctypes.c_uint64()
         _lib.call("bcn_planes_bytes", self._h, O, K, level, ctypes.byref(nb))
         planes = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
         p_arr = (ctypes.c_uint64 * (O * K))(*[p.data_ptr() for row in pts for p in row])
-        _lib.call("bcn_pack_planes", self._h, _ptr(planes), O, K, p_arr, level, _stream())
+        _lib.call("bcn_pack_planes_layout", self._h, _ptr(planes), O, K, p_arr, level, int(layout), _stream())
         return planes
 
-    def mac_multi_planes(self, cts, planes: torch.Tensor, n_out: int, level: int, rescale: bool = True) -> torch.Tensor:
+    def mac_multi_planes(self, cts, planes: torch.Tensor, n_out: int, level: int, rescale: bool = True,
+                         layout: int = 0) -> torch.Tensor:
         """Tensor-core mac_multi: out[o] = sum_k cts[k] (x) pt[o][k] with the
-        plaintexts given as pack_planes(...) output; bit-identical to mac_multi."""
+        plaintexts given as pack_planes(..., layout) output; bit-identical to
+        mac_multi in either layout."""
         K = len(cts)
         G = cts[0].shape[0]
         c_arr = (ctypes.c_uint64 * K)(*[c.data_ptr() for c in cts])
         nl = level if rescale else level + 1
         out = torch.empty((n_out, G, 2, nl, self.N), dtype=torch.int64, device=self.device)
-        _lib.call("bcn_mac_multi_planes", self._h, _ptr(out), n_out, K, c_arr, _ptr(planes), G, level, int(rescale),
-                  _stream())
+        _lib.call("bcn_mac_multi_planes_layout", self._h, _ptr(out), n_out, K, c_arr, _ptr(planes), G, level,
+                  int(rescale), int(layout), _stream())
         return out
 
     def mac_terms_acc(self, out: torch.Tensor, terms, level: int) -> torch.Tensor:

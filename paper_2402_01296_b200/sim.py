@@ -564,7 +564,7 @@ def _planes_for(ctx: HeContext, pts: list, level: int, ext: bool = False, layout
     if hit is not None and all(a is b for a, b in zip(hit[1], (p for row in pts for p in row))):
         ctx._pt_cache.move_to_end(key)
         return hit[0]
-    planes = ctx.engine.pack_planes_ext(pts, level, layout) if ext else ctx.engine.pack_planes(pts, level)
+    planes = ctx.engine.pack_planes_ext(pts, level, layout) if ext else ctx.engine.pack_planes(pts, level, layout)
     STATS["plane_pack"] += 1
     _cache_put(ctx, key, (planes, [p for row in pts for p in row]))
     return planes
@@ -849,7 +849,9 @@ def materialize_group(cts: list) -> None:
             cts_k = [t[1] for t in first._terms]
             pts_ok = [[t[2] for t in c._terms] for c in lazy]
             if _use_imma() and len(cts_k) <= 256:
-                out = eng.mac_multi_planes(cts_k, _planes_for(first.ctx, pts_ok, lvl), len(lazy), lvl)
+                layout = _conv_layout(int(cts_k[0].shape[0]))
+                out = eng.mac_multi_planes(cts_k, _planes_for(first.ctx, pts_ok, lvl, layout=layout), len(lazy), lvl,
+                                           layout=layout)
             else:
                 out = eng.mac_multi(cts_k, pts_ok, lvl)
             STATS["mac_launch"] += 1

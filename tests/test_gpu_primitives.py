@@ -289,12 +289,15 @@ def test_mac_multi_planes_matches_oracle_composition():
         _assert_ct(got[o], [exp])
 
 
+@pytest.mark.parametrize("layout", [0, 1], ids=["imma", "tcgen05"])
 @pytest.mark.parametrize("n_out,K,G,extreme", [(5, 7, 3, False), (16, 33, 1, False), (40, 144, 33, False),
-                                               (32, 256, 4, True)])
-def test_mac_multi_planes_bitexact(n_out, K, G, extreme):
-    """IMMA path == CUDA-core path bit for bit on uniform residues (60-bit
-    primes: all eight bytes live), several output / slot-set blocks, the
-    256-term maximum, and the all-(q-1) worst case of the int32 partials."""
+                                               (32, 256, 4, True), (16, 27, 70, False)])
+def test_mac_multi_planes_bitexact(n_out, K, G, extreme, layout):
+    """Tensor-core multi-output MAC (mma.sync IMMA and tcgen05 layouts) ==
+    CUDA-core path bit for bit on uniform residues (60-bit primes: all eight
+    bytes live), several output / slot-set blocks (G = 70: a partial second
+    tcgen05 block), the 256-term maximum, and the all-(q-1) worst case of the
+    int32 partials."""
     N, L = 4096, 2
     hp = make_params(N, L, 60, dnum=1, n_special=1)
     eng = Engine(hp)
@@ -312,7 +315,8 @@ def test_mac_multi_planes_bitexact(n_out, K, G, extreme):
                 for p in row:
                     p[:, t, :] = qm1
     want = to_numpy_u64(eng.mac_multi(cts, pts, L, rescale=False))
-    got = to_numpy_u64(eng.mac_multi_planes(cts, eng.pack_planes(pts, L), n_out, L, rescale=False))
+    got = to_numpy_u64(eng.mac_multi_planes(cts, eng.pack_planes(pts, L, layout), n_out, L, rescale=False,
+                                            layout=layout))
     np.testing.assert_array_equal(got, want)
 
 
