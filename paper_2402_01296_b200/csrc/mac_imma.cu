@@ -97,6 +97,14 @@ cudaError_t pack_planes_op(u8* planes, const u64* const* pts_dev, int n_out, int
 // touches HBM.  One CTA = (32 coefficients, limb, term).  Under X -> X^g an
 // aligned 32-block is the image of one aligned 32-block, so the gathers stay
 // inside one 256-byte segment.
+// a staged word congruent to acc mod q, in [0, 2^52): ND <= 2 (|acc| < 1.9q, the
+// P sigma(c0) term included): acc + 2q; else fred to [-q/2, q/2] then + q
+template <int ND>
+__device__ __forceinline__ u64 fstage(double acc, double stage_c, double qinv, double q) {
+    const double y = ND <= 2 ? acc : fred(acc, qinv, q);
+    return (u64)__double_as_longlong(__dadd_rn(y, stage_c)) & ((1ull << 52) - 1);
+}
+
 template <int ND>    // digits (1..4); 0: any count, key words re-read from L1
 #ifndef BCN_SMKS_MINB
 #define BCN_SMKS_MINB 4
@@ -159,6 +167,11 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                     kd[j] = fload(redc(0ull, k0[j], q, P.qinv_neg));
                     kq[j] = __dmul_rn(kd[j], f.y);
                 }
+                // staged words need only be < 2^56 and congruent mod q (the tensor-core
+                // epilogues reduce any such sum): ND <= 2 sums stay in (-1.9q, 1.9q), so the
+                // word is acc + 2q read off the mantissa of acc + (2^52 + 2q)
+                const double stage_c = ND <= 2 ? __dadd_rn(4503599627370496.0, __dadd_rn(f.x, f.x))
+                                               : __dadd_rn(4503599627370496.0, f.x);
 #if BCN_SMKS_FP64_BOTH
                 // component 1 on the FP64 pipe as well: the converted U words feed both sums
                 double kd1[ND], kq1[ND];
@@ -187,8 +200,8 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                         acc = __dadd_rn(acc, fmm(ud, kd[j], kq[j], f.x));
                         acc1 = __dadd_rn(acc1, fmm(ud, kd1[j], kq1[j], f.x));
                     }
-                    tile[2 * gi][nn] = fcanon(acc, f.y, f.x);
-                    tile[2 * gi + 1][nn] = fcanon(acc1, f.y, f.x);
+                    tile[2 * gi][nn] = fstage<ND>(acc, stage_c, f.y, f.x);
+                    tile[2 * gi + 1][nn] = fstage<ND>(acc1, stage_c, f.y, f.x);
 #else
                     Acc4 a1;
                     a1.zero();
