@@ -105,13 +105,17 @@ __device__ __forceinline__ u64 fstage(double acc, double stage_c, double qinv, d
     return (u64)__double_as_longlong(__dadd_rn(y, stage_c)) & ((1ull << 52) - 1);
 }
 
-template <int ND>    // digits (1..4); 0: any count, key words re-read from L1
 #ifndef BCN_SMKS_MINB
 #define BCN_SMKS_MINB 4
 #endif
-#ifndef BCN_SMKS_FP64_BOTH
-#define BCN_SMKS_FP64_BOTH 1      // both components on the FP64 pipe (0: component 1 on IMAD; A/B conv2 101 vs 108 ms)
+#ifndef BCN_SMKS_UNROLL
+#define BCN_SMKS_UNROLL 2
 #endif
+constexpr int kSmksUnroll = BCN_SMKS_UNROLL;    // (#pragma arguments are not macro-expanded)
+#ifndef BCN_SMKS_FP64_BOTH
+#define BCN_SMKS_FP64_BOTH 1      // both components on the FP64 pipe (0: component 1 on IMAD; A/B 108.9 vs 111.0 ms)
+#endif
+template <int ND>    // digits (1..4); 0: any count, key words re-read from L1
 __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* __restrict__ S, const KsTerms T, int g0, int gcnt,
                                                             int t0, int nq, int next, int ndig, int logn,
                                                             int spitch, long long kds, long long kcs, Limbs ext,
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
                 const long long ustep = (long long)nw * nd * dstr, cstep = (long long)nw * 2 * LNs;
                 const u64* Up = Ub + (long long)(g0 + w0) * nd * dstr;
                 const u64* Cp = src + (long long)(g0 + w0) * 2 * LNs + sn;
-#pragma unroll 2
+#pragma unroll kSmksUnroll
                 for (int gi = w0; gi < gcnt; gi += nw, Up += ustep, Cp += cstep) {
                     double acc = qlimb ? fmm(fload(__ldg(Cp)), pd, pq, f.x) : 0.0;
 #if BCN_SMKS_FP64_BOTH
