@@ -254,12 +254,233 @@ __global__ void __launch_bounds__(256, BCN_SMKS_MINB) slot_major_ks_kernel(u64* 
         for (int col = nn; col < ncol; col += 32) dst[(long long)r * T.n * spitch + col] = tile[col][r];
 }
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
+}
+
+// ---- source-shared form: every U word crosses L2 once, not once per rotation ----
+// ncu on the kernel above (conv2: 16 sources x 16 rotations, 64 slot sets, one
+// limb): 6.4 GB of L2 reads (each U word gathered by all 16 rotations of its
+// source) + 4.3 GB of staged writes per launch, ~5 TB/s through L2 whatever
+// the occupancy or the loads in flight (a warp-per-term variant with 12 loads
+// in flight per thread and half the instructions measured 2.27 vs 2.02 ms).
+// So the work is regrouped by SOURCE block: a CTA takes 32 source coefficients m of one limb and a run of
+// <= 16 consecutive terms over the same (src, U), loads the block's U digits and
+// c0 for every slot set into shared memory once (cp.async), and each warp then
+// evaluates whole terms from that tile: lane = m, output coefficient n =
+// sigma_g^-1(m) (X -> X^g maps the aligned 32-block of m onto ONE aligned
+// 32-block of n, permuted), keys gathered at n, staged words into the warp's
+// private tile at row n % 32 and flushed as 16-byte stores (__syncwarp only).
+// Bank conflicts: within the block lane -> n % 32 is brev5(c + g brev5(lane)),
+// which keeps each aligned group of 8 lanes inside one aligned group of 8 rows,
+// so the 16-byte tile stores (8 lanes per wavefront) never collide.
+struct KsGroups {
+    int n;
+    unsigned short start[BCN_IMMA_TERMS];
+    unsigned char count[BCN_IMMA_TERMS];
+};
+// CTA = 16 warps, one term each (a run of <= 16 terms); per 16 slot sets a
+// double-buffered operand tile (cp.async: the next 16 slot sets land while these
+// are evaluated), the run's key words in shared memory as well (loaded once,
+// gathered at n), 4 slot sets per flush (64-byte column runs).  82 KB and
+// 64 registers: two CTAs = 32 warps per SM.
+#ifndef BCN_KS3_GP
+#define BCN_KS3_GP 16
+#endif
+#ifndef BCN_KS3_TP
+#define BCN_KS3_TP 10
+#endif
+constexpr int KS3_GP = BCN_KS3_GP;                             // slot sets per operand phase
+constexpr int KS3_TP = BCN_KS3_TP;                             // out tile pitch (u64): 8 columns + pad
+template <int ND> constexpr size_t ks3_smem_bytes() {
+    return (size_t)2 * KS3_GP * (ND + 1) * 256 + (size_t)16 * ND * 2 * 256 + (size_t)16 * 32 * KS3_TP * 8;
+}
+template <int ND>
+__global__ void __launch_bounds__(512, 2)
+    slot_major_ks3_kernel(u64* __restrict__ S, const KsTerms T, const KsGroups GR, int g0, int gcnt, int t0, int nq,
+                          int next, int logn, int spitch, long long kds, long long kcs, Limbs ext,
+                          const PrimeInfo* __restrict__ pr, const u64* __restrict__ pmod,
+                          const double2* __restrict__ fq) {
+    extern __shared__ __align__(16) unsigned char ks3_smem[];
+    constexpr int NW = ND + 1;                                 // words per (slot set, coefficient): U digits + c0
+    typedef u64 UTile[KS3_GP][NW][32];
+    UTile* ut = reinterpret_cast<UTile*>(ks3_smem);                                            // [2]
+    u64(*keys)[ND][2][32] = reinterpret_cast<u64(*)[ND][2][32]>(ks3_smem + 2 * sizeof(UTile)); // [16 terms]
+    u64(*tiles)[32][KS3_TP] =
+        reinterpret_cast<u64(*)[32][KS3_TP]>(ks3_smem + 2 * sizeof(UTile) + (size_t)16 * ND * 2 * 256);   // [16 warps]
+    const int N = 1 << logn;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int m0 = blockIdx.x * 32, tl = blockIdx.y, t = t0 + tl;
+    const int kfirst = GR.start[blockIdx.z], kcount = GR.count[blockIdx.z];
+    const int kt = ext.prime[t];
+    const PrimeInfo& P = pr[kt];
+    const u64 q = P.q;
+    const long long LNs = (long long)nq * N;
+    const bool qlimb = t < nq;
+    const long long dstr = (long long)next * N;
+    const long long ustep = (long long)ND * dstr, cstep = 2 * LNs;
+    const int nph = (gcnt + KS3_GP - 1) / KS3_GP;
+    const u64* U0 = nullptr;                                   // the run's ModUp: its first rotation term's
+    for (int ki = 0; ki < kcount && !U0; ki++)
+        if (T.g[kfirst + ki] != 1u) U0 = T.U[kfirst + ki];
+    const u64* Ub = U0 ? U0 + (long long)t * N + m0 + (long long)g0 * ustep : nullptr;
+    const u64* Cb = T.src[kfirst] + (long long)t * N + m0 + (long long)g0 * cstep;
+    const int piece = threadIdx.x & 15;
+    auto load_phase = [&](int ph) {                            // rows of 256 bytes, 16 threads x 16 bytes each
+        UTile& dstt = ut[ph & 1];
+        const int gbase = ph * KS3_GP;
+        for (int row = threadIdx.x >> 4; row < KS3_GP * NW; row += 32) {
+            const int gl = row / NW, j = row - gl * NW, gs = gbase + gl;
+            if (gs >= gcnt) continue;
+            const u64* srcp = j < ND ? (Ub ? Ub + gs * ustep + j * dstr : nullptr) : (qlimb ? Cb + gs * cstep : nullptr);
+            u64* dstp = &dstt[gl][j][2 * piece];
+            if (srcp) cp_async16(dstp, srcp + 2 * piece);
+            else *reinterpret_cast<ulonglong2*>(dstp) = make_ulonglong2(0ull, 0ull);
+        }
+    };
+    // this warp's term
+    const bool has = w < kcount;
+    const int k = kfirst + (has ? w : 0);
+    const u32 g = T.g[k];
+    u32 ginv = g;                                              // g^-1 mod 2^32 (Newton; g g = 1 mod 8)
+#pragma unroll
+    for (int i = 0; i < 4; i++) ginv *= 2u - g * ginv;
+    const int n = g == 1u ? m0 + lane : (int)automorph_src((u32)(m0 + lane), ginv & ((2u << logn) - 1u), logn);
+    const int nrow = n & 31;
+    if (has && g != 1u) {                                      // the warp's key rows: (digit, component) x 256 bytes at n's block
+        const u64* kp = T.key[k] + (long long)kt * N + (n & ~31);
+        for (int x = lane; x < ND * 2 * 16; x += 32) {
+            const int r = x >> 4, pc = x & 15;
+            cp_async16(&keys[w][r >> 1][r & 1][2 * pc], kp + (r >> 1) * kds + (r & 1) * kcs + 2 * pc);
+        }
+    }
+    load_phase(0);
+    cp_async_commit();
+    const u64 pw = qlimb ? pmod[2 * t] : 0ull, pwp = qlimb ? pmod[2 * t + 1] : 0ull;
+    u64(*tw)[KS3_TP] = tiles[w];
+    const int fr = lane >> 2, fp = lane & 3;                   // flush: 8 rows x four 16-byte pieces per instruction
+    u64* dst = S + (((long long)tl * N + (n & ~31)) * T.n + k) * spitch + 2 * fp;
+    const long long rstride = (long long)T.n * spitch;
+    const double2 f = fq[kt];
+    const double stage_c = ND <= 2 ? __dadd_rn(4503599627370496.0, __dadd_rn(f.x, f.x))
+                                   : __dadd_rn(4503599627370496.0, f.x);
+    const double pd = qlimb ? fload(pw) : 0.0, pq = __dmul_rn(pd, f.y);
+    double kd[ND], kq[ND], kd1[ND], kq1[ND];
+    const u64* c1p = T.src[k] + (long long)t * N + n + LNs + (long long)g0 * cstep;     // identity term: c1 from HBM
+    for (int ph = 0; ph < nph; ph++) {
+        cp_async_wait<0>();
+        __syncthreads();                                       // phase ph landed; everyone is done with buffer (ph + 1) & 1
+        if (ph + 1 < nph) load_phase(ph + 1);
+        cp_async_commit();
+        if (!has) continue;
+        if (ph == 0 && g != 1u) {
+#pragma unroll
+            for (int j = 0; j < ND; j++) {                     // Montgomery key words -> {k, k/q} as doubles
+                kd[j] = fload(redc(0ull, keys[w][j][0][nrow], q, P.qinv_neg));
+                kq[j] = __dmul_rn(kd[j], f.y);
+                kd1[j] = fload(redc(0ull, keys[w][j][1][nrow], q, P.qinv_neg));
+                kq1[j] = __dmul_rn(kd1[j], f.y);
+            }
+        }
+        const UTile& cur = ut[ph & 1];
+#pragma unroll 1
+        for (int fb = 0; fb < KS3_GP / 4; fb++) {              // 4 slot sets per flush
+            const int gs0 = ph * KS3_GP + fb * 4;
+            if (gs0 >= gcnt) break;
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int gl = fb * 4 + b;
+                const bool live = gs0 + b < gcnt;
+                u64 v0 = 0ull, v1 = 0ull;
+                if (g == 1u) {
+                    if (qlimb && live) {
+                        v0 = shoup(cur[gl][ND][lane], pw, pwp, q);
+                        v1 = shoup(__ldg(c1p + (long long)(gs0 + b) * cstep), pw, pwp, q);
+                    }
+                } else if (live) {
+                    double acc = qlimb ? fmm(fload(cur[gl][ND][lane]), pd, pq, f.x) : 0.0;
+                    double acc1 = 0.0;
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const double ud = fload(cur[gl][j][lane]);
+                        acc = __dadd_rn(acc, fmm(ud, kd[j], kq[j], f.x));
+                        acc1 = __dadd_rn(acc1, fmm(ud, kd1[j], kq1[j], f.x));
+                    }
+                    v0 = fstage<ND>(acc, stage_c, f.y, f.x);
+                    v1 = fstage<ND>(acc1, stage_c, f.y, f.x);
+                }
+                *reinterpret_cast<ulonglong2*>(&tw[nrow][2 * b]) = make_ulonglong2(v0, v1);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int r = i * 8 + fr;
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&tw[r][2 * fp]);
+                *reinterpret_cast<ulonglong2*>(dst + (long long)r * rstride + gs0 * 2) = v;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int ND>
+static cudaError_t ks3_launch(u64* S, const KsTerms& T, const KsGroups& GR, int g0, int gcnt, int t0, int tcnt, int nq,
+                              int next, int logn, int spitch, long long kds, long long kcs, const Limbs& ext,
+                              const PrimeInfo* pr, const u64* pmod, const double2* fq, cudaStream_t st) {
+    const size_t smem = ks3_smem_bytes<ND>();
+    static unsigned long long cfg = 0;
+    unsigned long long bit = 0;
+    if (first_on_device(&cfg, &bit)) {
+        cudaError_t ae = cudaSuccess;
+        BCN_SMEM_ATTR(ae, (slot_major_ks3_kernel<ND>), (int)smem);
+        if (ae != cudaSuccess) return ae;
+        cfg |= bit;
+    }
+    dim3 grid((1 << logn) / 32, tcnt, GR.n);
+    slot_major_ks3_kernel<ND><<<grid, 512, smem, st>>>(S, T, GR, g0, gcnt, t0, nq, next, logn, spitch, kds, kcs, ext, pr,
+                                                       pmod, fq);
+    return launched();
+}
+
 cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,
                              int logn, int spitch, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
                              const u64* pmod, cudaStream_t st, const double2* fq) {
     if (2 * gcnt > spitch || spitch > 128) return cudaErrorInvalidValue;
     if (ndig > 12) fq = nullptr;
     const int N = 1 << logn;
+    static const bool shared_form = !(getenv("BCN_SMKS_SHARED") && getenv("BCN_SMKS_SHARED")[0] == '0');
+    if (shared_form && fq && ndig >= 1 && ndig <= 3 && gcnt <= 64 && spitch >= 8 * ((gcnt + 3) / 4)) {
+        // runs of consecutive terms over the same source (<= 16 per CTA)
+        KsGroups GR;
+        GR.n = 0;
+        for (int k = 0; k < T.n;) {
+            const u64* gu = T.g[k] == 1u ? nullptr : T.U[k];   // the run's ModUp (identity terms carry none)
+            int c = 1;
+            while (k + c < T.n && c < 16 && T.src[k + c] == T.src[k]) {
+                if (T.g[k + c] != 1u) {
+                    if (gu && T.U[k + c] != gu) break;
+                    gu = T.U[k + c];
+                }
+                c++;
+            }
+            GR.start[GR.n] = (unsigned short)k;
+            GR.count[GR.n] = (unsigned char)c;
+            GR.n++;
+            k += c;
+        }
+        switch (ndig) {
+            case 1: return ks3_launch<1>(S, T, GR, g0, gcnt, t0, tcnt, nq, next, logn, spitch, kds, kcs, ext, pr, pmod, fq, st);
+            case 2: return ks3_launch<2>(S, T, GR, g0, gcnt, t0, tcnt, nq, next, logn, spitch, kds, kcs, ext, pr, pmod, fq, st);
+            default: return ks3_launch<3>(S, T, GR, g0, gcnt, t0, tcnt, nq, next, logn, spitch, kds, kcs, ext, pr, pmod, fq, st);
+        }
+    }
     dim3 grid(N / 32, tcnt, T.n);
     switch (ndig) {
 #define BCN_SMK(D) case D: slot_major_ks_kernel<D><<<grid, 256, 0, st>>>(S, T, g0, gcnt, t0, nq, next, ndig, logn, \
@@ -302,16 +523,6 @@ __global__ void __launch_bounds__(256) slot_major_kernel(u64* __restrict__ S, co
 #define IM_BP 66          // B tile row pitch in words (2-way = conflict-optimal LDS.64)
 #define IM_GC 64          // max slot-set columns per CTA (32 slot sets x 2 components)
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int K> __device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
-}
 #ifndef IM_ST
 #define IM_ST 3           // pipeline stages
 #endif

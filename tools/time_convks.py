@@ -21,6 +21,8 @@ nsrc = int(os.environ.get("PROF_SRC", "16"))
 srcs = [eng.sample_uniform(2 * G, lvl + 1, 0, seed=9 + i).view(G, 2, lvl + 1, 16384) for i in range(nsrc)]
 Us = [eng.modup(x, lvl) for x in srcs]
 rots = [0, 1, 2, 16, 17, 18, 32, 33, 34]
+if os.environ.get("PROF_ROTS"):   # packed conv2 (current): PROF_LVL=8 PROF_OUT=8 PROF_ROTS=16
+    rots = [(i // 4) * 16 + (i % 4) for i in range(int(os.environ["PROF_ROTS"]))]
 terms = [(srcs[c], Us[c], ge(r, 16384) if r else 1) for c in range(nsrc) for r in rots]
 nb = ctypes.c_uint64()
 _lib.call("bcn_planes_ext_bytes", eng._h, O, len(terms), lvl, ctypes.byref(nb))
@@ -36,9 +38,10 @@ out = run()
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
-for _ in range(3):
+REPS = int(os.environ.get("PROF_REPS", "3"))
+for _ in range(REPS):
     out = run()
 e.record()
 torch.cuda.synchronize()
-print(f"{os.environ.get('BCN_LIB', 'default')}: conv_ks_mac G={G} {s.elapsed_time(e) / 3:.3f} ms "
+print(f"{os.environ.get('BCN_LIB', 'default')}: conv_ks_mac G={G} {s.elapsed_time(e) / max(REPS, 1):.3f} ms "
       f"checksum {int(out.view(-1)[::9973].sum())}")
