@@ -286,38 +286,33 @@ struct KsGroups {
     unsigned short start[BCN_IMMA_TERMS];
     unsigned char count[BCN_IMMA_TERMS];
 };
-// CTA = 16 warps, one term each (a run of <= 16 terms); per 16 slot sets a
-// double-buffered operand tile (cp.async: the next 16 slot sets land while these
-// are evaluated), the run's key words in shared memory as well (loaded once,
-// gathered at n), 4 slot sets per flush (64-byte column runs).  82 KB and
-// 64 registers: two CTAs = 32 warps per SM.
-#ifndef BCN_KS3_GP
-#define BCN_KS3_GP 16
-#endif
-#ifndef BCN_KS3_TP
-#define BCN_KS3_TP 10
-#endif
-constexpr int KS3_GP = BCN_KS3_GP;                             // slot sets per operand phase
-constexpr int KS3_TP = BCN_KS3_TP;                             // out tile pitch (u64): 8 columns + pad
+// Work split inside the CTA: by SLOT SET, not by term.  Warp w owns 4 slot sets
+// of the CTA's 32 and walks the run's terms: its U digits (as doubles) and the
+// rotation-independent P c0 product stay in registers for all <= 16 rotations,
+// so per (slot set, rotation) only the 2 ND key products remain (30 FP64
+// instructions at ND = 2 instead of 39 + 3 conversions).  The run's key words
+// are converted once per CTA -- warp w converts rotations w and w + 8 into
+// {k, k/q} doubles in shared memory, indexed by the SOURCE coefficient -- with
+// one __syncthreads; after it warps never wait on each other.
+constexpr int KS3_TP = 10;                                     // out tile pitch (u64): 8 columns + pad
 template <int ND> constexpr size_t ks3_smem_bytes() {
-    return (size_t)2 * KS3_GP * (ND + 1) * 256 + (size_t)16 * ND * 2 * 256 + (size_t)16 * 32 * KS3_TP * 8;
+    return (size_t)16 * ND * 4 * 256 + (size_t)8 * 32 * KS3_TP * 8 + 16 * 32 + 16 * 4;
 }
 template <int ND>
-__global__ void __launch_bounds__(512, 2)
-    slot_major_ks3_kernel(u64* __restrict__ S, const KsTerms T, const KsGroups GR, int g0, int gcnt, int t0, int nq,
-                          int next, int logn, int spitch, long long kds, long long kcs, Limbs ext,
+__global__ void __launch_bounds__(256, 3)
+    slot_major_ks3_kernel(u64* __restrict__ S, const KsTerms T, const KsGroups GR, int g0, int gcnt, int nsplit, int t0,
+                          int nq, int next, int logn, int spitch, long long kds, long long kcs, Limbs ext,
                           const PrimeInfo* __restrict__ pr, const u64* __restrict__ pmod,
                           const double2* __restrict__ fq) {
     extern __shared__ __align__(16) unsigned char ks3_smem[];
-    constexpr int NW = ND + 1;                                 // words per (slot set, coefficient): U digits + c0
-    typedef u64 UTile[KS3_GP][NW][32];
-    UTile* ut = reinterpret_cast<UTile*>(ks3_smem);                                            // [2]
-    u64(*keys)[ND][2][32] = reinterpret_cast<u64(*)[ND][2][32]>(ks3_smem + 2 * sizeof(UTile)); // [16 terms]
-    u64(*tiles)[32][KS3_TP] =
-        reinterpret_cast<u64(*)[32][KS3_TP]>(ks3_smem + 2 * sizeof(UTile) + (size_t)16 * ND * 2 * 256);   // [16 warps]
+    double(*kfp)[ND][4][32] = reinterpret_cast<double(*)[ND][4][32]>(ks3_smem);          // [16 terms]: kd, kq, kd1, kq1
+    u64(*tiles)[32][KS3_TP] = reinterpret_cast<u64(*)[32][KS3_TP]>(ks3_smem + (size_t)16 * ND * 4 * 256);   // [8 warps]
+    unsigned char(*nrow_s)[32] =
+        reinterpret_cast<unsigned char(*)[32]>(ks3_smem + (size_t)16 * ND * 4 * 256 + (size_t)8 * 32 * KS3_TP * 8);
+    int* nblk_s = reinterpret_cast<int*>(nrow_s + 16);
     const int N = 1 << logn;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int m0 = blockIdx.x * 32, tl = blockIdx.y, t = t0 + tl;
+    const int m0 = blockIdx.x * 32, tl = blockIdx.y / nsplit, half = blockIdx.y - tl * nsplit, t = t0 + tl;
     const int kfirst = GR.start[blockIdx.z], kcount = GR.count[blockIdx.z];
     const int kt = ext.prime[t];
     const PrimeInfo& P = pr[kt];
@@ -326,107 +321,114 @@ __global__ void __launch_bounds__(512, 2)
     const bool qlimb = t < nq;
     const long long dstr = (long long)next * N;
     const long long ustep = (long long)ND * dstr, cstep = 2 * LNs;
-    const int nph = (gcnt + KS3_GP - 1) / KS3_GP;
+    const double2 f = fq[kt];
+    const int gs0 = half * 32 + w * 4;                         // this warp's slot sets gs0 .. gs0 + 3
+    // ---- this thread's operands, once (12 loads in flight), before the key conversion's own loads
     const u64* U0 = nullptr;                                   // the run's ModUp: its first rotation term's
     for (int ki = 0; ki < kcount && !U0; ki++)
         if (T.g[kfirst + ki] != 1u) U0 = T.U[kfirst + ki];
-    const u64* Ub = U0 ? U0 + (long long)t * N + m0 + (long long)g0 * ustep : nullptr;
-    const u64* Cb = T.src[kfirst] + (long long)t * N + m0 + (long long)g0 * cstep;
-    const int piece = threadIdx.x & 15;
-    auto load_phase = [&](int ph) {                            // rows of 256 bytes, 16 threads x 16 bytes each
-        UTile& dstt = ut[ph & 1];
-        const int gbase = ph * KS3_GP;
-        for (int row = threadIdx.x >> 4; row < KS3_GP * NW; row += 32) {
-            const int gl = row / NW, j = row - gl * NW, gs = gbase + gl;
-            if (gs >= gcnt) continue;
-            const u64* srcp = j < ND ? (Ub ? Ub + gs * ustep + j * dstr : nullptr) : (qlimb ? Cb + gs * cstep : nullptr);
-            u64* dstp = &dstt[gl][j][2 * piece];
-            if (srcp) cp_async16(dstp, srcp + 2 * piece);
-            else *reinterpret_cast<ulonglong2*>(dstp) = make_ulonglong2(0ull, 0ull);
-        }
-    };
-    // this warp's term
-    const bool has = w < kcount;
-    const int k = kfirst + (has ? w : 0);
-    const u32 g = T.g[k];
-    u32 ginv = g;                                              // g^-1 mod 2^32 (Newton; g g = 1 mod 8)
+    u64 uw[4][ND], cw[4];
+    {
+        const u64* Up = U0 ? U0 + (long long)t * N + m0 + lane + (long long)g0 * ustep : nullptr;
+        const u64* Cp = T.src[kfirst] + (long long)t * N + m0 + lane + (long long)g0 * cstep;
 #pragma unroll
-    for (int i = 0; i < 4; i++) ginv *= 2u - g * ginv;
-    const int n = g == 1u ? m0 + lane : (int)automorph_src((u32)(m0 + lane), ginv & ((2u << logn) - 1u), logn);
-    const int nrow = n & 31;
-    if (has && g != 1u) {                                      // the warp's key rows: (digit, component) x 256 bytes at n's block
-        const u64* kp = T.key[k] + (long long)kt * N + (n & ~31);
-        for (int x = lane; x < ND * 2 * 16; x += 32) {
-            const int r = x >> 4, pc = x & 15;
-            cp_async16(&keys[w][r >> 1][r & 1][2 * pc], kp + (r >> 1) * kds + (r & 1) * kcs + 2 * pc);
+        for (int b = 0; b < 4; b++) {
+            const long long gs = gs0 + b < gcnt ? gs0 + b : 0;
+            cw[b] = qlimb ? __ldg(Cp + gs * cstep) : 0ull;
+#pragma unroll
+            for (int j = 0; j < ND; j++) uw[b][j] = Up ? __ldg(Up + gs * ustep + j * dstr) : 0ull;
         }
     }
-    load_phase(0);
-    cp_async_commit();
-    const u64 pw = qlimb ? pmod[2 * t] : 0ull, pwp = qlimb ? pmod[2 * t + 1] : 0ull;
-    u64(*tw)[KS3_TP] = tiles[w];
-    const int fr = lane >> 2, fp = lane & 3;                   // flush: 8 rows x four 16-byte pieces per instruction
-    u64* dst = S + (((long long)tl * N + (n & ~31)) * T.n + k) * spitch + 2 * fp;
-    const long long rstride = (long long)T.n * spitch;
-    const double2 f = fq[kt];
+    // ---- the run's keys: rotation r's words at n = sigma_r^-1(m), as doubles, by warps r % 8
+    for (int r = w; r < kcount; r += 8) {
+        const int k = kfirst + r;
+        const u32 g = T.g[k];
+        u32 ginv = g;                                          // g^-1 mod 2^32 (Newton; g g = 1 mod 8)
+#pragma unroll
+        for (int i = 0; i < 4; i++) ginv *= 2u - g * ginv;
+        const int n = g == 1u ? m0 + lane : (int)automorph_src((u32)(m0 + lane), ginv & ((2u << logn) - 1u), logn);
+        nrow_s[r][lane] = (unsigned char)(n & 31);
+        if (lane == 0) nblk_s[r] = n & ~31;
+        if (g != 1u) {
+            const u64* kp = T.key[k] + (long long)kt * N + n;
+            u64 kw[ND][2];
+#pragma unroll
+            for (int j = 0; j < ND; j++) { kw[j][0] = __ldg(kp + j * kds); kw[j][1] = __ldg(kp + j * kds + kcs); }
+#pragma unroll
+            for (int j = 0; j < ND; j++)
+#pragma unroll
+                for (int c = 0; c < 2; c++) {                  // Montgomery key word -> {k, k/q}
+                    const double kd = fload(redc(0ull, kw[j][c], q, P.qinv_neg));
+                    kfp[r][j][2 * c][lane] = kd;
+                    kfp[r][j][2 * c + 1][lane] = __dmul_rn(kd, f.y);
+                }
+        }
+    }
+    const u64 pw = qlimb ? pmod[2 * t] : 0ull;
+    const double pd = qlimb ? fload(pw) : 0.0, pq = __dmul_rn(pd, f.y);
     const double stage_c = ND <= 2 ? __dadd_rn(4503599627370496.0, __dadd_rn(f.x, f.x))
                                    : __dadd_rn(4503599627370496.0, f.x);
-    const double pd = qlimb ? fload(pw) : 0.0, pq = __dmul_rn(pd, f.y);
-    double kd[ND], kq[ND], kd1[ND], kq1[ND];
-    const u64* c1p = T.src[k] + (long long)t * N + n + LNs + (long long)g0 * cstep;     // identity term: c1 from HBM
-    for (int ph = 0; ph < nph; ph++) {
-        cp_async_wait<0>();
-        __syncthreads();                                       // phase ph landed; everyone is done with buffer (ph + 1) & 1
-        if (ph + 1 < nph) load_phase(ph + 1);
-        cp_async_commit();
-        if (!has) continue;
-        if (ph == 0 && g != 1u) {
+    double ud[4][ND], a0[4];
 #pragma unroll
-            for (int j = 0; j < ND; j++) {                     // Montgomery key words -> {k, k/q} as doubles
-                kd[j] = fload(redc(0ull, keys[w][j][0][nrow], q, P.qinv_neg));
-                kq[j] = __dmul_rn(kd[j], f.y);
-                kd1[j] = fload(redc(0ull, keys[w][j][1][nrow], q, P.qinv_neg));
-                kq1[j] = __dmul_rn(kd1[j], f.y);
-            }
-        }
-        const UTile& cur = ut[ph & 1];
-#pragma unroll 1
-        for (int fb = 0; fb < KS3_GP / 4; fb++) {              // 4 slot sets per flush
-            const int gs0 = ph * KS3_GP + fb * 4;
-            if (gs0 >= gcnt) break;
+    for (int b = 0; b < 4; b++) {
+        a0[b] = qlimb ? fmm(fload(cw[b]), pd, pq, f.x) : 0.0;  // P c0: the same for every rotation
+#pragma unroll
+        for (int j = 0; j < ND; j++) ud[b][j] = fload(uw[b][j]);
+    }
+    __syncthreads();
+    if (gs0 >= gcnt) return;
+    u64(*tw)[KS3_TP] = tiles[w];
+    const int fr = lane >> 2, fp = lane & 3;                   // flush: 8 rows x four 16-byte pieces per instruction
+    const long long rstride = (long long)T.n * spitch;
+    for (int r = 0; r < kcount; r++) {
+        const int k = kfirst + r;
+        const u32 g = T.g[k];
+        const int nrow = nrow_s[r][lane];
+        u64 v0[4], v1[4];
+        if (g == 1u) {                                         // P x (both components); c1 from HBM
+            const u64* c1p = T.src[k] + (long long)t * N + m0 + lane + LNs + (long long)g0 * cstep;
 #pragma unroll
             for (int b = 0; b < 4; b++) {
-                const int gl = fb * 4 + b;
-                const bool live = gs0 + b < gcnt;
-                u64 v0 = 0ull, v1 = 0ull;
-                if (g == 1u) {
-                    if (qlimb && live) {
-                        v0 = shoup(cur[gl][ND][lane], pw, pwp, q);
-                        v1 = shoup(__ldg(c1p + (long long)(gs0 + b) * cstep), pw, pwp, q);
-                    }
-                } else if (live) {
-                    double acc = qlimb ? fmm(fload(cur[gl][ND][lane]), pd, pq, f.x) : 0.0;
-                    double acc1 = 0.0;
+                const long long gs = gs0 + b < gcnt ? gs0 + b : 0;
+                const double a1 = qlimb ? fmm(fload(__ldg(c1p + gs * cstep)), pd, pq, f.x) : 0.0;
+                v0[b] = fstage<ND>(a0[b], stage_c, f.y, f.x);
+                v1[b] = fstage<ND>(a1, stage_c, f.y, f.x);
+            }
+        } else {
+            double kd[ND], kq[ND], kd1[ND], kq1[ND];
 #pragma unroll
-                    for (int j = 0; j < ND; j++) {
-                        const double ud = fload(cur[gl][j][lane]);
-                        acc = __dadd_rn(acc, fmm(ud, kd[j], kq[j], f.x));
-                        acc1 = __dadd_rn(acc1, fmm(ud, kd1[j], kq1[j], f.x));
-                    }
-                    v0 = fstage<ND>(acc, stage_c, f.y, f.x);
-                    v1 = fstage<ND>(acc1, stage_c, f.y, f.x);
+            for (int j = 0; j < ND; j++) {
+                kd[j] = kfp[r][j][0][lane];
+                kq[j] = kfp[r][j][1][lane];
+                kd1[j] = kfp[r][j][2][lane];
+                kq1[j] = kfp[r][j][3][lane];
+            }
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                double acc = a0[b], acc1 = 0.0;
+#pragma unroll
+                for (int j = 0; j < ND; j++) {
+                    acc = __dadd_rn(acc, fmm(ud[b][j], kd[j], kq[j], f.x));
+                    acc1 = __dadd_rn(acc1, fmm(ud[b][j], kd1[j], kq1[j], f.x));
                 }
-                *reinterpret_cast<ulonglong2*>(&tw[nrow][2 * b]) = make_ulonglong2(v0, v1);
+                v0[b] = fstage<ND>(acc, stage_c, f.y, f.x);
+                v1[b] = fstage<ND>(acc1, stage_c, f.y, f.x);
             }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int r = i * 8 + fr;
-                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&tw[r][2 * fp]);
-                *reinterpret_cast<ulonglong2*>(dst + (long long)r * rstride + gs0 * 2) = v;
-            }
-            __syncwarp();
         }
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const bool live = gs0 + b < gcnt;
+            *reinterpret_cast<ulonglong2*>(&tw[nrow][2 * b]) = make_ulonglong2(live ? v0[b] : 0ull, live ? v1[b] : 0ull);
+        }
+        __syncwarp();
+        u64* dst = S + (((long long)tl * N + nblk_s[r]) * T.n + k) * spitch + gs0 * 2 + 2 * fp;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int rr = i * 8 + fr;
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&tw[rr][2 * fp]);
+            *reinterpret_cast<ulonglong2*>(dst + (long long)rr * rstride) = v;
+        }
+        __syncwarp();
     }
 }
 
@@ -443,9 +445,10 @@ static cudaError_t ks3_launch(u64* S, const KsTerms& T, const KsGroups& GR, int 
         if (ae != cudaSuccess) return ae;
         cfg |= bit;
     }
-    dim3 grid((1 << logn) / 32, tcnt, GR.n);
-    slot_major_ks3_kernel<ND><<<grid, 512, smem, st>>>(S, T, GR, g0, gcnt, t0, nq, next, logn, spitch, kds, kcs, ext, pr,
-                                                       pmod, fq);
+    const int nsplit = (gcnt + 31) / 32;
+    dim3 grid((1 << logn) / 32, tcnt * nsplit, GR.n);
+    slot_major_ks3_kernel<ND><<<grid, 256, smem, st>>>(S, T, GR, g0, gcnt, nsplit, t0, nq, next, logn, spitch, kds, kcs,
+                                                       ext, pr, pmod, fq);
     return launched();
 }
 
