@@ -222,6 +222,22 @@ class KeyedPlain(np.ndarray):
         self.bcn_key = None
 
 
+class LazyPlain:
+    """A keyed plain vector whose values are only built on a plaintext-cache
+    miss (`np.asarray(x)` calls the builder): in steady state a weight-derived
+    multiplier is looked up by key alone, and the host never recomputes it."""
+
+    __slots__ = ("bcn_key", "_fn")
+
+    def __init__(self, fn, key):
+        self.bcn_key = key
+        self._fn = fn
+
+    def __array__(self, dtype=None, copy=None):
+        a = np.asarray(self._fn(), dtype=np.float64)
+        return a if dtype is None else a.astype(dtype, copy=False)
+
+
 class Ciphertext:
     """Batch of G RNS-CKKS ciphertexts + logical level / scale / id.
 
