@@ -1488,11 +1488,11 @@ static int keyswitch_tail(bcn_ctx* c, u64* out, long long os, const u64* U, int 
         // inner product of the special limbs only (the INTT needs them); the q-limbs'
         // inner products are computed by the ModDown NTT's epilogue (epilogue 4)
         CUDA_TRY(inner_op(A, U, G, next, ndig, c->logn, (u32)g, key, 2LL * c->nbasis * N, (long long)c->nbasis * N,
-                          ext, ext, c->pr, st, nl, c->K));
+                          ext, ext, c->pr, st, nl, c->K, c->fp_conv ? c->fq : nullptr));
         return moddown_tail(c, out, os, A, G, level, addend, as, add_c1, (u32)g, T, Z, st, U, key);
     }
     CUDA_TRY(inner_op(A, U, G, next, ndig, c->logn, (u32)g, key, 2LL * c->nbasis * N, (long long)c->nbasis * N, ext,
-                      ext, c->pr, st));
+                      ext, c->pr, st, 0, -1, c->fp_conv ? c->fq : nullptr));
     // INTT of the special limbs of both components
     return moddown_tail(c, out, os, A, G, level, addend, as, add_c1, (u32)g, T, Z, st);
 }
@@ -1567,7 +1567,7 @@ int bcn_rotsum_keys(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* cons
             R.fused[k] = (unsigned char)(pk != nullptr || R.pt[k] == nullptr);
         }
         CUDA_TRY(rotsum_op(B, C0, R, 2LL * nl * N, G, nl, next, ndig, c->logn, 2LL * c->nbasis * N,
-                           (long long)c->nbasis * N, ext, c->pr, t0 > 0, st));
+                           (long long)c->nbasis * N, ext, c->pr, t0 > 0, st, -1, -1, c->fp_conv ? c->fq : nullptr));
     }
     return moddown_tail(c, (u64*)out, 2LL * nl * N, B, G, level, C0, (long long)nl * N, 0, 1u, T, Z, st);
 }
@@ -1691,7 +1691,8 @@ int bcn_rotsum_rescale(bcn_ctx* c, uint64_t* out, int n_terms, const uint64_t* c
             R.fused[k] = (unsigned char)(pk != nullptr || R.pt[k] == nullptr);
         }
         CUDA_TRY(rotsum_op(B, Cf, R, 2LL * nl * N, G, nl, next, ndig, c->logn, 2LL * c->nbasis * N,
-                           (long long)c->nbasis * N, ext, c->pr, t0 > 0, st, 2LL * nl * N, (t0 > 0) || (n_ct > 0)));
+                           (long long)c->nbasis * N, ext, c->pr, t0 > 0, st, 2LL * nl * N, (t0 > 0) || (n_ct > 0),
+                           c->fp_conv ? c->fq : nullptr));
     }
     return mdr_tail(c, (u64*)out, B, Cf, n_ct > 0, G, level, T, Z, st);
 }
@@ -1785,7 +1786,8 @@ int bcn_mul_cc(bcn_ctx* c, uint64_t* out, const uint64_t* a, int a_nlimb, const 
         u64* A = tmp;                                   // [G][2][next][N]
         u64* Z = A + (size_t)G * 2 * next * N;          // staged path only
         CUDA_TRY(inner_op(A, U, G, next, T->ndig, c->logn, 1u, key_ptr(c, 2), 2LL * c->nbasis * N,
-                          (long long)c->nbasis * N, limbs_ext(c, level), limbs_ext(c, level), c->pr, st));
+                          (long long)c->nbasis * N, limbs_ext(c, level), limbs_ext(c, level), c->pr, st, 0, -1,
+                          c->fp_conv ? c->fq : nullptr));
         return mdr_tail(c, (u64*)out, A, d, 1, G, level, T, Z, st, 3LL * nl * N);
     }
     u64* dst = rescale ? R : (u64*)out;

@@ -599,12 +599,81 @@ __global__ void __launch_bounds__(256) inner_kernel(u64* __restrict__ A, const u
     }
 }
 
+// inner_fp: the key-switch inner product on the FP64 pipe (basis primes below
+// 2^50): a thread owns (coefficient, limb) for SS polynomials' worth of slot
+// sets, the 2 ND key words are converted to {k, k/q} doubles once, the SS x ND
+// digit words are loaded together (under X -> X^g the gather index is computed
+// once), and each product is one fmm.  ~65 instead of ~120 instructions per
+// output pair at ND = 3; the integer form re-read the key words per slot set.
+template <int ND>
+__global__ void __launch_bounds__(256, 3) inner_fp_kernel(u64* __restrict__ A, const u64* __restrict__ U, int npoly,
+                                                          int next, int logn, u32 g, const u64* __restrict__ key,
+                                                          long long kds, long long kcs, Limbs ext, Limbs keyl,
+                                                          const PrimeInfo* __restrict__ pr,
+                                                          const double2* __restrict__ fq, int t0) {
+    constexpr int SS = 4;
+    const int N = 1 << logn;
+    const int n = blockIdx.x * 256 + threadIdx.x;
+    const int t = t0 + blockIdx.y;
+    const long long p0 = (long long)blockIdx.z * SS;
+    const int kt = keyl.prime[t];
+    const PrimeInfo& P = pr[ext.prime[t]];
+    const u64 q = P.q;
+    const double2 f = fq[ext.prime[t]];
+    const int sn = g == 1u ? n : (int)automorph_src((u32)n, g, logn);
+    int live = npoly - (int)p0;
+    live = live > SS ? SS : live;
+    const long long dstr = (long long)next * N, ustep = (long long)ND * dstr;
+    const u64* Up = U + (p0 * ND * next + t) * (long long)N + sn;
+    u64 uw[SS][ND];
+#pragma unroll
+    for (int s = 0; s < SS; s++) {
+        const long long so = s < live ? s : 0;
+#pragma unroll
+        for (int j = 0; j < ND; j++) uw[s][j] = __ldg(Up + so * ustep + j * dstr);
+    }
+    double kd[ND], kq[ND], kd1[ND], kq1[ND];
+    const u64* kp = key + (long long)kt * N + n;
+#pragma unroll
+    for (int j = 0; j < ND; j++) {
+        kd[j] = fload(redc(0ull, __ldg(kp + j * kds), q, P.qinv_neg));
+        kq[j] = __dmul_rn(kd[j], f.y);
+        kd1[j] = fload(redc(0ull, __ldg(kp + j * kds + kcs), q, P.qinv_neg));
+        kq1[j] = __dmul_rn(kd1[j], f.y);
+    }
+#pragma unroll
+    for (int s = 0; s < SS; s++) {
+        if (s >= live) break;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < ND; j++) {
+            const double ud = fload(uw[s][j]);
+            a0 = __dadd_rn(a0, fmm(ud, kd[j], kq[j], f.x));
+            a1 = __dadd_rn(a1, fmm(ud, kd1[j], kq1[j], f.x));
+        }
+        u64* o = A + ((p0 + s) * 2 * next + t) * (long long)N + n;
+        o[0] = fcanon(a0, f.y, f.x);
+        o[(long long)next * N] = fcanon(a1, f.y, f.x);
+    }
+}
+
 cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
                      long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
-                     const PrimeInfo* pr, cudaStream_t st, int t0, int tcnt) {
+                     const PrimeInfo* pr, cudaStream_t st, int t0, int tcnt, const double2* fq) {
     const int N = 1 << logn;
     if (tcnt < 0) tcnt = next - t0;
     if (tcnt <= 0) return cudaSuccess;
+    static const bool fp_off = getenv("BCN_INNER_FP64") && getenv("BCN_INNER_FP64")[0] == '0';
+    if (fq && !fp_off && N >= 256 && ndig >= 1 && ndig <= 4) {
+        dim3 grid(N / 256, tcnt, (npoly + 3) / 4);
+        switch (ndig) {
+#define BCN_IFP(D) case D: inner_fp_kernel<D><<<grid, 256, 0, st>>>(A, U, npoly, next, logn, g, key, key_digit_stride, \
+                                                                  key_comp_stride, ext, keyl, pr, fq, t0); break;
+            BCN_IFP(1) BCN_IFP(2) BCN_IFP(3) BCN_IFP(4)
+#undef BCN_IFP
+        }
+        return launched();
+    }
     if (N >= 1024) {
         constexpr int BLK = 1024;
         size_t smem = (size_t)ndig * BLK * sizeof(u64);
@@ -944,9 +1013,121 @@ __global__ void __launch_bounds__(256, BCN_RS3_MINB) rotsum3_kernel(
     }
 }
 
+// rotsum4: rotsum3 on the FP64 pipe (every basis prime below 2^50).  The
+// integer form spends ~125 instructions per (term, output pair) -- u128 MACs on
+// the 32-bit IMAD datapath, the automorphism index and five key / plaintext
+// words re-read by every slot set.  Here a thread owns (coefficient, limb) for
+// SS slot sets: the term's index and its key / plaintext words (Montgomery ->
+// {w, w/q} doubles) are paid once per SS slot sets, the SS x (ND + 1) operand
+// loads go out together, and each product is one fmm (6 FP64 instructions);
+// the sums stay exact integers in doubles, folded to [-q/2, q/2] every 4 terms
+// (|sum| <= 0.5 q + 4 (ND <= 4 products) 0.61 q... kept below 2^53 by FOLD).
+#ifndef BCN_RS4_SS
+#define BCN_RS4_SS 4
+#endif
+#ifndef BCN_RS4_MINB
+#define BCN_RS4_MINB 3
+#endif
+template <int ND>
+__global__ void __launch_bounds__(256, BCN_RS4_MINB) rotsum4_kernel(
+        u64* __restrict__ B, u64* __restrict__ C0, const RotTerms T, long long c0_gstride, int G, int nq, int next,
+        int logn, long long kds, long long kcs, Limbs ext, const PrimeInfo* __restrict__ pr,
+        const double2* __restrict__ fq, int acc_flags, long long c0_ostride) {
+    constexpr int SS = BCN_RS4_SS;
+    constexpr int FOLD = ND <= 2 ? 4 : 2;          // products per sum between folds: FOLD * ND <= 8 (8 x 0.61 q + q/2 < 2^53 / q)
+    const int N = 1 << logn;
+    const int n = blockIdx.x * 256 + threadIdx.x;
+    const int t = blockIdx.y;
+    const long long p0 = (long long)blockIdx.z * SS;
+    const int kt = ext.prime[t];
+    const PrimeInfo& P = pr[kt];
+    const u64 q = P.q, qn = P.qinv_neg, one_m = P.r1;
+    const double2 f = fq[kt];
+    const bool has_c0 = t < nq;
+    const long long dstr = (long long)next * N;
+    const long long ustep = (long long)ND * dstr;                 // per slot set
+    const long long uoff = (p0 * ND * next + t) * (long long)N;
+    const long long coff = p0 * c0_gstride + (long long)t * N;
+    const long long koff = (long long)kt * N + n;
+    const long long poff = (long long)t * N + n;
+    int live = G - (int)p0;
+    live = live > SS ? SS : live;
+    double b0[SS], b1[SS], cc[SS];
+#pragma unroll
+    for (int s = 0; s < SS; s++) b0[s] = b1[s] = cc[s] = 0.0;
+    int kf = 0;
+    for (int k = 0; k < T.n; k++) {
+        const long long sn = automorph_src((u32)n, T.g[k], logn);
+        const u64* __restrict__ Uk = T.U[k] + (uoff + sn);
+        const u64* __restrict__ Ck = T.c0[k] + (coff + sn);
+        const u64* __restrict__ kp = T.key[k] + koff;
+        u64 uw[SS][ND], cw[SS], k0[ND], k1[ND];
+#pragma unroll
+        for (int j = 0; j < ND; j++) { k0[j] = __ldg(kp + j * kds); k1[j] = __ldg(kp + j * kds + kcs); }
+        const u64* pk = T.pt[k];
+        const u64 w = has_c0 && pk ? __ldg(pk + poff) : one_m;
+#pragma unroll
+        for (int s = 0; s < SS; s++) {                            // a slot set past G re-reads the first one
+            const long long so = s < live ? s : 0;
+#pragma unroll
+            for (int j = 0; j < ND; j++) uw[s][j] = __ldg(Uk + so * ustep + j * dstr);
+            cw[s] = has_c0 ? __ldg(Ck + so * c0_gstride) : 0ull;
+        }
+        double kd[ND], kq[ND], kd1[ND], kq1[ND];
+#pragma unroll
+        for (int j = 0; j < ND; j++) {
+            kd[j] = fload(redc(0ull, k0[j], q, qn));
+            kq[j] = __dmul_rn(kd[j], f.y);
+            kd1[j] = fload(redc(0ull, k1[j], q, qn));
+            kq1[j] = __dmul_rn(kd1[j], f.y);
+        }
+        const double wd = fload(redc(0ull, w, q, qn)), wq = __dmul_rn(wd, f.y);
+#pragma unroll
+        for (int s = 0; s < SS; s++) {
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                const double ud = fload(uw[s][j]);
+                b0[s] = __dadd_rn(b0[s], fmm(ud, kd[j], kq[j], f.x));
+                b1[s] = __dadd_rn(b1[s], fmm(ud, kd1[j], kq1[j], f.x));
+            }
+            if (has_c0) cc[s] = __dadd_rn(cc[s], fmm(fload(cw[s]), wd, wq, f.x));
+        }
+        if (++kf == FOLD) {
+#pragma unroll
+            for (int s = 0; s < SS; s++) {
+                b0[s] = fred(b0[s], f.y, f.x);
+                b1[s] = fred(b1[s], f.y, f.x);
+            }
+            kf = 0;
+        }
+        if ((k & 7) == 7) {
+#pragma unroll
+            for (int s = 0; s < SS; s++) cc[s] = fred(cc[s], f.y, f.x);
+        }
+    }
+    const int accumulate = acc_flags & 1, c0_acc = (acc_flags >> 1) & 1;
+#pragma unroll
+    for (int s = 0; s < SS; s++) {
+        if (s >= live) break;
+        const long long p = p0 + s;
+        u64* o0 = B + (p * 2 * next + t) * (long long)N + n;
+        u64* o1 = o0 + (long long)next * N;
+        u64 r0 = fcanon(b0[s], f.y, f.x), r1 = fcanon(b1[s], f.y, f.x);
+        if (accumulate) { r0 = add_mod(r0, *o0, q); r1 = add_mod(r1, *o1, q); }
+        *o0 = r0;
+        *o1 = r1;
+        if (has_c0) {
+            u64* oc = C0 + p * c0_ostride + (long long)t * N + n;
+            u64 rc = fcanon(cc[s], f.y, f.x);
+            if (c0_acc) rc = add_mod(rc, *oc, q);
+            *oc = rc;
+        }
+    }
+}
+
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
-                      int accumulate, cudaStream_t st, long long c0_ostride, int c0_accumulate) {
+                      int accumulate, cudaStream_t st, long long c0_ostride, int c0_accumulate, const double2* fq) {
     const int N = 1 << logn;
     if (terms.n <= 0 || G <= 0) return cudaSuccess;
     if (c0_ostride < 0) c0_ostride = (long long)nq * N;
@@ -960,6 +1141,17 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
         static const bool rs3_off = getenv("BCN_ROTSUM3") && getenv("BCN_ROTSUM3")[0] == '0';
         bool simple = !rs3_off && ndig >= 1 && ndig <= 4;
         for (int k = 0; k < terms.n && simple; k++) simple = terms.fused[k] && !terms.pt_batched[k];
+        static const bool rs4_off = getenv("BCN_ROTSUM4") && getenv("BCN_ROTSUM4")[0] == '0';
+        if (simple && fq && !rs4_off) {
+            dim3 grid4(N / 256, next, (G + BCN_RS4_SS - 1) / BCN_RS4_SS);
+            switch (ndig) {
+#define BCN_RS4(D) case D: rotsum4_kernel<D><<<grid4, 256, 0, st>>>(B, C0, terms, c0_gstride, G, nq, next, logn, kds, \
+                                                                  kcs, ext, pr, fq, flags, c0_ostride); break;
+                BCN_RS4(1) BCN_RS4(2) BCN_RS4(3) BCN_RS4(4)
+#undef BCN_RS4
+            }
+            return launched();
+        }
         if (simple) {
             switch (ndig) {
 #define BCN_RS3(D) case D: rotsum3_kernel<D><<<grid, 256, 0, st>>>(B, C0, terms, c0_gstride, nq, next, logn, kds, kcs, \

@@ -155,7 +155,7 @@ cudaError_t premul_key_op(u64* out, const u64* key, const u64* pt, int ndig, int
 cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstride, int G, int nq, int next,
                       int ndig, int logn, long long key_digit_stride, long long key_comp_stride, const Limbs& ext,
                       const PrimeInfo* pr, int accumulate, cudaStream_t st, long long c0_ostride = -1,
-                      int c0_accumulate = -1);
+                      int c0_accumulate = -1, const double2* fq = nullptr);
 // dst[p][n] = dst[p][n] + src[p][n] * w (mod q) on one limb (Shoup pair w, wp)
 cudaError_t axpy_limb_op(u64* dst, long long ds, const u64* src, long long ss, int npoly, u64 w, u64 wp, u64 q,
                          int logn, cudaStream_t st);
@@ -219,7 +219,7 @@ cudaError_t modup_op(u64* U, const u64* xc, long long xc_stride, const u64* xn, 
                      const ConvTable* tab, cudaStream_t st, const FConvSet* fc = nullptr);
 cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int logn, u32 g, const u64* key,
                      long long key_digit_stride, long long key_comp_stride, const Limbs& ext, const Limbs& keyl,
-                     const PrimeInfo* pr, cudaStream_t st, int t0 = 0, int tcnt = -1);
+                     const PrimeInfo* pr, cudaStream_t st, int t0 = 0, int tcnt = -1, const double2* fq = nullptr);
 cudaError_t moddown_conv_op(u64* Z, const u64* A, long long a_stride, int npoly, int nq, int K, int logn,
                             const Limbs& ext, const PrimeInfo* pr, const ConvTable* tab, cudaStream_t st,
                             const FConv* fc = nullptr);
