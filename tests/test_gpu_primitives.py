@@ -389,6 +389,44 @@ def test_conv_ks_mac_matches_oracle(N, L, layout, bits):
     assert np.abs(dec - exp).max() < 1e-4
 
 
+@pytest.mark.parametrize("level,dnum", [(5, 3), (3, 3), (1, 3), (4, 2)], ids=["3digits", "2digits", "1digit", "2digits-K3"])
+def test_conv_ks_mac_source_shared_staging_edges(level, dnum):
+    """The source-shared FP64 staging kernel (slot_major_ks3: runs of <= 16
+    terms over one source, 4 slot sets per warp, 32 per CTA) against the oracle
+    bit for bit on its edges: 1 / 2 / 3 key-switch digits, G = 37 slot sets (a
+    second CTA half with a partial 4-block), a run of 19 rotations of one source
+    (split 16 + 3), a run that starts with the identity tap, a lone identity
+    term, and a source whose rotations are not consecutive."""
+    N, L = 1024, 5
+    eng, orc, hp = _pair(N, L, 50, dnum=dnum)
+    rng = np.random.default_rng(53)
+    G = 37
+    from paper_2402_01296_b200.params import galois_element as ge
+    vs = [rng.standard_normal((G, N // 2)) * 0.5 for _ in range(3)]
+    xs = [eng.encrypt(v, level=level, counter=400 + 50 * i) for i, v in enumerate(vs)]
+    Us = [eng.modup(x, level) for x in xs]
+    check = [0, 3, 31, 32, 36]
+    ocs = [{g: orc.encrypt(v[g], 400 + 50 * i + g, level) for g in check} for i, v in enumerate(vs)]
+    taps = ([(0, r) for r in range(1, 20)] + [(1, 0), (1, 2), (1, 5)] + [(2, 0)] + [(0, 33), (1, 7)])
+    ql = float(hp.q[level])
+    n_out = 2
+    vals = rng.standard_normal((n_out, len(taps), N // 2)) * 0.3
+    pts = [[eng.encode_ext(vals[o, k], level, ql) if r else eng.encode(vals[o, k], level, ql, montgomery=True)
+            for k, (_, r) in enumerate(taps)] for o in range(n_out)]
+    got = eng.conv_ks_mac([xs[i] for i, _ in taps], [Us[i] if r else None for i, r in taps],
+                          [ge(r, N) if r else 1 for _, r in taps], eng.pack_planes_ext(pts, level, 0), n_out, level, 0)
+    got1 = eng.conv_ks_mac([xs[i] for i, _ in taps], [Us[i] if r else None for i, r in taps],
+                           [ge(r, N) if r else 1 for _, r in taps], eng.pack_planes_ext(pts, level, 1), n_out, level, 1)
+    assert torch.equal(got, got1)                       # IMMA (16-slot-set blocks) and tcgen05 (64) staging pitches
+    c = to_numpy_u64(got.reshape(n_out * G, 2, level, N)).reshape(n_out, G, 2, level, N)
+    for o in range(n_out):
+        for g in check:
+            want = orc.rotsum_rescale([(ocs[i][g], r, vals[o, k]) for k, (i, r) in enumerate(taps) if r],
+                                      [(ocs[i][g], vals[o, k]) for k, (i, r) in enumerate(taps) if not r], level)
+            np.testing.assert_array_equal(c[o, g, 0], want.c0)
+            np.testing.assert_array_equal(c[o, g, 1], want.c1)
+
+
 def test_conv_ks_mac_blocks_bitexact_vs_eager_path():
     """Lazy-ModDown conv over several output blocks (40 outputs: 32 + 8) and
     slot-set blocks (G = 20: 16 + 4), 60-bit primes with every byte live: the
