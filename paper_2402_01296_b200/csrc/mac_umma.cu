@@ -282,6 +282,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
     // pair's words and store them as 16-byte runs (half the store requests of
     // the 32-lines-per-instruction 8-byte stores)
     const bool paired = nob == 1 && opad <= UM_PAIR_MAXO && !(dbg & 16);
+#ifndef UM_ALT
+#define UM_ALT 1
+#endif
+    const bool alt = UM_ALT && nob == 1 && opad <= 16;       // every item has ONE 16-output block
     auto item_at = [&](long long k) -> long long {
         return paired ? 2 * ((long long)blockIdx.x + (k >> 1) * gridDim.x) + (k & 1)
                       : (long long)blockIdx.x + k * gridDim.x;
@@ -380,8 +384,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                     const u32 a0 = smem_addr(um_smem + (size_t)stage * UM_SBYTES);
                     const u32 b0 = a0 + UM_ABYTES;
                     for (int nb = 0; nb < nbo; nb++) {
+                        // one 16-output block per item: items alternate between the two TMEM
+                        // accumulators, so the next item's MMAs run while this one drains
+                        const int ai = alt ? (int)(kk & 1) : nb;
                         if (c == 0) {
-                            UM_TIMED(tw2, um_wait(&acce[nb], (use[nb] & 1) ^ 1));
+                            UM_TIMED(tw2, um_wait(&acce[ai], (use[ai] & 1) ^ 1));
                             tc_fence_after();
                         }
 #pragma unroll
@@ -389,15 +396,17 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                             if (j >= nplanes) break;              // every prime < 2^56: byte 7 is zero
                             const u64 ad = umma_sdesc(a0 + j * UM_APLANE, UM_COLS * 16, 128);
                             const u64 bd = umma_sdesc(b0 + (nb * 256 + 7 - j) * 16, UM_BHALF, 128);
-                            if (!(dbg & 4)) umma_i8(tmem + nb * 256, ad, bd, (c > 0 || j > 0) ? 1u : 0u);
+                            if (!(dbg & 4)) umma_i8(tmem + ai * 256, ad, bd, (c > 0 || j > 0) ? 1u : 0u);
                         }
-                        if (c == nch - 1) umma_commit(&accf[nb]);
+                        if (c == nch - 1) umma_commit(&accf[ai]);
                     }
                     umma_commit(&empty[stage]);
                 }
                 __syncwarp();
             }
-            for (int nb = 0; nb < nbo; nb++) use[nb]++;
+            if (alt) use[kk & 1]++;
+            else
+                for (int nb = 0; nb < nbo; nb++) use[nb]++;
         }
     } else {
         // ------------------------------------------------ epilogue
@@ -418,7 +427,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
             const RedcK P = redc_consts(pr, limbs.prime[(int)(b >> logn)]);
             u64* obase = out + (long long)(g0 + (col >> 1)) * 2 * LN + (col & 1) * LN + b;
             for (int nb = 0; nb < nbo; nb++) {
-                UM_TIMED(tw, um_wait(&accf[nb], use[nb] & 1));
+                const int ai = alt ? (int)(kk & 1) : nb;
+                UM_TIMED(tw, um_wait(&accf[ai], use[ai] & 1));
                 tc_fence_after();
                 // two groups of four outputs: four TMEM loads in flight per wait, four
                 // independent recombine+REDC chains; the accumulator is released as
@@ -430,11 +440,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                     const bool pair_st = paired && (kk & 1) == 1;     // odd slot: store both
 #pragma unroll
                     for (int x = 0; x < 4; x++)
-                        tmem_ld16(tmem + ((u32)(quarter * 32) << 16) + nb * 256 + (ohalf * 8 + og * 4 + x) * 16, d[x]);
+                        tmem_ld16(tmem + ((u32)(quarter * 32) << 16) + ai * 256 + (ohalf * 8 + og * 4 + x) * 16, d[x]);
                     tmem_wait_ld();
                     if (og == 1) {
                         tc_fence_before();
-                        mbar_arrive(&acce[nb]);
+                        mbar_arrive(&acce[ai]);
                     }
                     u64 r[4];                            // branch-free: four interleaved chains
 #pragma unroll
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1)
                         }
                     }
                 }
-                use[nb]++;
+                use[ai]++;
             }
         }
     }
