@@ -524,6 +524,43 @@ def test_fp64_base_conversions_match_oracle(N, L, dnum, monkeypatch):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("level,dnum", [(5, 3), (3, 3), (1, 3)], ids=["3digits", "2digits", "1digit"])
+def test_rotsum_fp64_slot_set_groups(level, dnum):
+    """rotsum4 / inner_fp own 4 slot sets per thread: G = 6 (a full group and a
+    partial one), 21 premultiplied-key terms over two sources (folds of the
+    exact double sums every 4 / 2 terms and of the c0 sum every 8), 1-3 digits,
+    against the oracle at slot sets 0, 3, 4, 5; eager hoisted rotation and
+    square + relinearise (inner_fp, identity and gathered) at the same G."""
+    N, L = 1024, 5
+    eng, orc, hp = _pair(N, L, 50, dnum=dnum, seed=9)
+    from paper_2402_01296_b200.params import galois_element as ge
+    rng = np.random.default_rng(61)
+    G, check = 6, [0, 3, 4, 5]
+    vs = [rng.standard_normal((G, N // 2)) * 0.5 for _ in range(2)]
+    xs = [eng.encrypt(v, level=level, counter=700 + 20 * i) for i, v in enumerate(vs)]
+    ocs = [{g: orc.encrypt(v[g], 700 + 20 * i + g, level) for g in check} for i, v in enumerate(vs)]
+    Us = [eng.modup(x, level) for x in xs]
+    ql = float(hp.q[level])
+    taps = [(i, r) for i in range(2) for r in range(1, 11)] + [(0, 77)]
+    vals = rng.standard_normal((len(taps), N // 2)) * 0.4
+    terms = [(xs[i], Us[i], ge(r, N), eng.encode_ext(vals[k], level, ql)) for k, (i, r) in enumerate(taps)]
+    got = eng.rotsum(terms, level, keys=[eng.premul_key(t[2], t[3], level) for t in terms])
+    c = to_numpy_u64(got)
+    for g in check:
+        want = orc.rotsum([(ocs[i][g], r, vals[k]) for k, (i, r) in enumerate(taps)], level)
+        np.testing.assert_array_equal(c[g, 0], want.c0)
+        np.testing.assert_array_equal(c[g, 1], want.c1)
+    rot = to_numpy_u64(eng.rotate(xs[0], 5, level))
+    eng.keygen_relin()
+    sq = to_numpy_u64(eng.mul_cc(xs[1], xs[1], level))
+    for g in check:
+        wr, ws = orc.rotate(ocs[0][g], 5), orc.mul_cc(ocs[1][g], ocs[1][g])
+        np.testing.assert_array_equal(rot[g, 0], wr.c0)
+        np.testing.assert_array_equal(rot[g, 1], wr.c1)
+        np.testing.assert_array_equal(sq[g, 0], ws.c0)
+        np.testing.assert_array_equal(sq[g, 1], ws.c1)
+
+
 @pytest.mark.parametrize("N,L,dnum", [(8192, 7, 2), (16384, 7, 2)])
 def test_single_special_prime_moddown_matches_oracle(N, L, dnum, monkeypatch):
     """K = 1 special prime (BASELINE config 3): the ModDown conversion is
