@@ -34,7 +34,8 @@ for name in ("rotsum", "mac_terms", "mac_multi_planes", "modup", "rotate", "resc
         return _fn(self, *a, **k)
     setattr(Engine, name, wrap)
 
-bundle, weights, sens, full = bench.cifar3_setup(32 * G)
+bundle, weights = bench.cifar3_weights()
+sens, full = bench.rank_inputs("cfg4", 32 * G, 0, 1)
 w = TensorArchive(weights)
 ctx = BCN.make_context(1 << 14, BCN.required_levels(bundle) + 1, 2.0 ** 50)
 dev = torch.device("cuda", 0)

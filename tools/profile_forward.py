@@ -13,7 +13,8 @@ import paper_2402_01296_b200 as BCN  # noqa: E402
 from paper_2402_01296_b200.archive import TensorArchive  # noqa: E402
 
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-bundle, weights, sens, full = bench.cifar3_setup(32 * G)
+bundle, weights = bench.cifar3_weights()
+sens, full = bench.rank_inputs("cfg4", 32 * G, 0, 1)
 w = TensorArchive(weights)
 ctx = BCN.make_context(1 << 14, BCN.required_levels(bundle) + 1, 2.0 ** 50)
 dev = torch.device("cuda", 0)

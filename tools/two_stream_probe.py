@@ -14,7 +14,8 @@ import paper_2402_01296_b200 as BCN  # noqa: E402
 from paper_2402_01296_b200.archive import TensorArchive  # noqa: E402
 
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-bundle, weights, sens, full = bench.cifar3_setup(32 * 2 * G)
+bundle, weights = bench.cifar3_weights()
+sens, full = bench.rank_inputs("cfg4", 32 * 2 * G, 0, 1)
 w = TensorArchive(weights)
 dev = torch.device("cuda", 0)
 inp_all = (torch.as_tensor(sens, device=dev), torch.as_tensor(full, device=dev))
