@@ -223,33 +223,36 @@ cudaError_t sample_small_op(u64* out, long long os, int npoly, int nlimb, int lo
 }
 
 // ct: [G][2][L][N]; c0 holds NTT(m + e) on entry.  c1 = a, c0 -= a s.
-__global__ void encrypt_combine_kernel(u64* __restrict__ ct, int nlimb, int logn, Limbs limbs,
-                                       const PrimeInfo* __restrict__ pr, const u64* __restrict__ s_mont, u64 seed,
-                                       u64 id_base, long long total, const u64* __restrict__ id_dev) {
+__global__ void __launch_bounds__(256) encrypt_combine_kernel(u64* __restrict__ ct, int nlimb, int logn, Limbs limbs,
+                                                              const PrimeInfo* __restrict__ pr,
+                                                              const u64* __restrict__ s_mont, u64 seed, u64 id_base,
+                                                              u64 g_off, const u64* __restrict__ id_dev) {
+    // grid (N / 256, limb, slot set): no 64-bit index division per word, the prime's constants per block
     const int N = 1 << logn;
     if (id_dev) id_base = *id_dev;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int n = (int)(idx & (N - 1));
-        long long rest = idx >> logn;
-        const int t = (int)(rest % nlimb);
-        const long long g = rest / nlimb;
-        const int pi = limbs.prime[t];
-        const PrimeInfo& P = pr[pi];
-        const u64 a = uniform_mod(draw(seed, 1u /*DOM_ENC_A*/, (u32)pi, id_base + (u64)g, (u32)n), P);
-        u64* c0 = ct + g * 2 * nlimb * (long long)N + (long long)t * N + n;
-        const u64 as = mont_mul(a, s_mont[(long long)pi * N + n], P.q, P.qinv_neg);
-        c0[0] = sub_mod(c0[0], as, P.q);
-        c0[(long long)nlimb * N] = a;
-    }
+    const int n = blockIdx.x * 256 + threadIdx.x;
+    if (n >= N) return;
+    const int t = blockIdx.y;
+    const long long g = blockIdx.z;
+    const int pi = limbs.prime[t];
+    const PrimeInfo& P = pr[pi];
+    const u64 a = uniform_mod(draw(seed, 1u /*DOM_ENC_A*/, (u32)pi, id_base + g_off + (u64)g, (u32)n), P);
+    u64* c0 = ct + g * 2 * nlimb * (long long)N + (long long)t * N + n;
+    const u64 as = mont_mul(a, s_mont[(long long)pi * N + n], P.q, P.qinv_neg);
+    c0[0] = sub_mod(c0[0], as, P.q);
+    c0[(long long)nlimb * N] = a;
 }
 
 cudaError_t encrypt_combine_op(u64* ct, int G, int nlimb, int logn, const Limbs& limbs, const PrimeInfo* pr,
                                const u64* s_mont, u64 seed, u64 id_base, cudaStream_t st, const u64* id_dev) {
-    long long total = (long long)G * nlimb << logn;
-    if (!total) return cudaSuccess;
-    encrypt_combine_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(ct, nlimb, logn, limbs, pr, s_mont, seed,
-                                                                       id_base, total, id_dev);
+    if (G <= 0 || nlimb <= 0) return cudaSuccess;
+    const int N = 1 << logn;
+    for (int g0 = 0; g0 < G; g0 += 65535) {                 // grid.z limit
+        const int gc = G - g0 < 65535 ? G - g0 : 65535;
+        dim3 grid((N + 255) / 256, nlimb, gc);
+        encrypt_combine_kernel<<<grid, 256, 0, st>>>(ct + (size_t)g0 * 2 * nlimb * N, nlimb, logn, limbs, pr, s_mont,
+                                                     seed, id_base, (u64)g0, id_dev);
+    }
     return launched();
 }
 
