@@ -330,14 +330,17 @@ def run_ours(args, rank: int, world: int, dist_on: bool, pool):
                                "the reference's golden fixtures in tests/test_host.py)",
                   "counts_per_forward": counts}
     # in-step NTT roofline: one more (untimed) step with every NTT launch bracketed by CUDA events
-    ntt_step = None
+    ntt_step = conv_step = None
     if rank == 0 and world == 1:
         torch.cuda.synchronize()
         _lib.ntt_timing(True)
+        _lib.conv_timing(True)
         finish(step(True), False)
         torch.cuda.synchronize()
         _lib.ntt_timing(False)
+        _lib.conv_timing(False)
         ntt_step = _lib.ntt_timing_read()
+        conv_step = _lib.conv_timing_read()
     h2d = sens_np.nbytes + full_np.nbytes
     d2h = total_images * 10 * 8 if rank == 0 else 0
     return {
@@ -348,6 +351,7 @@ def run_ours(args, rank: int, world: int, dist_on: bool, pool):
                                                             "step k) and reads its logits back to the host"},
         "gpu_launches": launches, "clocks": clocks, "counts_per_forward": counts, "keys_agree_across_ranks": keys_agree,
         "device_work_per_forward": dev_work, "parity": parity, "ctx": ctx, "ntt_step": ntt_step,
+        "conv_step": conv_step,
         "total_images": total_images,
     }
 
@@ -435,6 +439,21 @@ def ntt_roofline(ntt_step: dict, peak: float, peak_kind: str) -> dict:
         "launches": sum(v["launches"] for v in ntt_step.values()), "by_class": per,
         "timing": "CUDA event pair around every NTT launch on its stream (bcn_ntt_timing), one untimed step "
                   "after the timed region"}
+
+
+def conv_roofline(conv_step: dict, peak: float, step_ms: float) -> dict:
+    """The conv operand path of one forward step on the HBM roof: every slot-major staging launch
+    (slot_major_ks3 with the key-switch inner products, slot_major for the pre-rotated first conv) and
+    every tensor-core MAC launch (mac_umma), from a CUDA event pair around each (bcn_conv_timing)."""
+    out = {}
+    for k, v in conv_step.items():
+        gbps = v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] else None
+        out[k] = dict(v, GBps=gbps, frac=(gbps / peak if gbps else None), share_of_step=v["ms"] / step_ms)
+    out["algorithmic_bytes_per_launch"] = (
+        "staging: each distinct source's U digits, c0 and c1 and each term's key words once + the staged words "
+        "written (8 B x slots x terms x 2 x slot sets per limb); MAC: the staged words read once + the plaintext "
+        "byte planes + the outputs written (csrc/api.cu bcn_conv_ks_mac / bcn_mac_multi_planes_layout)")
+    return out
 
 
 # ------------------------------------------------------------ CPU columns
@@ -649,6 +668,7 @@ def main():
                            "ks_bound": ks_compute_bound(c3, n14)}
         peak, peak_kind = _peaks()
         extras["roofline"] = ntt_roofline(res["ntt_step"], peak, peak_kind)
+        extras["roofline_conv"] = conv_roofline(res["conv_step"], peak, res["ms_per_step"])
         extras["roofline_micro"] = {
             "ntt14_fwd": {"achieved": n14["fwd"]["GBps"], "frac": n14["fwd"]["GBps"] / peak,
                           "launch": "ntt_fwd_cluster<14,0,0>, 1536 limb-polys, 1 launch"},

@@ -84,6 +84,13 @@ int bcn_ntt_inv(bcn_ctx *ctx, uint64_t *data, int npoly, int nlimb, int prime0, 
  * coefficient) and launch counts.  Never used inside a CUDA-graph capture. */
 int bcn_ntt_timing(int enable);
 int bcn_ntt_timing_read(double *ms, uint64_t *bytes, uint64_t *launches);
+/* The same for the conv operand path (bcn_conv_ks_mac / bcn_mac_multi_planes*):
+ * 2 classes {slot-major staging (with the key-switch inner products when the
+ * conv has them), tensor-core MAC}; bytes = each distinct source / key word
+ * read once, the staged words written (class 0) and read (class 1) once, the
+ * plaintext planes, the outputs. */
+int bcn_conv_timing(int enable);
+int bcn_conv_timing_read(double *ms, uint64_t *bytes, uint64_t *launches);
 
 /* ---- K9: encode_plain (sim.py:172-181) + CKKS canonical embedding.
  * vals: f64[nplain][vstride] (first vlen used, rest zero).  out:

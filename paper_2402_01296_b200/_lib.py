@@ -47,6 +47,8 @@ SIGNATURES = {
     "bcn_ntt_inv": [_P, _P, _I, _I, _I, _P],
     "bcn_ntt_timing": [_I],
     "bcn_ntt_timing_read": [ctypes.POINTER(_D), ctypes.POINTER(_U64), ctypes.POINTER(_U64)],
+    "bcn_conv_timing": [_I],
+    "bcn_conv_timing_read": [ctypes.POINTER(_D), ctypes.POINTER(_U64), ctypes.POINTER(_U64)],
     "bcn_encode": [_P, _P, _I, _I, _I, _D, _I, _I, _P, _P],
     "bcn_encrypt": [_P, _P, _I, _I, _I, _I, _D, _U64, _P, _P],
     "bcn_encrypt_devctr": [_P, _P, _I, _I, _I, _I, _D, _P, _P, _P],
@@ -160,3 +162,19 @@ def ntt_timing_read() -> dict:
     nl = (_U64 * 4)()
     call("bcn_ntt_timing_read", ms, nb, nl)
     return {c: {"ms": ms[i], "bytes": int(nb[i]), "launches": int(nl[i])} for i, c in enumerate(NTT_CLASSES)}
+
+
+CONV_CLASSES = ("staging", "mac")
+
+
+def conv_timing(enable: bool) -> None:
+    """Bracket every conv staging / tensor-core MAC launch with CUDA events (measurement only, bcn.h)."""
+    call("bcn_conv_timing", int(bool(enable)))
+
+
+def conv_timing_read() -> dict:
+    ms = (ctypes.c_double * 2)()
+    nb = (_U64 * 2)()
+    nl = (_U64 * 2)()
+    call("bcn_conv_timing_read", ms, nb, nl)
+    return {c: {"ms": ms[i], "bytes": int(nb[i]), "launches": int(nl[i])} for i, c in enumerate(CONV_CLASSES)}

@@ -1025,6 +1025,59 @@ static int mdr_tail(bcn_ctx* c, u64* out, u64* B, const u64* C, int add_c1, int 
                     u64* Z, cudaStream_t st, long long c_gstride = 0);
 static u64* key_ptr(bcn_ctx* c, u64 id);
 
+// ---- in-step timing of the conv operand path (bcn_conv_timing): a CUDA event
+// pair around every staging launch (class 0: slot_major_ks3 / slot_major_ks /
+// slot_major) and every tensor-core MAC launch (class 1: mac_umma / mac_imma),
+// with the launch's algorithmic bytes, so bench.py can put both on the HBM roof.
+struct ConvTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cls;
+    std::vector<unsigned long long> bytes;
+    size_t used = 0;
+    int begin(int cls_, unsigned long long b, cudaStream_t st) {
+        if (!on) return -1;
+        if (used == cls.size()) {
+            cudaEvent_t e0, e1;
+            if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return -1;
+            ev.push_back(e0);
+            ev.push_back(e1);
+            cls.push_back(0);
+            bytes.push_back(0);
+        }
+        const size_t i = used++;
+        cls[i] = cls_;
+        bytes[i] = b;
+        cudaEventRecord(ev[2 * i], st);
+        return (int)i;
+    }
+    void end(int i, cudaStream_t st) {
+        if (i >= 0) cudaEventRecord(ev[2 * (size_t)i + 1], st);
+    }
+};
+static ConvTimer g_conv_timer;
+
+int bcn_conv_timing(int enable) {
+    g_conv_timer.on = enable != 0;
+    if (enable) g_conv_timer.used = 0;
+    return BCN_OK;
+}
+
+int bcn_conv_timing_read(double* ms, uint64_t* bytes, uint64_t* launches) {
+    ConvTimer& T = g_conv_timer;
+    for (int k = 0; k < 2; k++) { ms[k] = 0.0; bytes[k] = 0; launches[k] = 0; }
+    for (size_t i = 0; i < T.used; i++) {
+        if (cudaEventSynchronize(T.ev[2 * i + 1]) != cudaSuccess) return fail(BCN_ERR_CUDA, "conv timing event");
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, T.ev[2 * i], T.ev[2 * i + 1]) != cudaSuccess)
+            return fail(BCN_ERR_CUDA, "conv timing event");
+        ms[T.cls[i]] += t;
+        bytes[T.cls[i]] += T.bytes[i];
+        launches[T.cls[i]] += 1;
+    }
+    return BCN_OK;
+}
+
 int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uint64_t* const* srcs,
                     const uint64_t* const* Us, const uint64_t* gal, const uint8_t* planes, int layout, int G,
                     int level, void* stream) {
@@ -1087,15 +1140,30 @@ int bcn_conv_ks_mac(bcn_ctx* c, uint64_t* out, int n_out, int n_terms, const uin
         const int gcnt = std::min(GB, G - g0);
         for (int t0 = 0; t0 < next; t0 += tcnt) {
             const int tc = std::min(tcnt, next - t0);
+            // algorithmic bytes of the pair (per limb: each distinct source's U digits and c0 / c1 once, each
+            // term's key words once, the staged words written and read once, the plaintext planes, the outputs)
+            const unsigned long long wN = 8ull * (unsigned long long)N, cols = 2ull * (unsigned long long)gcnt;
+            const unsigned long long staged = (unsigned long long)tc * wN * n_terms * cols;
+            unsigned long long src_words = 0, key_words = 0;
+            for (int k = 0; k < n_terms; k++) {
+                const bool first = k == 0 || srcs[k] != srcs[k - 1];
+                if (first) src_words += (unsigned long long)(T->ndig + 2) * gcnt;     // U digits + c0 + c1 (upper bound)
+                if (gal[k] != 1) key_words += 2ull * T->ndig;
+            }
+            int ti = g_conv_timer.begin(0, (unsigned long long)tc * wN * (src_words + key_words) + staged, st);
             CUDA_TRY(slot_major_ks_op(S, KT, g0, gcnt, t0, tc, nl, next, T->ndig, c->logn, spitch,
                                       2LL * c->nbasis * N, (long long)c->nbasis * N, ext, c->pr, c->pmod, st,
                                       c->fp_conv ? c->fq : nullptr));
+            g_conv_timer.end(ti, st);
+            ti = g_conv_timer.begin(1, staged + (unsigned long long)tc * N * nch * opad * 256ull +
+                                           (unsigned long long)tc * wN * n_out * cols, st);
             if (tc05)
                 CUDA_TRY(mac_umma_op(acc, cw, n_out, n_terms, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad,
                                      next, c->logn, ext, c->pr, 0, st, planes7 ? 7 : 8));
             else
                 CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, next,
                                      c->logn, ext, c->pr, 0, st));
+            g_conv_timer.end(ti, st);
         }
     }
     // the O x G extended-basis sums -> one merged ModDown + rescale each
@@ -1147,13 +1215,20 @@ int bcn_mac_multi_planes_layout(bcn_ctx* c, uint64_t* out, int n_out, int n_term
         const int gcnt = std::min(GB, G - g0);
         for (int t0 = 0; t0 < nl; t0 += tcnt) {
             const int tc = std::min(tcnt, nl - t0);
+            const unsigned long long wN = 8ull * (unsigned long long)N, cols = 2ull * (unsigned long long)gcnt;
+            const unsigned long long staged = (unsigned long long)tc * wN * n_terms * cols;
+            int ti = g_conv_timer.begin(0, 2 * staged, st);           // a transposition: every word read and written
             CUDA_TRY(slot_major_op(S, M, g0, gcnt, t0, tc, nl, c->logn, st, spitch));
+            g_conv_timer.end(ti, st);
+            ti = g_conv_timer.begin(1, staged + (unsigned long long)tc * N * nch * opad * 256ull +
+                                           (unsigned long long)tc * wN * n_out * cols, st);
             if (tc05)
                 CUDA_TRY(mac_umma_op(acc, cw, n_out, n_terms, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad,
                                      nl, c->logn, l, c->pr, 0, st, planes7 ? 7 : 8));
             else
                 CUDA_TRY(mac_imma_op(acc, cw, M, (const unsigned char*)planes, S, g0, gcnt, t0, tc, opad, nl,
                                      c->logn, l, c->pr, 0, st));
+            g_conv_timer.end(ti, st);
         }
     }
     if (!rescale) return BCN_OK;
