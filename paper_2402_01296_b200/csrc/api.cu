@@ -219,6 +219,10 @@ static NttArgs ntt_args(const bcn_ctx* c, u64* data, long long poly_stride, cons
     a.copy_stride = 0;
     a.epi_tab2 = nullptr;
     a.epi_acs = 0;
+    a.enc_s = nullptr;
+    a.enc_seed = a.enc_id = 0;
+    a.enc_id_dev = nullptr;
+    a.enc_c1_off = 0;
     return a;
 }
 
@@ -717,6 +721,20 @@ static int encrypt_impl(bcn_ctx* c, const double* vals, int vlen, int vstride, i
     const long long cs = 2LL * nl * c->N;
     CUDA_TRY(encode_op((u64*)ct, cs, vals, vlen, vstride, G, scale, c->logn, l, c->pr, fft_tab(c), 1, c->seed,
                        counter0, st, (const u64*)counter_dev));
+    if ((c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_ENCRYPT")) {
+        // c0 = NTT(m + e) - a s and c1 = a in the NTT's epilogue (epilogue 5): the Philox draws and the
+        // IMAD-pipe products run beside the FP64-pipe butterflies of the other resident clusters, and c0
+        // is not read and written once more
+        NttArgs a = ntt_args(c, (u64*)ct, cs, l);
+        a.epi = 5;
+        a.enc_s = c->s_mont;
+        a.enc_seed = c->seed;
+        a.enc_id = counter0;
+        a.enc_id_dev = (const u64*)counter_dev;
+        a.enc_c1_off = (long long)nl * c->N;
+        CUDA_TRY(ntt_launch(false, c->logn, a, l.n, G, st));
+        return BCN_OK;
+    }
     CUDA_TRY(ntt_run(c, false, (u64*)ct, cs, l, G, st));
     CUDA_TRY(encrypt_combine_op((u64*)ct, G, nl, c->logn, l, c->pr, c->s_mont, c->seed, counter0, st,
                                 (const u64*)counter_dev));

@@ -294,6 +294,7 @@ static unsigned long long ntt_algorithmic_bytes(bool inverse, int logn, const Nt
     if (a.epi == 1) b += unit * nl * np;
     if (a.epi == 2 || a.epi == 3) b += unit * nl * np;
     if (a.epi == 4) b += unit * nl * (np / 2) * (unsigned long long)a.epi_ndig;
+    if (a.epi == 5) b += unit * nl * np;                        // the second component written (the key s is L2-resident)
     if ((a.epi == 2 || a.epi == 3 || a.epi == 4) && a.epi_add) b += unit * nl * (a.epi_add_c1 ? np : (np + 1) / 2);
     return b;
 }

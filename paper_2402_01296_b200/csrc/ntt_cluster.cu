@@ -107,7 +107,9 @@ struct Prologue {             // MODE 0 plain, 1 rescale lift, 2 ModDown base co
 template <int MODE>
 struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top^-1, 2 ModDown combine,
                               // 3 merged ModDown + rescale: (c - v) (P q_l)^-1 + addend q_l^-1,
-                              // 4 ModDown combine with c = the key-switch inner product computed here
+                              // 4 ModDown combine with c = the key-switch inner product computed here,
+                              // 5 encryption: c0 = v - a s with a drawn here (Philox) and stored as c1
+    static constexpr int kMode = MODE;
     u64* out;
     const u64* c;
     u64 q, w, wp;
@@ -120,12 +122,24 @@ struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top
     long long uds = 0, kds = 0;
     int ndig = 0;
     u64 qinv_neg = 0, inv1 = 0;
+    // mode 5 (encryption): c0 = v - a s, c1 = a
+    const u64* es = nullptr;    // s (Montgomery) for this limb
+    u64* out1 = nullptr;        // component 1 of this (ct, limb)
+    u64 eseed = 0, eid = 0, r1 = 0, r1s = 0;
+    u32 epi_prime = 0;
+    __device__ __forceinline__ u64 enc(int j, u64 v, u64& a_out) const {
+        PrimeInfo P;
+        P.q = q; P.qinv_neg = qinv_neg; P.r1 = r1; P.r1_shoup = r1s; P.pad[2] = inv1;
+        const u64 a = uniform_mod(draw(eseed, 1u /*DOM_ENC_A*/, epi_prime, eid, (u32)j), P);
+        a_out = a;
+        return sub_mod(v, mont_mul(a, __ldg(es + j), q, qinv_neg), q);
+    }
     // issue L2 bulk prefetches of everything operator() will read for the
     // words [j0, j0 + part) of this CTA, so those loads overlap the transform
     // instead of following it.  Under X -> X^g an aligned 32-block is the image
     // of one aligned 32-block, so a gathered operand is 256-byte runs.
     __device__ __forceinline__ void prefetch(int j0, int part, int tid, int nthr) const {
-        if constexpr (MODE == 0) {
+        if constexpr (MODE == 0 || MODE == 5) {
             return;
         } else {
             constexpr u32 RUN = 32 * sizeof(u64);
@@ -146,7 +160,7 @@ struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top
         }
     }
     __device__ __forceinline__ u64 operator()(int j, u64 v) const {
-        if constexpr (MODE == 0) {
+        if constexpr (MODE == 0 || MODE == 5) {
             return v;
         } else if constexpr (MODE == 4) {
             // the IMAD-pipe inner product runs inside the FP64-pipe NTT: no A round trip
@@ -258,8 +272,15 @@ __device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int r
         for (int m = 0; m < C::PART / (2 * C::T); m++) {
             const int e = 2 * tid + m * 2 * C::T;
             ulonglong2 v;
-            v.x = epi(j0 + e, sm[cswz(e)]);
-            v.y = epi(j0 + e + 1, sm[cswz(e + 1)]);
+            if constexpr (EPI::kMode == 5) {
+                ulonglong2 av;
+                v.x = epi.enc(j0 + e, sm[cswz(e)], av.x);
+                v.y = epi.enc(j0 + e + 1, sm[cswz(e + 1)], av.y);
+                *reinterpret_cast<ulonglong2*>(epi.out1 + j0 + e) = av;
+            } else {
+                v.x = epi(j0 + e, sm[cswz(e)]);
+                v.y = epi(j0 + e + 1, sm[cswz(e + 1)]);
+            }
             *reinterpret_cast<ulonglong2*>(epi.out + j0 + e) = v;
         }
     } else {
@@ -452,8 +473,15 @@ __device__ __forceinline__ void dfwd_pass(double* x, const EPI& epi, double* sm,
         for (int m = 0; m < C::PART / (2 * C::T); m++) {
             const int e = 2 * tid + m * 2 * C::T;
             ulonglong2 v;
-            v.x = epi(j0 + e, su[cswz(e)]);
-            v.y = epi(j0 + e + 1, su[cswz(e + 1)]);
+            if constexpr (EPI::kMode == 5) {
+                ulonglong2 av;
+                v.x = epi.enc(j0 + e, su[cswz(e)], av.x);
+                v.y = epi.enc(j0 + e + 1, su[cswz(e + 1)], av.y);
+                *reinterpret_cast<ulonglong2*>(epi.out1 + j0 + e) = av;
+            } else {
+                v.x = epi(j0 + e, su[cswz(e)]);
+                v.y = epi(j0 + e + 1, su[cswz(e + 1)]);
+            }
             *reinterpret_cast<ulonglong2*>(epi.out + j0 + e) = v;
         }
     } else {
@@ -662,12 +690,25 @@ __global__ void __cluster_dims__(CCfg<LOGN>::CS, 1, 1) __launch_bounds__(CCfg<LO
                 epi.wp2 = a.epi_tab2[2 * t + 1];
             }
         }
+    } else if constexpr (EM == 5) {
+        epi.c = nullptr;
+        epi.w = epi.wp = 0;
+        const PrimeInfo& PI = a.pr[pidx];
+        epi.qinv_neg = PI.qinv_neg;
+        epi.inv1 = PI.pad[2];
+        epi.r1 = PI.r1;
+        epi.r1s = PI.r1_shoup;
+        epi.epi_prime = (u32)pidx;
+        epi.es = a.enc_s + (size_t)pidx * C::N;
+        epi.eseed = a.enc_seed;
+        epi.eid = (a.enc_id_dev ? *a.enc_id_dev : a.enc_id) + (u64)poly;
+        epi.out1 = g + a.enc_c1_off;
     } else {
         epi.c = nullptr;
         epi.w = epi.wp = 0;
     }
     const int tid = threadIdx.x;
-    if constexpr (EM != 0) {
+    if constexpr (EM != 0 && EM != 5) {
         if (a.epi_pf) epi.prefetch(rank * C::PART, C::PART, tid, C::T);
     }
     if (a.twf && q < (1ull << 50)) {         // FP64 butterflies (uniform per cluster: one limb)
@@ -881,6 +922,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
         BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 1, 4>), (int)smem);
         BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 3>), (int)smem);
         BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 3, true>), (int)smem);
+        BCN_SMEM_ATTR(ae, (ntt_fwd_cluster<LOGN, 0, 5>), (int)smem);
         BCN_SMEM_ATTR(ae, (ntt_inv_cluster<LOGN, false>), (int)smem);
         BCN_SMEM_ATTR(ae, (ntt_inv_cluster<LOGN, true>), (int)smem);
         if (ae != cudaSuccess) return ae;
@@ -909,6 +951,7 @@ static cudaError_t launch_cluster(bool inverse, const NttArgs& a, int nlimbs, in
     else if (a.pro == 0 && a.epi == 4) ntt_fwd_cluster<LOGN, 0, 4><<<grid, C::T, smem, st>>>(b);
     else if (a.pro == 1 && a.epi == 4) ntt_fwd_cluster<LOGN, 1, 4><<<grid, C::T, smem, st>>>(b);
     else if (a.pro == 0 && a.epi == 3) ntt_fwd_cluster<LOGN, 0, 3><<<grid, C::T, smem, st>>>(b);
+    else if (a.pro == 0 && a.epi == 5) ntt_fwd_cluster<LOGN, 0, 5><<<grid, C::T, smem, st>>>(b);
     else ntt_fwd_cluster<LOGN, 0, 0><<<grid, C::T, smem, st>>>(b);
     return launched();
 }

@@ -89,6 +89,12 @@ struct NttArgs {
     const u64* epi_key;
     long long epi_kds, epi_kcs;
     int epi_ndig;
+    // epilogue 5 (encryption): out = NTT(m + e) - a (x) s, and a written as component 1
+    // (out + enc_c1_off): a = U(seed, DOM_ENC_A, prime, enc_id + poly [+ *enc_id_dev], n)
+    const u64* enc_s;        // secret key, Montgomery, [nbasis][N]
+    u64 enc_seed, enc_id;
+    const u64* enc_id_dev;   // graph replays: the id base lives in device memory
+    long long enc_c1_off;
     // skipped limbs (skip_alpha) copy copy_src[(poly / skip_dnum) * copy_stride + t * N + n]
     // instead of being left untouched (ModUp: the digit's own NTT-domain limbs)
     const u64* copy_src;
