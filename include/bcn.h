@@ -108,6 +108,14 @@ int bcn_encode_ext(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int 
  * ct_out: u64[G][2][level+1][N]; ciphertext g uses Philox id counter0 + g. */
 int bcn_encrypt(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int G, int level, double scale,
                 uint64_t counter0, uint64_t *ct_out, void *stream);
+/* Fresh encryptions of n_gal rotated copies of every row (the client holds the
+ * plaintext: network.py's first conv reads he_rotate(x, r) of the fresh input,
+ * sim.py:259-283): ct_out u64[n_gal][G][2][level+1][N]; copy c of row p is
+ * Enc(sigma_gal[c](encode(vals[p]))) with Philox id counter0 + c G + p, where
+ * sigma_g is X -> X^g on the integer plaintext (gal[c] = 5^r: slots rotated by
+ * r; 1: the row itself).  One canonical embedding per row. */
+int bcn_encrypt_rotated(bcn_ctx *ctx, const double *vals, int vlen, int vstride, int G, int level, double scale,
+                        uint64_t counter0, int n_gal, const uint64_t *gal, uint64_t *ct_out, void *stream);
 
 /* same, with the Philox id base read from DEVICE memory (*counter_dev) when the
  * kernels run -- lets a captured CUDA graph encrypt with fresh randomness on

@@ -52,6 +52,7 @@ SIGNATURES = {
     "bcn_encode": [_P, _P, _I, _I, _I, _D, _I, _I, _P, _P],
     "bcn_encrypt": [_P, _P, _I, _I, _I, _I, _D, _U64, _P, _P],
     "bcn_encrypt_devctr": [_P, _P, _I, _I, _I, _I, _D, _P, _P, _P],
+    "bcn_encrypt_rotated": [_P, _P, _I, _I, _I, _I, _D, _U64, _I, _P, _P, _P],
     "bcn_decrypt": [_P, _P, _I, _I, _I, _D, _P, _I, _P],
     "bcn_decrypt_poly": [_P, _P, _I, _I, _I, _P, _P],
     "bcn_add": [_P, _P, _P, _I, _P, _I, _I, _I, _I, _I, _P],

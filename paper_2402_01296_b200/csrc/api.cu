@@ -741,6 +741,49 @@ static int encrypt_impl(bcn_ctx* c, const double* vals, int vlen, int vstride, i
     return BCN_OK;
 }
 
+// ct: [(n_gal) x G][2][level+1][N]; copy c (Galois element gal[c], 1 = the plaintext itself) of row p is a
+// fresh encryption (id counter0 + c G + p) of sigma_gal[c](encode(vals[p])), i.e. of the slots rotated by
+// the r with 5^r = gal[c]: one canonical embedding per row instead of one per copy
+int bcn_encrypt_rotated(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
+                        uint64_t counter0, int n_gal, const uint64_t* gal, uint64_t* ct, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (vlen > c->N / 2) return fail(BCN_ERR_CAPACITY, "vector exceeds slot count");
+    if (n_gal < 1 || n_gal > 32) return fail(BCN_ERR_PARAM, "1..32 copies per plaintext");
+    if (G < 1 || G > 65535) return fail(BCN_ERR_PARAM, "1..65535 plaintexts per call");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nl = level + 1;
+    Limbs l = limbs_range(0, nl);
+    const long long cs = 2LL * nl * c->N;
+    u32 ginv[32];
+    for (int k = 0; k < n_gal; k++) {
+        if ((gal[k] & 1) == 0) return fail(BCN_ERR_PARAM, "Galois elements must be odd");
+        u32 g = (u32)gal[k], x = g;
+        for (int it = 0; it < 5; it++) x *= 2u - g * x;          // g^-1 mod 2^32
+        ginv[k] = x & (u32)(2 * c->N - 1);
+    }
+    int err = 0;
+    i64* raw = (i64*)scratch_get(c, (size_t)G * c->N, &err);
+    if (!raw) return err;
+    CUDA_TRY(encode_op(nullptr, 0, vals, vlen, vstride, G, scale, c->logn, l, c->pr, fft_tab(c), 0, c->seed, 0, st,
+                       nullptr, raw));
+    CUDA_TRY(encode_rot_op((u64*)ct, cs, raw, G, c->logn, l, c->pr, n_gal, ginv, c->seed, counter0, st));
+    const int rows = n_gal * G;
+    if ((c->logn == 13 || c->logn == 14) && !getenv_flag_off("BCN_FUSED_ENCRYPT")) {
+        NttArgs a = ntt_args(c, (u64*)ct, cs, l);
+        a.epi = 5;
+        a.enc_s = c->s_mont;
+        a.enc_seed = c->seed;
+        a.enc_id = counter0;
+        a.enc_c1_off = (long long)nl * c->N;
+        CUDA_TRY(ntt_launch(false, c->logn, a, l.n, rows, st));
+        return BCN_OK;
+    }
+    CUDA_TRY(ntt_run(c, false, (u64*)ct, cs, l, rows, st));
+    CUDA_TRY(encrypt_combine_op((u64*)ct, rows, nl, c->logn, l, c->pr, c->s_mont, c->seed, counter0, st, nullptr));
+    return BCN_OK;
+}
+
 int bcn_encrypt(bcn_ctx* c, const double* vals, int vlen, int vstride, int G, int level, double scale,
                 uint64_t counter0, uint64_t* ct, void* stream) {
     return encrypt_impl(c, vals, vlen, vstride, G, level, scale, counter0, nullptr, ct, stream);

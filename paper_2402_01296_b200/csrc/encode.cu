@@ -15,7 +15,8 @@ namespace bcn {
 // out[p][t][i] = round(scale * m_i) (+ e_i) mod q_t, coefficient domain.
 __global__ void encode_kernel(u64* __restrict__ out, long long os, const double* __restrict__ vals, int vlen,
                               long long vs, double scale, int logn, Limbs limbs, const PrimeInfo* __restrict__ pr,
-                              FftTab ft, int add_err, u64 seed, u64 id_base, const u64* __restrict__ id_dev) {
+                              FftTab ft, int add_err, u64 seed, u64 id_base, const u64* __restrict__ id_dev,
+                              i64* __restrict__ raw) {
     extern __shared__ double fsm[];
     const int N = 1 << logn, S = N >> 1, M = N << 1, logs = logn - 1;
     if (id_dev) id_base = *id_dev;   // graph replays: the encryption counter lives in device memory
@@ -52,6 +53,11 @@ __global__ void encode_kernel(u64* __restrict__ out, long long os, const double*
         const double wr = __dmul_rn(xr[src], invS), wi = __dmul_rn(xi[src], invS);
         i64 cr = (i64)rint(__dmul_rn(wr, scale));
         i64 ci = (i64)rint(__dmul_rn(wi, scale));
+        if (raw) {                                   // the integer coefficients only (encode_rot_kernel finishes)
+            raw[(long long)p * N + i] = cr;
+            raw[(long long)p * N + i + S] = ci;
+            continue;
+        }
         if (add_err) {
             cr += cbd21(draw(seed, 2u /*DOM_ENC_E*/, 0u, id_base + p, (u32)i));
             ci += cbd21(draw(seed, 2u, 0u, id_base + p, (u32)(i + S)));
@@ -66,7 +72,7 @@ __global__ void encode_kernel(u64* __restrict__ out, long long os, const double*
 
 cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long long vs, int nplain, double scale,
                       int logn, const Limbs& limbs, const PrimeInfo* pr, const FftTab& ft, int add_err, u64 seed,
-                      u64 id_base, cudaStream_t st, const u64* id_dev) {
+                      u64 id_base, cudaStream_t st, const u64* id_dev, i64* raw) {
     if (!nplain) return cudaSuccess;
     const int N = 1 << logn;
     const size_t smem = (size_t)N * sizeof(double);
@@ -80,7 +86,47 @@ cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long
     }
     int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
     encode_kernel<<<nplain, tpb, smem, st>>>(out, os, vals, vlen, vs, scale, logn, limbs, pr, ft, add_err, seed,
-                                             id_base, id_dev);
+                                             id_base, id_dev, raw);
+    return launched();
+}
+
+// Fresh encryptions of rotated copies of the same plaintexts: the plaintext of rot_r(x) is the
+// automorphism X -> X^g (g = 5^r) of the plaintext of x, an exact signed permutation of its integer
+// coefficients -- out[i] = +-m[i g^-1 mod 2N] -- so the canonical embedding runs once per plaintext and
+// each copy adds its own fresh error and reduces:
+//   out[(c G + p)][t][i] = (sigma_gc(m_p)[i] + e_{id + c G + p}[i]) mod q_t     (coefficient domain)
+struct RotCopies {
+    int n;
+    u32 ginv[32];                      // g^-1 mod 2N per copy (1: the plaintext itself)
+};
+__global__ void __launch_bounds__(256) encode_rot_kernel(u64* __restrict__ out, long long os,
+                                                         const i64* __restrict__ raw, int G, int logn, Limbs limbs,
+                                                         const PrimeInfo* __restrict__ pr, RotCopies rc, u64 seed,
+                                                         u64 id_base) {
+    const int N = 1 << logn;
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= N) return;
+    const int c = blockIdx.y, p = blockIdx.z;
+    const u32 j = ((u32)i * rc.ginv[c]) & (u32)(2 * N - 1);
+    const i64 m = j < (u32)N ? raw[(long long)p * N + j] : -raw[(long long)p * N + (j - N)];
+    const long long row = (long long)c * G + p;
+    const i64 v = m + cbd21(draw(seed, 2u /*DOM_ENC_E*/, 0u, id_base + (u64)row, (u32)i));
+    u64* o = out + row * os + i;
+    for (int t = 0; t < limbs.n; t++) {
+        const PrimeInfo& P = pr[limbs.prime[t]];
+        o[(long long)t * N] = signed_to_residue_fast(v, P.q, P.pad[2]);
+    }
+}
+
+cudaError_t encode_rot_op(u64* out, long long os, const i64* raw, int G, int logn, const Limbs& limbs,
+                          const PrimeInfo* pr, int n_copies, const u32* ginv, u64 seed, u64 id_base, cudaStream_t st) {
+    if (n_copies < 1 || n_copies > 32 || G > 65535) return cudaErrorInvalidValue;
+    RotCopies rc;
+    rc.n = n_copies;
+    for (int c = 0; c < n_copies; c++) rc.ginv[c] = ginv[c];
+    const int N = 1 << logn;
+    dim3 grid((N + 255) / 256, n_copies, G);
+    encode_rot_kernel<<<grid, 256, 0, st>>>(out, os, raw, G, logn, limbs, pr, rc, seed, id_base);
     return launched();
 }
 

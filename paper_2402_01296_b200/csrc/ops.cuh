@@ -250,7 +250,10 @@ struct FftTab {
 };
 cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long long vs, int nplain, double scale,
                       int logn, const Limbs& limbs, const PrimeInfo* pr, const FftTab& ft, int add_err, u64 seed,
-                      u64 id_base, cudaStream_t st, const u64* id_dev = nullptr);
+                      u64 id_base, cudaStream_t st, const u64* id_dev = nullptr, i64* raw = nullptr);
+// rotated fresh copies from the integer coefficients `raw` [G][N] (encode_op(..., raw)): see encode.cu
+cudaError_t encode_rot_op(u64* out, long long os, const i64* raw, int G, int logn, const Limbs& limbs,
+                          const PrimeInfo* pr, int n_copies, const u32* ginv, u64 seed, u64 id_base, cudaStream_t st);
 cudaError_t decode_op(double* out, int nout, const u64* poly, long long ps, int k, int npoly, double scale, int logn,
                       const PrimeInfo* pr, const FftTab& ft, u64 q0inv_mod_q1, u64 q0inv_p, cudaStream_t st);
 cudaError_t sample_uniform_op(u64* out, long long os, int npoly, int nlimb, int logn, const Limbs& limbs,

@@ -160,6 +160,29 @@ class Engine:
                   _ptr(ct), _stream())
         return ct
 
+    def encrypt_rotated(self, vals, rots, level: int | None = None, scale: float | None = None,
+                        counter: int | None = None) -> torch.Tensor:
+        """Fresh encryptions of every row and of its rotations by `rots` slots
+        (np.roll(row, -r)): (1 + len(rots), G, 2, level+1, N).  The plaintext
+        of a rotated row is the automorphism X -> X^(5^r) of the row's plaintext,
+        so the canonical embedding runs once per row (bcn_encrypt_rotated); copy
+        c of row p uses encryption id counter + c G + p, like encrypt() of the
+        stacked rolled rows."""
+        from .params import galois_element
+        level = self.L if level is None else level
+        scale = self.params.scale if scale is None else scale
+        self._check_mag(vals, scale)
+        v = self._dev_f64(vals)
+        if v.shape[1] > self.N // 2:
+            raise CapacityError(f"vector of length {v.shape[1]} exceeds {self.N // 2} slots")
+        G, ncopy = v.shape[0], 1 + len(rots)
+        gal = (ctypes.c_uint64 * ncopy)(1, *[galois_element(int(r), self.N) for r in rots])
+        ct = self.empty_ct(ncopy * G, level)
+        counter = self.next_counter(ncopy * G) if counter is None else counter
+        _lib.call("bcn_encrypt_rotated", self._h, _ptr(v), v.shape[1], v.shape[1], G, level, float(scale), counter,
+                  ncopy, gal, _ptr(ct), _stream())
+        return ct.view(ncopy, G, 2, level + 1, self.N)
+
     def decrypt(self, ct: torch.Tensor, level: int, scale: float, nout: int | None = None) -> torch.Tensor:
         G, two, nl, N = ct.shape
         nout = self.N // 2 if nout is None else nout

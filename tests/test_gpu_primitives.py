@@ -120,6 +120,28 @@ def _enc2(eng, orc, N, rng, counter=5):
     return v, ct, oc
 
 
+@pytest.mark.parametrize("N,L,level", [(1024, 3, 3), (8192, 4, 2), (16384, 4, 4)])
+def test_encrypt_rotated_matches_oracle(N, L, level):
+    """bcn_encrypt_rotated: every copy is the fresh encryption (its own id) of
+    the automorphism of the row's plaintext -- bit-identical to the oracle's
+    restatement, decrypting to np.roll(row, -r); the unrotated copy equals
+    encrypt().  N >= 8192 runs the NTT with the fused encryption epilogue."""
+    eng, orc, hp = _pair(N, L, 50 if N >= 8192 else 40, dnum=2)
+    rng = np.random.default_rng(71)
+    G, rots = 3, [1, 5, N // 2 - 3]
+    v = rng.standard_normal((G, N // 2))
+    cts = eng.encrypt_rotated(v, rots, level, counter=900)
+    assert tuple(cts.shape) == (1 + len(rots), G, 2, level + 1, N)
+    base = eng.encrypt(v, level, counter=900)
+    assert torch.equal(cts[0], base)
+    for c, r in enumerate([0] + rots):
+        want = [orc.encrypt_rotated(v[g], r, 900 + c * G + g, level) if r else orc.encrypt(v[g], 900 + g, level)
+                for g in range(G)]
+        _assert_ct(cts[c], want)
+        dec = eng.decrypt(cts[c], level, hp.scale).cpu().numpy()
+        assert np.abs(dec - np.roll(v, -r, axis=1)).max() < 1e-6
+
+
 def test_add_mulplain_rescale_match():
     N = 512
     eng, orc, hp = _pair(N, 4)
