@@ -427,7 +427,8 @@ def ntt_roofline(ntt_step: dict, peak: float, peak_kind: str) -> dict:
            for k, v in ntt_step.items()}
     return {
         "kernel": "NTT/INTT family (ntt_fwd_cluster<14,*>, ntt_inv_cluster<14>): every launch of one cifar3 "
-                  "forward step (4096 images), byte-weighted",
+                  "forward step (4096 images), byte-weighted; class encrypt_fwd is the encryption's forward NTT "
+                  "with c0 = NTT(m+e) - a s and c1 = a (Philox) computed in its epilogue",
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "peak_kind": peak_kind, "traffic": _traffic().get("ntt14_fwd"),
         "algorithmic_bytes_per_step": tot_b, "ntt_ms_per_step": tot_ms,

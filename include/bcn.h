@@ -79,9 +79,10 @@ int bcn_ntt_inv(bcn_ctx *ctx, uint64_t *data, int npoly, int nlimb, int prime0, 
 /* Measurement only (bench.py roofline): while enabled, every NTT/INTT launch
  * of every context is bracketed by a CUDA event pair on its stream.
  * bcn_ntt_timing(1) clears and starts recording, (0) stops.
- * bcn_ntt_timing_read syncs and fills 4 classes {plain fwd, plain inv,
- * fused fwd, fused inv}: summed launch ms, algorithmic bytes (16 B per
- * coefficient) and launch counts.  Never used inside a CUDA-graph capture. */
+ * bcn_ntt_timing_read syncs and fills 5 classes {plain fwd, plain inv,
+ * fused fwd, fused inv, encryption NTT with the combine in its epilogue}:
+ * summed launch ms, algorithmic bytes (16 B per coefficient + fused operands)
+ * and launch counts.  Never used inside a CUDA-graph capture. */
 int bcn_ntt_timing(int enable);
 int bcn_ntt_timing_read(double *ms, uint64_t *bytes, uint64_t *launches);
 /* The same for the conv operand path (bcn_conv_ks_mac / bcn_mac_multi_planes*):

@@ -149,7 +149,7 @@ def launch_count() -> int:
     return int(v.value)
 
 
-NTT_CLASSES = ("plain_fwd", "plain_inv", "fused_fwd", "fused_inv")
+NTT_CLASSES = ("plain_fwd", "plain_inv", "fused_fwd", "fused_inv", "encrypt_fwd")
 
 
 def ntt_timing(enable: bool) -> None:
@@ -158,9 +158,9 @@ def ntt_timing(enable: bool) -> None:
 
 
 def ntt_timing_read() -> dict:
-    ms = (ctypes.c_double * 4)()
-    nb = (_U64 * 4)()
-    nl = (_U64 * 4)()
+    ms = (ctypes.c_double * 5)()
+    nb = (_U64 * 5)()
+    nl = (_U64 * 5)()
     call("bcn_ntt_timing_read", ms, nb, nl)
     return {c: {"ms": ms[i], "bytes": int(nb[i]), "launches": int(nl[i])} for i, c in enumerate(NTT_CLASSES)}
 

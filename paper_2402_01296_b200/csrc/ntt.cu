@@ -266,7 +266,8 @@ static cudaError_t ntt_launch_impl(bool inverse, int logn, const NttArgs& a, int
 // NTT launch on its own stream, so bench.py can report the byte-weighted
 // roofline fraction of all NTT launches of a real forward step.  Classes:
 // 0 plain forward, 1 plain inverse, 2 fused forward, 3 fused inverse
-// (fused = prologue / epilogue / out-of-place forms).  Algorithmic bytes:
+// (fused = prologue / epilogue / out-of-place forms), 4 the forward NTT of an
+// encryption with the combine c0 = v - a s, c1 = a in its epilogue (epilogue 5).  Algorithmic bytes:
 // ntt_algorithmic_bytes() below (16 B per coefficient plus the fused
 // operands); the 16-B-only count is kept alongside for comparison.
 struct NttTimer {
@@ -315,7 +316,7 @@ cudaError_t ntt_launch(bool inverse, int logn, const NttArgs& a, int nlimbs, int
     }
     const size_t i = T.used++;
     const bool fused = a.pro || a.epi || a.copy_src || a.inv_scale || a.src;
-    T.cls[i] = (fused ? 2 : 0) + (inverse ? 1 : 0);
+    T.cls[i] = a.epi == 5 ? 4 : (fused ? 2 : 0) + (inverse ? 1 : 0);
     T.bytes[i] = ntt_algorithmic_bytes(inverse, logn, a, nlimbs, npolys);
     cudaEventRecord(T.ev[2 * i], st);
     cudaError_t e = ntt_launch_impl(inverse, logn, a, nlimbs, npolys, st);
@@ -333,7 +334,7 @@ extern "C" int bcn_ntt_timing(int enable) {
 
 extern "C" int bcn_ntt_timing_read(double* ms, uint64_t* bytes, uint64_t* launches) {
     bcn::NttTimer& T = bcn::g_ntt_timer;
-    for (int k = 0; k < 4; k++) { ms[k] = 0.0; bytes[k] = 0; launches[k] = 0; }
+    for (int k = 0; k < 5; k++) { ms[k] = 0.0; bytes[k] = 0; launches[k] = 0; }
     for (size_t i = 0; i < T.used; i++) {
         if (cudaEventSynchronize(T.ev[2 * i + 1]) != cudaSuccess) return 4;
         float t = 0.f;
