@@ -50,6 +50,13 @@ int bcn_version(void);
 /* number of kernels this library has launched in the process (bench evidence) */
 int bcn_launch_count(uint64_t *out);
 
+/* ---- plaintext branch (layers.py:329-346 conv_forward on clear tensors): float64
+ * conv2d over the whole batch, direct form.  x f64[B][C][H][W], w f64[O][C][kh][kw],
+ * bias f64[O] or NULL, out f64[B][O][OH][OW], OH = (H + 2 ph - kh) / sh + 1.
+ * Sums in (c, di, dj) order with FMAs (float64 rounding only). */
+int bcn_plain_conv2d(const double *x, const double *w, const double *bias, double *out, int B, int C, int H, int W,
+                     int O, int kh, int kw, int sh, int sw, int ph, int pw, void *stream);
+
 /* make_context (sim.py:142-169): ring degree N = 2^logn (8 <= N <= 16384),
  * ciphertext primes q[0..max_level], special primes p[0..n_special-1],
  * dnum key-switching digits, Philox seed for sk / keys / encryption. */

@@ -37,6 +37,7 @@ _D = ctypes.c_double
 # name -> argtypes (all return int)
 SIGNATURES = {
     "bcn_launch_count": [ctypes.POINTER(_U64)],
+    "bcn_plain_conv2d": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "bcn_ctx_create": [ctypes.POINTER(_P), _I, _I, ctypes.POINTER(_U64), _I, ctypes.POINTER(_U64), _I, _U64, _I],
     "bcn_ctx_set_fft": [_P, ctypes.POINTER(_D), ctypes.POINTER(_D)],
     "bcn_ctx_destroy": [_P],

@@ -459,6 +459,16 @@ extern "C" {
 const char* bcn_last_error(void) { return g_err.c_str(); }
 int bcn_version(void) { return 1; }
 
+int bcn_plain_conv2d(const double* x, const double* w, const double* bias, double* out, int B, int C, int H, int W,
+                     int O, int kh, int kw, int sh, int sw, int ph, int pw, void* stream) {
+    if (B < 1 || C < 1 || O < 1 || kh < 1 || kw < 1 || sh < 1 || sw < 1 || ph < 0 || pw < 0)
+        return fail(BCN_ERR_PARAM, "bad conv2d shape");
+    if ((size_t)C * kh * kw * 16 * sizeof(double) > 48 * 1024)
+        return fail(BCN_ERR_CAPACITY, "conv2d weights exceed the shared-memory tile (C kh kw <= 384)");
+    CUDA_TRY(plain_conv_op(x, w, bias, out, B, C, H, W, O, kh, kw, sh, sw, ph, pw, (cudaStream_t)stream));
+    return BCN_OK;
+}
+
 int bcn_launch_count(uint64_t* out) {
     *out = g_launches.load(std::memory_order_relaxed);
     return BCN_OK;

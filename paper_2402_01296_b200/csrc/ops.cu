@@ -703,6 +703,65 @@ cudaError_t inner_op(u64* A, const u64* U, int npoly, int next, int ndig, int lo
     return launched();
 }
 
+// ---------------------------------------------------------------- plaintext-branch conv (float64)
+// The plaintext branch's 3x3 convolutions (layers.py:329-346) over the whole batch: cuDNN's float64
+// implicit-GEMM takes 2.5-3.1 ms per layer for 4,096 32x32 images; the direct form -- a thread per
+// output pixel with all (<= 32) output channels in registers, the weights in shared memory -- is
+// bound by the 0.5 GB it writes.  x [B][C][H][W], w [O][C][kh][kw], out [B][O][OH][OW].
+template <int OB>
+__global__ void __launch_bounds__(128) plain_conv_kernel(const double* __restrict__ x, const double* __restrict__ w,
+                                                         const double* __restrict__ b, double* __restrict__ out,
+                                                         int B, int C, int H, int W, int O, int kh, int kw, int sh,
+                                                         int sw, int ph, int pw, int OH, int OW) {
+    extern __shared__ double wsm[];                         // [C kh kw][OB] of this output block
+    const int o0 = blockIdx.y * OB;
+    const int K = C * kh * kw;
+    for (int i = threadIdx.x; i < K * OB; i += blockDim.x) {
+        const int k = i / OB, o = i - k * OB;
+        wsm[i] = o0 + o < O ? w[(long long)(o0 + o) * K + k] : 0.0;
+    }
+    __syncthreads();
+    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long npix = (long long)B * OH * OW;
+    if (pix >= npix) return;
+    const int ow = (int)(pix % OW), oh = (int)((pix / OW) % OH);
+    const long long bi = pix / ((long long)OW * OH);
+    double acc[OB];
+#pragma unroll
+    for (int o = 0; o < OB; o++) acc[o] = (b && o0 + o < O) ? b[o0 + o] : 0.0;
+    const double* xb = x + bi * C * H * W;
+    for (int c = 0; c < C; c++)
+        for (int di = 0; di < kh; di++) {
+            const int ih = oh * sh - ph + di;
+            if (ih < 0 || ih >= H) continue;
+            for (int dj = 0; dj < kw; dj++) {
+                const int iw = ow * sw - pw + dj;
+                if (iw < 0 || iw >= W) continue;
+                const double v = __ldg(xb + ((long long)c * H + ih) * W + iw);
+                const double* wk = wsm + ((c * kh + di) * kw + dj) * OB;
+#pragma unroll
+                for (int o = 0; o < OB; o++) acc[o] = __fma_rn(v, wk[o], acc[o]);
+            }
+        }
+    double* ob = out + (bi * O + o0) * OH * OW + (long long)oh * OW + ow;
+#pragma unroll
+    for (int o = 0; o < OB; o++)
+        if (o0 + o < O) ob[(long long)o * OH * OW] = acc[o];
+}
+
+cudaError_t plain_conv_op(const double* x, const double* w, const double* b, double* out, int B, int C, int H, int W,
+                          int O, int kh, int kw, int sh, int sw, int ph, int pw, cudaStream_t st) {
+    const int OH = (H + 2 * ph - kh) / sh + 1, OW = (W + 2 * pw - kw) / sw + 1;
+    if (OH <= 0 || OW <= 0 || B <= 0) return cudaErrorInvalidValue;
+    constexpr int OB = 16;
+    const size_t smem = (size_t)C * kh * kw * OB * sizeof(double);
+    if (smem > 48 * 1024) return cudaErrorInvalidValue;
+    const long long npix = (long long)B * OH * OW;
+    dim3 grid((unsigned)((npix + 127) / 128), (O + OB - 1) / OB);
+    plain_conv_kernel<OB><<<grid, 128, smem, st>>>(x, w, b, out, B, C, H, W, O, kh, kw, sh, sw, ph, pw, OH, OW);
+    return launched();
+}
+
 // ------------------------------- lazy-ModDown rotation sum (K7 + K4 + K8)
 // For every output word (g, ext limb t, n) and every term k:
 //   a_c = REDC( sum_j sigma_gk(U_k,j)[n] * key_k[j][c][t][n] )      (c = 0, 1)

@@ -162,6 +162,9 @@ cudaError_t rotsum_op(u64* B, u64* C0, const RotTerms& terms, long long c0_gstri
                       int ndig, int logn, long long key_digit_stride, long long key_comp_stride, const Limbs& ext,
                       const PrimeInfo* pr, int accumulate, cudaStream_t st, long long c0_ostride = -1,
                       int c0_accumulate = -1, const double2* fq = nullptr);
+// plaintext-branch conv2d in float64 (direct form), x [B][C][H][W], w [O][C][kh][kw], out [B][O][OH][OW]
+cudaError_t plain_conv_op(const double* x, const double* w, const double* b, double* out, int B, int C, int H, int W,
+                          int O, int kh, int kw, int sh, int sw, int ph, int pw, cudaStream_t st);
 // dst[p][n] = dst[p][n] + src[p][n] * w (mod q) on one limb (Shoup pair w, wp)
 cudaError_t axpy_limb_op(u64* dst, long long ds, const u64* src, long long ss, int npoly, u64 w, u64 wp, u64 q,
                          int logn, cudaStream_t st);

@@ -10,6 +10,8 @@ rounding (summation order only).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 import torch.nn.functional as F
@@ -68,6 +70,22 @@ def to_device(x, device) -> torch.Tensor:
 def conv(x: torch.Tensor, w: torch.Tensor, b, stride, padding) -> torch.Tensor:
     if x.shape[1] != w.shape[1]:
         raise ShapeError(f"conv expects {w.shape[1]} input channels, got {x.shape[1]}")
+    O, C, kh, kw = w.shape
+    if (x.is_cuda and x.dtype == torch.float64 and x.dim() == 4 and C * kh * kw <= 384
+            and os.environ.get("BCN_PLAIN_CONV", "1") != "0"):
+        # libbcn's direct float64 conv (cuDNN's implicit-GEMM dgemm: 2.5-3.1 ms per cifar3 layer at 4,096
+        # images; this: bound by its output write)
+        from . import _lib
+        B, _, H, W = x.shape
+        (sh, sw), (ph, pw) = tuple(stride), tuple(padding)
+        oh, ow = (H + 2 * ph - kh) // sh + 1, (W + 2 * pw - kw) // sw + 1
+        xc, wc = x.contiguous(), w.contiguous()
+        bc = b.contiguous() if b is not None else None
+        out = torch.empty((B, O, oh, ow), dtype=torch.float64, device=x.device)
+        _lib.call("bcn_plain_conv2d", xc.data_ptr(), wc.data_ptr(), bc.data_ptr() if bc is not None else None,
+                  out.data_ptr(), B, C, H, W, O, kh, kw, sh, sw, ph, pw,
+                  torch.cuda.current_stream(x.device).cuda_stream)
+        return out
     return F.conv2d(x, w, b, stride=tuple(stride), padding=tuple(padding))
 
 

@@ -142,6 +142,26 @@ def test_encrypt_rotated_matches_oracle(N, L, level):
         assert np.abs(dec - np.roll(v, -r, axis=1)).max() < 1e-6
 
 
+@pytest.mark.parametrize("C,O,H,stride", [(3, 16, 32, 1), (16, 32, 32, 2), (1, 5, 28, 2), (5, 37, 9, 1)])
+def test_plain_conv2d_matches_torch(C, O, H, stride, monkeypatch):
+    """libbcn's direct float64 conv of the plaintext branch against cuDNN's
+    (summation order differs: float64 rounding only), with and without bias,
+    odd sizes and more than one 16-output block."""
+    from paper_2402_01296_b200 import plainbranch as PB
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn((7, C, H, H + 3), dtype=torch.float64, device="cuda", generator=g)
+    k = 5 if C == 1 else 3
+    w = torch.randn((O, C, k, k), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(O, dtype=torch.float64, device="cuda", generator=g)
+    for bias in (b, None):
+        got = PB.conv(x, w, bias, (stride, stride), (1, 1))
+        monkeypatch.setenv("BCN_PLAIN_CONV", "0")
+        want = PB.conv(x, w, bias, (stride, stride), (1, 1))
+        monkeypatch.delenv("BCN_PLAIN_CONV")
+        assert got.shape == want.shape
+        assert (got - want).abs().max().item() < 1e-12 * max(1.0, want.abs().max().item())
+
+
 def test_add_mulplain_rescale_match():
     N = 512
     eng, orc, hp = _pair(N, 4)
