@@ -205,9 +205,12 @@ class Engine:
                   _stream())
         return out
 
-    def add_plain(self, a: torch.Tensor, pt: torch.Tensor, level: int) -> torch.Tensor:
+    def add_plain(self, a: torch.Tensor, pt: torch.Tensor, level: int, inplace: bool = False) -> torch.Tensor:
+        """a + pt on component 0.  inplace (the caller owns `a`, which has exactly
+        level+1 limbs): component 0 is updated where it lies and component 1 is
+        not copied."""
         G = a.shape[0]
-        out = self.empty_ct(G, level)
+        out = a if inplace and a.shape[2] == level + 1 and a.is_contiguous() else self.empty_ct(G, level)
         _lib.call("bcn_add", self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(pt), pt.shape[1], 1, pt.shape[0], G,
                   level, _stream())
         return out

@@ -474,7 +474,11 @@ def _batch_of(a: Ciphertext, b: Ciphertext) -> None:
         raise UsageError(f"ciphertext batches differ ({a.batch} vs {b.batch})")
 
 
-def he_add_plain_many(cts: list, vecs, rec: OpRecorder) -> list:
+def _inplace_adds() -> bool:
+    return os.environ.get("BCN_INPLACE_ADD", "1") != "0"
+
+
+def he_add_plain_many(cts: list, vecs, rec: OpRecorder, *, consume: bool = False) -> list:
     """[he_add(ct_c, vecs[c])] (one Add_PC per channel, sim.py:208-218) with all
     channels' input-dependent plaintexts encoded by ONE batched launch when
     the ciphertexts share level and scale (vecs: (C, G, S) slots)."""
@@ -486,7 +490,7 @@ def he_add_plain_many(cts: list, vecs, rec: OpRecorder) -> list:
     same = isinstance(vecs, torch.Tensor) and all(c.level == cts[0].level and c.scale == cts[0].scale
                                                  and c.batch == cts[0].batch for c in cts)
     if not same or len(cts) == 1:
-        return [he_add(ct, vecs[c], rec) for c, ct in enumerate(cts)]
+        return [he_add(ct, vecs[c], rec, consume=consume) for c, ct in enumerate(cts)]
     ctx, lvl, G = cts[0].ctx, cts[0].level, cts[0].batch
     if tuple(vecs.shape[:2]) != (len(cts), G):
         raise UsageError(f"plain batch {tuple(vecs.shape[:2])} does not match ({len(cts)}, {G})")
@@ -495,7 +499,11 @@ def he_add_plain_many(cts: list, vecs, rec: OpRecorder) -> list:
     out = []
     for c, ct in enumerate(cts):
         rec.bump("Add_PC")
-        out.append(Ciphertext(ctx.engine.add_plain(ct._data, pts[c * G:(c + 1) * G], lvl), lvl, ct.scale, ctx))
+        if consume and _inplace_adds() and ct._data.shape[2] == lvl + 1 and not ct._rot:
+            data = ctx.engine.add_plain(_consume(ct), pts[c * G:(c + 1) * G], lvl, inplace=True)
+        else:
+            data = ctx.engine.add_plain(ct._data, pts[c * G:(c + 1) * G], lvl)
+        out.append(Ciphertext(data, lvl, ct.scale, ctx))
     return out
 
 
@@ -586,8 +594,21 @@ def _planes_for(ctx: HeContext, pts: list, level: int, ext: bool = False, layout
     return planes
 
 
-def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
-    """Add_CC (level = min) or Add_PC (level kept), sim.py:208-218."""
+def _consume(a: Ciphertext):
+    """Take over a's buffer for an in-place update: `a` itself becomes unusable
+    (any later read raises instead of seeing the modified words)."""
+    d = a._data
+    object.__setattr__(a, "_data", None)
+    object.__setattr__(a, "_terms", None)
+    object.__setattr__(a, "_modup", None)
+    return d
+
+
+def he_add(a: Ciphertext, b, rec: OpRecorder, *, consume: bool = False) -> Ciphertext:
+    """Add_CC (level = min) or Add_PC (level kept), sim.py:208-218.
+    consume (engine-internal, Add_PC only): the caller drops `a` -- a fresh
+    layer output nothing else references -- so the sum is written into a's own
+    buffer (no copy of component 1, no second ciphertext in HBM)."""
     ctx = a.ctx
     eng = ctx.engine
     if _same_ctx(a, b):
@@ -611,6 +632,8 @@ def he_add(a: Ciphertext, b, rec: OpRecorder) -> Ciphertext:
     rec.bump("Add_PC")
     a.materialize()       # a lazy sum's scale Delta*q_l would overflow a 64-bit encoding
     pt = _encode(ctx, b, a.level, a.scale, False, a.batch)
+    if consume and _inplace_adds() and a._data.shape[2] == a.level + 1 and not a._rot:
+        return Ciphertext(eng.add_plain(_consume(a), pt, a.level, inplace=True), a.level, a.scale, ctx)
     return Ciphertext(eng.add_plain(a._data, pt, a.level), a.level, a.scale, ctx)
 
 
