@@ -117,7 +117,7 @@ def ntt14(steps=10, warmup=3, npoly=128, limbs=12):
     return res
 
 
-def config3(steps=3, warmup=1, n_ct=1024, N=16384, limbs=8, batch=128):
+def config3(steps=3, warmup=1, n_ct=1024, N=16384, limbs=8, batch=128, many=True):
     """Keyswitch microbench, processed in batches of `batch` ciphertexts."""
     hp = make_params(N, limbs - 1, 50, dnum=2, n_special=1)
     eng = Engine(hp)
@@ -141,8 +141,11 @@ def config3(steps=3, warmup=1, n_ct=1024, N=16384, limbs=8, batch=128):
         for b0 in range(0, n_ct, batch):
             x = sq[b0:b0 + batch]
             U = eng.modup(x, L)
-            for i, r in enumerate(rots):
-                eng.rotate(x, r, L, U=U, out=outs[i])
+            if many:
+                eng.rotate_many(x, rots, L, U=U, out=outs)
+            else:
+                for i, r in enumerate(rots):
+                    eng.rotate(x, r, L, U=U, out=outs[i])
 
     a_ms = time_region(stage_a, steps, warmup)
     b_ms = time_region(stage_b, steps, warmup)

@@ -268,6 +268,11 @@ int bcn_rotate_hoisted(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_n
                        int level, uint64_t g, void *stream);
 int bcn_rotate(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb, int G, int level, uint64_t g,
                void *stream);
+/* n_rot hoisted rotations of one source (the baby steps of fc_forward_multi, layers.py:283-330, and
+ * BASELINE config 3's 14 rotations): out u64[n_rot][G][2][level+1][N], gal[k] = 5^r_k mod 2N.  Bit-identical to
+ * n_rot bcn_rotate_hoisted calls; the source's U digits are read once for all rotations. */
+int bcn_rotate_hoisted_many(bcn_ctx *ctx, uint64_t *out, const uint64_t *ct, int ct_nlimb, const uint64_t *U, int G,
+                            int level, int n_rot, const uint64_t *gal, void *stream);
 
 /* ---- switching keys (generated on device from the seed, cached) */
 int bcn_keygen_relin(bcn_ctx *ctx, void *stream);

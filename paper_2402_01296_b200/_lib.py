@@ -88,6 +88,7 @@ SIGNATURES = {
     "bcn_modup": [_P, _P, _P, _I, _I, _I, _P],
     "bcn_rotate_hoisted": [_P, _P, _P, _I, _P, _I, _I, _U64, _P],
     "bcn_rotate": [_P, _P, _P, _I, _I, _I, _U64, _P],
+    "bcn_rotate_hoisted_many": [_P, _P, _P, _I, _P, _I, _I, _I, ctypes.POINTER(_U64), _P],
     "bcn_keygen_relin": [_P, _P],
     "bcn_keygen_galois": [_P, _U64, _P],
     "bcn_export_key": [_P, _U64, _P, _P],

@@ -1867,6 +1867,63 @@ int bcn_rotate_hoisted(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nli
                           2LL * ct_nlimb * N, 0, tmp, st);
 }
 
+// n_rot hoisted rotations of ONE source: out u64[n_rot][G][2][level+1][N].  Source-shared form: one FP64 kernel
+// computes every rotation's key-switch inner products over all level+1+K limbs with the source's U digits (and
+// P c0) in registers across <= 16 rotations (mac_imma.cu, slot_major_ks3's natural-layout mode), so U crosses L2
+// once instead of once per rotation; the ModDown of ALL rotations is then one INTT launch and one NTT launch
+// with the combine epilogue (ModDown(B + P sigma(c0)) = ModDown(B) + sigma(c0) exactly).
+int bcn_rotate_hoisted_many(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, const uint64_t* U, int G,
+                            int level, int n_rot, const uint64_t* gal, void* stream) {
+    int e = check_level(c, level);
+    if (e) return e;
+    if (n_rot < 1) return fail(BCN_ERR_PARAM, "no rotations");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long N = c->N;
+    const int nl = level + 1, next = nl + c->K;
+    LevelTables* T;
+    e = build_level(c, level, &T);
+    if (e) return e;
+    bool shared = c->fp_conv && (c->logn == 13 || c->logn == 14) && T->ndig <= 3 && ct_nlimb == nl &&
+                  !getenv_flag_off("BCN_ROT_MANY") && !getenv_flag_off("BCN_FUSED_MODDOWN");
+    for (int k = 0; k < n_rot; k++) {
+        if ((gal[k] & 1) == 0) return fail(BCN_ERR_PARAM, "Galois elements are odd");
+        if (gal[k] == 1) shared = false;
+    }
+    const size_t ow = (size_t)G * 2 * nl * N;
+    if (!shared) {
+        for (int k = 0; k < n_rot; k++) {
+            e = bcn_rotate_hoisted(c, out + k * ow, ct, ct_nlimb, U, G, level, gal[k], stream);
+            if (e) return e;
+        }
+        return BCN_OK;
+    }
+    for (int k = 0; k < n_rot; k++)
+        if (!key_ptr(c, gal[k])) {
+            e = bcn_keygen_galois(c, gal[k], stream);
+            if (e) return e;
+        }
+    const int chunk = std::min(n_rot, 16);
+    int err = 0;
+    u64* A = scratch_get(c, tail_words(c, chunk * G, level), &err);   // [chunk][G][2][next][N] (+ Z)
+    if (!A) return err;
+    u64* Z = A + (size_t)chunk * G * 2 * next * N;
+    for (int k0 = 0; k0 < n_rot; k0 += chunk) {
+        KsTerms KT;
+        KT.n = std::min(chunk, n_rot - k0);
+        for (int k = 0; k < KT.n; k++) {
+            KT.src[k] = (const u64*)ct;
+            KT.U[k] = (const u64*)U;
+            KT.key[k] = key_ptr(c, gal[k0 + k]);
+            KT.g[k] = (u32)gal[k0 + k];
+        }
+        CUDA_TRY(ks_inner_multi_op(A, KT, G, nl, next, T->ndig, c->logn, 2LL * c->nbasis * N,
+                                   (long long)c->nbasis * N, limbs_ext(c, level), c->pr, c->pmod, c->fq, st));
+        e = moddown_tail(c, (u64*)out + k0 * ow, 2LL * nl * N, A, KT.n * G, level, nullptr, 0, 0, 1u, T, Z, st);
+        if (e) return e;
+    }
+    return BCN_OK;
+}
+
 int bcn_rotate(bcn_ctx* c, uint64_t* out, const uint64_t* ct, int ct_nlimb, int G, int level, uint64_t g,
                void* stream) {
     int e = check_level(c, level);

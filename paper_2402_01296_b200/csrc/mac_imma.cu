@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256, 3)
     slot_major_ks3_kernel(u64* __restrict__ S, const KsTerms T, const KsGroups GR, int g0, int gcnt, int nsplit, int t0,
                           int nq, int next, int logn, int spitch, long long kds, long long kcs, Limbs ext,
                           const PrimeInfo* __restrict__ pr, const u64* __restrict__ pmod,
-                          const double2* __restrict__ fq) {
+                          const double2* __restrict__ fq, int nat_gtot) {
     extern __shared__ __align__(16) unsigned char ks3_smem[];
     double(*kfp)[ND][4][32] = reinterpret_cast<double(*)[ND][4][32]>(ks3_smem);          // [16 terms]: kd, kq, kd1, kq1
     u64(*tiles)[32][KS3_TP] = reinterpret_cast<u64(*)[32][KS3_TP]>(ks3_smem + (size_t)16 * ND * 4 * 256);   // [8 warps]
@@ -391,8 +391,8 @@ __global__ void __launch_bounds__(256, 3)
             for (int b = 0; b < 4; b++) {
                 const long long gs = gs0 + b < gcnt ? gs0 + b : 0;
                 const double a1 = qlimb ? fmm(fload(__ldg(c1p + gs * cstep)), pd, pq, f.x) : 0.0;
-                v0[b] = fstage<ND>(a0[b], stage_c, f.y, f.x);
-                v1[b] = fstage<ND>(a1, stage_c, f.y, f.x);
+                v0[b] = nat_gtot ? fcanon(a0[b], f.y, f.x) : fstage<ND>(a0[b], stage_c, f.y, f.x);
+                v1[b] = nat_gtot ? fcanon(a1, f.y, f.x) : fstage<ND>(a1, stage_c, f.y, f.x);
             }
         } else {
             double kd[ND], kq[ND], kd1[ND], kq1[ND];
@@ -411,9 +411,22 @@ __global__ void __launch_bounds__(256, 3)
                     acc = __dadd_rn(acc, fmm(ud[b][j], kd[j], kq[j], f.x));
                     acc1 = __dadd_rn(acc1, fmm(ud[b][j], kd1[j], kq1[j], f.x));
                 }
-                v0[b] = fstage<ND>(acc, stage_c, f.y, f.x);
-                v1[b] = fstage<ND>(acc1, stage_c, f.y, f.x);
+                v0[b] = nat_gtot ? fcanon(acc, f.y, f.x) : fstage<ND>(acc, stage_c, f.y, f.x);
+                v1[b] = nat_gtot ? fcanon(acc1, f.y, f.x) : fstage<ND>(acc1, stage_c, f.y, f.x);
             }
+        }
+        if (nat_gtot) {
+            // natural layout (hoisted multi-rotation key switch): out[term][slot set][component][limb][n],
+            // canonical residues; the lanes' n are a permutation of one aligned 32-block
+            const int n = nblk_s[r] + nrow;
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                if (gs0 + b >= gcnt) break;
+                u64* o = S + ((((long long)k * nat_gtot + g0 + gs0 + b) * 2) * next + t) * (long long)N + n;
+                o[0] = v0[b];
+                o[(long long)next * N] = v1[b];
+            }
+            continue;
         }
 #pragma unroll
         for (int b = 0; b < 4; b++) {
@@ -435,7 +448,8 @@ __global__ void __launch_bounds__(256, 3)
 template <int ND>
 static cudaError_t ks3_launch(u64* S, const KsTerms& T, const KsGroups& GR, int g0, int gcnt, int t0, int tcnt, int nq,
                               int next, int logn, int spitch, long long kds, long long kcs, const Limbs& ext,
-                              const PrimeInfo* pr, const u64* pmod, const double2* fq, cudaStream_t st) {
+                              const PrimeInfo* pr, const u64* pmod, const double2* fq, cudaStream_t st,
+                              int nat_gtot = 0) {
     const size_t smem = ks3_smem_bytes<ND>();
     static unsigned long long cfg = 0;
     unsigned long long bit = 0;
@@ -448,8 +462,32 @@ static cudaError_t ks3_launch(u64* S, const KsTerms& T, const KsGroups& GR, int 
     const int nsplit = (gcnt + 31) / 32;
     dim3 grid((1 << logn) / 32, tcnt * nsplit, GR.n);
     slot_major_ks3_kernel<ND><<<grid, 256, smem, st>>>(S, T, GR, g0, gcnt, nsplit, t0, nq, next, logn, spitch, kds, kcs,
-                                                       ext, pr, pmod, fq);
+                                                       ext, pr, pmod, fq, nat_gtot);
     return launched();
+}
+
+// B'_k = sum_j sigma_k(U_j) (x) key_k,j + [c = 0] P sigma_k(c0) for <= 16 rotations k of ONE source, written in
+// the natural layout out[k][G][2][next][N] (canonical): the source's U digits cross L2 once for all the rotations
+// (bcn_rotate_hoisted_many).  Every T.src / T.U must be the same source; G in blocks of 64.
+cudaError_t ks_inner_multi_op(u64* out, const KsTerms& T, int G, int nq, int next, int ndig, int logn, long long kds,
+                              long long kcs, const Limbs& ext, const PrimeInfo* pr, const u64* pmod,
+                              const double2* fq, cudaStream_t st) {
+    if (!fq || ndig < 1 || ndig > 3 || T.n < 1 || T.n > 16) return cudaErrorInvalidValue;
+    KsGroups GR;
+    GR.n = 1;
+    GR.start[0] = 0;
+    GR.count[0] = (unsigned char)T.n;
+    for (int g0 = 0; g0 < G; g0 += 64) {
+        const int gcnt = G - g0 < 64 ? G - g0 : 64;
+        cudaError_t e;
+        switch (ndig) {
+            case 1: e = ks3_launch<1>(out, T, GR, g0, gcnt, 0, next, nq, next, logn, 128, kds, kcs, ext, pr, pmod, fq, st, G); break;
+            case 2: e = ks3_launch<2>(out, T, GR, g0, gcnt, 0, next, nq, next, logn, 128, kds, kcs, ext, pr, pmod, fq, st, G); break;
+            default: e = ks3_launch<3>(out, T, GR, g0, gcnt, 0, next, nq, next, logn, 128, kds, kcs, ext, pr, pmod, fq, st, G);
+        }
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,

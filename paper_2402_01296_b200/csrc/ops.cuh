@@ -205,6 +205,10 @@ struct KsTerms {
 cudaError_t slot_major_ks_op(u64* S, const KsTerms& T, int g0, int gcnt, int t0, int tcnt, int nq, int next, int ndig,
                              int logn, int spitch, long long kds, long long kcs, const Limbs& ext, const PrimeInfo* pr,
                              const u64* pmod, cudaStream_t st, const double2* fq = nullptr);
+// <= 16 rotations of one source in the natural layout out[k][G][2][next][N] (mac_imma.cu, slot_major_ks3's other mode)
+cudaError_t ks_inner_multi_op(u64* out, const KsTerms& T, int G, int nq, int next, int ndig, int logn, long long kds,
+                              long long kcs, const Limbs& ext, const PrimeInfo* pr, const u64* pmod,
+                              const double2* fq, cudaStream_t st);
 // tcgen05 conv MAC (mac_umma.cu): planes in the strip layout, S with a 128-word pitch, gcnt <= 64
 cudaError_t pack_planes_umma_op(unsigned char* planes, const u64* const* pts_dev, int n_out, int n_terms, int opad,
                                 int nch, int nl, int logn, cudaStream_t st, const int* tlimbs_dev = nullptr);

@@ -259,6 +259,22 @@ class Engine:
                       _stream())
         return out
 
+    def rotate_many(self, a: torch.Tensor, rots, level: int, U: torch.Tensor | None = None,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+        """Hoisted rotations of one source by every r in `rots` (bcn_rotate_hoisted_many):
+        out[k] = rotate(a, rots[k]), bit-identical to separate calls; U = modup(a) is
+        read once for all of them."""
+        G = a.shape[0]
+        n = len(rots)
+        if out is None:
+            out = torch.empty((n, G, 2, level + 1, self.N), dtype=torch.int64, device=self.device)
+        if U is None:
+            U = self.modup(a, level)
+        gal = (ctypes.c_uint64 * n)(*[galois_element(r, self.N) for r in rots])
+        _lib.call("bcn_rotate_hoisted_many", self._h, _ptr(out), _ptr(a), a.shape[2], _ptr(U), G, level, n, gal,
+                  _stream())
+        return out
+
     def keygen_galois(self, g: int) -> None:
         _lib.call("bcn_keygen_galois", self._h, g, _stream())
 

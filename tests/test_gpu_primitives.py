@@ -708,6 +708,36 @@ def test_config3_relin_no_rescale_and_rotation_match_oracle():
         _assert_ct(eng.rotate(sq, r, L, U=U), [orc.rotate(o, r) for o in osq])
 
 
+@pytest.mark.parametrize("N,L,dnum,K,G,nrot", [(16384, 7, 2, 1, 3, 14), (8192, 5, 3, 2, 5, 18), (16384, 4, 3, 5, 66, 3)])
+def test_rotate_many_matches_oracle_and_single_rotations(N, L, dnum, K, G, nrot, monkeypatch):
+    """bcn_rotate_hoisted_many (source-shared inner products, one batched ModDown):
+    config 3's 14 rotations by +-2^k at its real shape (K = 1, dnum = 2), more than 16
+    rotations (two runs), ragged slot-set counts (G = 3, 5, 66: a partial warp quad and
+    a second block of 64), K = 2 / 5 special primes (the split base conversion) -- bit
+    for bit against one bcn_rotate_hoisted per rotation, against the oracle for the
+    first slot sets, and against the fallback (BCN_ROT_MANY=0)."""
+    hp = make_params(N, L, 50, dnum=dnum, n_special=K, seed=5)
+    op = O.make_params(N, L, 50, dnum=dnum, n_special=K, seed=5)
+    assert list(hp.q) == op.q and list(hp.p) == op.p and hp.K == K
+    eng, orc = Engine(hp), O.Oracle(op)
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal((G, N // 2)) * 0.5
+    ct = eng.encrypt(v, counter=21)
+    rots = [s * (1 << k) for k in range(7) for s in (1, -1)]
+    rots = (rots + [3, 5, 7, N // 2 - 1])[:nrot]
+    U = eng.modup(ct, L)
+    got = eng.rotate_many(ct, rots, L, U=U)
+    assert got.shape == (nrot, G, 2, L + 1, N)
+    for k, r in enumerate(rots):
+        assert torch.equal(got[k], eng.rotate(ct, r, L, U=U)), (k, r)
+    n_or = 2 if N == 16384 and nrot > 3 else 1
+    oc = [orc.encrypt(v[i], 21 + i) for i in range(n_or)]
+    for k in (0, nrot - 1):
+        _assert_ct(got[k][:n_or], [orc.rotate(o, rots[k]) for o in oc])
+    monkeypatch.setenv("BCN_ROT_MANY", "0")
+    assert torch.equal(got, eng.rotate_many(ct, rots, L, U=U))
+
+
 def test_encryption_ids_are_partitioned_by_rank(monkeypatch):
     """Every rank derives the same keys from the shared seed, so two ranks must
     never draw the same Philox encryption randomness: rank r's ids start at
