@@ -395,7 +395,9 @@ static int build_level(bcn_ctx* c, int level, LevelTables** out) {
         std::vector<u64> l1(2 * (level + 1));
         for (int i = 0; i <= level; i++) {
             l1[2 * i] = 0;
-            l1[2 * i + 1] = (u64)(((u128)1 << 64) / c->primes[i]);
+            // 0: one conditional subtraction reduces a residue of the (single) special prime mod q_i
+            l1[2 * i + 1] = (c->K == 1 && c->primes[c->nq] < 2 * c->primes[i] && !getenv_flag_off("BCN_LIFT_CSUB"))
+                                ? 0ull : (u64)(((u128)1 << 64) / c->primes[i]);
         }
         CUDA_TRY(dmalloc((void**)&T.lift1, sizeof(u64) * l1.size(), &c->table_bytes));
         CUDA_TRY(cudaMemcpy(T.lift1, l1.data(), sizeof(u64) * l1.size(), cudaMemcpyHostToDevice));

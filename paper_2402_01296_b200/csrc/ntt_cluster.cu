@@ -86,7 +86,7 @@ struct Prologue {             // MODE 0 plain, 1 rescale lift, 2 ModDown base co
             return src[j];
         } else if constexpr (MODE == 1) {
             const u64 v = src[j];                   // canonical mod qtop, centred lift -> mod q
-            u64 r = shoup(v, 1ull, inv_p, q);
+            u64 r = inv_p ? shoup(v, 1ull, inv_p, q) : csub(v, q);   // inv_p = 0: v < 2q (api.cu, lift1)
             if (v > (qtop >> 1)) r = sub_mod(r, qtop_mod_q, q);
             return r;
         } else {                                    // sum_k y_k[j] * [P/p_k]_q (Montgomery table)
@@ -159,6 +159,25 @@ struct Epilogue {             // MODE 0 store, 1 rescale combine (c - v) * q_top
             }
         }
     }
+    // modes 1-3 split into operand loads and arithmetic, so the caller can issue the loads of several
+    // outputs before the first store (c / add and out are not restrict: the compiler keeps program order)
+    __device__ __forceinline__ ulonglong2 load_c(int j) const { return *reinterpret_cast<const ulonglong2*>(c + j); }
+    __device__ __forceinline__ ulonglong2 load_add(int j) const {
+        if constexpr (MODE == 2) {
+            if (g != 1u) return make_ulonglong2(add[(int)automorph_src((u32)j, g, logn)],
+                                                add[(int)automorph_src((u32)(j + 1), g, logn)]);
+        }
+        return *reinterpret_cast<const ulonglong2*>(add + j);
+    }
+    __device__ __forceinline__ u64 combine(u64 v, u64 cj, u64 aj) const {
+        u64 r = shoup(cj + q - v, w, wp, q);
+        if constexpr (MODE == 2) {
+            if (add) r = add_mod(r, aj, q);
+        } else if constexpr (MODE == 3) {
+            if (add) r = add_mod(r, shoup(aj, w2, wp2, q), q);
+        }
+        return r;
+    }
     __device__ __forceinline__ u64 operator()(int j, u64 v) const {
         if constexpr (MODE == 0 || MODE == 5) {
             return v;
@@ -201,6 +220,36 @@ __device__ __forceinline__ constexpr bool fwd_reduce(int s) { return s >= 2 && (
 __device__ __forceinline__ u64 fwd_rbound(u64 q) { return 4 * q; }
 __device__ __forceinline__ u64 fwd_final(u64 x, u64 q) { return csub(csub(csub(x, 4 * q), 2 * q), q); }
 #endif
+
+// Last-pass stores of the combine epilogues (modes 1-3), called right after the thread's canonical results
+// went to `su` and BEFORE the CTA barrier: the c (and addend) words of HB outputs are in flight per thread,
+// the first batch across the barrier.  One dependent 8-byte load per output measured 28% of the ModDown
+// tail's stall samples on the load -> combine edge (profiles/ncu_cfg3_tail_r02_summary.txt).
+template <int LOGN, class EPI>
+__device__ __forceinline__ void epi_store_batched(const EPI& epi, const u64* su, int rank, int tid) {
+    using C = CCfg<LOGN>;
+    constexpr int M = C::PART / (2 * C::T), HB = M < 4 ? M : 4;
+    const int j0 = rank * C::PART;
+    ulonglong2 cv[HB], av[HB];
+#pragma unroll
+    for (int m0 = 0; m0 < M; m0 += HB) {
+#pragma unroll
+        for (int i = 0; i < HB; i++) {
+            const int e = 2 * tid + (m0 + i) * 2 * C::T;
+            cv[i] = epi.load_c(j0 + e);
+            av[i] = epi.add ? epi.load_add(j0 + e) : make_ulonglong2(0ull, 0ull);
+        }
+        if (m0 == 0) __syncthreads();
+#pragma unroll
+        for (int i = 0; i < HB; i++) {
+            const int e = 2 * tid + (m0 + i) * 2 * C::T;
+            ulonglong2 v;
+            v.x = epi.combine(su[cswz(e)], cv[i].x, av[i].x);
+            v.y = epi.combine(su[cswz(e + 1)], cv[i].y, av[i].y);
+            *reinterpret_cast<ulonglong2*>(epi.out + j0 + e) = v;
+        }
+    }
+}
 
 template <int LOGN, class PRO>
 __device__ __forceinline__ void cfwd_passA(u64* x, const PRO& pro, u64* const* peers, int rank,
@@ -266,6 +315,12 @@ __device__ __forceinline__ void cfwd_pass(u64* x, const EPI& epi, u64* sm, int r
         static_assert(TL == 1, "last pass is contiguous");   // coalesced stores via SMEM (see dfwd_pass)
 #pragma unroll
         for (int k = 0; k < BS; k++) sm[cswz(lbase + k)] = fwd_final(x[k], q);
+#ifndef BCN_EPI_SERIAL
+        if constexpr (EPI::kMode >= 1 && EPI::kMode <= 3) {
+            epi_store_batched<LOGN, EPI>(epi, sm, rank, tid);
+            return;
+        }
+#endif
         __syncthreads();
         const int j0 = rank * C::PART;
 #pragma unroll
@@ -467,6 +522,12 @@ __device__ __forceinline__ void dfwd_pass(double* x, const EPI& epi, double* sm,
         u64* su = reinterpret_cast<u64*>(sm);
 #pragma unroll
         for (int k = 0; k < BS; k++) su[cswz(lbase + k)] = fcanon(x[k], f.qinv, f.q);
+#ifndef BCN_EPI_SERIAL
+        if constexpr (EPI::kMode >= 1 && EPI::kMode <= 3) {
+            epi_store_batched<LOGN, EPI>(epi, su, rank, tid);
+            return;
+        }
+#endif
         __syncthreads();
         const int j0 = rank * C::PART;
 #pragma unroll
