@@ -1632,9 +1632,12 @@ static int keyswitch_tail(bcn_ctx* c, u64* out, long long os, const u64* U, int 
     u64* A = tmp;                                   // [G][2][next][N]
     u64* Z = A + (size_t)G * 2 * next * N;          // [G][2][nl][N]
     if ((c->logn == 13 || c->logn == 14) && os == 2LL * nl * N && !getenv_flag_off("BCN_FUSED_MODDOWN") &&
-        !getenv_flag_off("BCN_FUSED_INNER")) {
-        // inner product of the special limbs only (the INTT needs them); the q-limbs'
-        // inner products are computed by the ModDown NTT's epilogue (epilogue 4)
+        getenv_flag_on("BCN_FUSED_INNER")) {
+        // BCN_FUSED_INNER=1: inner product of the special limbs only (the INTT needs them); the
+        // q-limbs' inner products are computed by the ModDown NTT's epilogue (epilogue 4).  Off by
+        // default since the combine epilogue batches its operand loads: materialising every limb and
+        // combining in epilogue 2 measured relin 8.93 -> 8.31 ms, single rotations 70.6 -> 63.3 ms
+        // (config 3, one box)
         CUDA_TRY(inner_op(A, U, G, next, ndig, c->logn, (u32)g, key, 2LL * c->nbasis * N, (long long)c->nbasis * N,
                           ext, ext, c->pr, st, nl, c->K, c->fp_conv ? c->fq : nullptr));
         return moddown_tail(c, out, os, A, G, level, addend, as, add_c1, (u32)g, T, Z, st, U, key);

@@ -686,11 +686,15 @@ def test_config2_mac_matches_oracle():
             np.testing.assert_array_equal(got[g, comp], acc)
 
 
-def test_config3_relin_no_rescale_and_rotation_match_oracle():
+@pytest.mark.parametrize("fused_inner", ["0", "1"])
+def test_config3_relin_no_rescale_and_rotation_match_oracle(fused_inner, monkeypatch):
     """BASELINE config 3 at its real shape: N = 16384, 8 limbs of 50-bit
     primes, K = 1 special prime, dnum = 2.  Stage A: ct x ct + relinearise
     WITHOUT rescale (mul_cc(rescale=False)); stage B: a hoisted rotation by
-    +-2^k of the result -- both bit for bit against the oracle."""
+    +-2^k of the result -- both bit for bit against the oracle, with the q-limb
+    inner products materialised (default) and inside the ModDown NTT's
+    epilogue (BCN_FUSED_INNER=1)."""
+    monkeypatch.setenv("BCN_FUSED_INNER", fused_inner)
     N, L = 16384, 7
     hp = make_params(N, L, 50, dnum=2, n_special=1, seed=5)
     op = O.make_params(N, L, 50, dnum=2, n_special=1, seed=5)
