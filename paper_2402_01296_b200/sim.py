@@ -887,7 +887,10 @@ def materialize_group(cts: list) -> None:
             lvl = first.data_level
             cts_k = [t[1] for t in first._terms]
             pts_ok = [[t[2] for t in c._terms] for c in lazy]
-            if _use_imma() and len(cts_k) <= 256:
+            # fewer than BCN_CONV_TC_MIN_G slot sets fill 2 G of the tensor-core MAC's 32+ columns:
+            # the CUDA-core multi-output MAC is faster there (config-1 latency 3.56 -> 2.86 ms)
+            small = int(cts_k[0].shape[0]) < int(os.environ.get("BCN_CONV_TC_MIN_G", "4"))
+            if _use_imma() and len(cts_k) <= 256 and not small:
                 layout = _conv_layout(int(cts_k[0].shape[0]))
                 out = eng.mac_multi_planes(cts_k, _planes_for(first.ctx, pts_ok, lvl, layout=layout), len(lazy), lvl,
                                            layout=layout)
