@@ -716,6 +716,37 @@ def he_mul(a: Ciphertext, b, rec: OpRecorder, *, mask: bool = False) -> Cipherte
     return Ciphertext(data, lvl - 1, (a.scale * b.scale) / ctx.q(lvl), ctx)
 
 
+def he_square_many(cts: list, rec: OpRecorder) -> list:
+    """[he_mul(c, c)] for the channels of one layer (one Mul_CC each, sim.py:221-248).
+    Below BCN_CONV_TC_MIN_G slot sets (the single-image path, where every launch is a
+    latency, not a throughput) channels that share level, scale and shape run as ONE
+    Mul_CC call on the stacked batch: slot sets are independent, so every channel's
+    ciphertext is bit-identical to its own call."""
+    first = cts[0] if cts else None
+    small = (len(cts) > 1 and os.environ.get("BCN_BATCH_SQUARE", "1") != "0"
+             and first.batch < int(os.environ.get("BCN_CONV_TC_MIN_G", "4")))
+    if small:
+        for c in cts:
+            c.materialize()
+        small = all(c.ctx is first.ctx and c.level == first.level and c.scale == first.scale
+                    and c._data.shape == first._data.shape for c in cts)
+    if not small:
+        return [he_mul(c, c, rec) for c in cts]
+    ctx, lvl, G = first.ctx, first.level, first.batch
+    if lvl < 1:
+        raise _depth_error(rec, ctx)
+    import torch
+
+    rec.bump("Mul_CC", len(cts))
+    stacked = torch.cat([c._data for c in cts], 0)
+    data = ctx.engine.mul_cc(stacked, stacked, lvl)
+    STATS["modup"] += 1
+    STATS["keyswitch"] += 1
+    STATS["rescale"] += 1
+    scale = (first.scale * first.scale) / ctx.q(lvl)
+    return [Ciphertext(data[i * G:(i + 1) * G], lvl - 1, scale, ctx) for i in range(len(cts))]
+
+
 def he_mul_support_mask(a: Ciphertext, rec: OpRecorder, *, drop: bool = True) -> Ciphertext:
     """he_mul(a, mask, mask=True) for a 0/1 mask that is 1 on a's whole slot
     support (a conv layer's output mask: every tap pattern is already zero off

@@ -308,3 +308,25 @@ def test_sharded_forward_two_ranks_gather_matches_reference():
     assert logits.shape == (32 * n_sets, 10)
     _check(logits, ref)
     assert not np.array_equal(c1s[0], c1s[1])
+
+
+def test_batched_square_is_bit_identical_to_per_channel_calls(monkeypatch):
+    """sim.he_square_many (single-image path: the channels of a square layer as ONE
+    Mul_CC call on the stacked batch) returns every channel's ciphertext bit for bit
+    as its own he_mul(c, c) does, with the same counts."""
+    import torch
+    from paper_2402_01296_b200.sim import OpRecorder, encrypt_vector, he_mul, he_square_many
+
+    ctx = B.make_context(8192, 4, 2.0 ** 50)
+    rng = np.random.default_rng(2)
+    cts = [encrypt_vector(rng.standard_normal(ctx.slot_count) * 0.5, ctx) for _ in range(5)]
+    rec_a, rec_b = OpRecorder(), OpRecorder()
+    got = he_square_many(cts, rec_a)
+    want = [he_mul(c, c, rec_b) for c in cts]
+    assert rec_a.counters == rec_b.counters and rec_a.counters["Mul_CC"] == 5
+    for g, w in zip(got, want):
+        assert g.level == w.level and g.scale == w.scale
+        assert torch.equal(g.data, w.data)
+    monkeypatch.setenv("BCN_BATCH_SQUARE", "0")
+    for g, w in zip(he_square_many(cts, OpRecorder()), want):
+        assert torch.equal(g.data, w.data)
