@@ -723,8 +723,7 @@ def he_square_many(cts: list, rec: OpRecorder) -> list:
     Mul_CC call on the stacked batch: slot sets are independent, so every channel's
     ciphertext is bit-identical to its own call."""
     first = cts[0] if cts else None
-    small = (len(cts) > 1 and os.environ.get("BCN_BATCH_SQUARE", "1") != "0"
-             and first.batch < int(os.environ.get("BCN_CONV_TC_MIN_G", "4")))
+    small = bool(cts) and small_batch(cts) and os.environ.get("BCN_BATCH_SQUARE", "1") != "0"
     if small:
         for c in cts:
             c.materialize()
@@ -745,6 +744,43 @@ def he_square_many(cts: list, rec: OpRecorder) -> list:
     STATS["rescale"] += 1
     scale = (first.scale * first.scale) / ctx.q(lvl)
     return [Ciphertext(data[i * G:(i + 1) * G], lvl - 1, scale, ctx) for i in range(len(cts))]
+
+
+def small_batch(cts: list) -> bool:
+    """The single-image regime (fewer than BCN_CONV_TC_MIN_G slot sets): every launch is a
+    latency, so per-channel work is worth stacking into one batch."""
+    return (len(cts) > 1 and os.environ.get("BCN_BATCH_CHANNELS", "1") != "0"
+            and cts[0].batch < int(os.environ.get("BCN_CONV_TC_MIN_G", "4")))
+
+
+def stack_batch(cts: list):
+    """The channels' ciphertexts as ONE ciphertext whose batch is their slot sets back to
+    back (slot sets are independent, so any op on it is the op on every channel), or None
+    when they do not share context, level, scale and shape."""
+    import torch
+
+    first = cts[0]
+    for c in cts:
+        c.materialize()
+    if not all(c.ctx is first.ctx and c.level == first.level and c.scale == first.scale
+               and c._data.shape == first._data.shape for c in cts):
+        return None
+    return Ciphertext(torch.cat([c._data for c in cts], 0), first.level, first.scale, first.ctx)
+
+
+def split_batch(ct: Ciphertext, n: int, *, modup: bool = False) -> list:
+    """Inverse of stack_batch: n ciphertexts viewing ct's slot sets.  modup: the ModUp of the
+    whole stacked batch is computed once and each piece gets its slice (for pieces that are
+    about to be rotated)."""
+    ct.materialize()
+    G = ct.batch // n
+    outs = [Ciphertext(ct._data[i * G:(i + 1) * G], ct.level, ct.scale, ct.ctx) for i in range(n)]
+    if modup:
+        U = ct.ctx.engine.modup(ct._data, ct.level).view(ct.batch, -1)
+        STATS["modup"] += 1
+        for i, o in enumerate(outs):
+            object.__setattr__(o, "_modup", U[i * G:(i + 1) * G])
+    return outs
 
 
 def he_mul_support_mask(a: Ciphertext, rec: OpRecorder, *, drop: bool = True) -> Ciphertext:
