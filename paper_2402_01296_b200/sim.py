@@ -839,6 +839,24 @@ def _rotated(c: Ciphertext, r: int) -> Ciphertext:
     return out
 
 
+def _rotate_many(c: Ciphertext, rs) -> None:
+    """Fill c's rotation memo for every r in rs with ONE bcn_rotate_hoisted_many call (the
+    source's ModUp digits read once, every ModDown in one launch); each entry is bit-identical
+    to what _rotated(c, r) would have computed."""
+    c.materialize()
+    rs = [r for r in dict.fromkeys(int(r) for r in rs) if r != 0 and r not in c._rot]
+    if len(rs) < 2 or os.environ.get("BCN_ROT_MANY_BSGS", "1") == "0":
+        return
+    eng = c.ctx.engine
+    if c._modup is None:
+        object.__setattr__(c, "_modup", eng.modup(c._data, c.level))
+        STATS["modup"] += 1
+    data = eng.rotate_many(c._data, rs, c.level, U=c._modup)
+    STATS["keyswitch"] += len(rs)
+    for k, r in enumerate(rs):
+        c._rot[r] = Ciphertext(data[k], c.level, c.scale, c.ctx)
+
+
 def release(c: Ciphertext) -> None:
     """Drop the hoisting / memo buffers of a ciphertext (device memory)."""
     object.__setattr__(c, "_modup", None)
@@ -905,6 +923,7 @@ def linear_bsgs(parts, rec: OpRecorder) -> Ciphertext:
         b = max(1, math.isqrt(D - 1) + 1) if D > 1 else 1
         by_d = {d: (v, key) for d, v, key in diags}
         ql = ctx.q(level)
+        _rotate_many(x, [i % S for j in range(-(-D // b)) for i in range(b) if dmin + j * b + i in by_d])
         for j in range(-(-D // b)):
             R = dmin + j * b
             pairs = []
