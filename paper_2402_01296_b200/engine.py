@@ -426,7 +426,7 @@ class Engine:
         _lib.call("bcn_mac_terms_acc", self._h, _ptr(out), n, cts, pts, bat, G, level, _stream())
         return out
 
-    def mac_terms(self, terms, level: int, rescale: bool = True) -> torch.Tensor:
+    def mac_terms(self, terms, level: int, rescale: bool = True, out: torch.Tensor | None = None) -> torch.Tensor:
         """sum_t ct_t (x) pt_t (one fused launch per 160 terms), optionally rescaled.
         terms: [(ct u64[G,2,>=level+1,N] with exactly level+1 limbs, pt_mont u64[G|1,level+1,N])]."""
         G = terms[0][0].shape[0]
@@ -434,7 +434,8 @@ class Engine:
         cts = (ctypes.c_uint64 * n)(*[t[0].data_ptr() for t in terms])
         pts = (ctypes.c_uint64 * n)(*[t[1].data_ptr() for t in terms])
         bat = (ctypes.c_int * n)(*[int(t[1].shape[0] != 1) for t in terms])
-        out = self.empty_ct(G, level - 1 if rescale else level)
+        if out is None:
+            out = self.empty_ct(G, level - 1 if rescale else level)
         _lib.call("bcn_mac_terms", self._h, _ptr(out), n, cts, pts, bat, G, level, int(rescale), _stream())
         return out
 

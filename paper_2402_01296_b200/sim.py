@@ -910,7 +910,7 @@ def linear_bsgs(parts, rec: OpRecorder) -> Ciphertext:
     x0 = parts[0][0]
     if x0.level < 1:
         raise _depth_error(rec, ctx)
-    giants = []          # (P_j data, R_j)
+    giants = []          # (baby-step terms of P_j, R_j)
     level = None
     for x, diags in parts:
         x.materialize()
@@ -936,16 +936,27 @@ def linear_bsgs(parts, rec: OpRecorder) -> Ciphertext:
                 pt = _encode(ctx, pv, level, float(ql), True, x.batch)
                 pairs.append((_rotated(x, i % S)._data, pt))
             if pairs:
-                giants.append((eng.mac_terms(pairs, level, rescale=False), R % S))
-                STATS["mac_launch"] += 1
+                giants.append((pairs, R % S))
+    # every giant's partial sum into one buffer, the rotated ones first: ONE ModUp launch
+    # sequence for all of them (a slot-set batch of n_rot x G) instead of one per giant
+    import torch
+    giants.sort(key=lambda t: t[1] == 0)
+    n_rot = sum(1 for _, R in giants if R)
+    G = x0.batch
+    buf = torch.empty((len(giants), G, 2, level + 1, ctx.poly_degree), dtype=torch.int64, device=x0._data.device)
+    for k, (pairs, _) in enumerate(giants):
+        eng.mac_terms(pairs, level, rescale=False, out=buf[k])
+        STATS["mac_launch"] += 1
     rot_terms = []
     out = None
-    for data, R in giants:
+    if n_rot:
+        U = eng.modup(buf[:n_rot].view(n_rot * G, 2, level + 1, ctx.poly_degree), level).view(n_rot * G, -1)
+        STATS["modup"] += n_rot
+    for k, (_, R) in enumerate(giants):
         if R == 0:
-            out = data if out is None else eng.add(out, data, level)
+            out = buf[k] if out is None else eng.add(out, buf[k], level)
         else:
-            rot_terms.append((data, eng.modup(data, level), galois_element(R, ctx.poly_degree), None))
-            STATS["modup"] += 1
+            rot_terms.append((buf[k], U[k * G:(k + 1) * G], galois_element(R, ctx.poly_degree), None))
     if rot_terms:
         rs = eng.rotsum(rot_terms, level)
         STATS["moddown"] += 1
