@@ -84,7 +84,10 @@ cudaError_t encode_op(u64* out, long long os, const double* vals, int vlen, long
         if (ae != cudaSuccess) return ae;
         smem_cfg |= smem_bit;
     }
-    int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
+    // threads per plaintext: a stage is N/4 butterflies behind one barrier, each with two table loads from
+    // L2, so the fewer butterflies per thread the shorter the chain (BCN_FFT_TPB: 512 was the default before)
+    static const int tpb_max = getenv("BCN_FFT_TPB") ? atoi(getenv("BCN_FFT_TPB")) : 1024;
+    int tpb = N / 4 < tpb_max ? (N / 4 < 32 ? 32 : N / 4) : tpb_max;
     encode_kernel<<<nplain, tpb, smem, st>>>(out, os, vals, vlen, vs, scale, logn, limbs, pr, ft, add_err, seed,
                                              id_base, id_dev, raw);
     return launched();
@@ -212,7 +215,10 @@ cudaError_t decode_op(double* out, int nout, const u64* poly, long long ps, int 
         if (ae != cudaSuccess) return ae;
         smem_cfg |= smem_bit;
     }
-    int tpb = N / 2 < 512 ? (N / 2 < 32 ? 32 : N / 2) : 512;
+    // threads per plaintext: a stage is N/4 butterflies behind one barrier, each with two table loads from
+    // L2, so the fewer butterflies per thread the shorter the chain (BCN_FFT_TPB: 512 was the default before)
+    static const int tpb_max = getenv("BCN_FFT_TPB") ? atoi(getenv("BCN_FFT_TPB")) : 1024;
+    int tpb = N / 4 < tpb_max ? (N / 4 < 32 ? 32 : N / 4) : tpb_max;
     decode_kernel<<<npoly, tpb, smem, st>>>(out, nout, poly, ps, k, scale, logn, pr, ft, q0inv_mod_q1, q0inv_p);
     return launched();
 }
