@@ -240,7 +240,6 @@ __device__ __forceinline__ void ipass(W* x, W* a, const typename Ar<W>::TW* __re
         const int gi = b / TL;
         const int base = gi * (C::N >> S0) + (b % TL);
         const int pbase = base + (base >> 5);
-#pragma unroll
         if constexpr (GIN) {                            // first pass straight from HBM: contiguous 16-word runs
             static_assert(TL == 1 && BS == 16, "global input needs a contiguous first pass");
             constexpr int PER = 16 / sizeof(W);
